@@ -1,0 +1,105 @@
+"""Oracle: the sparse-input MLP of the paper, one SGD step, in fp64.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Model (section 5.1 "3-layer Multi-Layer Perceptron (MLP) model having
+ReLU layer activation, softmax multi-class probability, and cross-entropy
+loss"; reading R1: input -> one ReLU hidden layer -> softmax output):
+
+    a_r   = b1 + sum_{(f, v) in x_r} v * W1[f]          (sparse x_r)
+    h_r   = max(a_r, 0)
+    z_r   = W2T h_r + b2                                (length C)
+    LSE_r = log sum_c exp(z_rc)
+    loss  = (1/B) sum_r [LSE_r - (1/k_r) sum_{y in Y_r} z_ry]     (reading R3)
+
+Backward ("the backward pass implements the chain rule"), all from the
+pre-update parameters:
+
+    dz_rc = (softmax(z_r)_c - [c in Y_r]/k_r) / B
+    dW2T  = dz^T H,  db2 = sum_r dz_r,  dH = dz W2T,  dA = dH * [A > 0]  (R4)
+    dW1[f] = sum_{r: f in x_r} v_rf dA_r,  db1 = sum_r dA_r
+
+Update ("the third pass ... updates the model with the computed gradient
+using the learning rate"):  theta <- theta - lr * dtheta, computed in
+fp64 and stored in fp32 (parameters are fp32 in the packed layout, R2).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def spmm(row_ptr, col, val, W1, b1):
+    """A = X W1 + b1 for a CSR batch X (P:51 forward pass, first layer)."""
+    B = len(row_ptr) - 1
+    W1 = np.asarray(W1, np.float64)
+    A = np.empty((B, W1.shape[1]), np.float64)
+    for r in range(B):
+        s, e = int(row_ptr[r]), int(row_ptr[r + 1])
+        A[r] = np.asarray(b1, np.float64) + np.asarray(val[s:e], np.float64) @ W1[col[s:e]]
+    return A
+
+
+def target_matrix_rows(lab_ptr, lab):
+    """(rows, cols, weights) of the sparse target T_rc = [c in Y_r]/k_r (R3)."""
+    B = len(lab_ptr) - 1
+    rows, cols, w = [], [], []
+    for r in range(B):
+        s, e = int(lab_ptr[r]), int(lab_ptr[r + 1])
+        k = e - s
+        if k < 1:
+            raise ValueError("row %d has no label (reading R3 rejects k_r = 0)" % r)
+        for y in lab[s:e]:
+            rows.append(r); cols.append(int(y)); w.append(1.0 / k)
+    return np.array(rows, np.int64), np.array(cols, np.int64), np.array(w, np.float64)
+
+
+def forward(batch, params):
+    """Forward pass.  Returns dict with A, H, Z (logits), LSE, loss (fp64)."""
+    W1, b1, W2T, b2 = (np.asarray(params[k], np.float64) for k in ("W1", "b1", "W2T", "b2"))
+    A = spmm(batch.row_ptr, batch.col, batch.val, W1, b1)
+    H = np.maximum(A, 0.0)
+    Z = H @ W2T.T + b2
+    zmax = Z.max(axis=1, keepdims=True)
+    LSE = zmax[:, 0] + np.log(np.exp(Z - zmax).sum(axis=1))
+    tr, tc, tw = target_matrix_rows(batch.lab_ptr, batch.lab)
+    B = A.shape[0]
+    label_term = np.zeros(B)
+    np.add.at(label_term, tr, tw * Z[tr, tc])
+    loss = float(np.mean(LSE - label_term))
+    return {"A": A, "H": H, "Z": Z, "LSE": LSE, "loss": loss}
+
+
+def gradients(batch, params, fwd=None):
+    """All four gradients of the loss w.r.t. the packed parameters (fp64)."""
+    if fwd is None:
+        fwd = forward(batch, params)
+    W2T = np.asarray(params["W2T"], np.float64)
+    A, H, Z, LSE = fwd["A"], fwd["H"], fwd["Z"], fwd["LSE"]
+    B = A.shape[0]
+    G = np.exp(Z - LSE[:, None])                    # softmax(z_r)
+    tr, tc, tw = target_matrix_rows(batch.lab_ptr, batch.lab)
+    np.add.at(G, (tr, tc), -tw)                     # - T
+    G /= B                                          # dz
+    dW2T = G.T @ H
+    db2 = G.sum(axis=0)
+    dH = G @ W2T
+    dA = dH * (A > 0)
+    d = np.asarray(params["W1"]).shape[0]
+    dW1 = np.zeros((d, A.shape[1]), np.float64)
+    rid = np.repeat(np.arange(B), np.diff(np.asarray(batch.row_ptr)))
+    np.add.at(dW1, np.asarray(batch.col, np.int64),
+              np.asarray(batch.val, np.float64)[:, None] * dA[rid])
+    db1 = dA.sum(axis=0)
+    return {"W1": dW1, "b1": db1, "W2T": dW2T, "b2": db2, "dZ": G, "dH": dH, "dA": dA}
+
+
+def sgd_step(batch, params, lr):
+    """One SGD step (P:51 three passes).  params: dict of fp32 arrays.
+    Returns (new fp32 params dict, loss, grads)."""
+    fwd = forward(batch, params)
+    g = gradients(batch, params, fwd)
+    lr = float(np.float32(lr))
+    new = {}
+    for k in ("W1", "b1", "W2T", "b2"):
+        new[k] = (np.asarray(params[k], np.float64) - lr * g[k]).astype(np.float32)
+    return new, fwd["loss"], g

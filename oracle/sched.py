@@ -1,0 +1,112 @@
+"""Oracle: the scheduler -- replay routing, Alg. 1, Alg. 2 weights.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain Python integers and
+doubles, written out in the paper's order and notation.
+"""
+from __future__ import annotations
+
+MASK64 = (1 << 64) - 1
+
+
+# --------------------------------------------------------------------------
+# Stream order (reading R10: not in the paper).  Fisher-Yates driven by
+# SplitMix64; the bounded draw is j = (r * (i + 1)) >> 64.
+# --------------------------------------------------------------------------
+def splitmix64(state):
+    state = (state + 0x9E3779B97F4A7C15) & MASK64
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return state, z ^ (z >> 31)
+
+
+def permutation(n, seed):
+    perm = list(range(n))
+    s = seed & MASK64
+    for i in range(n - 1, 0, -1):
+        s, r = splitmix64(s)
+        j = (r * (i + 1)) >> 64
+        perm[i], perm[j] = perm[j], perm[i]
+    return perm
+
+
+# --------------------------------------------------------------------------
+# Dynamic scheduling, replay mode (section 3.1: "batches are dispatched
+# one-by-one based on GPU availability. Whenever a GPU finishes an epoch, it is
+# assigned the next batch ... controlled by fixing the number of training
+# samples processed between model merging stages -- we call these samples a
+# mega-batch").  GPU availability is replayed from integer cost models
+# (reading R9); ties go to the lowest id and the last batch is truncated
+# (reading R8); u_i counts dispatched batches.
+# --------------------------------------------------------------------------
+def batch_cost(cm, rows, nnz):
+    return ((cm.c0 + cm.c_row * rows + cm.c_nnz * nnz) * cm.num) // cm.den
+
+
+def route_replay(costs, b, M, nnz_of):
+    """costs: list of CostModel; b: batch sizes; M: samples in this mega-batch;
+    nnz_of(start, rows) -> nnz of that slice of the mega-batch.
+    Returns (log [(replica, start, rows)], u, clocks)."""
+    N = len(costs)
+    t = [0] * N
+    u = [0] * N
+    log = []
+    assigned = 0
+    while assigned < M:
+        i = min(range(N), key=lambda k: (t[k], k))       # earliest free, lowest id
+        rows = min(b[i], M - assigned)
+        log.append((i, assigned, rows))
+        t[i] += batch_cost(costs[i], rows, nnz_of(assigned, rows))
+        u[i] += 1
+        assigned += rows
+    return log, u, t
+
+
+# --------------------------------------------------------------------------
+# Algorithm 1 "Batch Size Scaling", reading R11/R23 for the
+# rounding of beta*(u_i - mu) and the bound check, and the linear scaling rule
+# for lr.
+# --------------------------------------------------------------------------
+def alg1(u, b, beta, b_min, b_max, lr0):
+    N = len(u)
+    U = sum(u)                            # line 1: mu = U / N
+    b_new = list(b)
+    for i in range(N):                    # line 2: for all GPU_i
+        D = N * u[i] - U                  # N * (u_i - mu), exact integer
+        step = (2 * beta * abs(D) + N) // (2 * N)   # round(beta*|u_i - mu|), half away from 0
+        if D > 0 and b[i] + step <= b_max:          # lines 2-4 (faster GPU)
+            b_new[i] = b[i] + step
+        elif D < 0 and b[i] - step >= b_min:        # lines 5-7 (slower GPU)
+            b_new[i] = b[i] - step
+    lr_new = [float(_f32(float(lr0) * bi / b_max)) for bi in b_new]
+    return b_new, lr_new
+
+
+def _f32(x):
+    import numpy as np
+    return np.float32(x)
+
+
+# --------------------------------------------------------------------------
+# Algorithm 2 "Normalized Model Merging", weights part; readings
+# R13 (exact equality), R14 (lexicographic argmax/argmin of (u_i, b_i), skip
+# when identical), R15 (strict <), R16 (no renormalisation).
+# --------------------------------------------------------------------------
+def alg2(u, b, norms, delta, pert_thr):
+    N = len(u)
+    if all(x == u[0] for x in u):                 # line 2
+        sb = float(sum(b))
+        alpha = [float(bi) / sb for bi in b]      # line 3
+    else:
+        su = float(sum(u))
+        alpha = [float(ui) / su for ui in u]      # line 5
+    perturbed = 0
+    if all(nrm < pert_thr for nrm in norms):      # line 7
+        keys = [(u[i], b[i]) for i in range(N)]
+        r = max(range(N), key=lambda i: (keys[i], -i))    # argmax, lowest id on ties
+        s = min(range(N), key=lambda i: (keys[i], i))     # argmin, lowest id on ties
+        if keys[r] != keys[s]:
+            alpha[r] = alpha[r] * (1.0 + delta)   # line 9
+            alpha[s] = alpha[s] * (1.0 - delta)
+            perturbed = 1
+    return alpha, perturbed

@@ -1,0 +1,148 @@
+"""Pins for oracle/sched.py and oracle/csr.py (CPU only).
+
+Golden cases under tests/golden/ are worked by hand from the paper's
+Algorithms 1-2 and section 3.1 (citations inside each file)."""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+from hypothesis import given, settings, strategies as st
+
+import synthgen
+from oracle import csr as ocsr
+from oracle import sched as osched
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _cm(c):
+    return synthgen.CostModel(*c)
+
+
+def test_routing_golden():
+    for case in _load("routing_cases.json")["cases"]:
+        costs = [_cm(c) for c in case["costs"]]
+        log, u, t = osched.route_replay(costs, case["b"], case["M"], lambda s, r: 0)
+        assert [list(x) for x in log] == case["log"]
+        assert u == case["u"] and t == case["clocks"]
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 6), st.integers(1, 400), st.data())
+def test_routing_conserves_samples(N, M, data):
+    b = [data.draw(st.integers(1, 40)) for _ in range(N)]
+    costs = [synthgen.CostModel(data.draw(st.integers(0, 50)), data.draw(st.integers(0, 9)),
+                                data.draw(st.integers(0, 3)), data.draw(st.integers(1, 5)), 1)
+             for _ in range(N)]
+    log, u, _ = osched.route_replay(costs, b, M, lambda s, r: 3 * r)
+    covered = []
+    for i, s, r in log:
+        assert 1 <= r <= b[i]
+        covered.extend(range(s, s + r))
+    assert covered == list(range(M))              # every sample exactly once, in stream order
+    assert sum(u) == len(log)
+    # only the last batch may be truncated
+    for i, s, r in log[:-1]:
+        assert r == b[i]
+
+
+def test_alg1_golden():
+    for case in _load("alg1_cases.json")["cases"]:
+        b, lr = osched.alg1(case["u"], case["b"], case["beta"], case["b_min"], case["b_max"], 0.1)
+        assert b == case["b_out"], case["why"]
+        for bi, li in zip(b, lr):
+            assert li == float(np.float32(0.1 * bi / case["b_max"]))
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.integers(1, 8), st.data())
+def test_alg1_invariants(N, data):
+    b_max = data.draw(st.sampled_from([16, 64, 1024]))
+    b_min = b_max // 8
+    beta = max(1, b_min // 2)
+    b = [data.draw(st.integers(b_min, b_max)) for _ in range(N)]
+    u = [data.draw(st.integers(0, 30)) for _ in range(N)]
+    bn, lr = osched.alg1(u, b, beta, b_min, b_max, 0.5)
+    assert all(b_min <= x <= b_max for x in bn)
+    mu = Fraction(sum(u), N)
+    for i in range(N):
+        if u[i] > mu:
+            assert bn[i] >= b[i]
+        elif u[i] < mu:
+            assert bn[i] <= b[i]
+        else:
+            assert bn[i] == b[i]
+        assert abs(lr[i] - 0.5 * bn[i] / b_max) <= 1e-7 * lr[i]
+
+
+def test_alg2_golden():
+    for case in _load("alg2_cases.json")["cases"]:
+        norms = [0.0 if case["norms_below"] else 1.0] * len(case["u"])
+        alpha, pert = osched.alg2(case["u"], case["b"], norms, 0.1, 0.1)
+        exp = [Fraction(a) for a in case["alpha"]]
+        for a, e in zip(alpha, exp):
+            assert abs(Fraction(a) - e) <= Fraction(1, 10**15) * e
+        assert abs(Fraction(sum(alpha)) - Fraction(case["sum"])) <= Fraction(1, 10**14)
+        assert pert == case["perturbed"]
+
+
+@settings(max_examples=100, deadline=None)
+@given(st.integers(1, 8), st.data())
+def test_alg2_invariants(N, data):
+    u = [data.draw(st.integers(0, 20)) for _ in range(N)]
+    if sum(u) == 0:
+        u[0] = 1
+    b = [data.draw(st.integers(1, 64)) for _ in range(N)]
+    a0, p0 = osched.alg2(u, b, [1.0] * N, 0.1, 0.1)          # not regularised: no perturbation
+    assert p0 == 0 and abs(sum(a0) - 1.0) <= 1e-15 * N
+    a1, p1 = osched.alg2(u, b, [0.0] * N, 0.1, 0.1)
+    if p1:
+        r = max(range(N), key=lambda i: ((u[i], b[i]), -i))
+        s = min(range(N), key=lambda i: ((u[i], b[i]), i))
+        assert abs(sum(a1) - (1.0 + 0.1 * (a0[r] - a0[s]))) <= 1e-14
+    a2, p2 = osched.alg2(u, b, [0.0] * N, 0.1, 0.0)          # pert_thr = 0: never perturb
+    assert p2 == 0 and a2 == a0
+
+
+def test_splitmix64_reference_vector():
+    # SplitMix64 (Steele, Lea, Flood 2014) from state 0: first output 0xE220A8397B1DCDAF
+    _, z = osched.splitmix64(0)
+    assert z == 0xE220A8397B1DCDAF
+
+
+def test_permutation_is_permutation():
+    for n, seed in [(1, 0), (2, 5), (100, 7), (1000, 123)]:
+        p = osched.permutation(n, seed)
+        assert sorted(p) == list(range(n))
+    assert osched.permutation(100, 1) != osched.permutation(100, 2)
+
+
+def test_transpose_against_lexsort_and_roundtrip():
+    ds = synthgen.tiny_dataset(n=50, d=30, C=20, seed=4)
+    keys, sptr, srow, sval = ocsr.transpose(ds.row_ptr, ds.col, ds.val)
+    rid = np.repeat(np.arange(ds.n), np.diff(ds.row_ptr))
+    order = np.lexsort((rid, ds.col))            # library sort by (feature, row)
+    assert np.array_equal(srow, rid[order]) and np.array_equal(sval, ds.val[order])
+    assert np.array_equal(keys, np.unique(ds.col))
+    assert sptr[-1] == len(ds.col) and np.all(np.diff(sptr) > 0)
+    # transpose of the transpose is the original CSR
+    k2, p2, r2, v2 = ocsr.transpose(sptr, srow, sval)
+    assert np.array_equal(k2, np.arange(ds.n)) and np.array_equal(p2, ds.row_ptr)
+    assert np.array_equal(keys[r2], ds.col)
+    assert np.array_equal(v2, ds.val)
+
+
+def test_stream_ids_and_batch_csr():
+    ds = synthgen.tiny_dataset(n=10, d=30, C=20, seed=4)
+    ids = ocsr.stream_ids(8, 5, ds.n)
+    assert list(ids) == [8, 9, 0, 1, 2]
+    rp, col, val, lp, lab = ocsr.batch_csr(ds, ids)
+    ref = ds.rows(ids)
+    assert np.array_equal(rp, ref.row_ptr) and np.array_equal(col, ref.col)
+    assert np.array_equal(lp, ref.lab_ptr) and np.array_equal(lab, ref.lab)
