@@ -1,0 +1,252 @@
+/*
+ * adasgd.h -- C-ABI of the B200-native Adaptive SGD hot path
+ * (Ma, Rusu, Wu, Sim, "Adaptive Elastic Training for Sparse Deep Learning on
+ * Heterogeneous Multi-GPU Servers", arXiv 2110.07029).
+ *
+ * Citations "P:N" refer to line N of the paper text; readings
+ * "Rk" are the interpretations listed in DESIGN.md section 3.
+ *
+ * One as_ctx = one model replica = one GPU = one process (section 2.2
+ * "allocate a separate model replica to every GPU"; "GPU managers").
+ * Every pointer in this header is a plain host or device pointer; no torch
+ * types cross the boundary.  Unless a function says otherwise:
+ *   - host arrays are owned by the caller and are copied (through pinned
+ *     staging) or consumed before the call returns;
+ *   - device work is enqueued on the ctx stream (as_config.stream) and the call
+ *     returns without waiting;
+ *   - the return value is AS_OK or a negative AS_E_* code, and
+ *     as_last_error() gives a thread-local message for the last failure;
+ *   - AS_E_INVALID leaves the ctx unchanged; AS_E_CUDA / AS_E_NCCL are sticky:
+ *     every later call on that ctx returns AS_E_STATE.
+ *
+ * Packed parameter vector (R2): fp32, P = d*h + h + C*h + C floats,
+ *     [ W1 (d x h, row-major) | b1 (h) | W2T (C x h, row-major, label-major) | b2 (C) ]
+ * "model dimensionality" |w| of Alg. 2 line 7 is P.
+ */
+#ifndef ADASGD_H
+#define ADASGD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+  AS_OK = 0,
+  AS_E_INVALID = -1, /* argument / input validation failed; no state change   */
+  AS_E_CUDA = -2,    /* a CUDA call or kernel failed (sticky)                  */
+  AS_E_NCCL = -3,    /* an NCCL call failed (sticky)                           */
+  AS_E_OOM = -4,     /* workspace too small / host allocation failed           */
+  AS_E_STATE = -5    /* ctx poisoned by an earlier sticky error, or wrong order */
+};
+
+/* ---- arithmetic of the output layer (steps a5/a6) -------------------------
+ * AS_FP32: SIMT fp32 everywhere (parity mode, |rel err| <= 1e-4 vs oracle).
+ * AS_BF16: tcgen05 tensor cores, bf16 operands (H, W2T shadow, softmax grad),
+ *          fp32 accumulation in TMEM, fp32 master weights (parity 2e-2).   */
+enum { AS_FP32 = 0, AS_BF16 = 1 };
+
+/* ---- flags --------------------------------------------------------------- */
+enum {
+  AS_FLAG_DEBUG_GRADS = 1 /* keep every gradient of the last step in device
+                             memory for as_debug_get (tests only)            */
+};
+
+typedef struct as_ctx as_ctx; /* opaque */
+
+typedef struct {
+  int64_t n_features;     /* d  (Table 1 "features")                  */
+  int64_t n_labels;       /* C  ("classes")                                     */
+  int32_t hidden;         /* h  hidden width, 128 or 256 (R1)                    */
+  int32_t b_max;          /* largest batch (P:201 memory provisioned for it)    */
+  int32_t b_min;          /* b_max / 8                                   */
+  int32_t beta;           /* b_min / 2                                   */
+  int64_t megabatch;      /* M samples between merges (R7: 100*b_max)    */
+  int32_t max_row_nnz;    /* capacity: largest nnz of one sample                 */
+  int32_t max_row_labels; /* capacity: largest label count of one sample        */
+  double lr0;             /* learning rate at b_max                     */
+  double gamma;           /* momentum, 0.9                              */
+  double delta;           /* perturbation factor, 0.1                   */
+  double pert_thr;        /* perturbation threshold, 0.1                */
+  int32_t precision;      /* AS_FP32 | AS_BF16                                  */
+  int32_t flags;          /* AS_FLAG_*                                          */
+  int32_t rank;           /* replica id i, 0 <= rank < world                    */
+  int32_t world;          /* number of replicas N                               */
+  const void *nccl_unique_id; /* 128-byte ncclUniqueId from as_nccl_unique_id()
+                                 on rank 0, broadcast by the caller; NULL when
+                                 world == 1 or in local-group mode             */
+  void *workspace;        /* device arena, >= as_workspace_size() bytes, 256-B
+                             aligned; owned by the caller, alive until destroy */
+  size_t workspace_bytes;
+  void *stream;           /* cudaStream_t borrowed from the caller             */
+  int32_t device;         /* CUDA device ordinal of this replica               */
+} as_config;
+
+/* Bytes of device workspace the ctx needs for cfg (validates cfg). */
+int as_workspace_size(const as_config *cfg, size_t *bytes);
+
+/* Write a fresh 128-byte NCCL unique id into out (rank 0 only). */
+int as_nccl_unique_id(void *out128);
+
+/* Create the replica.  init_params: HOST pointer to the packed fp32 vector
+ * (P floats), identical on every rank ("All the algorithms are initialized
+ * with the same model").  Sets w_i = wbar = wbar_p = init (R17),
+ * b_i = b_max, lr_i = lr0.  When world > 1 and nccl_unique_id is
+ * non-NULL this is collective (ncclCommInitRank).  Blocks until done. */
+int as_init(const as_config *cfg, const float *init_params, as_ctx **out);
+
+int as_destroy(as_ctx *ctx);
+const char *as_last_error(void);
+
+/* ---- batches (step a2) ------------------------------------------------------
+ * Load the next training batch of `rows` samples from HOST CSR arrays
+ * ("moving the training batch ... to the GPU"; P:217 libSVM sparse):
+ *   row_ptr[rows+1] int64 (row_ptr[0] may be non-zero: the batch is rebased),
+ *   col[nnz] int32 feature ids, strictly increasing inside a row, in [0, d);
+ *   val[nnz] float32;  lab_ptr[rows+1] int64;  lab[L] int32 label ids,
+ *   strictly increasing inside a row, in [0, C), at least one per row (R3).
+ * Validation failures (rows not in [1, b_i] with b_i this rank's batch size,
+ * non-monotone pointers, ids out of range, unsorted/duplicate ids, a row with
+ * zero labels, capacity exceeded) return AS_E_INVALID with no state change. */
+int as_load_batch_csr(as_ctx *ctx, int32_t rows, const int64_t *row_ptr,
+                      const int32_t *col, const float *val,
+                      const int64_t *lab_ptr, const int32_t *lab);
+
+/* Device-resident dataset: bytes of device memory needed for n samples with
+ * nnz features and L labels in total. */
+int as_dataset_bytes(int64_t n, int64_t nnz, int64_t L, size_t *bytes);
+
+/* Upload a whole dataset (HOST CSR arrays as above, n samples) into the
+ * caller-owned DEVICE buffer dev_buf (>= as_dataset_bytes).  order[n] (host,
+ * nullable = identity) fixes the stream order (R10): stream position p maps
+ * to sample order[p mod n].  Validates every row.  Blocks until copied. */
+int as_dataset_upload(as_ctx *ctx, void *dev_buf, size_t dev_bytes, int64_t n,
+                      const int64_t *row_ptr, const int32_t *col,
+                      const float *val, const int64_t *lab_ptr,
+                      const int32_t *lab, const int64_t *order);
+
+/* Load the batch = stream positions [pos, pos+rows) of the resident dataset,
+ * built on the device (gather + rebase).  rows in [1, b_i]. */
+int as_load_batch_stream(as_ctx *ctx, int64_t pos, int32_t rows);
+
+/* ---- one SGD step on this replica (steps a3-a8) ------------------------------
+ * On the last loaded batch, with this rank's lr_i: batch transposes (a3),
+ * SpMM forward (a4), output layer forward + softmax cross-entropy (a5),
+ * backward (a5/a6/a7) and the SGD update of W1, b1, W2T, b2 ("SGD
+ * requires three passes").  loss_out (nullable): mean loss over the rows of
+ * the batch (R3); non-NULL forces a stream synchronisation. */
+int as_train_step(as_ctx *ctx, float *loss_out);
+
+/* ---- merge (steps a9-a13, Alg. 2) ------------------------------------
+ * Collective over all `world` ranks, called with identical u[world] (updates
+ * since the last merge) and b[world] (batch sizes in force during the
+ * mega-batch, R12).  Computes n_i = ||w_i||_2 / P (a9), all-gathers the norms,
+ * alpha (a10, R13-R16, identical on every rank), prescales w_i by alpha_i
+ * (a11), all-reduces (a12, NCCL over NVLink) and applies the momentum update
+ * w' = sum alpha_i w_i + gamma (wbar - wbar_p); wbar_p <- wbar; wbar <- w';
+ * w_i <- w' (a13, P:187 replicas restart from the global model).
+ * alpha_out[world] and perturbed_out are nullable; non-NULL synchronises. */
+int as_merge(as_ctx *ctx, const int32_t *u, const int32_t *b,
+             double *alpha_out, int32_t *perturbed_out);
+
+/* Local-group merge: the n contexts ctxs[0..n-1] live in THIS process (one per
+ * device, or several on one device for testing), were created with
+ * world == n, rank == index and nccl_unique_id == NULL.  Same semantics as
+ * as_merge, the reduction reads every replica directly (same-device or peer
+ * pointers).  Blocks until done. */
+int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u,
+                   const int32_t *b, double *alpha_out, int32_t *perturbed_out);
+
+/* Set the batch sizes of all ranks (b[world], used by the next merge's
+ * Alg. 2 line 3) and this rank's learning rate lr[rank] (Alg. 1 output).
+ * b[i] must lie in [b_min, b_max]. */
+int as_set_batch_sizes(as_ctx *ctx, const int32_t *b, const float *lr);
+
+/* ---- inspection (tests) -------------------------------------------------------- */
+enum { AS_PARAMS_REPLICA = 0, AS_PARAMS_GLOBAL = 1, AS_PARAMS_GLOBAL_PREV = 2 };
+/* Copy P floats of the chosen parameter vector to host_out (synchronises). */
+int as_get_params(as_ctx *ctx, int32_t which, float *host_out);
+/* Overwrite the replica parameters from a host vector (tests; synchronises). */
+int as_set_params(as_ctx *ctx, int32_t which, const float *host_in);
+
+enum {
+  AS_DBG_H = 0,     /* float [rows*h]   ReLU(X W1 + b1) of the last step      */
+  AS_DBG_LSE = 1,   /* float [rows]     log-sum-exp of the logits (natural)   */
+  AS_DBG_LOSS = 2,  /* float [rows]     per-row loss (R3)                     */
+  AS_DBG_DA = 3,    /* float [rows*h]   dL/dA1                                */
+  AS_DBG_DB1 = 4,   /* float [h]                                              */
+  AS_DBG_DW2T = 5,  /* float [C*h]      needs AS_FLAG_DEBUG_GRADS             */
+  AS_DBG_DB2 = 6,   /* float [C]        needs AS_FLAG_DEBUG_GRADS             */
+  AS_DBG_DW1 = 7,   /* float [U*h]      rows of the unique features, ascending;
+                       needs AS_FLAG_DEBUG_GRADS                              */
+  AS_DBG_FSEG = 8,  /* int32 [1+U+(U+1)+nnz+nnz]: U, feature ids, seg ptr,
+                       csc rows, csc vals (float bits) -- step a3           */
+  AS_DBG_LSEG = 9,  /* int32 [1+V+(V+1)+L]: V, label ids, seg ptr, rows      */
+  AS_DBG_BATCH = 10,/* int32 [4]: rows, nnz, L, U of the loaded batch        */
+  AS_DBG_LOGITS = 11 /* float [rows*C] logits (AS_FP32 only)                 */
+};
+/* Copy a debug view of the last step to host_out (capacity `bytes`);
+ * *written receives the byte count.  Synchronises. */
+int as_debug_get(as_ctx *ctx, int32_t which, void *host_out, size_t bytes,
+                 size_t *written);
+
+/* Tensor-core self-test (tests only): A, B are DEVICE bf16 [128][128]
+ * row-major; writes DEVICE fp32 [128][128] results of the three operand
+ * layouts the output layer uses:  S = A B^T;  P = bf16(S/16);  O = P B;
+ * T = A^T P^T  (i.e. T[j][n] = sum_r A[r][j] P[n][r]).  Synchronises. */
+int as_tc_selftest(const void *A, const void *B, float *S, float *O, float *T);
+
+/* ---- scheduler (pure host functions, steps a1, a10, a14) --------------------- */
+typedef struct {        /* replay cost of a batch in picoseconds (R9):        */
+  int64_t c0, c_row, c_nnz, num, den;  /* (c0 + c_row*rows + c_nnz*nnz)*num/den */
+} as_cost_model;
+
+typedef struct {
+  int32_t replica;      /* i                                                   */
+  int32_t rows;         /* rows of this batch (last one may be truncated, R8)  */
+  int64_t start;        /* offset inside the mega-batch                         */
+} as_route;
+
+/* Replay routing of one mega-batch (next batch to the GPU that frees
+ * first; R8 ties -> lowest id, truncated last batch; R9 integer clocks).
+ * nnz_prefix[M+1] (host) = cumulative nnz of the mega-batch's samples.
+ * out_log capacity max_log entries; *n_log, u_out[N], clocks_out[N] written.
+ * Returns AS_E_INVALID if out_log is too small. */
+int as_sched_route_replay(int32_t N, const as_cost_model *cost, const int32_t *b,
+                          int64_t M, const int64_t *nnz_prefix, as_route *out_log,
+                          int64_t max_log, int64_t *n_log, int32_t *u_out,
+                          int64_t *clocks_out);
+
+/* Alg. 1 with R11 integer rounding; lr_out[i] =
+ * (float)(lr0 * b_out[i] / b_max) (linear scaling rule). */
+int as_sched_alg1(int32_t N, const int32_t *u, const int32_t *b, int32_t beta,
+                  int32_t b_min, int32_t b_max, double lr0, int32_t *b_out,
+                  float *lr_out);
+
+/* Alg. 2 lines 1-10 with R13-R16. */
+int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b,
+                  const double *norms, double delta, double pert_thr,
+                  double *alpha_out, int32_t *perturbed_out);
+
+/* Fisher-Yates permutation of [0, n) driven by SplitMix64(seed) (R10). */
+int as_sched_permutation(int64_t n, uint64_t seed, int64_t *out);
+
+/* Live routing: a cross-process shared cursor.  as_live_open
+ * maps (creating if rank 0) a POSIX shm segment `name`; as_live_claim
+ * atomically claims the next `b` samples of a mega-batch of M samples and
+ * returns the start in *start and the (possibly truncated) row count in *rows
+ * (0 when the mega-batch is exhausted); as_live_reset rearms for the next
+ * mega-batch (call from one rank between barriers). */
+typedef struct as_live as_live;
+int as_live_open(const char *name, int32_t create, as_live **out);
+int as_live_claim(as_live *lv, int64_t M, int32_t b, int64_t *start, int32_t *rows);
+int as_live_reset(as_live *lv);
+int as_live_close(as_live *lv, int32_t unlink_segment);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADASGD_H */

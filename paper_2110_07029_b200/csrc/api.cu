@@ -1,0 +1,713 @@
+// C-ABI of the Adaptive SGD hot path (include/adasgd.h): replica context,
+// workspace arena, input validation, step and merge orchestration.
+// P:N = PAPER.md line N; Rk = DESIGN.md reading k.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "adasgd.h"
+#include "common.cuh"
+#include "common_host.h"
+
+thread_local char g_as_err[512] = "";
+
+using as::StepDesc;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr int kNormBlocks = 148 * 8;
+
+struct Layout {
+  size_t off[64];
+  int n = 0;
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    const size_t o = total;
+    total += (bytes + kAlign - 1) / kAlign * kAlign;
+    return o;
+  }
+};
+
+struct Dims {
+  long long d, C, P;
+  int h, b_max, bpad, nnz_cap, lab_cap, sort_cap, max_splits, splitk;
+};
+
+int key_bits(long long n) {
+  int b = 1;
+  while ((1ll << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct as_ctx {
+  as_config cfg;
+  Dims D;
+  cudaStream_t stream;
+  int num_sms;
+  int sticky;
+  // arena
+  float *w, *wbar, *wbarp;
+  __nv_bfloat16 *w2b;
+  int64_t *row_ptr, *lab_ptr, *ids;
+  int32_t *col, *lab;
+  float *val;
+  StepDesc *desc;
+  uint32_t *sk0, *sv0, *sk1, *sv1, *hist;
+  int32_t *rowid, *flags, *scan_tmp;
+  int32_t *fseg_id, *fseg_ptr, *fseg_row, *long_list;
+  float *fseg_val;
+  int32_t *lseg_id, *lseg_ptr, *lseg_row, *cls_seg;
+  float *Hf;
+  __nv_bfloat16 *Hb;
+  float *dA, *lse2, *zsum, *labW, *lossr, *loss;
+  float *pm, *pl, *pO;
+  float *Z, *dH, *dW2, *splitk_tmp;
+  float *dbg_dW2, *dbg_db2, *dbg_dW1, *dbg_db1;
+  double *norm_part, *norm_dev, *norms_all;
+  float *alpha_dev;
+  const float **reps_dev;
+  as::TcPlan *plan;
+  // host state
+  std::vector<int32_t> b_all;
+  float lr;
+  int loaded_rows;
+  bool has_batch;
+  void *pin[2];
+  size_t pin_bytes;
+  cudaEvent_t pin_ev[2];
+  int pin_idx;
+  // resident dataset
+  const int64_t *ds_row_ptr, *ds_lab_ptr, *ds_order;
+  const int32_t *ds_col, *ds_lab;
+  const float *ds_val;
+  int64_t ds_n;
+  ncclComm_t comm;
+};
+
+namespace {
+
+int validate_cfg(const as_config *c) {
+  if (!c) return as_fail(AS_E_INVALID, "config is NULL");
+  if (c->n_features < 1 || c->n_labels < 1 || c->n_features >= (1ll << 31) ||
+      c->n_labels >= (1ll << 31))
+    return as_fail(AS_E_INVALID, "n_features / n_labels out of range");
+  if (c->hidden != 128 && c->hidden != 256) return as_fail(AS_E_INVALID, "hidden must be 128 or 256");
+  if (c->b_max < 1 || c->b_min < 1 || c->b_min > c->b_max || c->b_max > 65536)
+    return as_fail(AS_E_INVALID, "need 1 <= b_min <= b_max <= 65536");
+  if (c->beta < 0) return as_fail(AS_E_INVALID, "beta < 0");
+  if (c->max_row_nnz < 1 || c->max_row_labels < 1)
+    return as_fail(AS_E_INVALID, "max_row_nnz / max_row_labels must be >= 1");
+  if ((long long)c->b_max * c->max_row_nnz >= (1ll << 31) ||
+      (long long)c->b_max * c->max_row_labels >= (1ll << 31))
+    return as_fail(AS_E_INVALID, "batch capacity exceeds 2^31 entries");
+  if (c->precision != AS_FP32 && c->precision != AS_BF16)
+    return as_fail(AS_E_INVALID, "precision must be AS_FP32 or AS_BF16");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
+    return as_fail(AS_E_INVALID, "need 0 <= rank < world");
+  if (!(c->lr0 > 0.0)) return as_fail(AS_E_INVALID, "lr0 must be > 0");
+  return AS_OK;
+}
+
+Dims dims_of(const as_config *c) {
+  Dims D;
+  D.d = c->n_features;
+  D.C = c->n_labels;
+  D.h = c->hidden;
+  D.P = D.d * D.h + D.h + D.C * D.h + D.C;
+  D.b_max = c->b_max;
+  D.bpad = (c->b_max + 127) / 128 * 128;
+  D.nnz_cap = c->b_max * c->max_row_nnz;
+  D.lab_cap = c->b_max * c->max_row_labels;
+  D.sort_cap = std::max(D.nnz_cap, D.lab_cap);
+  D.max_splits = as::tc_splits(D.h, D.b_max, D.C, 160);  // >= CTAs of pass 1
+  D.splitk = (int)std::min<long long>(64, std::max<long long>(1, D.C / 4096));
+  return D;
+}
+
+// The arena carve: every buffer of the step sized for b_max ("we
+// provision memory for the largest batch size").  Order fixed; `ctx` NULL ->
+// just the total.
+size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
+  Layout L;
+  auto P = [&](size_t bytes) -> void * { const size_t o = L.add(bytes); return base ? base + o : nullptr; };
+  const size_t S = (size_t)D.sort_cap;
+  const bool bf16 = c->precision == AS_BF16;
+  const bool dbg = (c->flags & AS_FLAG_DEBUG_GRADS) != 0;
+  void *p;
+  p = P(4 * D.P); if (x) x->w = (float *)p;
+  p = P(4 * D.P); if (x) x->wbar = (float *)p;
+  p = P(4 * D.P); if (x) x->wbarp = (float *)p;
+  p = P(2 * D.C * D.h); if (x) x->w2b = (__nv_bfloat16 *)p;
+  p = P(8 * (D.b_max + 1)); if (x) x->row_ptr = (int64_t *)p;
+  p = P(8 * (D.b_max + 1)); if (x) x->lab_ptr = (int64_t *)p;
+  p = P(8 * D.b_max); if (x) x->ids = (int64_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->col = (int32_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->val = (float *)p;
+  p = P(4 * (size_t)D.lab_cap); if (x) x->lab = (int32_t *)p;
+  p = P(sizeof(StepDesc)); if (x) x->desc = (StepDesc *)p;
+  p = P(4 * S); if (x) x->sk0 = (uint32_t *)p;
+  p = P(4 * S); if (x) x->sv0 = (uint32_t *)p;
+  p = P(4 * S); if (x) x->sk1 = (uint32_t *)p;
+  p = P(4 * S); if (x) x->sv1 = (uint32_t *)p;
+  p = P(4 * 256 * (S / as::kSortTile + 1)); if (x) x->hist = (uint32_t *)p;
+  p = P(4 * S); if (x) x->rowid = (int32_t *)p;
+  p = P(4 * S); if (x) x->flags = (int32_t *)p;
+  p = P(4 * (S + S / as::kScanTile + 2)); if (x) x->scan_tmp = (int32_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_id = (int32_t *)p;
+  p = P(4 * ((size_t)D.nnz_cap + 1)); if (x) x->fseg_ptr = (int32_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_row = (int32_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_val = (float *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->long_list = (int32_t *)p;
+  p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_id = (int32_t *)p;
+  p = P(4 * ((size_t)D.lab_cap + 1)); if (x) x->lseg_ptr = (int32_t *)p;
+  p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_row = (int32_t *)p;
+  p = P(4 * D.C); if (x) x->cls_seg = (int32_t *)p;
+  p = P(4 * (size_t)D.bpad * D.h); if (x) x->Hf = (float *)p;
+  p = P(2 * (size_t)D.bpad * D.h); if (x) x->Hb = (__nv_bfloat16 *)p;
+  p = P(4 * (size_t)D.b_max * D.h); if (x) x->dA = (float *)p;
+  p = P(4 * (size_t)D.bpad); if (x) x->lse2 = (float *)p;
+  p = P(4 * (size_t)D.b_max); if (x) x->zsum = (float *)p;
+  p = P(4 * (size_t)D.b_max * D.h); if (x) x->labW = (float *)p;
+  p = P(4 * (size_t)D.b_max); if (x) x->lossr = (float *)p;
+  p = P(4); if (x) x->loss = (float *)p;
+  if (bf16) {
+    p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pm = (float *)p;
+    p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pl = (float *)p;
+    p = P(4 * (size_t)D.max_splits * D.bpad * D.h); if (x) x->pO = (float *)p;
+  } else {
+    p = P(4 * (size_t)D.b_max * D.C); if (x) x->Z = (float *)p;
+    p = P(4 * (size_t)D.b_max * D.h); if (x) x->dH = (float *)p;
+    p = P(4 * (size_t)D.C * D.h); if (x) x->dW2 = (float *)p;
+    p = P(4 * (size_t)D.splitk * D.b_max * D.h); if (x) x->splitk_tmp = (float *)p;
+  }
+  if (dbg) {
+    p = P(4 * (size_t)D.C * D.h); if (x) x->dbg_dW2 = (float *)p;
+    p = P(4 * (size_t)D.C); if (x) x->dbg_db2 = (float *)p;
+    p = P(4 * (size_t)D.nnz_cap * D.h); if (x) x->dbg_dW1 = (float *)p;
+    p = P(4 * (size_t)D.h); if (x) x->dbg_db1 = (float *)p;
+  }
+  p = P(8 * kNormBlocks); if (x) x->norm_part = (double *)p;
+  p = P(8); if (x) x->norm_dev = (double *)p;
+  p = P(8 * (size_t)c->world); if (x) x->norms_all = (double *)p;
+  p = P(4 * (size_t)c->world); if (x) x->alpha_dev = (float *)p;
+  p = P(8 * (size_t)c->world); if (x) x->reps_dev = (const float **)p;
+  return L.total;
+}
+
+int cuda_check(as_ctx *x, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (x) x->sticky = AS_E_CUDA;
+    return as_fail(AS_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  }
+  return AS_OK;
+}
+
+#define AS_GUARD(x)                                                               \
+  do {                                                                            \
+    if (!(x)) return as_fail(AS_E_INVALID, "ctx is NULL");                        \
+    if ((x)->sticky) return as_fail(AS_E_STATE, "ctx poisoned by an earlier error"); \
+    cudaSetDevice((x)->cfg.device);                                               \
+  } while (0)
+
+// Host validation of one CSR batch (SURVEY 8(b) conventions).  Returns nnz/L.
+int validate_csr(const as_ctx *x, int64_t rows, const int64_t *row_ptr, const int32_t *col,
+                 const float *val, const int64_t *lab_ptr, const int32_t *lab, int64_t *nnz_out,
+                 int64_t *L_out) {
+  if (!row_ptr || !lab_ptr) return as_fail(AS_E_INVALID, "row_ptr / lab_ptr is NULL");
+  const int64_t nnz = row_ptr[rows] - row_ptr[0], L = lab_ptr[rows] - lab_ptr[0];
+  if (nnz < 0 || L < 0) return as_fail(AS_E_INVALID, "pointers not monotone");
+  if ((nnz > 0 && (!col || !val)) || !lab) return as_fail(AS_E_INVALID, "col/val/lab is NULL");
+  for (int64_t r = 0; r < rows; ++r) {
+    const int64_t s = row_ptr[r], e = row_ptr[r + 1];
+    if (e < s) return as_fail(AS_E_INVALID, "row_ptr not monotone at row %lld", (long long)r);
+    if (e - s > x->cfg.max_row_nnz)
+      return as_fail(AS_E_INVALID, "row %lld has %lld nnz > max_row_nnz", (long long)r, (long long)(e - s));
+    for (int64_t j = s; j < e; ++j) {
+      if (col[j] < 0 || col[j] >= x->D.d)
+        return as_fail(AS_E_INVALID, "feature id %d out of range in row %lld", col[j], (long long)r);
+      if (j > s && col[j] <= col[j - 1])
+        return as_fail(AS_E_INVALID, "features of row %lld not strictly increasing", (long long)r);
+    }
+    const int64_t ls = lab_ptr[r], le = lab_ptr[r + 1];
+    if (le <= ls) return as_fail(AS_E_INVALID, "row %lld has no label (R3)", (long long)r);
+    if (le - ls > x->cfg.max_row_labels)
+      return as_fail(AS_E_INVALID, "row %lld has too many labels", (long long)r);
+    for (int64_t j = ls; j < le; ++j) {
+      if (lab[j] < 0 || lab[j] >= x->D.C)
+        return as_fail(AS_E_INVALID, "label id %d out of range in row %lld", lab[j], (long long)r);
+      if (j > ls && lab[j] <= lab[j - 1])
+        return as_fail(AS_E_INVALID, "labels of row %lld not strictly increasing", (long long)r);
+    }
+  }
+  *nnz_out = nnz;
+  *L_out = L;
+  return AS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *as_last_error(void) { return g_as_err; }
+
+int as_workspace_size(const as_config *cfg, size_t *bytes) {
+  const int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!bytes) return as_fail(AS_E_INVALID, "bytes is NULL");
+  *bytes = carve(cfg, dims_of(cfg), nullptr, nullptr);
+  return AS_OK;
+}
+
+int as_nccl_unique_id(void *out128) {
+  if (!out128) return as_fail(AS_E_INVALID, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return as_fail(AS_E_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  memcpy(out128, &id, 128);
+  return AS_OK;
+}
+
+int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!init_params || !out) return as_fail(AS_E_INVALID, "init_params / out is NULL");
+  const Dims D = dims_of(cfg);
+  const size_t need = carve(cfg, D, nullptr, nullptr);
+  if (!cfg->workspace || cfg->workspace_bytes < need)
+    return as_fail(AS_E_OOM, "workspace too small: need %zu bytes", need);
+  if (((uintptr_t)cfg->workspace) % kAlign)
+    return as_fail(AS_E_INVALID, "workspace must be %zu-byte aligned", kAlign);
+  if (cudaSetDevice(cfg->device) != cudaSuccess)
+    return as_fail(AS_E_CUDA, "cudaSetDevice(%d) failed", cfg->device);
+  as_ctx *x = new as_ctx();
+  x->cfg = *cfg;
+  x->D = D;
+  x->stream = (cudaStream_t)cfg->stream;
+  cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  carve(cfg, D, x, (uint8_t *)cfg->workspace);
+  x->b_all.assign(cfg->world, cfg->b_max);
+  x->lr = (float)cfg->lr0;
+  const size_t P4 = 4 * (size_t)D.P;
+  rc = cuda_check(x, cudaMemcpyAsync(x->w, init_params, P4, cudaMemcpyHostToDevice, x->stream), "init H2D");
+  if (!rc) rc = cuda_check(x, cudaMemcpyAsync(x->wbar, x->w, P4, cudaMemcpyDeviceToDevice, x->stream), "init copy");
+  if (!rc) rc = cuda_check(x, cudaMemcpyAsync(x->wbarp, x->w, P4, cudaMemcpyDeviceToDevice, x->stream), "init copy");
+  if (!rc) {
+    as::launch_f32_to_bf16(x->stream, x->w + D.d * D.h + D.h, x->w2b, D.C * D.h);
+    rc = cuda_check(x, cudaMemsetAsync(x->cls_seg, 0xFF, 4 * D.C, x->stream), "memset");
+  }
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->Hb, 0, 2 * (size_t)D.bpad * D.h, x->stream), "memset");
+  // pinned double-buffered staging for host batches
+  x->pin_bytes = 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
+  for (int i = 0; i < 2 && !rc; ++i) {
+    rc = cuda_check(x, cudaMallocHost(&x->pin[i], x->pin_bytes), "cudaMallocHost");
+    if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->pin_ev[i], cudaEventDisableTiming), "event");
+  }
+  if (!rc && cfg->precision == AS_BF16) {
+    x->plan = (as::TcPlan *)malloc(as::tc_plan_bytes());
+    if (as::tc_plan_init(x->plan, D.h, D.b_max, D.C, x->num_sms, x->Hb, x->w2b) != 0)
+      rc = as_fail(AS_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
+  }
+  if (!rc && cfg->world > 1 && cfg->nccl_unique_id) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, 128);
+    const ncclResult_t r = ncclCommInitRank(&x->comm, cfg->world, id, cfg->rank);
+    if (r != ncclSuccess) rc = as_fail(AS_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "init sync");
+  if (rc) {
+    as_destroy(x);
+    return rc;
+  }
+  *out = x;
+  return AS_OK;
+}
+
+int as_destroy(as_ctx *x) {
+  if (!x) return AS_OK;
+  cudaSetDevice(x->cfg.device);
+  if (x->stream) cudaStreamSynchronize(x->stream);
+  for (int i = 0; i < 2; ++i) {
+    if (x->pin[i]) cudaFreeHost(x->pin[i]);
+    if (x->pin_ev[i]) cudaEventDestroy(x->pin_ev[i]);
+  }
+  if (x->comm) ncclCommDestroy(x->comm);
+  free(x->plan);
+  delete x;
+  return AS_OK;
+}
+
+int as_load_batch_csr(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t *col,
+                      const float *val, const int64_t *lab_ptr, const int32_t *lab) {
+  AS_GUARD(x);
+  const int bi = x->b_all[x->cfg.rank];
+  if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
+  int64_t nnz = 0, L = 0;
+  int rc = validate_csr(x, rows, row_ptr, col, val, lab_ptr, lab, &nnz, &L);
+  if (rc) return rc;
+  if (nnz > x->D.nnz_cap || L > x->D.lab_cap) return as_fail(AS_E_INVALID, "batch exceeds capacity");
+  const int k = x->pin_idx;
+  x->pin_idx ^= 1;
+  rc = cuda_check(x, cudaEventSynchronize(x->pin_ev[k]), "staging wait");
+  if (rc) return rc;
+  uint8_t *p = (uint8_t *)x->pin[k];
+  int64_t *rp = (int64_t *)p;
+  int64_t *lp = rp + (rows + 1);
+  int32_t *cc = (int32_t *)(lp + (rows + 1));
+  float *vv = (float *)(cc + nnz);
+  int32_t *ll = (int32_t *)(vv + nnz);
+  StepDesc *dd = (StepDesc *)(((uintptr_t)(ll + L) + 63) & ~(uintptr_t)63);
+  for (int r = 0; r <= rows; ++r) {
+    rp[r] = row_ptr[r] - row_ptr[0];
+    lp[r] = lab_ptr[r] - lab_ptr[0];
+  }
+  memcpy(cc, col + row_ptr[0], 4 * nnz);
+  memcpy(vv, val + row_ptr[0], 4 * nnz);
+  memcpy(ll, lab + lab_ptr[0], 4 * L);
+  memset(dd, 0, sizeof(StepDesc));
+  dd->rows = rows;
+  dd->nnz = (int32_t)nnz;
+  dd->nlab = (int32_t)L;
+  cudaStream_t s = x->stream;
+  cudaMemcpyAsync(x->row_ptr, rp, 8 * (rows + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(x->lab_ptr, lp, 8 * (rows + 1), cudaMemcpyHostToDevice, s);
+  if (nnz) cudaMemcpyAsync(x->col, cc, 4 * nnz, cudaMemcpyHostToDevice, s);
+  if (nnz) cudaMemcpyAsync(x->val, vv, 4 * nnz, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(x->lab, ll, 4 * L, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(x->desc, dd, sizeof(StepDesc), cudaMemcpyHostToDevice, s);
+  rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], s), "batch H2D");
+  if (rc) return rc;
+  x->loaded_rows = rows;
+  x->has_batch = true;
+  return AS_OK;
+}
+
+int as_dataset_bytes(int64_t n, int64_t nnz, int64_t L, size_t *bytes) {
+  if (n < 1 || nnz < 0 || L < n || !bytes) return as_fail(AS_E_INVALID, "bad dataset sizes");
+  Layout Lo;
+  Lo.add(8 * (n + 1));
+  Lo.add(4 * nnz);
+  Lo.add(4 * nnz);
+  Lo.add(8 * (n + 1));
+  Lo.add(4 * L);
+  Lo.add(8 * n);
+  *bytes = Lo.total;
+  return AS_OK;
+}
+
+int as_dataset_upload(as_ctx *x, void *dev_buf, size_t dev_bytes, int64_t n,
+                      const int64_t *row_ptr, const int32_t *col, const float *val,
+                      const int64_t *lab_ptr, const int32_t *lab, const int64_t *order) {
+  AS_GUARD(x);
+  if (n < 1 || !row_ptr || !lab_ptr) return as_fail(AS_E_INVALID, "bad dataset");
+  if (row_ptr[0] != 0 || lab_ptr[0] != 0) return as_fail(AS_E_INVALID, "dataset pointers must start at 0");
+  int64_t nnz = 0, L = 0;
+  int rc = validate_csr(x, n, row_ptr, col, val, lab_ptr, lab, &nnz, &L);
+  if (rc) return rc;
+  if (order)
+    for (int64_t i = 0; i < n; ++i)
+      if (order[i] < 0 || order[i] >= n) return as_fail(AS_E_INVALID, "order[%lld] out of range", (long long)i);
+  size_t need = 0;
+  as_dataset_bytes(n, nnz, L, &need);
+  if (!dev_buf || dev_bytes < need) return as_fail(AS_E_OOM, "dataset buffer too small: need %zu", need);
+  Layout Lo;
+  uint8_t *b = (uint8_t *)dev_buf;
+  int64_t *drp = (int64_t *)(b + Lo.add(8 * (n + 1)));
+  int32_t *dcol = (int32_t *)(b + Lo.add(4 * nnz));
+  float *dval = (float *)(b + Lo.add(4 * nnz));
+  int64_t *dlp = (int64_t *)(b + Lo.add(8 * (n + 1)));
+  int32_t *dlab = (int32_t *)(b + Lo.add(4 * L));
+  int64_t *dord = (int64_t *)(b + Lo.add(8 * n));
+  cudaStream_t s = x->stream;
+  cudaMemcpyAsync(drp, row_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, s);
+  if (nnz) cudaMemcpyAsync(dcol, col, 4 * nnz, cudaMemcpyHostToDevice, s);
+  if (nnz) cudaMemcpyAsync(dval, val, 4 * nnz, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dlp, lab_ptr, 8 * (n + 1), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dlab, lab, 4 * L, cudaMemcpyHostToDevice, s);
+  if (order) cudaMemcpyAsync(dord, order, 8 * n, cudaMemcpyHostToDevice, s);
+  rc = cuda_check(x, cudaStreamSynchronize(s), "dataset upload");
+  if (rc) return rc;
+  x->ds_row_ptr = drp; x->ds_col = dcol; x->ds_val = dval; x->ds_lab_ptr = dlp; x->ds_lab = dlab;
+  x->ds_order = order ? dord : nullptr;
+  x->ds_n = n;
+  return AS_OK;
+}
+
+int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
+  AS_GUARD(x);
+  if (!x->ds_row_ptr) return as_fail(AS_E_STATE, "no resident dataset (as_dataset_upload)");
+  const int bi = x->b_all[x->cfg.rank];
+  if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
+  if (pos < 0) return as_fail(AS_E_INVALID, "pos < 0");
+  as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
+                          x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
+                          x->lab, x->ids, x->desc, x->D.nnz_cap, x->D.lab_cap);
+  const int rc = cuda_check(x, cudaSuccess, "gather batch");
+  if (rc) return rc;
+  x->loaded_rows = rows;
+  x->has_batch = true;
+  return AS_OK;
+}
+
+int as_train_step(as_ctx *x, float *loss_out) {
+  AS_GUARD(x);
+  if (!x->has_batch) return as_fail(AS_E_STATE, "no batch loaded");
+  const Dims &D = x->D;
+  cudaStream_t s = x->stream;
+  StepDesc *d = x->desc;
+  const int rows = x->loaded_rows;
+  const float lr = x->lr;
+  const bool dbg = (x->cfg.flags & AS_FLAG_DEBUG_GRADS) != 0;
+  float *W1 = x->w, *b1 = x->w + D.d * D.h, *W2T = b1 + D.h, *b2 = W2T + D.C * D.h;
+
+  // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2)
+  as::launch_transpose(s, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
+                       x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->fseg_id,
+                       x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val);
+  as::launch_transpose(s, x->lab_ptr, x->lab, rows, &d->nlab, D.lab_cap, key_bits(D.C), x->sk0,
+                       x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->lseg_id,
+                       x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr);
+  as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
+  // a4: SpMM forward
+  as::launch_spmm(s, D.h, d, D.bpad, x->row_ptr, x->col, x->val, W1, b1, x->Hf, x->Hb);
+  // a5: label terms of the loss and of dH (R3)
+  as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
+  if (x->cfg.precision == AS_BF16) {
+    // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
+    as::launch_out_fwd_tc(s, x->plan, d, b2, x->pm, x->pl, x->pO);
+    as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
+                            x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lse2, x->lossr, x->dA);
+    as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
+    // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
+    as::launch_out_bwd_tc(s, x->plan, d, x->lse2, b2, x->cls_seg, x->lseg_ptr, x->lseg_row,
+                          x->lab_ptr, x->Hf, W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
+                          dbg ? x->dbg_db2 : nullptr, nullptr);
+  } else {
+    // fp32 parity mode: logits materialised
+    const long long C = D.C;
+    as::launch_gemm_f32(s, D.b_max, (int)C, D.h, x->Hf, D.h, 1, W2T, 1, D.h, x->Z, C, b2, 1,
+                        nullptr, &d->rows);
+    as::launch_row_lse(s, d, D.b_max, (int)C, x->Z, x->lse2);
+    as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2);
+    as::launch_gemm_f32(s, D.b_max, D.h, (int)C, x->Z, C, 1, W2T, D.h, 1, x->dH, D.h, nullptr,
+                        D.splitk, x->splitk_tmp, &d->rows);
+    as::launch_gemm_f32_kdev(s, (int)C, D.h, D.b_max, x->Z, 1, C, x->Hf, D.h, 1, x->dW2, D.h,
+                             &d->rows);
+    as::launch_finish_f32(s, D.h, d, D.b_max, x->dH, x->Hf, x->zsum, x->lse2, x->lossr, x->dA);
+    as::launch_colsum_sgd(s, d, D.b_max, (int)C, x->Z, C, b2, lr, dbg ? x->dbg_db2 : nullptr);
+    as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
+    if (dbg) cudaMemcpyAsync(x->dbg_dW2, x->dW2, 4 * (size_t)C * D.h, cudaMemcpyDeviceToDevice, s);
+    as::launch_sgd_dense(s, C * D.h, W2T, x->dW2, lr, x->w2b);
+  }
+  // a7: first-layer gradient (deterministic segmented reduction) + SGD
+  as::launch_dw1_sgd(s, D.h, d, D.nnz_cap, x->fseg_id, x->fseg_ptr, x->fseg_row, x->fseg_val, x->dA,
+                     W1, lr, x->long_list, dbg ? x->dbg_dW1 : nullptr);
+  as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 0);
+  as::launch_loss_mean(s, d, x->lossr, x->loss);
+  int rc = cuda_check(x, cudaSuccess, "train step launch");
+  if (rc) return rc;
+  if (loss_out) {
+    rc = cuda_check(x, cudaMemcpyAsync(loss_out, x->loss, 4, cudaMemcpyDeviceToHost, s), "loss D2H");
+    if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "train step");
+  }
+  return rc;
+}
+
+int as_set_batch_sizes(as_ctx *x, const int32_t *b, const float *lr) {
+  AS_GUARD(x);
+  if (!b || !lr) return as_fail(AS_E_INVALID, "b / lr is NULL");
+  for (int i = 0; i < x->cfg.world; ++i)
+    if (b[i] < x->cfg.b_min || b[i] > x->cfg.b_max)
+      return as_fail(AS_E_INVALID, "b[%d]=%d not in [b_min, b_max]", i, b[i]);
+  if (!(lr[x->cfg.rank] > 0.f)) return as_fail(AS_E_INVALID, "lr must be > 0");
+  x->b_all.assign(b, b + x->cfg.world);
+  x->lr = lr[x->cfg.rank];
+  return AS_OK;
+}
+
+int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
+             int32_t *perturbed_out) {
+  AS_GUARD(x);
+  if (!u || !b) return as_fail(AS_E_INVALID, "u / b is NULL");
+  const int N = x->cfg.world;
+  if (N > 1 && !x->comm)
+    return as_fail(AS_E_STATE, "as_merge needs an NCCL ctx (use as_group_merge in local-group mode)");
+  const Dims &D = x->D;
+  cudaStream_t s = x->stream;
+  // a9: replica norm
+  as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
+  if (N > 1) {
+    const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
+    if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r)); }
+  } else {
+    cudaMemcpyAsync(x->norms_all, x->norm_dev, 8, cudaMemcpyDeviceToDevice, s);
+  }
+  std::vector<double> norms(N), alpha(N);
+  int rc = cuda_check(x, cudaMemcpyAsync(norms.data(), x->norms_all, 8 * N, cudaMemcpyDeviceToHost, s), "norms D2H");
+  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "norms");
+  if (rc) return rc;
+  // a10: merge weights (host, identical on all ranks)
+  int32_t pert = 0;
+  rc = as_sched_alg2(N, u, b, norms.data(), x->cfg.delta, x->cfg.pert_thr, alpha.data(), &pert);
+  if (rc) return rc;
+  // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset
+  as::launch_scale(s, x->w, D.P, (float)alpha[x->cfg.rank]);
+  if (N > 1) {
+    const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, ncclSum, x->comm, s);
+    if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
+  }
+  as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, D.d * D.h + D.h,
+                      D.C * D.h, x->w2b);
+  std::swap(x->wbar, x->wbarp);
+  rc = cuda_check(x, cudaSuccess, "merge launch");
+  if (rc) return rc;
+  if (alpha_out) std::copy(alpha.begin(), alpha.end(), alpha_out);
+  if (perturbed_out) *perturbed_out = pert;
+  return AS_OK;
+}
+
+int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32_t *b,
+                   double *alpha_out, int32_t *perturbed_out) {
+  if (!ctxs || n < 1 || !u || !b) return as_fail(AS_E_INVALID, "bad arguments");
+  for (int i = 0; i < n; ++i) {
+    AS_GUARD(ctxs[i]);
+    if (ctxs[i]->cfg.world != n || ctxs[i]->cfg.rank != i)
+      return as_fail(AS_E_INVALID, "ctx %d: need world == n and rank == index", i);
+    if (ctxs[i]->D.P != ctxs[0]->D.P) return as_fail(AS_E_INVALID, "model sizes differ");
+  }
+  as_ctx *x0 = ctxs[0];
+  const Dims &D = x0->D;
+  std::vector<double> norms(n), alpha(n);
+  for (int i = 0; i < n; ++i) {
+    as_ctx *x = ctxs[i];
+    cudaSetDevice(x->cfg.device);
+    as::launch_sumsq(x->stream, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
+    int rc = cuda_check(x, cudaMemcpyAsync(&norms[i], x->norm_dev, 8, cudaMemcpyDeviceToHost, x->stream), "norm");
+    if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "norm sync");
+    if (rc) return rc;
+  }
+  int32_t pert = 0;
+  int rc = as_sched_alg2(n, u, b, norms.data(), x0->cfg.delta, x0->cfg.pert_thr, alpha.data(), &pert);
+  if (rc) return rc;
+  std::vector<float> af(n);
+  std::vector<const float *> reps(n);
+  for (int i = 0; i < n; ++i) { af[i] = (float)alpha[i]; reps[i] = ctxs[i]->w; }
+  cudaSetDevice(x0->cfg.device);
+  cudaMemcpyAsync(x0->alpha_dev, af.data(), 4 * n, cudaMemcpyHostToDevice, x0->stream);
+  cudaMemcpyAsync(x0->reps_dev, reps.data(), 8 * n, cudaMemcpyHostToDevice, x0->stream);
+  as::launch_group_reduce(x0->stream, x0->reps_dev, x0->alpha_dev, n, D.P, x0->wbar, x0->wbarp,
+                          (float)x0->cfg.gamma);
+  rc = cuda_check(x0, cudaStreamSynchronize(x0->stream), "group reduce");
+  if (rc) return rc;
+  const float *src = x0->wbarp;
+  for (int i = 0; i < n; ++i) {
+    as_ctx *x = ctxs[i];
+    cudaSetDevice(x->cfg.device);
+    as::launch_reset_from(x->stream, src, x->w, x->wbarp, D.P, D.d * D.h + D.h, D.C * D.h, x->w2b);
+    rc = cuda_check(x, cudaStreamSynchronize(x->stream), "group reset");
+    if (rc) return rc;
+  }
+  for (int i = 0; i < n; ++i) std::swap(ctxs[i]->wbar, ctxs[i]->wbarp);
+  if (alpha_out) std::copy(alpha.begin(), alpha.end(), alpha_out);
+  if (perturbed_out) *perturbed_out = pert;
+  return AS_OK;
+}
+
+int as_get_params(as_ctx *x, int32_t which, float *host_out) {
+  AS_GUARD(x);
+  if (!host_out) return as_fail(AS_E_INVALID, "host_out is NULL");
+  const float *src = which == AS_PARAMS_REPLICA ? x->w
+                     : which == AS_PARAMS_GLOBAL ? x->wbar
+                     : which == AS_PARAMS_GLOBAL_PREV ? x->wbarp : nullptr;
+  if (!src) return as_fail(AS_E_INVALID, "bad `which`");
+  int rc = cuda_check(x, cudaMemcpyAsync(host_out, src, 4 * (size_t)x->D.P, cudaMemcpyDeviceToHost, x->stream), "params D2H");
+  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "params sync");
+  return rc;
+}
+
+int as_set_params(as_ctx *x, int32_t which, const float *host_in) {
+  AS_GUARD(x);
+  if (!host_in) return as_fail(AS_E_INVALID, "host_in is NULL");
+  float *dst = which == AS_PARAMS_REPLICA ? x->w
+               : which == AS_PARAMS_GLOBAL ? x->wbar
+               : which == AS_PARAMS_GLOBAL_PREV ? x->wbarp : nullptr;
+  if (!dst) return as_fail(AS_E_INVALID, "bad `which`");
+  const Dims &D = x->D;
+  int rc = cuda_check(x, cudaMemcpyAsync(dst, host_in, 4 * (size_t)D.P, cudaMemcpyHostToDevice, x->stream), "params H2D");
+  if (!rc && which == AS_PARAMS_REPLICA)
+    as::launch_f32_to_bf16(x->stream, x->w + D.d * D.h + D.h, x->w2b, D.C * D.h);
+  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "params sync");
+  return rc;
+}
+
+int as_debug_get(as_ctx *x, int32_t which, void *host_out, size_t bytes, size_t *written) {
+  AS_GUARD(x);
+  if (!host_out || !written) return as_fail(AS_E_INVALID, "NULL output");
+  cudaStream_t s = x->stream;
+  StepDesc dd;
+  int rc = cuda_check(x, cudaMemcpyAsync(&dd, x->desc, sizeof(dd), cudaMemcpyDeviceToHost, s), "desc");
+  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "desc sync");
+  if (rc) return rc;
+  const Dims &D = x->D;
+  const bool dbg = (x->cfg.flags & AS_FLAG_DEBUG_GRADS) != 0;
+  std::vector<std::pair<const void *, size_t>> parts;
+  std::vector<int32_t> head;
+  switch (which) {
+    case AS_DBG_H: parts.push_back({x->Hf, 4 * (size_t)dd.rows * D.h}); break;
+    case AS_DBG_LSE: parts.push_back({x->lse2, 4 * (size_t)dd.rows}); break;  // log2 units
+    case AS_DBG_LOSS: parts.push_back({x->lossr, 4 * (size_t)dd.rows}); break;
+    case AS_DBG_DA: parts.push_back({x->dA, 4 * (size_t)dd.rows * D.h}); break;
+    case AS_DBG_DB1: if (!dbg) return as_fail(AS_E_STATE, "needs AS_FLAG_DEBUG_GRADS"); parts.push_back({x->dbg_db1, 4 * (size_t)D.h}); break;
+    case AS_DBG_DW2T: if (!dbg) return as_fail(AS_E_STATE, "needs AS_FLAG_DEBUG_GRADS"); parts.push_back({x->dbg_dW2, 4 * (size_t)D.C * D.h}); break;
+    case AS_DBG_DB2: if (!dbg) return as_fail(AS_E_STATE, "needs AS_FLAG_DEBUG_GRADS"); parts.push_back({x->dbg_db2, 4 * (size_t)D.C}); break;
+    case AS_DBG_DW1: if (!dbg) return as_fail(AS_E_STATE, "needs AS_FLAG_DEBUG_GRADS"); parts.push_back({x->dbg_dW1, 4 * (size_t)dd.U * D.h}); break;
+    case AS_DBG_FSEG:
+      head.push_back(dd.U);
+      parts.push_back({x->fseg_id, 4 * (size_t)dd.U});
+      parts.push_back({x->fseg_ptr, 4 * ((size_t)dd.U + 1)});
+      parts.push_back({x->fseg_row, 4 * (size_t)dd.nnz});
+      parts.push_back({x->fseg_val, 4 * (size_t)dd.nnz});
+      break;
+    case AS_DBG_LSEG:
+      head.push_back(dd.V);
+      parts.push_back({x->lseg_id, 4 * (size_t)dd.V});
+      parts.push_back({x->lseg_ptr, 4 * ((size_t)dd.V + 1)});
+      parts.push_back({x->lseg_row, 4 * (size_t)dd.nlab});
+      break;
+    case AS_DBG_BATCH: head = {dd.rows, dd.nnz, dd.nlab, dd.U}; break;
+    case AS_DBG_LOGITS:
+      if (x->cfg.precision != AS_FP32) return as_fail(AS_E_STATE, "logits exist only in AS_FP32");
+      parts.push_back({x->Z, 4 * (size_t)dd.rows * D.C});
+      break;
+    default: return as_fail(AS_E_INVALID, "bad `which`");
+  }
+  size_t total = 4 * head.size();
+  for (auto &p : parts) total += p.second;
+  if (total > bytes) return as_fail(AS_E_INVALID, "buffer too small: need %zu", total);
+  uint8_t *o = (uint8_t *)host_out;
+  memcpy(o, head.data(), 4 * head.size());
+  o += 4 * head.size();
+  for (auto &p : parts) {
+    if (p.second) cudaMemcpyAsync(o, p.first, p.second, cudaMemcpyDeviceToHost, s);
+    o += p.second;
+  }
+  rc = cuda_check(x, cudaStreamSynchronize(s), "debug D2H");
+  *written = total;
+  return rc;
+}
+
+int as_tc_selftest(const void *A, const void *B, float *S, float *O, float *T) {
+  if (!A || !B || !S || !O || !T) return as_fail(AS_E_INVALID, "NULL argument");
+  if (as::tc_selftest(A, B, S, O, T, 0) != 0) return as_fail(AS_E_CUDA, "tensor map creation failed");
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return as_fail(AS_E_CUDA, "selftest: %s", cudaGetErrorString(e));
+  return cuda_check(nullptr, cudaSuccess, "selftest");
+}
+
+}  // extern "C"

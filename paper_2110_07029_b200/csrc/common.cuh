@@ -1,0 +1,124 @@
+// Device-side helpers and the internal kernel-launcher interface of the
+// Adaptive SGD hot path (sm_100a).  Internal: not part of the C-ABI.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace as {
+
+// Per-step descriptor kept in device memory so that kernels read the batch
+// extents (which the device-side batch builder produces) without a host sync.
+struct StepDesc {
+  int32_t rows;    // B, rows of the batch
+  int32_t nnz;     // features in the batch
+  int32_t nlab;    // labels in the batch
+  int32_t U;       // unique features (feature segments)
+  int32_t V;       // unique labels (label segments)
+  int32_t n_long;  // long feature segments queued for the block path
+  int32_t err;     // device-side validation error (0 = ok)
+  int32_t pad;
+};
+
+constexpr int kLongSeg = 64;     // feature segments longer than this use a block
+constexpr int kScanTile = 4096;  // elements per block in the device scan
+constexpr int kSortTile = 4096;  // elements per block in the radix sort
+constexpr int kSortBits = 8;     // radix digit width
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&t);
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- launchers
+// batch construction (step a2)
+void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_t *ds_col,
+                         const float *ds_val, const int64_t *ds_lab_ptr, const int32_t *ds_lab,
+                         const int64_t *order, int64_t n, int64_t pos, int rows,
+                         int64_t *row_ptr, int32_t *col, float *val, int64_t *lab_ptr,
+                         int32_t *lab, int64_t *ids, StepDesc *desc, int nnz_cap, int lab_cap);
+// batch transposes (step a3)
+void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, int rows,
+                      const int *n_dev, int cap, int key_bits, uint32_t *k0, uint32_t *v0,
+                      uint32_t *k1, uint32_t *v1, uint32_t *hist, int32_t *rowid, int32_t *flags,
+                      int32_t *scan_tmp, int32_t *seg_id, int32_t *seg_ptr, int32_t *seg_row,
+                      int *nseg_dev, const float *val_in, float *seg_val);
+void launch_class_map(cudaStream_t s, const int32_t *lseg_id, const int *V_dev, int cap,
+                      int32_t *cls_seg, int value_is_index);
+// SpMM forward (step a4)
+void launch_spmm(cudaStream_t s, int h, const StepDesc *desc, int bpad, const int64_t *row_ptr,
+                 const int32_t *col, const float *val, const float *W1, const float *b1, float *Hf,
+                 __nv_bfloat16 *Hb);
+// label terms of loss and dH (steps a5)
+void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
+                        const int64_t *lab_ptr, const int32_t *lab, const float *Hf,
+                        const float *W2T, const float *b2, float *zsum, float *labW);
+// combine of the bf16 pass-1 partials -> LSE, loss rows, dA (steps a5)
+void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max, int bpad,
+                         int splits, const float *pm, const float *pl, const float *pO,
+                         const float *labW, const float *zsum, const float *Hf, float *lse2,
+                         float *lossr, float *dA);
+// fp32 (SIMT) output layer (steps a5/a6 in parity mode)
+void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
+                     long long sak, const float *B, long long sbk, long long sbn, float *Cm,
+                     long long ldc, const float *bias_n, int splitk, float *splitk_tmp,
+                     const int *M_dev);
+void launch_row_lse(cudaStream_t s, const StepDesc *desc, int b_max, int C, const float *Z,
+                    float *lse2);
+void launch_softmax_grad(cudaStream_t s, const StepDesc *desc, int b_max, int C,
+                         const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2);
+void launch_finish_f32(cudaStream_t s, int h, const StepDesc *desc, int b_max, const float *dH,
+                       const float *Hf, const float *zsum, const float *lse2, float *lossr,
+                       float *dA);
+// column sums with fused SGD (db1 / db2)
+void launch_colsum_sgd(cudaStream_t s, const StepDesc *desc, int n_rows_cap, int ncols,
+                       const float *X, long long ldx, float *param, float lr, float *grad_out);
+void launch_sgd_dense(cudaStream_t s, long long n, float *param, const float *grad, float lr,
+                      __nv_bfloat16 *shadow);
+// first-layer gradient + SGD (step a7)
+void launch_dw1_sgd(cudaStream_t s, int h, StepDesc *desc, int cap, const int32_t *seg_id,
+                    const int32_t *seg_ptr, const int32_t *seg_row, const float *seg_val,
+                    const float *dA, float *W1, float lr, int32_t *long_list, float *dbg_dW1);
+void launch_loss_mean(cudaStream_t s, const StepDesc *desc, const float *lossr, float *loss);
+// merge (steps a9-a13)
+void launch_sumsq(cudaStream_t s, const float *w, long long P, double *partials, int nblocks,
+                  double *out_norm);
+void launch_scale(cudaStream_t s, float *w, long long P, float alpha);
+void launch_momentum(cudaStream_t s, float *w, float *wbar_p_to_new, const float *wbar,
+                     long long P, float gamma, long long w2_off, long long w2_len,
+                     __nv_bfloat16 *shadow);
+void launch_group_reduce(cudaStream_t s, const float *const *reps_dev, const float *alpha_dev,
+                         int n, long long P, const float *wbar, float *wbar_p_to_new,
+                         float gamma);
+void launch_reset_from(cudaStream_t s, const float *src, float *w, float *wbar_new, long long P,
+                       long long w2_off, long long w2_len, __nv_bfloat16 *shadow);
+void launch_f32_to_bf16(cudaStream_t s, const float *src, __nv_bfloat16 *dst, long long n);
+
+// tcgen05 output layer (steps a5/a6, AS_BF16)
+struct TcPlan;
+size_t tc_plan_bytes();
+int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const void *Hb,
+                 const void *W2b);
+int tc_splits(int h, int b_max, long long C, int num_sms);
+void launch_out_fwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
+                       const float *b2, float *pm, float *pl, float *pO);
+int tc_fwd_splits_host(const TcPlan *plan, int B);
+int tc_selftest(const void *A, const void *B, float *S, float *O, float *T, cudaStream_t s);
+void launch_gemm_f32_kdev(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
+                          long long sak, const float *B, long long sbk, long long sbn, float *Cm,
+                          long long ldc, const int *K_dev);
+void launch_out_bwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
+                       const float *lse2, const float *b2_in, const int32_t *cls_seg,
+                       const int32_t *lseg_ptr, const int32_t *lrow, const int64_t *lab_ptr,
+                       const float *Hf, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
+                       float *dbg_dW2T, float *dbg_db2, float *db2_tmp);
+
+}  // namespace as

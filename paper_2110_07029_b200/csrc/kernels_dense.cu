@@ -1,0 +1,336 @@
+// fp32 SIMT output layer (the AS_FP32 parity mode of steps a5/a6) and the
+// merge kernels (steps a9-a13).  P:N = PAPER.md line N; Rk = DESIGN.md.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace as {
+
+// =====================================================================
+// Generic fp32 tiled GEMM  C[m][n] = sum_k A(m,k) B(k,n) (+ bias[n]) with
+// arbitrary strides, optional split-K (partials reduced in a fixed order).
+// A(m,k) = A[m*sam + k*sak], B(k,n) = B[k*sbk + n*sbn].  M and K may be capped
+// by device counters (the batch rows).  64x64x16 tiles, 4x4 per thread.
+// =====================================================================
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm_f32(int M, int N, int K, const float *__restrict__ A,
+                                                  long long sam, long long sak,
+                                                  const float *__restrict__ B, long long sbk,
+                                                  long long sbn, float *__restrict__ Cm,
+                                                  long long ldc, const float *__restrict__ bias,
+                                                  int kchunk, const int *__restrict__ M_dev,
+                                                  const int *__restrict__ K_dev, int to_tmp) {
+  __shared__ float As[GBK][GBM + 4];
+  __shared__ float Bs[GBK][GBN + 4];
+  if (M_dev) M = min(M, *M_dev);
+  if (K_dev) K = min(K, *K_dev);
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  if (m0 >= M) return;
+  const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  float acc[4][4] = {};
+  for (int k0 = kb; k0 < ke; k0 += GBK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = t + 256 * i;
+      int m, k;
+      if (sak == 1) { m = e >> 4; k = e & 15; } else { m = e & 63; k = e >> 6; }
+      const int gm = m0 + m, gk = k0 + k;
+      As[k][m] = (gm < M && gk < ke) ? A[(long long)gm * sam + (long long)gk * sak] : 0.f;
+      int n, kk;
+      if (sbn == 1) { kk = e >> 6; n = e & 63; } else { n = e >> 4; kk = e & 15; }
+      const int gn = n0 + n, gk2 = k0 + kk;
+      Bs[kk][n] = (gn < N && gk2 < ke) ? B[(long long)gk2 * sbk + (long long)gn * sbn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < GBK; ++k) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float *out = Cm + (to_tmp ? (long long)blockIdx.z * M * ldc : 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      out[(long long)gm * ldc + gn] = acc[i][j] + ((bias && !to_tmp) ? bias[gn] : 0.f);
+    }
+  }
+}
+
+__global__ void k_splitk_reduce(int M, int N, int splits, const float *__restrict__ tmp,
+                                float *__restrict__ Cm, long long ldc, const float *__restrict__ bias,
+                                const int *__restrict__ M_dev) {
+  if (M_dev) M = min(M, *M_dev);
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)M * N) return;
+  const int m = (int)(i / N), n = (int)(i % N);
+  float a = 0.f;
+  for (int z = 0; z < splits; ++z) a += tmp[(long long)z * M * N + i];
+  Cm[(long long)m * ldc + n] = a + (bias ? bias[n] : 0.f);
+}
+
+void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
+                     long long sak, const float *B, long long sbk, long long sbn, float *Cm,
+                     long long ldc, const float *bias_n, int splitk, float *splitk_tmp,
+                     const int *M_dev) {
+  if (splitk < 1) splitk = 1;
+  int kchunk = ceil_div(K, splitk);
+  kchunk = ceil_div(kchunk, GBK) * GBK;
+  splitk = ceil_div(K, kchunk);
+  dim3 grid(ceil_div(N, GBN), ceil_div(M, GBM), splitk);
+  if (splitk == 1) {
+    k_gemm_f32<<<grid, 256, 0, s>>>(M, N, K, A, sam, sak, B, sbk, sbn, Cm, ldc, bias_n, kchunk,
+                                    M_dev, nullptr, 0);
+  } else {
+    k_gemm_f32<<<grid, 256, 0, s>>>(M, N, K, A, sam, sak, B, sbk, sbn, splitk_tmp, N, nullptr,
+                                    kchunk, M_dev, nullptr, 1);
+    k_splitk_reduce<<<ceil_div((long long)M * N, 256), 256, 0, s>>>(M, N, splitk, splitk_tmp, Cm,
+                                                                    ldc, bias_n, M_dev);
+  }
+}
+
+// K capped by the batch rows (dW2T = dZ^T H has K = B)
+void launch_gemm_f32_kdev(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
+                          long long sak, const float *B, long long sbk, long long sbn, float *Cm,
+                          long long ldc, const int *K_dev) {
+  dim3 grid(ceil_div(N, GBN), ceil_div(M, GBM), 1);
+  k_gemm_f32<<<grid, 256, 0, s>>>(M, N, K, A, sam, sak, B, sbk, sbn, Cm, ldc, nullptr,
+                                  ceil_div(K, GBK) * GBK, nullptr, K_dev, 0);
+}
+
+// LSE_r (stored in log2 units) of the fp32 logits, fixed-order block reduction
+__global__ void __launch_bounds__(256) k_row_lse(const StepDesc *__restrict__ desc, int C,
+                                                 const float *__restrict__ Z,
+                                                 float *__restrict__ lse2) {
+  __shared__ float red[256];
+  const int r = blockIdx.x;
+  if (r >= desc->rows) return;
+  const float *z = Z + (size_t)r * C;
+  float m = -FLT_MAX;
+  for (int c = threadIdx.x; c < C; c += 256) m = fmaxf(m, z[c]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  m = red[0];
+  __syncthreads();
+  float sum = 0.f;
+  for (int c = threadIdx.x; c < C; c += 256) sum += expf(z[c] - m);
+  red[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lse2[r] = (m + logf(red[0])) * 1.4426950408889634f;
+}
+
+void launch_row_lse(cudaStream_t s, const StepDesc *desc, int b_max, int C, const float *Z,
+                    float *lse2) {
+  k_row_lse<<<b_max, 256, 0, s>>>(desc, C, Z, lse2);
+}
+
+// dZ = (softmax(z_r) - T_r)/B in place (R3)
+__global__ void k_softmax(const StepDesc *__restrict__ desc, int C, float *__restrict__ Z,
+                          const float *__restrict__ lse2) {
+  const int r = blockIdx.y;
+  if (r >= desc->rows) return;
+  const float invB = 1.0f / (float)desc->rows;
+  const float lse = lse2[r] * 0.69314718055994531f;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    float *z = Z + (size_t)r * C + c;
+    *z = expf(*z - lse) * invB;
+  }
+}
+
+__global__ void k_softmax_labels(const StepDesc *__restrict__ desc, int C,
+                                 const int64_t *__restrict__ lab_ptr,
+                                 const int32_t *__restrict__ lab, float *__restrict__ Z) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int B = desc->rows;
+  if (r >= B) return;
+  const int64_t s = lab_ptr[r], e = lab_ptr[r + 1];
+  const float w = (1.0f / (float)B) / (float)(e - s);
+  for (int64_t j = s; j < e; ++j) Z[(size_t)r * C + lab[j]] -= w;
+}
+
+void launch_softmax_grad(cudaStream_t s, const StepDesc *desc, int b_max, int C,
+                         const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2) {
+  dim3 g(ceil_div(C, 256 * 8) < 64 ? ceil_div(C, 256 * 8) : 64, b_max);
+  if (g.x < 1) g.x = 1;
+  k_softmax<<<g, 256, 0, s>>>(desc, C, Z, lse2);
+  k_softmax_labels<<<ceil_div(b_max, 128), 128, 0, s>>>(desc, C, lab_ptr, lab, Z);
+}
+
+// dA = dH * [A > 0]; loss_r = LSE_r - zsum_r
+__global__ void k_finish_f32(const StepDesc *__restrict__ desc, int h, const float *__restrict__ dH,
+                             const float *__restrict__ Hf, const float *__restrict__ zsum,
+                             const float *__restrict__ lse2, float *__restrict__ lossr,
+                             float *__restrict__ dA) {
+  const int r = blockIdx.x, j = threadIdx.x;
+  if (r >= desc->rows) return;
+  const size_t i = (size_t)r * h + j;
+  dA[i] = Hf[i] > 0.f ? dH[i] : 0.f;
+  if (j == 0) lossr[r] = lse2[r] * 0.69314718055994531f - zsum[r];
+}
+
+void launch_finish_f32(cudaStream_t s, int h, const StepDesc *desc, int b_max, const float *dH,
+                       const float *Hf, const float *zsum, const float *lse2, float *lossr,
+                       float *dA) {
+  k_finish_f32<<<b_max, h, 0, s>>>(desc, h, dH, Hf, zsum, lse2, lossr, dA);
+}
+
+__global__ void k_sgd_dense(long long n, float *__restrict__ p, const float *__restrict__ g,
+                            float lr, __nv_bfloat16 *__restrict__ shadow) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = p[i] - lr * g[i];
+    p[i] = v;
+    if (shadow) shadow[i] = __float2bfloat16_rn(v);
+  }
+}
+
+void launch_sgd_dense(cudaStream_t s, long long n, float *param, const float *grad, float lr,
+                      __nv_bfloat16 *shadow) {
+  k_sgd_dense<<<148 * 8, 256, 0, s>>>(n, param, grad, lr, shadow);
+}
+
+// =====================================================================
+// Merge (Alg. 2)
+// =====================================================================
+// a9: ||w||_2 / P, fixed-order two-level reduction in fp64 (R15)
+__global__ void __launch_bounds__(256) k_sumsq(const float *__restrict__ w, long long P,
+                                               long long chunk, double *__restrict__ partials) {
+  __shared__ double red[256];
+  const long long b0 = (long long)blockIdx.x * chunk, b1 = min(P, b0 + chunk);
+  double a = 0.0;
+  for (long long i = b0 + threadIdx.x; i < b1; i += 256) {
+    const double x = (double)w[i];
+    a = fma(x, x, a);
+  }
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(1024) k_sumsq_final(const double *__restrict__ partials, int nb,
+                                                      long long P, double *__restrict__ out) {
+  __shared__ double red[1024];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 1024) a += partials[i];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sqrt(red[0]) / (double)P;
+}
+
+void launch_sumsq(cudaStream_t s, const float *w, long long P, double *partials, int nblocks,
+                  double *out_norm) {
+  const long long chunk = (P + nblocks - 1) / nblocks;
+  k_sumsq<<<nblocks, 256, 0, s>>>(w, P, chunk, partials);
+  k_sumsq_final<<<1, 1024, 0, s>>>(partials, nblocks, P, out_norm);
+}
+
+// a11: w_i <- alpha_i w_i
+__global__ void k_scale(float *__restrict__ w, long long P, float alpha) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x)
+    w[i] *= alpha;
+}
+
+void launch_scale(cudaStream_t s, float *w, long long P, float alpha) {
+  k_scale<<<148 * 8, 256, 0, s>>>(w, P, alpha);
+}
+
+// a13: w' = S + gamma (wbar - wbar_p) written over wbar_p (pointer rotation
+// makes it the new wbar; the old wbar becomes wbar_p), w_i <- w',
+// bf16 shadow of W2T refreshed.
+__global__ void k_momentum(float *__restrict__ w, float *__restrict__ wp,
+                           const float *__restrict__ wbar, long long P, float gamma,
+                           long long w2_off, long long w2_len, __nv_bfloat16 *__restrict__ shadow) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float nv = w[i] + gamma * (wbar[i] - wp[i]);
+    wp[i] = nv;
+    w[i] = nv;
+    if (shadow && i >= w2_off && i < w2_off + w2_len) shadow[i - w2_off] = __float2bfloat16_rn(nv);
+  }
+}
+
+void launch_momentum(cudaStream_t s, float *w, float *wbar_p_to_new, const float *wbar,
+                     long long P, float gamma, long long w2_off, long long w2_len,
+                     __nv_bfloat16 *shadow) {
+  k_momentum<<<148 * 8, 256, 0, s>>>(w, wbar_p_to_new, wbar, P, gamma, w2_off, w2_len, shadow);
+}
+
+// local-group merge: S = sum_i alpha_i w_i read directly from every replica
+__global__ void k_group_reduce(const float *const *__restrict__ reps,
+                               const float *__restrict__ alpha, int n, long long P,
+                               const float *__restrict__ wbar, float *__restrict__ wp, float gamma) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x) {
+    float a = 0.f;
+    for (int k = 0; k < n; ++k) a = fmaf(alpha[k], reps[k][i], a);
+    wp[i] = a + gamma * (wbar[i] - wp[i]);
+  }
+}
+
+void launch_group_reduce(cudaStream_t s, const float *const *reps_dev, const float *alpha_dev,
+                         int n, long long P, const float *wbar, float *wbar_p_to_new,
+                         float gamma) {
+  k_group_reduce<<<148 * 8, 256, 0, s>>>(reps_dev, alpha_dev, n, P, wbar, wbar_p_to_new, gamma);
+}
+
+__global__ void k_reset_from(const float *__restrict__ src, float *__restrict__ w,
+                             float *__restrict__ wnew, long long P, long long w2_off,
+                             long long w2_len, __nv_bfloat16 *__restrict__ shadow) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float v = src[i];
+    w[i] = v;
+    if (wnew != src) wnew[i] = v;
+    if (shadow && i >= w2_off && i < w2_off + w2_len) shadow[i - w2_off] = __float2bfloat16_rn(v);
+  }
+}
+
+void launch_reset_from(cudaStream_t s, const float *src, float *w, float *wbar_new, long long P,
+                       long long w2_off, long long w2_len, __nv_bfloat16 *shadow) {
+  k_reset_from<<<148 * 8, 256, 0, s>>>(src, w, wbar_new, P, w2_off, w2_len, shadow);
+}
+
+__global__ void k_f32_to_bf16(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
+                              long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+void launch_f32_to_bf16(cudaStream_t s, const float *src, __nv_bfloat16 *dst, long long n) {
+  k_f32_to_bf16<<<148 * 8, 256, 0, s>>>(src, dst, n);
+}
+
+}  // namespace as

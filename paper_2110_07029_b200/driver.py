@@ -1,0 +1,112 @@
+"""The Adaptive SGD mega-batch loop on top of the C-ABI.
+
+Per mega-batch: route batches (replay: identical pure function on every rank),
+run the SGD steps of this rank's batches on the device, merge (Alg. 2), then
+rescale batch sizes (Alg. 1).  Replicas restart from the global model inside
+the merge.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import sched
+
+
+def stream_nnz_prefix(row_ptr, n, pos, M, order=None):
+    """Cumulative nnz of stream positions [pos, pos+M) (input to replay routing)."""
+    p = (np.arange(M, dtype=np.int64) + int(pos)) % int(n)
+    ids = p if order is None else np.asarray(order, np.int64)[p]
+    rl = row_ptr[ids + 1] - row_ptr[ids]
+    out = np.zeros(M + 1, np.int64)
+    np.cumsum(rl, out=out[1:])
+    return out
+
+
+class ReplayState:
+    """Host scheduler state shared (identically) by every rank."""
+
+    def __init__(self, world, b_max, b_min, beta, lr0, costs):
+        self.world, self.b_max, self.b_min, self.beta, self.lr0 = world, b_max, b_min, beta, lr0
+        self.costs = [tuple(int(v) for v in (c.c0, c.c_row, c.c_nnz, c.num, c.den)) if hasattr(c, "c0")
+                      else tuple(c) for c in costs]
+        self.b = [b_max] * world
+        self.lr = [float(np.float32(lr0))] * world
+
+    def route(self, row_ptr, n, pos, M, order=None):
+        pre = stream_nnz_prefix(row_ptr, n, pos, M, order)
+        return sched.route_replay(self.costs, self.b, M, pre)
+
+    def rescale(self, u):
+        b_used = list(self.b)
+        self.b, self.lr = sched.alg1(u, self.b, self.beta, self.b_min, self.b_max, self.lr0)
+        return b_used
+
+
+def run_local(replicas, ds, state, total, order=None, resident=True, want_loss=False):
+    """All replicas in this process (local-group merge).  Returns per-mega-batch
+    records (log, u, b, alpha, perturbed, losses)."""
+    from .api import group_merge
+    n = len(ds.row_ptr) - 1
+    M = replicas[0].cfg.megabatch
+    pos, recs = 0, []
+    if resident:
+        for r in replicas:
+            if r.dataset_buf is None:
+                r.upload_dataset(ds, order)
+    while pos < total:
+        Mm = int(min(M, total - pos))
+        log, u, clocks = state.route(ds.row_ptr, n, pos, Mm, order)
+        losses = []
+        for (i, start, rows) in log:
+            rep = replicas[i]
+            if resident:
+                rep.load_batch_stream(pos + start, rows)
+            else:
+                p = (np.arange(rows) + pos + start) % n
+                ids = p if order is None else np.asarray(order)[p]
+                sub = ds.rows(ids)
+                rep.load_batch_csr(rows, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+            losses.append(rep.train_step(want_loss))
+        b_used = list(state.b)
+        alpha, pert = group_merge(replicas, u, b_used)
+        state.rescale(u)
+        for rep in replicas:
+            rep.set_batch_sizes(state.b, state.lr)
+        recs.append({"log": log, "u": u, "clocks": clocks, "b": b_used, "alpha": list(alpha),
+                     "perturbed": pert, "b_next": list(state.b), "lr_next": list(state.lr),
+                     "losses": losses})
+        pos += Mm
+    return recs
+
+
+def run_rank(rep, ds_row_ptr, n, state, total, order=None, want_alpha=False):
+    """One rank of a torchrun job (NCCL merge).  The dataset must be resident."""
+    M = rep.cfg.megabatch
+    pos, recs = 0, []
+    while pos < total:
+        Mm = int(min(M, total - pos))
+        log, u, _ = state.route(ds_row_ptr, n, pos, Mm, order)
+        for (i, start, rows) in log:
+            if i == rep.rank:
+                rep.load_batch_stream(pos + start, rows)
+                rep.train_step(False)
+        b_used = list(state.b)
+        alpha, pert = rep.merge(u, b_used, want_alpha=want_alpha)
+        state.rescale(u)
+        rep.set_batch_sizes(state.b, state.lr)
+        recs.append({"u": u, "b": b_used, "alpha": alpha, "perturbed": pert, "samples": Mm})
+        pos += Mm
+    return recs
+
+
+def broadcast_nccl_id(dist, rank, device=None, make_id=None):
+    """Rank 0 draws the 128-byte ncclUniqueId and every rank receives it over
+    the torch.distributed process group (plumbing only)."""
+    import torch
+    if make_id is None:
+        from .api import nccl_unique_id as make_id
+    buf = torch.zeros(128, dtype=torch.uint8, device=device or "cpu")
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(make_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0)
+    return bytes(buf.cpu().numpy().tobytes())

@@ -1,0 +1,166 @@
+"""CPU tests of the C-ABI library (no GPU needed):
+
+* libadasgd.so loads and exports every symbol include/adasgd.h declares;
+* the C++ scheduler is bit-exact with the oracle's scheduler (routing logs,
+  batch sizes, lr bits, alpha bits, permutations) on the golden cases and on
+  random cases;
+* config validation returns AS_E_INVALID;
+* the live cursor conserves samples.
+"""
+import ctypes as C
+import json
+import os
+import re
+import struct
+import subprocess
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+import synthgen
+from oracle import sched as osched
+from paper_2110_07029_b200 import _lib as L
+from paper_2110_07029_b200 import sched as psched
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def _header_functions():
+    txt = open(os.path.join(ROOT, "include", "adasgd.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(as_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = L.load()
+    declared = _header_functions()
+    assert declared, "no declarations parsed"
+    assert sorted(L.EXPORTS) == declared
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (as_[a-z0-9_]+)\b", out))
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    for s in declared:
+        assert hasattr(lib, s)
+
+
+def _f32bits(x):
+    return struct.unpack("<I", struct.pack("<f", x))[0]
+
+
+def test_routing_golden_cpp():
+    for case in json.load(open(os.path.join(GOLD, "routing_cases.json")))["cases"]:
+        log, u, t = psched.route_replay(case["costs"], case["b"], case["M"], [0] * (case["M"] + 1))
+        assert [list(x) for x in log] == case["log"] and u == case["u"] and t == case["clocks"]
+
+
+@settings(max_examples=80, deadline=None)
+@given(st.integers(1, 8), st.integers(1, 500), st.data())
+def test_routing_bit_exact_vs_oracle(N, M, data):
+    b = [data.draw(st.integers(1, 64)) for _ in range(N)]
+    costs = [(data.draw(st.integers(0, 10**6)), data.draw(st.integers(0, 10**5)),
+              data.draw(st.integers(0, 10**3)), data.draw(st.integers(1, 140)), data.draw(st.integers(1, 100)))
+             for _ in range(N)]
+    nnz = np.array([data.draw(st.integers(1, 50)) for _ in range(M)], np.int64)
+    pre = np.zeros(M + 1, np.int64); pre[1:] = np.cumsum(nnz)
+    log, u, t = psched.route_replay(costs, b, M, pre)
+    ocosts = [synthgen.CostModel(*c) for c in costs]
+    olog, ou, ot = osched.route_replay(ocosts, b, M, lambda s, r: int(pre[s + r] - pre[s]))
+    assert log == olog and u == ou and t == ot
+
+
+def test_alg1_golden_cpp():
+    for case in json.load(open(os.path.join(GOLD, "alg1_cases.json")))["cases"]:
+        b, lr = psched.alg1(case["u"], case["b"], case["beta"], case["b_min"], case["b_max"], 0.1)
+        ob, olr = osched.alg1(case["u"], case["b"], case["beta"], case["b_min"], case["b_max"], 0.1)
+        assert b == case["b_out"] == ob
+        assert [_f32bits(x) for x in lr] == [_f32bits(x) for x in olr]
+
+
+@settings(max_examples=150, deadline=None)
+@given(st.integers(1, 8), st.data())
+def test_alg1_bit_exact_vs_oracle(N, data):
+    b_max = data.draw(st.sampled_from([64, 512, 1024, 2048]))
+    b_min = b_max // 8
+    beta = data.draw(st.integers(0, b_min))
+    lr0 = data.draw(st.floats(1e-4, 10.0))
+    b = [data.draw(st.integers(b_min, b_max)) for _ in range(N)]
+    u = [data.draw(st.integers(0, 100)) for _ in range(N)]
+    cb, clr = psched.alg1(u, b, beta, b_min, b_max, lr0)
+    ob, olr = osched.alg1(u, b, beta, b_min, b_max, lr0)
+    assert cb == ob and [_f32bits(x) for x in clr] == [_f32bits(x) for x in olr]
+
+
+def test_alg2_golden_cpp():
+    for case in json.load(open(os.path.join(GOLD, "alg2_cases.json")))["cases"]:
+        norms = [0.0 if case["norms_below"] else 1.0] * len(case["u"])
+        a, p = psched.alg2(case["u"], case["b"], norms, 0.1, 0.1)
+        oa, op = osched.alg2(case["u"], case["b"], norms, 0.1, 0.1)
+        assert a == oa and p == op == case["perturbed"]       # bit-identical doubles
+
+
+@settings(max_examples=150, deadline=None)
+@given(st.integers(1, 8), st.data())
+def test_alg2_bit_exact_vs_oracle(N, data):
+    u = [data.draw(st.integers(0, 30)) for _ in range(N)]
+    if sum(u) == 0:
+        u[0] = 1
+    b = [data.draw(st.integers(1, 2048)) for _ in range(N)]
+    norms = [data.draw(st.floats(0.0, 0.2)) for _ in range(N)]
+    delta = data.draw(st.floats(0.0, 0.5))
+    thr = data.draw(st.floats(0.0, 0.2))
+    assert psched.alg2(u, b, norms, delta, thr) == tuple(osched.alg2(u, b, norms, delta, thr))
+
+
+@pytest.mark.parametrize("n,seed", [(1, 0), (7, 3), (1000, 0x211007029), (4096, 12345678901234)])
+def test_permutation_bit_exact_vs_oracle(n, seed):
+    assert psched.permutation(n, seed).tolist() == osched.permutation(n, seed)
+
+
+def _cfg(**kw):
+    c = L.Config()
+    base = dict(n_features=1000, n_labels=100, hidden=128, b_max=64, b_min=8, beta=4, megabatch=6400,
+                max_row_nnz=32, max_row_labels=8, lr0=0.1, gamma=0.9, delta=0.1, pert_thr=0.1,
+                precision=L.AS_BF16, flags=0, rank=0, world=1, device=0)
+    base.update(kw)
+    for k, v in base.items():
+        setattr(c, k, v)
+    return c
+
+
+def test_workspace_size_and_validation():
+    lib = L.load()
+    n = C.c_size_t()
+    assert lib.as_workspace_size(C.byref(_cfg()), C.byref(n)) == L.AS_OK and n.value > 0
+    n32 = C.c_size_t()
+    assert lib.as_workspace_size(C.byref(_cfg(precision=L.AS_FP32)), C.byref(n32)) == L.AS_OK
+    for bad in [dict(hidden=64), dict(b_min=128), dict(world=2, rank=2), dict(precision=7),
+                dict(lr0=0.0), dict(n_labels=0), dict(max_row_nnz=0)]:
+        assert lib.as_workspace_size(C.byref(_cfg(**bad)), C.byref(n)) == L.AS_E_INVALID, bad
+        assert lib.as_last_error()
+    assert lib.as_sched_alg1(0, None, None, 1, 1, 1, 0.1, None, None) == L.AS_E_INVALID
+    # init with a too-small workspace fails before touching the device
+    c = _cfg()
+    c.workspace, c.workspace_bytes = 256, 16
+    ctx = C.c_void_p()
+    p = np.zeros(10, np.float32)
+    assert lib.as_init(C.byref(c), L.ptr(p, C.c_float), C.byref(ctx)) == L.AS_E_OOM
+
+
+def test_live_cursor_conserves_samples():
+    name = "/adasgd_test_%d" % os.getpid()
+    cur = psched.LiveCursor(name, create=True)
+    try:
+        M, got = 1000, []
+        for k in range(40):
+            s, r = cur.claim(M, [64, 48, 40][k % 3])
+            if r == 0:
+                break
+            got.extend(range(s, s + r))
+        assert got == list(range(M))
+        cur.reset()
+        assert cur.claim(M, 10) == (0, 10)
+    finally:
+        cur.close()
