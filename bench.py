@@ -1,0 +1,335 @@
+"""Benchmark of the Adaptive SGD hot path (arXiv 2110.07029) on B200.
+
+One bench "step" = one mega-batch of the method (all
+rows): M = 100 * b_max samples routed by the replay scheduler (a1) to the
+replicas, every batch built on the device (a2), transposed (a3), and trained
+(a4-a8); then the replica norm, Alg. 2 weights, prescale, NCCL allreduce and
+momentum merge (a9-a13) and Alg. 1 batch scaling (a14).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config amazon670k]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  python bench.py --impl reference      # the CPU oracle on a bounded sample
+
+Prints one JSON line (rank 0).  `value` = samples/s of the whole job with the
+dataset resident in HBM; `e2e` = the same through the public API with the
+batches copied from pinned host memory every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthgen  # noqa: E402
+
+METRIC = "samples/s/box & SpMM HBM GB/s, Amazon-670K-shaped MLP, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="amazon670k", choices=list(synthgen.CONFIGS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hetero", action="store_true", help="replay with injected per-GPU slowdowns")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(device)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [l.strip().split(", ") for l in self.f if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_sample_step(ds, params, cfg, rows, pos):
+    """One bounded sample of the workload on the CPU oracle: one SGD step on
+    `rows` stream samples (oracle.model.sgd_step, fp64, as it stands)."""
+    from oracle import csr as ocsr
+    from oracle import model as om
+    from oracle import train as otrain
+    ids = ocsr.stream_ids(pos, rows, ds.n)
+    bt = otrain.batch_of(ds, ids)
+    t0 = time.perf_counter()
+    om.sgd_step(bt, params, 0.1)
+    return time.perf_counter() - t0
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import train as otrain
+    cfg = synthgen.CONFIGS[args.config]
+    ds = synthgen.make_dataset(cfg, n=min(cfg.n, 20_000))
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    prm = otrain.unpack(p, cfg.d, cfg.C, cfg.h)
+    rows = 32
+    for w in range(args.warmup):
+        oracle_sample_step(ds, prm, cfg, rows, w * rows)
+    ts = [oracle_sample_step(ds, prm, cfg, rows, (args.warmup + k) * rows) for k in range(args.steps)]
+    t = sum(ts)
+    v = rows * args.steps / t
+    sample = "oracle.model.sgd_step (fp64 numpy) on %d-row batches of the %s-shaped stream, %d steps" % (
+        rows, args.config, args.steps)
+    line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (synthgen, Table-1-shaped, seed %d)" % cfg.seed,
+            "config": {"workload": args.config, "rows_per_sample_step": rows},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_07029_b200 import _lib as L
+    from paper_2110_07029_b200 import driver
+    from paper_2110_07029_b200.api import Replica
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, "--gpus must match WORLD_SIZE"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synthgen.CONFIGS[args.config]
+    ds = synthgen.make_dataset(cfg)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    nccl_id = driver.broadcast_nccl_id(dist, rank, device=dev) if world > 1 else None
+    stream = torch.cuda.Stream(dev)
+    lr0 = 0.1
+    rep = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta, megabatch=cfg.megabatch,
+                  max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
+                  lr0=lr0, precision=args.precision, rank=rank, world=world, nccl_id=nccl_id, device=local,
+                  stream=stream)
+    rep.upload_dataset(ds)
+    costs = synthgen.make_cost_models(world, hetero=args.hetero)
+    state = driver.ReplayState(world, cfg.b_max, cfg.b_min, cfg.beta, lr0, costs)
+    M = cfg.megabatch
+    lib = rep.lib
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    pos = [0]
+
+    def mega_step(host=False):
+        """One mega-batch: a1 route, a2-a8 steps of my batches, a9-a13 merge, a14 scaling."""
+        log, u, _ = state.route(ds.row_ptr, ds.n, pos[0], M)
+        h2d = 0
+        mine = [(s, r) for (i, s, r) in log if i == rank]
+        for k, (s, r) in enumerate(mine):
+            gp = pos[0] + s
+            if host:
+                a = gp % ds.n
+                if a + r <= ds.n:                       # contiguous host slice, rebased by the library
+                    rp = ds.row_ptr[a:a + r + 1]; lp = ds.lab_ptr[a:a + r + 1]
+                    c0, c1, l0, l1 = rp[0], rp[-1], lp[0], lp[-1]
+                    rep.load_batch_csr(r, rp - c0, ds.col[c0:c1], ds.val[c0:c1], lp - l0, ds.lab[l0:l1])
+                else:
+                    sub = ds.rows((np.arange(r) + gp) % ds.n)
+                    rp, lp = sub.row_ptr, sub.lab_ptr
+                    c0, c1, l0, l1 = 0, rp[-1], 0, lp[-1]
+                    rep.load_batch_csr(r, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+                h2d += 16 * (r + 1) + 8 * int(c1 - c0) + 4 * int(l1 - l0) + 32
+                rep.train_step(want_loss=(k == len(mine) - 1))   # D2H of the step's loss
+            else:
+                rep.load_batch_stream(gp, r)
+                rep.train_step(False)
+        b_used = list(state.b)
+        rep.merge(u, b_used, want_alpha=host)            # D2H of alpha on the e2e path
+        state.rescale(u)
+        rep.set_batch_sizes(state.b, state.lr)
+        pos[0] += M
+        return h2d
+
+    # ---------------- warm-up
+    for _ in range(args.warmup):
+        mega_step()
+    torch.cuda.synchronize()
+    barrier()
+    # ---------------- timed region (device events on the replica stream)
+    lib.as_profile(rep.ctx, 1)
+    lib.as_profile_read(rep.ctx, None, None, None)
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        mega_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    ms = C.c_double * 8
+    ph_ms, ph_calls, launches = ms(), (C.c_int64 * 8)(), C.c_int64()
+    lib.as_profile_read(rep.ctx, ph_ms, ph_calls, C.byref(launches))
+    lib.as_profile(rep.ctx, 0)
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    samples = args.steps * M
+    value = samples / (t_ms / 1e3)
+    launches_total = int(sum_over_ranks(launches.value))
+    # ---------------- e2e: public API with host CSR batches (H2D every step) + D2H results
+    ke = args.e2e_steps or max(2, args.steps // 2)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    h2d = 0
+    for _ in range(ke):
+        h2d += mega_step(host=True)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = ke * M / e2e_s
+    h2d_step = sum_over_ranks(h2d) / ke
+
+    # ---------------- roofline of the dominant kernel (output layer: pass 1 + pass 2)
+    pk, pk_kind = peaks()
+    names = L.AS_PH_NAMES
+    phase = {names[i]: {"ms": ph_ms[i], "calls": ph_calls[i]} for i in range(8)}
+    my_samples = samples / world                      # replay with equal costs splits ~evenly
+    fl_alg = 6.0 * cfg.h * cfg.C * my_samples         # 6 b h C algorithmic
+    fl_iss = 8.0 * cfg.h * cfg.C * my_samples
+    t_out = (ph_ms[3] + ph_ms[5]) / 1e3
+    calls_out = max(1, ph_calls[3])
+    tflops_alg = fl_alg / t_out / 1e12 if t_out > 0 else 0.0
+    peak_t = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    if args.precision == "fp32":
+        peak_t = 0.0
+    spmm_bytes = (4 * cfg.h + 8) * cfg.avg_nnz * my_samples + 8 * my_samples + 4 * cfg.h * my_samples
+    spmm_gbs = spmm_bytes / (ph_ms[2] / 1e3) / 1e9 if ph_ms[2] > 0 else 0.0
+    roof = {"bound": "tensor", "kernel": "out_fwd+out_bwd (tcgen05 passes 1+2, one launch each per SGD step)",
+            "achieved": tflops_alg, "peak": peak_t, "unit": "TFLOP/s",
+            "frac": tflops_alg / peak_t if peak_t else None, "traffic": None,
+            "flops_per_launch_alg": 6.0 * cfg.h * cfg.C * cfg.b_max,
+            "issued_frac": (fl_iss / t_out / 1e12) / peak_t if (peak_t and t_out) else None,
+            "peak_kind": "%s bf16_tflops_sustained (kernel timed inside a long step)" % pk_kind,
+            "avg_launch_ms": {"out_fwd": ph_ms[3] / calls_out, "out_bwd": ph_ms[5] / max(1, ph_calls[5])},
+            "spmm": {"bound": "hbm", "achieved": spmm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": spmm_gbs / pk["hbm_gbs"], "avg_launch_ms": ph_ms[2] / max(1, ph_calls[2])}}
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import train as otrain
+        prm = otrain.unpack(p, cfg.d, cfg.C, cfg.h)
+        ts, k = [], 0
+        t_start = time.perf_counter()
+        while k < 3 or (time.perf_counter() - t_start < 10 and k < 8):
+            ts.append(oracle_sample_step(ds, prm, cfg, 64, 64 * k))
+            k += 1
+        cpu = {"value": 64 * len(ts) / sum(ts), "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": "%d SGD steps of 64 stream rows (oracle.model.sgd_step, fp64 numpy), no merge" % len(ts)}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
+                "data": "synthetic (synthgen, Table-1-shaped, seed %d); random-init (Glorot) weights" % cfg.seed,
+                "config": {"workload": args.config, "d": cfg.d, "C": cfg.C, "h": cfg.h, "n": cfg.n,
+                           "b_max": cfg.b_max, "megabatch": M, "step": "one mega-batch (all of SURVEY 8(a))",
+                           "routing": "replay, %s cost models" % ("heterogeneous" if args.hetero else "equal"),
+                           "parallelism": "dp%d (one replica per GPU, NCCL merge)" % world,
+                           "l2": "inputs larger than L2 (W2T fp32 343 MB + bf16 171 MB streamed per step)"},
+                "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_step),
+                        "d2h_bytes_per_step": int(world * (4 + 8 * world))},
+                "gpu_launches": launches_total, "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
+                "phases_ms": phase}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

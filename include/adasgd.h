@@ -193,6 +193,27 @@ enum {
 int as_debug_get(as_ctx *ctx, int32_t which, void *host_out, size_t bytes,
                  size_t *written);
 
+/* ---- live profiling (bench) ------------------------------------------------
+ * When enabled, the ctx records CUDA events on its stream around every phase
+ * of as_train_step / as_load_batch_* / as_merge.  as_profile_read synchronises
+ * and returns, per phase, the summed device milliseconds and the number of
+ * timed calls, plus the number of kernels the library launched since the
+ * last read (all phases, profiled or not); counters are then reset. */
+enum {
+  AS_PH_BATCH = 0,     /* a2: batch H2D / device gather                         */
+  AS_PH_TRANSPOSE = 1, /* a3                                                     */
+  AS_PH_SPMM = 2,      /* a4                                                     */
+  AS_PH_OUT_FWD = 3,   /* a5: tcgen05 pass 1 (or the fp32 logits GEMM + LSE)      */
+  AS_PH_COMBINE = 4,   /* a5: label terms, combine, db1                          */
+  AS_PH_OUT_BWD = 5,   /* a6: tcgen05 pass 2 with fused SGD (or fp32 GEMMs + SGD) */
+  AS_PH_DW1 = 6,       /* a7                                                     */
+  AS_PH_MERGE = 7,     /* a9-a13                                                 */
+  AS_PH_COUNT = 8
+};
+int as_profile(as_ctx *ctx, int32_t enable);
+int as_profile_read(as_ctx *ctx, double *ms_out, int64_t *calls_out,
+                    int64_t *launches_out);
+
 /* Tensor-core self-test (tests only): A, B are DEVICE bf16 [128][128]
  * row-major; writes DEVICE fp32 [128][128] results of the three operand
  * layouts the output layer uses:  S = A B^T;  P = bf16(S/16);  O = P B;

@@ -103,3 +103,40 @@ def sgd_step(batch, params, lr):
     for k in ("W1", "b1", "W2T", "b2"):
         new[k] = (np.asarray(params[k], np.float64) - lr * g[k]).astype(np.float32)
     return new, fwd["loss"], g
+
+
+def gradients_chunked(batch, params, chunk=64):
+    """The same forward/backward as forward() + gradients(), evaluated `chunk`
+    rows at a time so that the b x C logits never exist at once (memory only:
+    every quantity is the same definition; used for the full-size sampled
+    parity checks).  Returns dict with LSE, loss, dA, db1, dW1, dW2T, db2."""
+    W1, b1, W2T, b2 = (np.asarray(params[k], np.float64) for k in ("W1", "b1", "W2T", "b2"))
+    A = spmm(batch.row_ptr, batch.col, batch.val, W1, b1)
+    H = np.maximum(A, 0.0)
+    B = A.shape[0]
+    tr, tc, tw = target_matrix_rows(batch.lab_ptr, batch.lab)
+    LSE = np.empty(B)
+    label_term = np.zeros(B)
+    dH = np.empty_like(H)
+    dW2T = np.zeros_like(W2T)
+    db2 = np.zeros_like(b2)
+    for r0 in range(0, B, chunk):
+        r1 = min(B, r0 + chunk)
+        Z = H[r0:r1] @ W2T.T + b2
+        zmax = Z.max(axis=1, keepdims=True)
+        LSE[r0:r1] = zmax[:, 0] + np.log(np.exp(Z - zmax).sum(axis=1))
+        sel = (tr >= r0) & (tr < r1)
+        np.add.at(label_term, tr[sel], tw[sel] * Z[tr[sel] - r0, tc[sel]])
+        G = np.exp(Z - LSE[r0:r1, None])
+        np.add.at(G, (tr[sel] - r0, tc[sel]), -tw[sel])
+        G /= B
+        dW2T += G.T @ H[r0:r1]
+        db2 += G.sum(axis=0)
+        dH[r0:r1] = G @ W2T
+    dA = dH * (A > 0)
+    d = W1.shape[0]
+    dW1 = np.zeros((d, A.shape[1]), np.float64)
+    rid = np.repeat(np.arange(B), np.diff(np.asarray(batch.row_ptr)))
+    np.add.at(dW1, np.asarray(batch.col, np.int64), np.asarray(batch.val, np.float64)[:, None] * dA[rid])
+    return {"A": A, "H": H, "LSE": LSE, "loss": float(np.mean(LSE - label_term)), "dA": dA,
+            "db1": dA.sum(axis=0), "dW1": dW1, "dW2T": dW2T, "db2": db2}

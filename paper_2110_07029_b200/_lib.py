@@ -28,8 +28,9 @@ EXPORTS = [
     "as_train_step", "as_merge", "as_group_merge", "as_set_batch_sizes", "as_get_params",
     "as_set_params", "as_debug_get", "as_tc_selftest", "as_sched_route_replay", "as_sched_alg1",
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
-    "as_live_close",
+    "as_live_close", "as_profile", "as_profile_read",
 ]
+AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
 
 class ASError(RuntimeError):
@@ -104,6 +105,8 @@ def load():
         "as_live_claim": [VP, I64, I32, P(I64), P(I32)],
         "as_live_reset": [VP],
         "as_live_close": [VP, I32],
+        "as_profile": [VP, I32],
+        "as_profile_read": [VP, P(D), P(I64), P(I64)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

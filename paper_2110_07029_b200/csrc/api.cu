@@ -87,6 +87,13 @@ struct as_ctx {
   const float *ds_val;
   int64_t ds_n;
   ncclComm_t comm;
+  // live profiling (as_profile)
+  bool prof_on;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t ph_start[AS_PH_COUNT];
+  struct Pend { int ph; cudaEvent_t a, b; };
+  std::vector<Pend> pending;
+  long long launches;
 };
 
 namespace {
@@ -207,6 +214,30 @@ int cuda_check(as_ctx *x, cudaError_t e, const char *what) {
   }
   return AS_OK;
 }
+
+cudaEvent_t get_event(as_ctx *x) {
+  if (!x->ev_pool.empty()) {
+    cudaEvent_t e = x->ev_pool.back();
+    x->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+inline void ph_begin(as_ctx *x, int ph) {
+  if (!x->prof_on) return;
+  x->ph_start[ph] = get_event(x);
+  cudaEventRecord(x->ph_start[ph], x->stream);
+}
+inline void ph_end(as_ctx *x, int ph) {
+  if (!x->prof_on) return;
+  cudaEvent_t e = get_event(x);
+  cudaEventRecord(e, x->stream);
+  x->pending.push_back({ph, x->ph_start[ph], e});
+}
+// kernels launched by the transpose of a key space with `bits` bits
+inline int n_transpose_launches(int bits) { return 6 + 3 * ((bits + as::kSortBits - 1) / as::kSortBits); }
 
 #define AS_GUARD(x)                                                               \
   do {                                                                            \
@@ -338,6 +369,8 @@ int as_destroy(as_ctx *x) {
     if (x->pin_ev[i]) cudaEventDestroy(x->pin_ev[i]);
   }
   if (x->comm) ncclCommDestroy(x->comm);
+  for (auto &p : x->pending) { x->ev_pool.push_back(p.a); x->ev_pool.push_back(p.b); }
+  for (auto e : x->ev_pool) cudaEventDestroy(e);
   free(x->plan);
   delete x;
   return AS_OK;
@@ -375,12 +408,14 @@ int as_load_batch_csr(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int
   dd->nnz = (int32_t)nnz;
   dd->nlab = (int32_t)L;
   cudaStream_t s = x->stream;
+  ph_begin(x, AS_PH_BATCH);
   cudaMemcpyAsync(x->row_ptr, rp, 8 * (rows + 1), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(x->lab_ptr, lp, 8 * (rows + 1), cudaMemcpyHostToDevice, s);
   if (nnz) cudaMemcpyAsync(x->col, cc, 4 * nnz, cudaMemcpyHostToDevice, s);
   if (nnz) cudaMemcpyAsync(x->val, vv, 4 * nnz, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(x->lab, ll, 4 * L, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(x->desc, dd, sizeof(StepDesc), cudaMemcpyHostToDevice, s);
+  ph_end(x, AS_PH_BATCH);
   rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], s), "batch H2D");
   if (rc) return rc;
   x->loaded_rows = rows;
@@ -445,9 +480,12 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   const int bi = x->b_all[x->cfg.rank];
   if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
   if (pos < 0) return as_fail(AS_E_INVALID, "pos < 0");
+  ph_begin(x, AS_PH_BATCH);
+  x->launches += 3;
   as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
                           x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
                           x->lab, x->ids, x->desc, x->D.nnz_cap, x->D.lab_cap);
+  ph_end(x, AS_PH_BATCH);
   const int rc = cuda_check(x, cudaSuccess, "gather batch");
   if (rc) return rc;
   x->loaded_rows = rows;
@@ -467,6 +505,8 @@ int as_train_step(as_ctx *x, float *loss_out) {
   float *W1 = x->w, *b1 = x->w + D.d * D.h, *W2T = b1 + D.h, *b2 = W2T + D.C * D.h;
 
   // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2)
+  ph_begin(x, AS_PH_TRANSPOSE);
+  x->launches += n_transpose_launches(key_bits(D.d)) + n_transpose_launches(key_bits(D.C)) + 1;
   as::launch_transpose(s, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->fseg_id,
                        x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val);
@@ -474,27 +514,46 @@ int as_train_step(as_ctx *x, float *loss_out) {
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->lseg_id,
                        x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr);
   as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
+  ph_end(x, AS_PH_TRANSPOSE);
   // a4: SpMM forward
+  ph_begin(x, AS_PH_SPMM);
+  x->launches += 1;
   as::launch_spmm(s, D.h, d, D.bpad, x->row_ptr, x->col, x->val, W1, b1, x->Hf, x->Hb);
-  // a5: label terms of the loss and of dH (R3)
-  as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
+  ph_end(x, AS_PH_SPMM);
   if (x->cfg.precision == AS_BF16) {
     // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
+    ph_begin(x, AS_PH_OUT_FWD);
+    x->launches += 1;
     as::launch_out_fwd_tc(s, x->plan, d, b2, x->pm, x->pl, x->pO);
+    ph_end(x, AS_PH_OUT_FWD);
+    ph_begin(x, AS_PH_COMBINE);
+    x->launches += 3;
+    // label terms of the loss and of dH (R3)
+    as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
                             x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lse2, x->lossr, x->dA);
     as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
+    ph_end(x, AS_PH_COMBINE);
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
+    ph_begin(x, AS_PH_OUT_BWD);
+    x->launches += 1;
     as::launch_out_bwd_tc(s, x->plan, d, x->lse2, b2, x->cls_seg, x->lseg_ptr, x->lseg_row,
                           x->lab_ptr, x->Hf, W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
                           dbg ? x->dbg_db2 : nullptr, nullptr);
+    ph_end(x, AS_PH_OUT_BWD);
   } else {
     // fp32 parity mode: logits materialised
     const long long C = D.C;
+    ph_begin(x, AS_PH_OUT_FWD);
+    x->launches += 1 + 1 + 1 + 2;
+    as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
     as::launch_gemm_f32(s, D.b_max, (int)C, D.h, x->Hf, D.h, 1, W2T, 1, D.h, x->Z, C, b2, 1,
                         nullptr, &d->rows);
     as::launch_row_lse(s, d, D.b_max, (int)C, x->Z, x->lse2);
     as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2);
+    ph_end(x, AS_PH_OUT_FWD);
+    ph_begin(x, AS_PH_OUT_BWD);
+    x->launches += (D.splitk > 1 ? 2 : 1) + 1 + 1 + 2 + 1 + (dbg ? 0 : 0);
     as::launch_gemm_f32(s, D.b_max, D.h, (int)C, x->Z, C, 1, W2T, D.h, 1, x->dH, D.h, nullptr,
                         D.splitk, x->splitk_tmp, &d->rows);
     as::launch_gemm_f32_kdev(s, (int)C, D.h, D.b_max, x->Z, 1, C, x->Hf, D.h, 1, x->dW2, D.h,
@@ -504,12 +563,16 @@ int as_train_step(as_ctx *x, float *loss_out) {
     as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
     if (dbg) cudaMemcpyAsync(x->dbg_dW2, x->dW2, 4 * (size_t)C * D.h, cudaMemcpyDeviceToDevice, s);
     as::launch_sgd_dense(s, C * D.h, W2T, x->dW2, lr, x->w2b);
+    ph_end(x, AS_PH_OUT_BWD);
   }
   // a7: first-layer gradient (deterministic segmented reduction) + SGD
+  ph_begin(x, AS_PH_DW1);
+  x->launches += 2 + 1 + 1;
   as::launch_dw1_sgd(s, D.h, d, D.nnz_cap, x->fseg_id, x->fseg_ptr, x->fseg_row, x->fseg_val, x->dA,
                      W1, lr, x->long_list, dbg ? x->dbg_dW1 : nullptr);
   as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 0);
   as::launch_loss_mean(s, d, x->lossr, x->loss);
+  ph_end(x, AS_PH_DW1);
   int rc = cuda_check(x, cudaSuccess, "train step launch");
   if (rc) return rc;
   if (loss_out) {
@@ -541,6 +604,8 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   const Dims &D = x->D;
   cudaStream_t s = x->stream;
   // a9: replica norm
+  ph_begin(x, AS_PH_MERGE);
+  x->launches += 4;
   as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
   if (N > 1) {
     const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
@@ -565,6 +630,7 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, D.d * D.h + D.h,
                       D.C * D.h, x->w2b);
   std::swap(x->wbar, x->wbarp);
+  ph_end(x, AS_PH_MERGE);
   rc = cuda_check(x, cudaSuccess, "merge launch");
   if (rc) return rc;
   if (alpha_out) std::copy(alpha.begin(), alpha.end(), alpha_out);
@@ -700,6 +766,34 @@ int as_debug_get(as_ctx *x, int32_t which, void *host_out, size_t bytes, size_t 
   rc = cuda_check(x, cudaStreamSynchronize(s), "debug D2H");
   *written = total;
   return rc;
+}
+
+int as_profile(as_ctx *x, int32_t enable) {
+  AS_GUARD(x);
+  x->prof_on = enable != 0;
+  return AS_OK;
+}
+
+int as_profile_read(as_ctx *x, double *ms_out, int64_t *calls_out, int64_t *launches_out) {
+  AS_GUARD(x);
+  int rc = cuda_check(x, cudaStreamSynchronize(x->stream), "profile sync");
+  if (rc) return rc;
+  double ms[AS_PH_COUNT] = {0};
+  int64_t calls[AS_PH_COUNT] = {0};
+  for (auto &p : x->pending) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, p.a, p.b);
+    ms[p.ph] += t;
+    calls[p.ph] += 1;
+    x->ev_pool.push_back(p.a);
+    x->ev_pool.push_back(p.b);
+  }
+  x->pending.clear();
+  if (ms_out) std::copy(ms, ms + AS_PH_COUNT, ms_out);
+  if (calls_out) std::copy(calls, calls + AS_PH_COUNT, calls_out);
+  if (launches_out) *launches_out = x->launches;
+  x->launches = 0;
+  return AS_OK;
 }
 
 int as_tc_selftest(const void *A, const void *B, float *S, float *O, float *T) {

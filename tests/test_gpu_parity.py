@@ -1,0 +1,304 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the oracle.
+
+Tolerances (north star, reading R22: per tensor
+||a-o||_2/||o||_2 <= tol AND max|a-o| <= tol * max|o|):
+  bit-exact  batch transposes (integer/index work), replay routing, b_i
+  1e-4       AS_FP32 mode: logits (LSE), loss, gradients after one step
+  2e-2       AS_BF16 mode (tcgen05 tensor-core output layer)
+  1e-5       merged weights
+"""
+import math
+import struct
+
+import numpy as np
+import pytest
+
+import synthgen
+from oracle import csr as ocsr
+from oracle import merge as omerge
+from oracle import model as om
+from oracle import sched as osched
+from oracle import train as otrain
+
+pytestmark = pytest.mark.gpu
+
+LN2 = math.log(2.0)
+
+
+def rel_err(a, o):
+    a = np.asarray(a, np.float64); o = np.asarray(o, np.float64)
+    n = np.linalg.norm(o)
+    e1 = np.linalg.norm(a - o) / max(n, 1e-300)
+    e2 = np.max(np.abs(a - o)) / max(np.max(np.abs(o)), 1e-300) if o.size else 0.0
+    return max(e1, e2)
+
+
+def assert_close(name, a, o, tol):
+    e = rel_err(a, o)
+    assert e <= tol, "%s: rel err %.3e > %.1e" % (name, e, tol)
+    return e
+
+
+def _cfg(d, C, h, n, b_max, avg_nnz=20.0, avg_labels=3.0, seed=0):
+    return synthgen.XMLConfig("t", d, C, n, avg_nnz, avg_labels, h, b_max, 1, seed)
+
+
+def _params(cfg, seed=3, bias=0.2):
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, seed)
+    lay = synthgen.param_layout(cfg.d, cfg.C, cfg.h)
+    rng = np.random.default_rng(seed)
+    for k in ("b1", "b2"):
+        o, shp = lay[k]
+        p[o:o + shp[0]] = rng.normal(0, bias, shp[0]).astype(np.float32)
+    return p
+
+
+def _replica(cfg, p, ds, precision, lr=0.5, debug=True, b_min=None):
+    from paper_2110_07029_b200.api import Replica
+    return Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=b_min or max(1, cfg.b_max // 8),
+                   max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
+                   lr0=lr, precision=precision, debug_grads=debug)
+
+
+def _f32(buf):
+    return np.frombuffer(buf.tobytes(), np.float32)
+
+
+def _i32(buf):
+    return np.frombuffer(buf.tobytes(), np.int32)
+
+
+def test_tc_selftest_descriptors(gpu_lib):
+    import torch
+    from paper_2110_07029_b200.api import tc_selftest
+    g = torch.Generator(device="cuda").manual_seed(0)
+    A = torch.randn(128, 128, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(128, 128, device="cuda", generator=g).to(torch.bfloat16)
+    S, O, T = tc_selftest(A, B)
+    Af, Bf = A.double(), B.double()
+    assert rel_err(S.cpu().numpy(), (Af @ Bf.T).cpu().numpy()) < 1e-5
+    P = (S / 16).to(torch.bfloat16).double()
+    assert rel_err(O.cpu().numpy(), (P @ Bf).cpu().numpy()) < 1e-5
+    assert rel_err(T.cpu().numpy(), (Af.T @ P.T).cpu().numpy()) < 1e-5
+
+
+CASES = [
+    # d, C, h, n, B (rows of the batch), b_max
+    (2000, 1000, 128, 600, 200, 256),    # ragged: 2 row tiles (72 rows in the 2nd), C % 128 = 104
+    (3000, 700, 256, 400, 130, 192),     # h = 256
+    (500, 50, 128, 64, 1, 64),           # a single row, C < 128
+    (1500, 2048, 128, 700, 512, 512),    # exact tiles
+]
+
+
+def _one_step(case, precision):
+    d, C, h, n, B, b_max = case
+    cfg = _cfg(d, C, h, n, b_max, seed=hash(case) % 97)
+    ds = synthgen.make_dataset(cfg, n=n)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, precision, lr=0.5)
+    ids = np.arange(B) + 7
+    sub = ds.rows(ids)
+    rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    loss = rep.train_step(want_loss=True)
+    prm = otrain.unpack(p, d, C, h)
+    ref = om.gradients_chunked(sub, prm, chunk=64)
+    return cfg, ds, sub, rep, loss, ref, p
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_transposes_bit_exact(gpu_lib, case):
+    cfg, ds, sub, rep, loss, ref, p = _one_step(case, "fp32")
+    keys, sptr, srow, sval = ocsr.transpose(sub.row_ptr, sub.col, sub.val)
+    buf = rep.debug_get(8, 64 << 20)
+    w = _i32(buf)
+    U = int(w[0])
+    nnz = len(sub.col)
+    assert U == len(keys)
+    got_ids = w[1:1 + U]; o = 1 + U
+    got_ptr = w[o:o + U + 1]; o += U + 1
+    got_row = w[o:o + nnz]; o += nnz
+    got_val = w[o:o + nnz]
+    assert np.array_equal(got_ids, keys) and np.array_equal(got_ptr, sptr)
+    assert np.array_equal(got_row, srow)
+    assert np.array_equal(got_val, sval.view(np.int32))            # bit-exact values
+    lkeys, lptr, lrow, _ = ocsr.transpose(sub.lab_ptr, sub.lab)
+    w = _i32(rep.debug_get(9, 64 << 20))
+    V = int(w[0])
+    assert V == len(lkeys)
+    assert np.array_equal(w[1:1 + V], lkeys) and np.array_equal(w[1 + V:2 + 2 * V], lptr)
+    assert np.array_equal(w[2 + 2 * V:2 + 2 * V + len(sub.lab)], lrow)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 2e-2)])
+@pytest.mark.parametrize("case", CASES)
+def test_one_step_parity(gpu_lib, case, precision, tol):
+    cfg, ds, sub, rep, loss, ref, p = _one_step(case, precision)
+    d, C, h, n, B, b_max = case
+    H = _f32(rep.debug_get(0, 4 * B * h)).reshape(B, h)
+    assert_close("H", H, ref["H"], 1e-5)                       # SpMM is fp32 in both modes
+    lse = _f32(rep.debug_get(1, 4 * B)) * LN2
+    assert_close("LSE", lse, ref["LSE"], tol)
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    dA = _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h)
+    assert_close("dA", dA, ref["dA"], tol)
+    db1 = _f32(rep.debug_get(4, 4 * h))
+    assert_close("db1", db1, ref["db1"], tol)
+    dW2T = _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h)
+    assert_close("dW2T", dW2T, ref["dW2T"], tol)
+    db2 = _f32(rep.debug_get(6, 4 * C))
+    assert_close("db2", db2, ref["db2"], tol)
+    keys = np.unique(sub.col)
+    dW1 = _f32(rep.debug_get(7, 4 * len(keys) * h)).reshape(len(keys), h)
+    assert_close("dW1", dW1, ref["dW1"][keys], tol)
+    # the SGD update applied the gradients with lr (P:51 third pass)
+    new = rep.get_params()
+    dnew = otrain.unpack(new.astype(np.float64) - p.astype(np.float64), d, C, h)
+    assert_close("W2T update", dnew["W2T"], -0.5 * ref["dW2T"], max(tol, 1e-3))
+    assert_close("W1 update", dnew["W1"][keys], -0.5 * ref["dW1"][keys], max(tol, 1e-3))
+    untouched = np.setdiff1d(np.arange(d), keys)
+    assert np.all(dnew["W1"][untouched] == 0)                  # untouched rows bit-identical
+
+
+def test_invalid_batch_is_rejected_without_state_change(gpu_lib):
+    from paper_2110_07029_b200._lib import ASError
+    cfg = _cfg(800, 300, 128, 100, 64)
+    ds = synthgen.make_dataset(cfg, n=100)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, "bf16")
+    sub = ds.rows(np.arange(10))
+    bad_col = sub.col.copy(); bad_col[1], bad_col[0] = bad_col[0], bad_col[1]
+    for args in [(0, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab),
+                 (65, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab),
+                 (10, sub.row_ptr, bad_col, sub.val, sub.lab_ptr, sub.lab),
+                 (10, sub.row_ptr, sub.col, sub.val, np.zeros(11, np.int64), sub.lab)]:
+        with pytest.raises(ASError) as e:
+            rep.load_batch_csr(*args)
+        assert e.value.code == -1
+    with pytest.raises(ASError):
+        rep.train_step()                                       # nothing loaded yet
+    assert np.array_equal(rep.get_params(), p)
+    rep.load_batch_csr(10, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    assert np.isfinite(rep.train_step(want_loss=True))
+
+
+def test_resident_stream_batch_equals_host_batch(gpu_lib):
+    cfg = _cfg(1200, 400, 128, 300, 128)
+    ds = synthgen.make_dataset(cfg, n=300)
+    p = _params(cfg)
+    order = osched.permutation(300, 99)
+    r1 = _replica(cfg, p, ds, "bf16", debug=False)
+    r2 = _replica(cfg, p, ds, "bf16", debug=False)
+    r1.upload_dataset(ds, order)
+    pos, rows = 250, 100                                       # wraps the data epoch
+    r1.load_batch_stream(pos, rows)
+    l1 = r1.train_step(True)
+    sub = ds.rows(ocsr.stream_ids(pos, rows, 300, order))
+    r2.load_batch_csr(rows, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    l2 = r2.train_step(True)
+    assert l1 == l2
+    assert np.array_equal(r1.get_params(), r2.get_params())     # deterministic, bit-identical
+
+
+def test_step_is_deterministic(gpu_lib):
+    cfg = _cfg(3000, 2000, 128, 700, 512, avg_nnz=40)
+    ds = synthgen.make_dataset(cfg, n=700)
+    p = _params(cfg)
+    outs = []
+    for _ in range(2):
+        rep = _replica(cfg, p, ds, "bf16", debug=False)
+        sub = ds.rows(np.arange(512))
+        rep.load_batch_csr(512, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+        rep.train_step()
+        outs.append(rep.get_params())
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_group_merge_parity(gpu_lib, precision):
+    from paper_2110_07029_b200.api import group_merge
+    cfg = _cfg(1000, 500, 128, 200, 64)
+    ds = synthgen.make_dataset(cfg, n=200)
+    p = _params(cfg)
+    reps = [_replica(cfg, p, ds, precision, debug=False) for _ in range(3)]
+    for i, r in enumerate(reps):
+        r.set_batch_sizes([64, 64, 64], [0.5, 0.5, 0.5])
+        for k in range(i + 1):                                 # u = (1, 2, 3)
+            sub = ds.rows(np.arange(32) + 40 * i + 8 * k)
+            r.load_batch_csr(32, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+            r.train_step()
+    ws = [r.get_params() for r in reps]
+    u, b = [1, 2, 3], [64, 64, 64]
+    alpha, pert = group_merge(reps, u, b)
+    norms = [omerge.replica_norm(w) for w in ws]
+    oa, op = osched.alg2(u, b, norms, 0.1, 0.1)
+    assert list(alpha) == oa and pert == op == 1
+    wbar, wbar_p = omerge.merge(ws, oa, p, p, 0.9)
+    for r in reps:
+        assert_close("wbar", r.get_params(1), wbar, 1e-5)
+        assert np.array_equal(r.get_params(2), p)              # wbar_p <- wbar
+        assert np.array_equal(r.get_params(0), r.get_params(1))  # replicas restart from wbar
+    # second merge exercises the momentum term gamma (wbar - wbar_p)
+    ws2 = [r.get_params() for r in reps]
+    alpha2, _ = group_merge(reps, [2, 2, 2], b)
+    oa2, _ = osched.alg2([2, 2, 2], b, [omerge.replica_norm(w) for w in ws2], 0.1, 0.1)
+    wbar2, _ = omerge.merge(ws2, oa2, wbar, p, 0.9)
+    assert_close("wbar2", reps[0].get_params(1), wbar2, 1e-5)
+
+
+def test_end_to_end_tiny_two_replicas_replay(gpu_lib):
+    """T5: config 'tiny' (BASELINE.json configs[0]): 2 replicas, replay with a
+    32% slowdown, 1 epoch, 4 merges, fp32 mode.  Routing, b_i, lr_i and alpha
+    are bit-exact; the global model matches the oracle after every merge."""
+    from paper_2110_07029_b200 import driver
+    cfg = synthgen.CONFIGS["tiny"]
+    ds = synthgen.make_dataset(cfg)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    costs = synthgen.make_cost_models(2, hetero=True)
+    lr0 = 0.5
+    reps = []
+    for rank in range(2):
+        from paper_2110_07029_b200.api import Replica
+        reps.append(Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta,
+                            megabatch=1024, max_row_nnz=int(np.diff(ds.row_ptr).max()),
+                            max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=lr0, precision="fp32",
+                            rank=rank, world=2))
+    st = driver.ReplayState(2, cfg.b_max, cfg.b_min, cfg.beta, lr0, costs)
+    recs = driver.run_local(reps, ds, st, ds.n)
+    ocfg = otrain.RunConfig(d=cfg.d, C=cfg.C, h=cfg.h, b_max=cfg.b_max, b_min=cfg.b_min, beta=cfg.beta,
+                            M=1024, lr0=lr0, world=2)
+    orecs, owbar = otrain.run(ds, p, ocfg, costs, ds.n)
+    assert len(recs) == len(orecs) == 4
+    for g, o in zip(recs, orecs):
+        assert [tuple(x) for x in g["log"]] == [tuple(x) for x in o["log"]]
+        assert g["u"] == o["u"] and g["b"] == o["b"] and g["b_next"] == o["b_next"]
+        assert g["lr_next"] == o["lr_next"]
+        assert g["alpha"] == o["alpha"] and g["perturbed"] == o["perturbed"]
+    assert any(g["u"][0] != g["u"][1] for g in recs)           # heterogeneity exercised
+    assert_close("wbar after 4 merges", reps[0].get_params(1), owbar, 1e-4)
+
+
+@pytest.mark.slow
+def test_full_size_amazon670k_sampled(gpu_lib):
+    """Amazon-670K shape at b = 1024 in the bench's launch configuration
+    (bf16, resident dataset, stream batch): the oracle recomputes the whole
+    step in fp64 (chunked over rows) and every output is compared."""
+    cfg = synthgen.CONFIGS["amazon670k"]
+    ds = synthgen.make_dataset(cfg, n=40_000)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    rep = _replica(cfg, p, ds, "bf16", lr=0.5)
+    rep.upload_dataset(ds)
+    rep.load_batch_stream(1000, 1024)
+    loss = rep.train_step(True)
+    sub = ds.rows(ocsr.stream_ids(1000, 1024, ds.n))
+    ref = om.gradients_chunked(sub, otrain.unpack(p, cfg.d, cfg.C, cfg.h), chunk=128)
+    tol = 2e-2
+    assert abs(loss - ref["loss"]) <= tol * ref["loss"]
+    assert_close("LSE", _f32(rep.debug_get(1, 4 * 1024)) * LN2, ref["LSE"], tol)
+    assert_close("dA", _f32(rep.debug_get(3, 4 * 1024 * 128)).reshape(1024, 128), ref["dA"], tol)
+    dW2T = _f32(rep.debug_get(5, 4 * cfg.C * 128)).reshape(cfg.C, 128)
+    assert_close("dW2T", dW2T, ref["dW2T"], tol)
+    assert_close("db2", _f32(rep.debug_get(6, 4 * cfg.C)), ref["db2"], tol)
+    keys = np.unique(sub.col)
+    dW1 = _f32(rep.debug_get(7, 4 * len(keys) * 128)).reshape(len(keys), 128)
+    assert_close("dW1", dW1, ref["dW1"][keys], tol)

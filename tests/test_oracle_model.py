@@ -129,3 +129,15 @@ def test_sgd_step_moves_against_gradient_and_lowers_loss():
     # untouched W1 rows stay bit-identical
     untouched = np.setdiff1d(np.arange(ds.d), np.unique(ds.col))
     assert np.array_equal(new["W1"][untouched], np.asarray(prm["W1"])[untouched])
+
+
+def test_chunked_gradients_equal_plain():
+    ds, p = _tiny(seed=12, n=40)
+    prm = otrain.unpack(p, ds.d, ds.C, 8)
+    g = om.gradients(ds, prm)
+    f = om.forward(ds, prm)
+    gc = om.gradients_chunked(ds, prm, chunk=7)
+    assert abs(gc["loss"] - f["loss"]) <= 1e-13
+    np.testing.assert_allclose(gc["LSE"], f["LSE"], rtol=1e-14)
+    for k, kc in (("W1", "dW1"), ("W2T", "dW2T"), ("b2", "db2"), ("b1", "db1"), ("dA", "dA")):
+        np.testing.assert_allclose(gc[kc], g[k], rtol=1e-12, atol=1e-15)
