@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hetero", action="store_true", help="replay with injected per-GPU slowdowns")
+    ap.add_argument("--verbose", action="store_true", help="progress on stderr")
     return ap.parse_args()
 
 
@@ -76,8 +77,11 @@ class Clocks:
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
+        self.p.kill()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            pass
         self.f.seek(0)
         rows = [l.strip().split(", ") for l in self.f if l.strip()]
         os.unlink(self.f.name)
@@ -147,8 +151,19 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+T0 = time.time()
+VERBOSE = False
+
+
+def log(*a):
+    if VERBOSE:
+        print("[bench %.1fs]" % (time.time() - T0), *a, file=sys.stderr, flush=True)
+
+
 def main():
+    global VERBOSE
     args = parse()
+    VERBOSE = args.verbose
     if args.impl == "reference":
         return run_reference(args)
     import ctypes as C
@@ -171,6 +186,7 @@ def main():
     cfg = synthgen.CONFIGS[args.config]
     ds = synthgen.make_dataset(cfg)
     p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    log("dataset + init generated")
     nccl_id = driver.broadcast_nccl_id(dist, rank, device=dev) if world > 1 else None
     stream = torch.cuda.Stream(dev)
     lr0 = 0.1
@@ -179,6 +195,7 @@ def main():
                   lr0=lr0, precision=args.precision, rank=rank, world=world, nccl_id=nccl_id, device=local,
                   stream=stream)
     rep.upload_dataset(ds)
+    log("replica ready, dataset resident")
     costs = synthgen.make_cost_models(world, hetero=args.hetero)
     state = driver.ReplayState(world, cfg.b_max, cfg.b_min, cfg.beta, lr0, costs)
     M = cfg.megabatch
@@ -235,14 +252,17 @@ def main():
         return h2d
 
     # ---------------- warm-up
-    for _ in range(args.warmup):
+    for w in range(args.warmup):
         mega_step()
+        torch.cuda.synchronize()
+        log("warmup mega-batch", w)
     torch.cuda.synchronize()
     barrier()
     # ---------------- timed region (device events on the replica stream)
     lib.as_profile(rep.ctx, 1)
     lib.as_profile_read(rep.ctx, None, None, None)
     clocks = Clocks(local)
+    log("clock sampler started")
     time.sleep(0.3)
     torch.cuda.synchronize()
     barrier()
@@ -253,12 +273,15 @@ def main():
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    log("timed steps done")
     ck = clocks.stop()
+    log("clock sampler stopped")
     ms = C.c_double * 8
     ph_ms, ph_calls, launches = ms(), (C.c_int64 * 8)(), C.c_int64()
     lib.as_profile_read(rep.ctx, ph_ms, ph_calls, C.byref(launches))
     lib.as_profile(rep.ctx, 0)
     t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    log("timed region done: %.1f ms" % t_ms)
     samples = args.steps * M
     value = samples / (t_ms / 1e3)
     launches_total = int(sum_over_ranks(launches.value))
@@ -273,6 +296,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
+    log("e2e done: %.2f s" % e2e_s)
     e2e = ke * M / e2e_s
     h2d_step = sum_over_ranks(h2d) / ke
 

@@ -504,7 +504,8 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // =====================================================================
 // Combine the split-C partials of output pass 1 (online softmax in log2
 // units): LSE_r, loss_r = LSE_r - zsum_r, dH_r = (O_r/l_r - labW_r)/B and
-// dA_r = dH_r * [A_r > 0]  (R3, R4).  One CTA (h threads) per row.
+// dA_r = dH_r * [A_r > 0]  (R3, R4).  One CTA (h threads) per row.  Partial
+// layout: pm, pl [split][bpad]; pO [split][h][bpad] (coalesced TC epilogue).
 // =====================================================================
 __global__ void k_combine_bf16(const StepDesc *__restrict__ desc, int h, int bpad, int splits,
                                const float *__restrict__ pm, const float *__restrict__ pl,
@@ -522,7 +523,7 @@ __global__ void k_combine_bf16(const StepDesc *__restrict__ desc, int h, int bpa
     const float ms = pm[(size_t)s * bpad + r];
     const float sc = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
     l = fmaf(pl[(size_t)s * bpad + r], sc, l);
-    o = fmaf(pO[((size_t)s * bpad + r) * h + j], sc, o);
+    o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc, o);
   }
   const float L2 = M + log2f(l);
   const float invB = 1.0f / (float)B;

@@ -298,22 +298,23 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(o_done, (j - 1) & 1);   // O_{j-1} done: P buffer free, O stable
         fence_after();
       }
-      if (m_new != m_used) {
-        const float sc = (m_used == -FLT_MAX) ? 0.f : ex2(m_used - m_new);
-        l *= sc;
-        if (j > 0) {
+      // lazy rescale (per row); tcgen05.ld/st are warp-collective, so the TMEM
+      // pass runs for the whole warp when any of its rows needs it (sc = 1 else)
+      const bool need = m_new != m_used;
+      const float sc = need ? ((m_used == -FLT_MAX) ? 0.f : ex2(m_used - m_new)) : 1.f;
+      l *= sc;
+      m_used = m_new;
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
-          for (int ch = 0; ch < H / 32; ++ch) {
-            uint32_t r[32];
-            AS_TMEM_LD32(tl + 2 * BM + ch * 32, r);
-            AS_TMEM_WAIT_LD(r);
+        for (int ch = 0; ch < H / 32; ++ch) {
+          uint32_t r[32];
+          AS_TMEM_LD32(tl + 2 * BM + ch * 32, r);
+          AS_TMEM_WAIT_LD(r);
 #pragma unroll
-            for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * sc);
-            AS_TMEM_ST32(tl + 2 * BM + ch * 32, r);
-          }
-          tmem_wait_st();
+          for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * sc);
+          AS_TMEM_ST32(tl + 2 * BM + ch * 32, r);
         }
-        m_used = m_new;
+        tmem_wait_st();
       }
       l += rs;
 #pragma unroll
@@ -527,7 +528,9 @@ __global__ void __launch_bounds__(192, 1)
         if (lane == 0) mbar_arrive(g_full);
         ++gj;
       }
-      // ---- dW epilogue: thread = hidden unit j, loop over the block's classes
+      // ---- dW epilogue: thread = hidden unit j, loop over the block's classes.
+      // All loads of a 32-class chunk are issued before any use (latency hiding);
+      // the label term (R3) is applied from the label-sorted batch.
       mbar_wait(dw_full, kb & 1);
       fence_after();
 #pragma unroll 1
@@ -538,25 +541,37 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t r[32];
           AS_TMEM_LD32(tl + 2 * BM + half * BM + ch * 32, r);
           AS_TMEM_WAIT_LD(r);
-#pragma unroll 4
-          for (int k = 0; k < 32; ++k) {
-            const int cls = cb * BM + ch * 32 + k;
-            if (cls >= C) break;
-            float g = __uint_as_float(r[k]);
-            const int sg = cls_seg[cls];
-            if (sg >= 0) {
-              const int s0 = lseg_ptr[sg], s1 = lseg_ptr[sg + 1];
-              for (int u = s0; u < s1; ++u) {
-                const int rr = lrow[u];
-                const float kr = (float)(lab_ptr[rr + 1] - lab_ptr[rr]);
-                g -= Hf[(size_t)rr * H + j] * (invB / kr);
-              }
+          const int c0 = cb * BM + ch * 32;
+          const int my_seg = (c0 + lane < C) ? cls_seg[c0 + lane] : -1;
+          float w[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            w[k] = (c0 + k < C) ? W2T[(size_t)(c0 + k) * H + j] : 0.f;
+          unsigned any = __ballot_sync(0xffffffffu, my_seg >= 0);
+          while (any) {                       // classes of this chunk that carry labels
+            const int k = __ffs(any) - 1;
+            any &= any - 1;
+            const int sg = __shfl_sync(0xffffffffu, my_seg, k);
+            float corr = 0.f;
+            for (int u = lseg_ptr[sg]; u < lseg_ptr[sg + 1]; ++u) {
+              const int rr = lrow[u];
+              const float kr = (float)(lab_ptr[rr + 1] - lab_ptr[rr]);
+              corr += Hf[(size_t)rr * H + j] * (invB / kr);
             }
-            const size_t idx = (size_t)cls * H + j;
-            const float w = W2T[idx] - lr * g;
-            W2T[idx] = w;
-            W2b[idx] = __float2bfloat16_rn(w);
-            if (dbg_dW2T) dbg_dW2T[idx] = g;
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (q == k) r[q] = __float_as_uint(__uint_as_float(r[q]) - corr);
+          }
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            if (c0 + k < C) {
+              const float g = __uint_as_float(r[k]);
+              const size_t idx = (size_t)(c0 + k) * H + j;
+              const float nw = w[k] - lr * g;
+              W2T[idx] = nw;
+              W2b[idx] = __float2bfloat16_rn(nw);
+              if (dbg_dW2T) dbg_dW2T[idx] = g;
+            }
           }
         }
       }

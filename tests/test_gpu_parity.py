@@ -53,11 +53,11 @@ def _params(cfg, seed=3, bias=0.2):
     return p
 
 
-def _replica(cfg, p, ds, precision, lr=0.5, debug=True, b_min=None):
+def _replica(cfg, p, ds, precision, lr=0.5, debug=True, b_min=None, rank=0, world=1):
     from paper_2110_07029_b200.api import Replica
     return Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=b_min or max(1, cfg.b_max // 8),
                    max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
-                   lr0=lr, precision=precision, debug_grads=debug)
+                   lr0=lr, precision=precision, debug_grads=debug, rank=rank, world=world)
 
 
 def _f32(buf):
@@ -88,6 +88,8 @@ CASES = [
     (3000, 700, 256, 400, 130, 192),     # h = 256
     (500, 50, 128, 64, 1, 64),           # a single row, C < 128
     (1500, 2048, 128, 700, 512, 512),    # exact tiles
+    (4000, 30000, 128, 1200, 1024, 1024),  # multi-block pipelines: 13 class blocks per pass-1 CTA
+    (3000, 20000, 256, 800, 512, 512),   # h = 256, W ring wraps (2 stages)
 ]
 
 
@@ -160,6 +162,32 @@ def test_one_step_parity(gpu_lib, case, precision, tol):
     assert np.all(dnew["W1"][untouched] == 0)                  # untouched rows bit-identical
 
 
+@pytest.mark.parametrize("h", [128, 256])
+def test_bf16_online_softmax_rescale_paths(gpu_lib, h):
+    """b2 ramps up over the classes and the rows differ in scale, so the lazy
+    online-softmax rescale (pass 1) fires at different class blocks for
+    different rows of the same warp."""
+    d, C, n, B = 2500, 12000, 600, 384
+    cfg = _cfg(d, C, h, n, 512, seed=21)
+    ds = synthgen.make_dataset(cfg, n=n)
+    p = _params(cfg)
+    lay = synthgen.param_layout(d, C, h)
+    o, _ = lay["b2"]
+    p[o:o + C] = np.linspace(0.0, 40.0, C, dtype=np.float32)
+    o, _ = lay["W2T"]
+    p[o:o + C * h] *= np.float32(8.0)
+    rep = _replica(cfg, p, ds, "bf16")
+    sub = ds.rows(np.arange(B))
+    sub.val[:] = sub.val * np.repeat(np.linspace(0.2, 3.0, B), np.diff(sub.row_ptr)).astype(np.float32)
+    rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    loss = rep.train_step(want_loss=True)
+    ref = om.gradients_chunked(sub, otrain.unpack(p, d, C, h), chunk=64)
+    assert abs(loss - ref["loss"]) <= 2e-2 * abs(ref["loss"])
+    assert_close("LSE", _f32(rep.debug_get(1, 4 * B)) * LN2, ref["LSE"], 2e-2)
+    assert_close("dA", _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h), ref["dA"], 2e-2)
+    assert_close("dW2T", _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h), ref["dW2T"], 2e-2)
+
+
 def test_invalid_batch_is_rejected_without_state_change(gpu_lib):
     from paper_2110_07029_b200._lib import ASError
     cfg = _cfg(800, 300, 128, 100, 64)
@@ -220,7 +248,7 @@ def test_group_merge_parity(gpu_lib, precision):
     cfg = _cfg(1000, 500, 128, 200, 64)
     ds = synthgen.make_dataset(cfg, n=200)
     p = _params(cfg)
-    reps = [_replica(cfg, p, ds, precision, debug=False) for _ in range(3)]
+    reps = [_replica(cfg, p, ds, precision, debug=False, rank=i, world=3) for i in range(3)]
     for i, r in enumerate(reps):
         r.set_batch_sizes([64, 64, 64], [0.5, 0.5, 0.5])
         for k in range(i + 1):                                 # u = (1, 2, 3)
