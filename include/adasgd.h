@@ -220,6 +220,21 @@ int as_profile_read(as_ctx *ctx, double *ms_out, int64_t *calls_out,
  * T = A^T P^T  (i.e. T[j][n] = sum_r A[r][j] P[n][r]).  Synchronises. */
 int as_tc_selftest(const void *A, const void *B, float *S, float *O, float *T);
 
+/* Self-test of the TMEM-A tensor-core path (tests only): A, B DEVICE bf16
+ * [128][128]; A and P = bf16(A/4) are written row-per-lane into TMEM and
+ * V = A B^T, U = P B are computed with A from TMEM.  Synchronises. */
+int as_tc_selftest2(const void *A, const void *B, float *V, float *U);
+
+/* tcgen05 issue-rate micro-benchmark (tools only): one CTA issues `iters`
+ * groups of 128x128x128 bf16 MMAs (mode 0: K/K-major; 1: A MN-major; 2: B
+ * MN-major; 3: N = 256) and returns the elapsed SM cycles in *cycles. */
+int as_tc_bench(int32_t mode, int32_t iters, int64_t *cycles);
+
+/* Event log of the tcgen05 kernels (tools only; non-empty only in a build
+ * compiled with -DAS_TRACE): copies up to max_events {clock, code, tile}
+ * int64 triples to out, clears the log, returns the count (>= 0). */
+int as_trace_dump(int64_t *out, int32_t max_events);
+
 /* ---- scheduler (pure host functions, steps a1, a10, a14) --------------------- */
 typedef struct {        /* replay cost of a batch in picoseconds (R9):        */
   int64_t c0, c_row, c_nnz, num, den;  /* (c0 + c_row*rows + c_nnz*nnz)*num/den */

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libadasgd.so")
+LIB_PATH = os.environ.get("ADASGD_LIB", os.path.join(HERE, "libadasgd.so"))
 
 AS_OK, AS_E_INVALID, AS_E_CUDA, AS_E_NCCL, AS_E_OOM, AS_E_STATE = 0, -1, -2, -3, -4, -5
 AS_FP32, AS_BF16 = 0, 1
@@ -28,7 +28,7 @@ EXPORTS = [
     "as_train_step", "as_merge", "as_group_merge", "as_set_batch_sizes", "as_get_params",
     "as_set_params", "as_debug_get", "as_tc_selftest", "as_sched_route_replay", "as_sched_alg1",
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
-    "as_live_close", "as_profile", "as_profile_read",
+    "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -106,6 +106,9 @@ def load():
         "as_live_reset": [VP],
         "as_live_close": [VP, I32],
         "as_profile": [VP, I32],
+        "as_tc_bench": [I32, I32, P(I64)],
+        "as_tc_selftest2": [VP, VP, P(F), P(F)],
+        "as_trace_dump": [P(I64), I32],
         "as_profile_read": [VP, P(D), P(I64), P(I64)],
     }
     for name, args in sig.items():

@@ -167,3 +167,16 @@ def tc_selftest(A, B):
                                C.cast(C.c_void_p(O.data_ptr()), C.POINTER(C.c_float)),
                                C.cast(C.c_void_p(T.data_ptr()), C.POINTER(C.c_float))))
     return S, O, T
+
+
+def tc_selftest2(A, B):
+    """A, B: torch bf16 [128,128] -> (V = A B^T, U = bf16(A/4) B) via TMEM-A MMAs."""
+    torch = _torch()
+    lib = L.load()
+    V = torch.empty(128, 128, dtype=torch.float32, device=A.device)
+    U = torch.empty_like(V)
+    torch.cuda.synchronize()
+    L.check(lib.as_tc_selftest2(C.c_void_p(A.data_ptr()), C.c_void_p(B.data_ptr()),
+                                C.cast(C.c_void_p(V.data_ptr()), C.POINTER(C.c_float)),
+                                C.cast(C.c_void_p(U.data_ptr()), C.POINTER(C.c_float))))
+    return V, U

@@ -10,6 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libadasgd.so")
+OUT_TRACE = os.path.join(HERE, "libadasgd_trace.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
@@ -25,17 +26,18 @@ def _needs_build():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False, jobs=5):
-    if not force and not _needs_build():
+def build(force=False, verbose=False, jobs=5, trace=False):
+    out = OUT_TRACE if trace else OUT
+    if not force and not trace and not _needs_build():
         return OUT
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build_trace" if trace else "build")
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         objs.append(obj)
-        cmd = [NVCC] + ARCH + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + ARCH + FLAGS + (["-DAS_TRACE"] if trace else []) + ["-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         else:
@@ -43,19 +45,18 @@ def build(force=False, verbose=False, jobs=5):
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     failed = False
     for src, p in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0 or verbose:
-            sys.stderr.write(out.decode())
+            sys.stderr.write(log.decode())
         if p.returncode != 0:
             failed = True
             sys.stderr.write("nvcc failed on %s\n" % src)
     if failed:
         raise RuntimeError("build failed")
-    link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs + ["-lnccl", "-lrt"]
+    link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs + ["-lnccl", "-lrt"]
     subprocess.check_call(link)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

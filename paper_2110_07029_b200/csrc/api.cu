@@ -62,6 +62,7 @@ struct as_ctx {
   int32_t *fseg_id, *fseg_ptr, *fseg_row, *long_list;
   float *fseg_val;
   int32_t *lseg_id, *lseg_ptr, *lseg_row, *cls_seg;
+  float *lw;
   float *Hf;
   __nv_bfloat16 *Hb;
   float *dA, *lse2, *zsum, *labW, *lossr, *loss;
@@ -131,7 +132,7 @@ Dims dims_of(const as_config *c) {
   D.nnz_cap = c->b_max * c->max_row_nnz;
   D.lab_cap = c->b_max * c->max_row_labels;
   D.sort_cap = std::max(D.nnz_cap, D.lab_cap);
-  D.max_splits = as::tc_splits(D.h, D.b_max, D.C, 160);  // >= CTAs of pass 1
+  D.max_splits = 2 * as::tc_splits(D.h, D.b_max, D.C, 160);  // partial slots (2 per pass-1 CTA)
   D.splitk = (int)std::min<long long>(64, std::max<long long>(1, D.C / 4096));
   return D;
 }
@@ -173,6 +174,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.lab_cap + 1)); if (x) x->lseg_ptr = (int32_t *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_row = (int32_t *)p;
+  p = P(4 * (size_t)D.lab_cap); if (x) x->lw = (float *)p;
   p = P(4 * D.C); if (x) x->cls_seg = (int32_t *)p;
   p = P(4 * (size_t)D.bpad * D.h); if (x) x->Hf = (float *)p;
   p = P(2 * (size_t)D.bpad * D.h); if (x) x->Hb = (__nv_bfloat16 *)p;
@@ -506,7 +508,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
 
   // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2)
   ph_begin(x, AS_PH_TRANSPOSE);
-  x->launches += n_transpose_launches(key_bits(D.d)) + n_transpose_launches(key_bits(D.C)) + 1;
+  x->launches += n_transpose_launches(key_bits(D.d)) + n_transpose_launches(key_bits(D.C)) + 2;
   as::launch_transpose(s, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->fseg_id,
                        x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val);
@@ -514,6 +516,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->lseg_id,
                        x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr);
   as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
+  as::launch_label_weights(s, d, D.lab_cap, x->lseg_row, x->lab_ptr, x->lw);
   ph_end(x, AS_PH_TRANSPOSE);
   // a4: SpMM forward
   ph_begin(x, AS_PH_SPMM);
@@ -537,9 +540,9 @@ int as_train_step(as_ctx *x, float *loss_out) {
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
     ph_begin(x, AS_PH_OUT_BWD);
     x->launches += 1;
-    as::launch_out_bwd_tc(s, x->plan, d, x->lse2, b2, x->cls_seg, x->lseg_ptr, x->lseg_row,
-                          x->lab_ptr, x->Hf, W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
-                          dbg ? x->dbg_db2 : nullptr, nullptr);
+    as::launch_out_bwd_tc(s, x->plan, d, x->lse2, x->cls_seg, x->lseg_ptr, x->lseg_row, x->lw,
+                          W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
+                          dbg ? x->dbg_db2 : nullptr);
     ph_end(x, AS_PH_OUT_BWD);
   } else {
     // fp32 parity mode: logits materialised
@@ -793,6 +796,27 @@ int as_profile_read(as_ctx *x, double *ms_out, int64_t *calls_out, int64_t *laun
   if (calls_out) std::copy(calls, calls + AS_PH_COUNT, calls_out);
   if (launches_out) *launches_out = x->launches;
   x->launches = 0;
+  return AS_OK;
+}
+
+int as_trace_dump(int64_t *out, int32_t max_events) {
+  if (!out || max_events < 0) return as_fail(AS_E_INVALID, "bad arguments");
+  return as::tc_trace_dump((long long *)out, max_events);
+}
+
+int as_tc_bench(int32_t mode, int32_t iters, int64_t *cycles) {
+  if (!cycles || mode < 0 || mode > 7 || iters < 1) return as_fail(AS_E_INVALID, "bad arguments");
+  long long c = 0;
+  if (as::tc_bench(mode, iters, &c) != 0) return as_fail(AS_E_CUDA, "tc_bench failed");
+  *cycles = c;
+  return AS_OK;
+}
+
+int as_tc_selftest2(const void *A, const void *B, float *V, float *U) {
+  if (!A || !B || !V || !U) return as_fail(AS_E_INVALID, "NULL argument");
+  if (as::tc_selftest2(A, B, V, U, 0) != 0) return as_fail(AS_E_CUDA, "tensor map creation failed");
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return as_fail(AS_E_CUDA, "selftest2: %s", cudaGetErrorString(e));
   return AS_OK;
 }
 

@@ -111,14 +111,19 @@ int tc_splits(int h, int b_max, long long C, int num_sms);
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
                        const float *b2, float *pm, float *pl, float *pO);
 int tc_fwd_splits_host(const TcPlan *plan, int B);
+int tc_bench(int mode, int iters, long long *cycles_host);
+int tc_selftest2(const void *A, const void *B, float *V, float *U, cudaStream_t s);
+int tc_trace_dump(long long *out, int max_events);
 int tc_selftest(const void *A, const void *B, float *S, float *O, float *T, cudaStream_t s);
 void launch_gemm_f32_kdev(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
                           long long sak, const float *B, long long sbk, long long sbn, float *Cm,
                           long long ldc, const int *K_dev);
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
-                       const float *lse2, const float *b2_in, const int32_t *cls_seg,
-                       const int32_t *lseg_ptr, const int32_t *lrow, const int64_t *lab_ptr,
-                       const float *Hf, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
-                       float *dbg_dW2T, float *dbg_db2, float *db2_tmp);
+                       const float *lse2, const int32_t *cls_seg, const int32_t *lseg_ptr,
+                       const int32_t *lrow, const float *lw, float *W2T, float *b2,
+                       __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2);
+// per label entry of the label-sorted batch: lw[u] = 1 / (k_r B), r = lrow[u]  (R3)
+void launch_label_weights(cudaStream_t s, const StepDesc *desc, int cap, const int32_t *lrow,
+                          const int64_t *lab_ptr, float *lw);
 
 }  // namespace as

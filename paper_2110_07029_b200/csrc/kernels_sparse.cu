@@ -352,6 +352,20 @@ void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, in
   k_seg_write<<<g, 256, 0, s>>>(ki, flags, idx, n_dev, seg_id, seg_ptr, nseg_dev);
 }
 
+// lw[u] = 1 / (k_r B) for label entry u of the label-sorted batch (R3)
+__global__ void k_label_weights(const StepDesc *__restrict__ desc, const int32_t *__restrict__ lrow,
+                                const int64_t *__restrict__ lab_ptr, float *__restrict__ lw) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= desc->nlab) return;
+  const int r = lrow[u];
+  lw[u] = (1.0f / (float)desc->rows) / (float)(lab_ptr[r + 1] - lab_ptr[r]);
+}
+
+void launch_label_weights(cudaStream_t s, const StepDesc *desc, int cap, const int32_t *lrow,
+                          const int64_t *lab_ptr, float *lw) {
+  k_label_weights<<<ceil_div(cap > 0 ? cap : 1, 256), 256, 0, s>>>(desc, lrow, lab_ptr, lw);
+}
+
 // class -> label-segment map (value_is_index=1) or reset to -1 (value_is_index=0)
 __global__ void k_class_map(const int32_t *__restrict__ lseg_id, const int *__restrict__ V_dev,
                             int32_t *__restrict__ cls_seg, int value_is_index) {

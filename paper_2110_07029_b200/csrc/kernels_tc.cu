@@ -32,6 +32,24 @@ constexpr int BM = 128;                 // rows per tile == classes per block
 constexpr int ATOM_BYTES = 128 * 128;   // one 64-col bf16 atom of a 128-row tile
 constexpr float LOG2E = 1.4426950408889634f;
 
+#ifdef AS_TRACE
+// event log of CTA 0 (trace builds only): per role {clock, event, tile}, plain
+// stores from one thread per role (no atomics on the timed path)
+__device__ long long g_trace[4][4096][3];
+__device__ int g_trace_n[4];
+#define TRACE_INIT int _trk = 0
+#define TRACE(role, cond, ev, tile)                                           \
+  do {                                                                        \
+    if ((cond) && blockIdx.x == 0 && _trk < 4096) {                          \
+      g_trace[role][_trk][0] = clock64(); g_trace[role][_trk][1] = (ev);      \
+      g_trace[role][_trk][2] = (tile); ++_trk; g_trace_n[role] = _trk;        \
+    }                                                                         \
+  } while (0)
+#else
+#define TRACE_INIT
+#define TRACE(role, cond, ev, tile) do {} while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -97,6 +115,43 @@ __device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A from TMEM (lane = row of A, two bf16 per 32-bit column along K), B from smem
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+}  // namespace tc
+#include "mma_groups.h"
+namespace tc {
+// Warp-converged variants: all 32 lanes execute the call, one elected lane
+// issues (no divergent single-lane region => no ELECT/branch loop per MMA).
+__device__ __forceinline__ void mma_ss_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -147,14 +202,16 @@ __device__ __forceinline__ uint32_t swz(int i, int c) {
 
 template <int H>
 struct FwdCfg {
-  static constexpr int NST = H == 128 ? 4 : 2;   // W stages
+  static constexpr int NST = H == 128 ? 4 : 2;    // W stages
   static constexpr int TILE = BM * H * 2;         // bytes of a 128 x H bf16 tile
-  static constexpr int SMEM = TILE /*H*/ + NST * TILE /*W*/ + BM * BM * 2 /*P*/ + 2 * BM * 4 +
-                              1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr int THREADS = 10 * 32;
+  static constexpr int SMEM = TILE /*H*/ + NST * TILE + 2 * 2 * BM * 4 /*b2*/ + 256;
+  static_assert(SMEM <= 232448, "pass-1 shared memory exceeds 227 KB");
+  static_assert(H == 128 || H == 256, "h");
 };
 
 // splits of the class range for pass 1 given the batch rows (same formula on
-// the device in the combine)
+// the host for the combine).  Every CTA writes 2 partial slots (one per WG).
 __host__ __device__ inline int fwd_splits(int B, int n_cblocks, int num_ctas, int max_splits) {
   const int RT = (B + BM - 1) / BM;
   int s = num_ctas / (RT > 0 ? RT : 1);
@@ -164,26 +221,36 @@ __host__ __device__ inline int fwd_splits(int B, int n_cblocks, int num_ctas, in
 }
 
 // =====================================================================
-// pass 1
+// pass 1 (v3: ping-pong warpgroups)
+//   warps 0-7  softmax: WG g handles the class blocks j with j % 2 == g of this
+//              CTA's range, with its own online-softmax state (log2 units, lazy
+//              rescale) and its own O accumulator; thread = row = TMEM lane.
+//              P is written back into TMEM over the S it came from.
+//   warp 8     TMA producer (H tile once, W2T class blocks)
+//   warp 9     MMA issuer + TMEM owner:
+//                S_j   = H . W2T_blk^T        (SS, TMEM buffer j % 2)
+//                O_g  += P_j . W2T_blk        (A = P from TMEM, B MN-major)
+// TMEM: S[2] at columns 0, 128; O[2] at 256, 384 (h = 128; h = 256 uses one
+// WG and O at 256..511).  Partial slot of (CTA split sp, WG g) = 2 sp + g.
 // =====================================================================
 template <int H>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     k_out_fwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
-              const StepDesc *__restrict__ desc, const float *__restrict__ b2, int C,
-              int n_cblocks, int max_splits, int bpad, float *__restrict__ pm,
-              float *__restrict__ pl, float *__restrict__ pO) {
+              const StepDesc *__restrict__ desc, const __nv_bfloat16 *__restrict__ Hb,
+              const float *__restrict__ b2, int C, int n_cblocks, int max_splits, int bpad,
+              float *__restrict__ pm, float *__restrict__ pl, float *__restrict__ pO) {
   using Cfg = FwdCfg<H>;
   constexpr int NST = Cfg::NST, TILE = Cfg::TILE;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t *sH = sm;
-  uint8_t *sW = sH + TILE;
-  uint8_t *sP = sW + NST * TILE;
-  float *sB2 = (float *)(sP + BM * BM * 2);
-  uint64_t *bars = (uint64_t *)(sB2 + 2 * BM);
+  constexpr int NWG = H == 128 ? 2 : 1;             // softmax warpgroups (O accumulators)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sH = smem_raw;
+  uint8_t *sW = smem_raw + TILE;
+  float *sB2 = (float *)(sW + NST * TILE);          // [2 WG][2][128]
+  uint64_t *bars = (uint64_t *)(sB2 + 4 * BM);
   uint64_t *h_full = bars, *w_full = bars + 1, *w_empty = w_full + NST, *s_full = w_empty + NST,
-           *s_empty = s_full + 2, *p_full = s_empty + 2, *o_done = p_full + 1;
+           *p_full = s_full + 2, *o_fin = p_full + 2, *o_done = o_fin + 1;
   uint32_t *tmem_slot = (uint32_t *)(o_done + 1);
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
 
   const int B = desc->rows;
   const int RT = (B + BM - 1) / BM;
@@ -193,22 +260,23 @@ __global__ void __launch_bounds__(192, 1)
   const int cb0 = (int)((long long)sp * n_cblocks / splits);
   const int nloc = (int)((long long)(sp + 1) * n_cblocks / splits) - cb0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kProdWarp = 8, kMmaWarp = 9;   // highest ids: scheduler priority
 
   if (threadIdx.x == 0) {
     mbar_init(h_full, 1);
     for (int i = 0; i < NST; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4); }
-    mbar_init(p_full, 4);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+    mbar_init(o_fin, 1);
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     if (lane == 0) {  // ---------------- TMA producer
       mbar_expect_tx(h_full, TILE);
       for (int a = 0; a < H / 64; ++a) tma_load_2d(&mapH, h_full, sH + a * ATOM_BYTES, a * 64, rt * BM);
@@ -220,82 +288,80 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_2d(&mapW, &w_full[st], sW + st * TILE + a * ATOM_BYTES, a * 64, (cb0 + j) * BM);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+  } else if (warp == kMmaWarp) {
+    {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
       constexpr uint32_t idS = idesc_bf16(BM, BM, 0, 0);
       constexpr uint32_t idO = idesc_bf16(BM, H, 0, 1);
-      const uint32_t aH = smem_u32(sH), aW = smem_u32(sW), aP = smem_u32(sP);
+      const uint32_t aH = smem_u32(sH), aW = smem_u32(sW);
       mbar_wait(h_full, 0);
       fence_after();
+      const uint64_t dH = sdesc(aH, 16, 1024);
       auto issue_S = [&](int j) {
         const int st = j % NST, b = j & 1;
         mbar_wait(&w_full[st], (j / NST) & 1);
-        if (j >= 2) mbar_wait(&s_empty[b], ((j >> 1) - 1) & 1);
         fence_after();
-#pragma unroll
-        for (int kk = 0; kk < H / 16; ++kk)
-          mma_bf16(tmem + b * BM, desc_k(aH, kk), desc_k(aW + st * TILE, kk), idS, kk > 0);
-        mma_commit(&s_full[b]);
+        // S_j overwrites buffer b; O of block j-2 (the last reader of P_{j-2}
+        // there) was issued earlier by this warp: tcgen05.mma executes in order.
+        if constexpr (H == 128)
+          mma_grp_ss_kk_8(tmem + b * BM, dH, sdesc(aW + st * TILE, 16, 1024), idS, 0u);
+        else
+          mma_grp_ss_kk_16(tmem + b * BM, dH, sdesc(aW + st * TILE, 16, 1024), idS, 0u);
+        mma_commit_w(&s_full[b]);
       };
       if (nloc > 0) issue_S(0);
+      if (nloc > 1) issue_S(1);
       for (int j = 0; j < nloc; ++j) {
-        if (j + 1 < nloc) issue_S(j + 1);
-        mbar_wait(p_full, j & 1);
+        const int st = j % NST, b = j & 1;
+        const int g = NWG == 2 ? b : 0;
+        mbar_wait(&p_full[b], (j >> 1) & 1);
         fence_after();
-        const int st = j % NST;
-#pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk)
-          mma_bf16(tmem + 2 * BM, desc_k(aP, kk), desc_mn(aW + st * TILE, kk), idO,
-                   (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&w_empty[st]);
-        mma_commit(o_done);
+        mma_grp_ts_mn_8(tmem + 2 * BM + g * BM, tmem + b * BM, sdesc(aW + st * TILE, ATOM_BYTES, 1024),
+                        idO, j >= NWG ? 1u : 0u);
+        mma_commit_w(&w_empty[st]);
+        if (NWG == 1) mma_commit_w(o_done);     // single WG: O_{j} before the rescale at j+1
+        if (j + 2 < nloc) issue_S(j + 2);
       }
+      mma_commit_w(o_fin);
     }
-  } else {  // ---------------- softmax / epilogue warps (one thread per row)
+  } else if (warp < 4 * NWG) {  // ---------------- softmax warpgroups (thread = row)
+    const int g = warp >> 2;
     const int q = warp & 3;
-    const int e = threadIdx.x - 64;           // 0..127 loader index
-    const int row = q * 32 + lane;            // TMEM lane == tile row
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t aP = smem_u32(sP);
+    const int row = q * 32 + lane;            // TMEM lane == tile row == loader index
+    const uint32_t tlq = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t tO = tlq + 2 * BM + g * BM;
     float m_used = -FLT_MAX, l = 0.f;
-    for (int j = 0; j < nloc; ++j) {
-      const int cb = cb0 + j;
-      {
-        const int c = cb * BM + e;
-        sB2[(j & 1) * BM + e] = c < C ? b2[c] * LOG2E : -INFINITY;
+    float b2n = 0.f;                          // prefetched b2 of this WG's next class block
+    if (g < nloc) { const int c = (cb0 + g) * BM + row; b2n = c < C ? b2[c] * LOG2E : -INFINITY; }
+    int jj = 0;                               // blocks processed by this WG
+    for (int j = g; j < nloc; j += NWG, ++jj) {
+      const int b = j & 1;
+      float *myB2 = sB2 + (g * 2 + (jj & 1)) * BM;
+      myB2[row] = b2n;
+      if (j + NWG < nloc) {
+        const int c = (cb0 + j + NWG) * BM + row;
+        b2n = c < C ? b2[c] * LOG2E : -INFINITY;
       }
-      named_bar(1, 128);
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      named_bar(1 + g, 128);
+      // s_full(j) also implies that the O MMA of this WG's previous block (issued
+      // before S_j) completed: O is stable and the P region of buffer b is free.
+      mbar_wait(&s_full[b], (j >> 1) & 1);
       fence_after();
-      float v[BM];
+      const uint32_t tS = tlq + b * BM;
+      const float *bb = myB2;
+      // pass A: block max (log2 units)
+      float mx = -FLT_MAX;
 #pragma unroll
       for (int ch = 0; ch < BM / 32; ++ch) {
         uint32_t r[32];
-        AS_TMEM_LD32(tl + (j & 1) * BM + ch * 32, r);
+        AS_TMEM_LD32(tS + ch * 32, r);
         AS_TMEM_WAIT_LD(r);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v[ch * 32 + k] = __uint_as_float(r[k]);
-      }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[j & 1]);
-      float mx = -FLT_MAX;
-      const float *bb = sB2 + (j & 1) * BM;
-#pragma unroll
-      for (int k = 0; k < BM; ++k) {
-        v[k] = fmaf(v[k], LOG2E, bb[k]);
-        mx = fmaxf(mx, v[k]);
+        for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fmaf(__uint_as_float(r[k]), LOG2E, bb[ch * 32 + k]));
       }
       float m_new = m_used;
       if (mx > m_used + 8.f) m_new = mx;   // lazy rescale: p <= 2^8 otherwise
-      float rs = 0.f;
-#pragma unroll
-      for (int k = 0; k < BM; ++k) {
-        v[k] = ex2(v[k] - m_new);
-        rs += v[k];
-      }
-      if (j > 0) {
-        mbar_wait(o_done, (j - 1) & 1);   // O_{j-1} done: P buffer free, O stable
+      if (NWG == 1 && jj > 0) {               // single WG: O of block j-1 must be done
+        mbar_wait(o_done, (jj - 1) & 1);
         fence_after();
       }
       // lazy rescale (per row); tcgen05.ld/st are warp-collective, so the TMEM
@@ -304,113 +370,150 @@ __global__ void __launch_bounds__(192, 1)
       const float sc = need ? ((m_used == -FLT_MAX) ? 0.f : ex2(m_used - m_new)) : 1.f;
       l *= sc;
       m_used = m_new;
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
+      if (jj > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
         for (int ch = 0; ch < H / 32; ++ch) {
           uint32_t r[32];
-          AS_TMEM_LD32(tl + 2 * BM + ch * 32, r);
+          AS_TMEM_LD32(tO + ch * 32, r);
           AS_TMEM_WAIT_LD(r);
 #pragma unroll
           for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * sc);
-          AS_TMEM_ST32(tl + 2 * BM + ch * 32, r);
+          AS_TMEM_ST32(tO + ch * 32, r);
         }
-        tmem_wait_st();
+      }
+      // pass B: P = 2^(s - m) chunk by chunk, packed bf16 written over the S
+      // columns already consumed (chunk ch -> columns [16ch, 16ch + 16))
+      float rs = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < BM / 32; ++ch) {
+        uint32_t r[32];
+        AS_TMEM_LD32(tS + ch * 32, r);
+        AS_TMEM_WAIT_LD(r);
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const float p0 = ex2(fmaf(__uint_as_float(r[2 * u]), LOG2E, bb[ch * 32 + 2 * u]) - m_new);
+          const float p1 = ex2(fmaf(__uint_as_float(r[2 * u + 1]), LOG2E, bb[ch * 32 + 2 * u + 1]) - m_new);
+          rs += p0 + p1;
+          pk[u] = pack_bf16x2(p0, p1);
+        }
+        AS_TMEM_ST16(tS + ch * 16, pk);
       }
       l += rs;
-#pragma unroll
-      for (int c = 0; c < BM / 8; ++c)
-        st_shared_v4(aP + swz(row, c), pack_bf16x2(v[8 * c], v[8 * c + 1]),
-                     pack_bf16x2(v[8 * c + 2], v[8 * c + 3]), pack_bf16x2(v[8 * c + 4], v[8 * c + 5]),
-                     pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
-      fence_proxy_async();
+      tmem_wait_st();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[b]);
     }
-    // epilogue: partials of this split
+    // epilogue: the partial slot (sp, g)
     const int grow = rt * BM + row;
-    if (nloc > 0) {
-      mbar_wait(o_done, (nloc - 1) & 1);
+    const size_t slot = (size_t)sp * 2 + g;
+    if (jj > 0) {
+      mbar_wait(o_fin, 0);
       fence_after();
 #pragma unroll 1
       for (int ch = 0; ch < H / 32; ++ch) {
         uint32_t r[32];
-        AS_TMEM_LD32(tl + 2 * BM + ch * 32, r);
+        AS_TMEM_LD32(tO + ch * 32, r);
         AS_TMEM_WAIT_LD(r);
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          pO[((size_t)sp * H + ch * 32 + k) * bpad + grow] = __uint_as_float(r[k]);
+        for (int k = 0; k < 32; ++k) pO[(slot * H + ch * 32 + k) * bpad + grow] = __uint_as_float(r[k]);
       }
     } else {
-      for (int k = 0; k < H; ++k) pO[((size_t)sp * H + k) * bpad + grow] = 0.f;
+      for (int k = 0; k < H; ++k) pO[(slot * H + k) * bpad + grow] = 0.f;
     }
-    pm[(size_t)sp * bpad + grow] = m_used;
-    pl[(size_t)sp * bpad + grow] = l;
+    pm[slot * bpad + grow] = m_used;
+    pl[slot * bpad + grow] = l;
+  } else if (NWG == 1 && warp < 8) {          // h = 256: idle second WG fills its empty slot
+    const int q = warp & 3;
+    const int grow = rt * BM + q * 32 + lane;
+    const size_t slot = (size_t)sp * 2 + 1;
+    for (int k = 0; k < H; ++k) pO[(slot * H + k) * bpad + grow] = 0.f;
+    pm[slot * bpad + grow] = -FLT_MAX;
+    pl[slot * bpad + grow] = 0.f;
   }
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
-// =====================================================================
-// pass 2
-// =====================================================================
 template <int H>
 struct BwdCfg {
-  static constexpr int NW = H == 128 ? 2 : 1;    // W2T block buffers
-  static constexpr int NSH = 2 + (H == 128);      // H tile stages
+  static constexpr int NW = H == 128 ? 2 : 1;     // W2T block buffers
+  static constexpr int NSH = H == 128 ? 4 : 2;    // H tile stages (TMA latency off the chain)
+  static constexpr int NDW = H == 128 ? 2 : 1;    // dW2T accumulators in TMEM
   static constexpr int TILE = BM * H * 2;
-  static constexpr int SMEM = NW * TILE + NSH * TILE + BM * BM * 2 /*G*/ + 2 * BM * 4 /*lse*/ +
-                              1024 + 1024;
+  static constexpr int THREADS = 14 * 32;
+  static constexpr int TSTAGE = BM * 36 * 4;      // update-warp transpose stage (16-B rows)
+  static constexpr int SMEM = NW * TILE + NSH * TILE + TSTAGE + 4 * BM * 4 /*lse*/ +
+                              2 * BM * 4 /*db2*/ + 256 /*barriers*/;
+  static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
 };
 
+// =====================================================================
+// pass 2 (v3: G^T lives in TMEM)
+//   warps 0-7   softmax: two warpgroups ping-pong over the S^T tiles (WG g takes
+//               tiles t with t % 2 == g, i.e. S buffer g); thread = class (TMEM
+//               lane).  G^T = softmax^T / B is written back into TMEM over the
+//               S^T columns it came from.
+//   warps 8-11  update: dW2T (lane = class) -> smem transpose -> fused SGD of
+//               W2T and the bf16 shadow (coalesced); db2, b2.
+// The label term of R3 (-1/(k_r B) at the row's labels) is folded into G^T by
+// the softmax threads, so the MMA produces the complete gradient.
+//   warp 12     TMA producer (W2T block, H row tiles)
+//   warp 13     MMA issuer + TMEM owner:
+//                 S^T_t  = W2T_blk . H_t^T          (SS, TMEM cols 128*b)
+//                 dW2T  += G^T_t . H_t              (A = G^T from TMEM, B MN-major)
+// =====================================================================
 template <int H>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
               const StepDesc *__restrict__ desc, const float *__restrict__ lse2, int C,
               int n_cblocks, const int32_t *__restrict__ cls_seg,
               const int32_t *__restrict__ lseg_ptr, const int32_t *__restrict__ lrow,
-              const int64_t *__restrict__ lab_ptr, const float *__restrict__ Hf,
-              float *__restrict__ W2T, float *__restrict__ b2, __nv_bfloat16 *__restrict__ W2b,
-              float lr, float *__restrict__ dbg_dW2T, float *__restrict__ dbg_db2) {
+              const float *__restrict__ lw, float *__restrict__ W2T, float *__restrict__ b2,
+              __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
+              float *__restrict__ dbg_db2) {
   using Cfg = BwdCfg<H>;
-  constexpr int NW = Cfg::NW, NSH = Cfg::NSH, TILE = Cfg::TILE;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t *sW = sm;
+  constexpr int NW = Cfg::NW, NSH = Cfg::NSH, NDW = Cfg::NDW, TILE = Cfg::TILE;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sW = smem_raw;
   uint8_t *sHt = sW + NW * TILE;
-  uint8_t *sG = sHt + NSH * TILE;
-  float *sL = (float *)(sG + BM * BM * 2);
-  uint64_t *bars = (uint64_t *)(sL + 2 * BM);
+  float *sT = (float *)(sHt + NSH * TILE);      // [128][36] transpose stage
+  float *sL = sT + BM * 36;                     // [2 WG][2][128] lse of the WG's tiles
+  float *sDB = sL + 4 * BM;                     // [2][128] db2 partials of the two WGs
+  uint64_t *bars = (uint64_t *)(sDB + 2 * BM);
   uint64_t *w_full = bars, *w_empty = w_full + NW, *h_full = w_empty + NW, *h_empty = h_full + NSH,
-           *s_full = h_empty + NSH, *s_empty = s_full + 2, *g_full = s_empty + 2,
-           *g_empty = g_full + 1, *dw_full = g_empty + 1, *dw_empty = dw_full + 1;
-  uint32_t *tmem_slot = (uint32_t *)(dw_empty + 1);
+           *s_full = h_empty + NSH, *p_full = s_full + 2, *dw_full = p_full + 2,
+           *dw_empty = dw_full + NDW, *db_full = dw_empty + NDW, *db_empty = db_full + 1;
+  uint32_t *tmem_slot = (uint32_t *)(db_empty + 1);
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
 
   const int B = desc->rows;
   const int RT = (B + BM - 1) / BM;
   const float invB = 1.0f / (float)B;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kProdWarp = 12, kMmaWarp = 13;   // highest ids: scheduler priority
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NW; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
     for (int i = 0; i < NSH; ++i) { mbar_init(&h_full[i], 1); mbar_init(&h_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4); }
-    mbar_init(g_full, 4);
-    mbar_init(g_empty, 1);
-    mbar_init(dw_full, 1);
-    mbar_init(dw_empty, 4);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+    for (int i = 0; i < NDW; ++i) { mbar_init(&dw_full[i], 1); mbar_init(&dw_empty[i], 4); }
+    mbar_init(db_full, 8);
+    mbar_init(db_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     if (lane == 0) {  // ---------------- TMA producer
+      TRACE_INIT;
       int kb = 0, it = 0;
       for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
         const int wb = kb % NW;
@@ -421,180 +524,234 @@ __global__ void __launch_bounds__(192, 1)
         for (int t = 0; t < RT; ++t, ++it) {
           const int st = it % NSH;
           if (it >= NSH) mbar_wait(&h_empty[st], ((it / NSH) - 1) & 1);
+          TRACE(2, true, 10, t);
           mbar_expect_tx(&h_full[st], TILE);
           for (int a = 0; a < H / 64; ++a)
             tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+  } else if (warp == kMmaWarp) {
+    {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
       constexpr uint32_t idS = idesc_bf16(BM, BM, 0, 0);   // S^T = W2T_blk . H_t^T
-      constexpr uint32_t idW = idesc_bf16(BM, BM, 1, 0);   // dW^T += H_t^T . G^T^T
-      const uint32_t aW = smem_u32(sW), aH = smem_u32(sHt), aG = smem_u32(sG);
-      int kb = 0, it = 0, sj = 0, gj = 0;
-      auto do_dw = [&](int t, int st) {
-        mbar_wait(g_full, gj & 1);
-        if (t == 0 && kb >= 1) mbar_wait(dw_empty, (kb - 1) & 1);
+      constexpr uint32_t idW = idesc_bf16(BM, H, 0, 1);    // dW2T += G^T . H_t
+      const uint32_t aW = smem_u32(sW), aH = smem_u32(sHt);
+      int kb = 0, it = 0, sj = 0;
+      TRACE_INIT;
+      auto do_dw = [&](int t, int st, int sjt) {
+        const int b = sjt & 1, db = kb % NDW;
+        TRACE(0, lane == 0, 1, t);
+        mbar_wait(&p_full[b], (sjt >> 1) & 1);
+        TRACE(0, lane == 0, 2, t);
+        if (t == 0 && kb >= NDW) mbar_wait(&dw_empty[db], ((kb / NDW) - 1) & 1);
         fence_after();
-#pragma unroll
-        for (int half = 0; half < H / 128; ++half)
-#pragma unroll
-          for (int kk = 0; kk < BM / 16; ++kk)
-            mma_bf16(tmem + 2 * BM + half * BM, desc_mn(aH + st * TILE + half * 2 * ATOM_BYTES, kk),
-                     desc_k(aG, kk), idW, (t > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&h_empty[st]);
-        mma_commit(g_empty);
-        ++gj;
+        mma_grp_ts_mn_8(tmem + 2 * BM + db * BM, tmem + b * BM,
+                        sdesc(aH + st * TILE, ATOM_BYTES, 1024), idW, t > 0 ? 1u : 0u);
+        mma_commit_w(&h_empty[st]);
       };
       for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
         const int wb = kb % NW;
         mbar_wait(&w_full[wb], (kb / NW) & 1);
+        const uint64_t dW = sdesc(aW + wb * TILE, 16, 1024);
         int st_prev = 0;
         for (int t = 0; t < RT; ++t, ++it) {
           const int st = it % NSH, b = sj & 1;
+          TRACE(0, lane == 0, 3, t);
           mbar_wait(&h_full[st], (it / NSH) & 1);
-          if (sj >= 2) mbar_wait(&s_empty[b], ((sj >> 1) - 1) & 1);
+          TRACE(0, lane == 0, 5, t);
           fence_after();
-#pragma unroll
-          for (int kk = 0; kk < H / 16; ++kk)
-            mma_bf16(tmem + b * BM, desc_k(aW + wb * TILE, kk), desc_k(aH + st * TILE, kk), idS,
-                     kk > 0);
-          mma_commit(&s_full[b]);
+          // S^T_t overwrites buffer b: the previous user (dW of tile t-2, which
+          // read its G^T there) was issued earlier by this warp (in order).
+          if constexpr (H == 128)
+            mma_grp_ss_kk_8(tmem + b * BM, dW, sdesc(aH + st * TILE, 16, 1024), idS, 0u);
+          else
+            mma_grp_ss_kk_16(tmem + b * BM, dW, sdesc(aH + st * TILE, 16, 1024), idS, 0u);
+          mma_commit_w(&s_full[b]);
           ++sj;
-          if (t == RT - 1) mma_commit(&w_empty[wb]);
-          if (t > 0) do_dw(t - 1, st_prev);
+          if (t == RT - 1) mma_commit_w(&w_empty[wb]);
+          if (t > 0) do_dw(t - 1, st_prev, sj - 2);
           st_prev = st;
         }
-        do_dw(RT - 1, st_prev);
-        mma_commit(dw_full);
+        do_dw(RT - 1, st_prev, sj - 1);
+        mma_commit_w(&dw_full[kb % NDW]);
       }
     }
-  } else {  // ---------------- epilogue warps
+  } else if (warp < 8) {  // ---------------- softmax warpgroups (ping-pong over tiles)
+    const int g = warp >> 2;                  // WG g takes the tiles with sj % 2 == g (S buffer g)
     const int q = warp & 3;
-    const int e = threadIdx.x - 64;
-    const int i = q * 32 + lane;                       // TMEM lane
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t aG = smem_u32(sG);
-    int kb = 0, sj = 0, gj = 0;
+    const int i = q * 32 + lane;              // class inside the block (TMEM lane) == loader index
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + g * BM;
+    const float log2B = __log2f((float)B);
+    int kb = 0, sj = 0;
+    TRACE_INIT;
+    // lse prefetch (log2 units, 1/B folded in): thread i owns row i of the WG's next tile
+    float nxt = 0.f;
+    {
+      const int t0 = g < RT ? g : (g - RT) % RT;   // first tile index this WG will see
+      const int r = t0 * BM + i;
+      nxt = r < B ? lse2[r] + log2B : INFINITY;
+    }
     for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
       const int c = cb * BM + i;
       const bool cvalid = c < C;
-      const float b2c = cvalid ? b2[c] * LOG2E : 0.f;
+      const float b2c = cvalid ? b2[c] * LOG2E : -INFINITY;   // invalid class -> p = 0
       float db2 = 0.f;
-      for (int t = 0; t < RT; ++t) {
-        const int b = sj & 1;
-        {
-          const int r = t * BM + e;
-          sL[b * BM + e] = r < B ? lse2[r] : INFINITY;
-        }
-        named_bar(1, 128);
-        mbar_wait(&s_full[b], (sj >> 1) & 1);
-        fence_after();
-        float v[BM];
-#pragma unroll
-        for (int ch = 0; ch < BM / 32; ++ch) {
-          uint32_t r[32];
-          AS_TMEM_LD32(tl + b * BM + ch * 32, r);
-          AS_TMEM_WAIT_LD(r);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) v[ch * 32 + k] = __uint_as_float(r[k]);
-        }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[b]);
-        ++sj;
-        const float *ls = sL + b * BM;
-        float rs = 0.f;
-#pragma unroll
-        for (int k = 0; k < BM; ++k) {
-          const float p = cvalid ? ex2(fmaf(v[k], LOG2E, b2c) - ls[k]) * invB : 0.f;
-          v[k] = p;
-          rs += p;
-        }
-        db2 += rs;
-        if (gj >= 1) {
-          mbar_wait(g_empty, (gj - 1) & 1);
-        }
-#pragma unroll
-        for (int cc = 0; cc < BM / 8; ++cc)
-          st_shared_v4(aG + swz(i, cc), pack_bf16x2(v[8 * cc], v[8 * cc + 1]),
-                       pack_bf16x2(v[8 * cc + 2], v[8 * cc + 3]),
-                       pack_bf16x2(v[8 * cc + 4], v[8 * cc + 5]),
-                       pack_bf16x2(v[8 * cc + 6], v[8 * cc + 7]));
-        fence_proxy_async();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(g_full);
-        ++gj;
-      }
-      // ---- dW epilogue: thread = hidden unit j, loop over the block's classes.
-      // All loads of a 32-class chunk are issued before any use (latency hiding);
-      // the label term (R3) is applied from the label-sorted batch.
-      mbar_wait(dw_full, kb & 1);
-      fence_after();
-#pragma unroll 1
-      for (int half = 0; half < H / 128; ++half) {
-        const int j = half * BM + i;
-#pragma unroll 1
-        for (int ch = 0; ch < BM / 32; ++ch) {
-          uint32_t r[32];
-          AS_TMEM_LD32(tl + 2 * BM + half * BM + ch * 32, r);
-          AS_TMEM_WAIT_LD(r);
-          const int c0 = cb * BM + ch * 32;
-          const int my_seg = (c0 + lane < C) ? cls_seg[c0 + lane] : -1;
-          float w[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k)
-            w[k] = (c0 + k < C) ? W2T[(size_t)(c0 + k) * H + j] : 0.f;
-          unsigned any = __ballot_sync(0xffffffffu, my_seg >= 0);
-          while (any) {                       // classes of this chunk that carry labels
-            const int k = __ffs(any) - 1;
-            any &= any - 1;
-            const int sg = __shfl_sync(0xffffffffu, my_seg, k);
-            float corr = 0.f;
-            for (int u = lseg_ptr[sg]; u < lseg_ptr[sg + 1]; ++u) {
-              const int rr = lrow[u];
-              const float kr = (float)(lab_ptr[rr + 1] - lab_ptr[rr]);
-              corr += Hf[(size_t)rr * H + j] * (invB / kr);
-            }
-#pragma unroll
-            for (int q = 0; q < 32; ++q)
-              if (q == k) r[q] = __float_as_uint(__uint_as_float(r[q]) - corr);
-          }
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            if (c0 + k < C) {
-              const float g = __uint_as_float(r[k]);
-              const size_t idx = (size_t)(c0 + k) * H + j;
-              const float nw = w[k] - lr * g;
-              W2T[idx] = nw;
-              W2b[idx] = __float2bfloat16_rn(nw);
-              if (dbg_dW2T) dbg_dW2T[idx] = g;
-            }
-          }
-        }
-      }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dw_empty);
+      int lc = 0, le = 0, lnr = 0x7fffffff;
+      float lnw = 0.f;
       if (cvalid) {
         const int sg = cls_seg[c];
         if (sg >= 0) {
-          for (int u = lseg_ptr[sg]; u < lseg_ptr[sg + 1]; ++u) {
-            const int rr = lrow[u];
-            db2 -= invB / (float)(lab_ptr[rr + 1] - lab_ptr[rr]);
+          lc = lseg_ptr[sg]; le = lseg_ptr[sg + 1];
+          lnr = lrow[lc]; lnw = lw[lc];
+        }
+      }
+      for (int t = 0; t < RT; ++t, ++sj) {
+        if ((sj & 1) != g) continue;
+        float *myL = sL + (g * 2 + ((sj >> 1) & 1)) * BM;   // double-buffered per WG
+        myL[i] = nxt;
+        {  // prefetch the lse of this WG's next tile (global tile counter sj + 2)
+          int tn = t + 2, cbn = cb;
+          if (tn >= RT) { tn -= RT; cbn += gridDim.x; if (tn >= RT) tn %= RT; }
+          const int r = tn * BM + i;
+          nxt = (cbn < n_cblocks && r < B) ? lse2[r] + log2B : INFINITY;
+        }
+        named_bar(1 + g, 128);
+        TRACE(1, threadIdx.x == 0, 6, t);
+        mbar_wait(&s_full[g], (sj >> 1) & 1);
+        TRACE(1, threadIdx.x == 0, 7, t);
+        fence_after();
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {        // two halves of 64 rows
+          uint32_t r0[32], r1[32];
+          AS_TMEM_LD32(tl + 64 * hh, r0);
+          AS_TMEM_LD32(tl + 64 * hh + 32, r1);
+          AS_TMEM_WAIT_LD(r0);
+          AS_TMEM_WAIT_LD(r1);
+          const float *ls = myL + 64 * hh;
+          float v[64];
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const uint32_t x = k < 32 ? r0[k] : r1[k - 32];
+            v[k] = ex2(fmaf(__uint_as_float(x), LOG2E, b2c) - ls[k]);
+          }
+          const int base = t * BM + 64 * hh;
+          while (lnr < base + 64) {             // rare: labels of class c in these rows
+            if (lnr >= base) {
+              const int kk = lnr - base;
+#pragma unroll
+              for (int k = 0; k < 64; ++k)
+                if (k == kk) v[k] -= lnw;
+            }
+            ++lc;
+            lnr = lc < le ? lrow[lc] : 0x7fffffff;
+            lnw = lc < le ? lw[lc] : 0.f;
+          }
+          uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            db2 += v[2 * u] + v[2 * u + 1];
+            pk[u] = pack_bf16x2(v[2 * u], v[2 * u + 1]);
+          }
+          // G^T rows 64hh.. into columns [32hh, 32hh + 32) of this S buffer (consumed)
+          AS_TMEM_ST32(tl + 32 * hh, pk);
+        }
+        TRACE(1, threadIdx.x == 0, 8, t);
+        tmem_wait_st();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[g]);
+      }
+      // db2 partial of this WG for class i -> update warps
+      if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
+      sDB[g * BM + i] = db2;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(db_full);
+    }
+  } else if (warp < 12) {  // ---------------- update warps
+    const int q = warp & 3;
+    const int i = q * 32 + lane;              // thread = class (TMEM lane) for the loads
+    const int ut = threadIdx.x - 256;         // 0..127
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    constexpr int NCH = H / 32;               // 32-column chunks of dW2T
+    // transposed phase: warp q owns classes 32q..32q+31; per instruction the
+    // warp covers 4 classes (lane / 8) x 32 hidden units (4 per lane, 128-bit)
+    const int sub = lane >> 3, hq = (lane & 7) * 4;
+    int kb = 0;
+    TRACE_INIT;
+    float4 wn[8];
+    auto load_w = [&](int cb_, int ch_) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int cls = cb_ * BM + q * 32 + 4 * m + sub;
+        wn[m] = cls < C ? *reinterpret_cast<const float4 *>(W2T + (size_t)cls * H + ch_ * 32 + hq)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    if (blockIdx.x < n_cblocks) load_w(blockIdx.x, 0);
+    for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
+      const int db = kb % NDW;
+      TRACE(3, ut == 0, 11, kb);
+      mbar_wait(&dw_full[db], (kb / NDW) & 1);
+      TRACE(3, ut == 0, 12, kb);
+      fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        uint32_t r[32];
+        AS_TMEM_LD32(tl + 2 * BM + db * BM + ch * 32, r);
+        AS_TMEM_WAIT_LD(r);
+        if (ch == NCH - 1) {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dw_empty[db]);   // TMEM fully read
+        }
+        named_bar(3, 128);                              // previous chunk's reads done
+#pragma unroll
+        for (int k = 0; k < 32; k += 4)
+          *reinterpret_cast<float4 *>(sT + i * 36 + k) =
+              make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]), __uint_as_float(r[k + 2]),
+                          __uint_as_float(r[k + 3]));
+        named_bar(3, 128);
+        float4 w[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) w[m] = wn[m];
+        // prefetch the next chunk (or chunk 0 of the next block) before storing
+        if (ch + 1 < NCH) load_w(cb, ch + 1);
+        else if (cb + (int)gridDim.x < n_cblocks) load_w(cb + gridDim.x, 0);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int cl = q * 32 + 4 * m + sub;          // class inside the block
+          const int cls = cb * BM + cl;
+          if (cls < C) {
+            const float4 g = *reinterpret_cast<const float4 *>(sT + cl * 36 + hq);
+            float4 nw;
+            nw.x = w[m].x - lr * g.x; nw.y = w[m].y - lr * g.y;
+            nw.z = w[m].z - lr * g.z; nw.w = w[m].w - lr * g.w;
+            const size_t idx = (size_t)cls * H + ch * 32 + hq;
+            *reinterpret_cast<float4 *>(W2T + idx) = nw;
+            *reinterpret_cast<uint2 *>(W2b + idx) = make_uint2(pack_bf16x2(nw.x, nw.y),
+                                                               pack_bf16x2(nw.z, nw.w));
+            if (dbg_dW2T) *reinterpret_cast<float4 *>(dbg_dW2T + idx) = g;
           }
         }
-        b2[c] -= lr * db2;
-        if (dbg_db2) dbg_db2[c] = db2;
       }
+      // db2 (thread ut = class ut of the block), label term, SGD on b2
+      TRACE(3, ut == 0, 13, kb);
+      mbar_wait(db_full, kb & 1);
+      float dsum = sDB[ut] + sDB[BM + ut];
+      named_bar(3, 128);
+      if (lane == 0) mbar_arrive(db_empty);
+      const int c = cb * BM + ut;
+      if (c < C) {
+        b2[c] -= lr * dsum;
+        if (dbg_db2) dbg_db2[c] = dsum;
+      }
+      TRACE(3, ut == 0, 14, kb);
     }
   }
   fence_before();
   __syncthreads();
   fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 // =====================================================================
@@ -685,6 +842,144 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+
+// =====================================================================
+// micro-benchmark of tcgen05 issue rates for the operand layouts used above
+// (tests/tools only): one CTA, `iters` groups of 128x128x128 (or 128x256x128)
+// bf16 MMAs accumulated into TMEM; returns elapsed SM cycles.
+//   mode 0: A K-major,  B K-major,  N = 128     (S tiles)
+//   mode 1: A MN-major, B K-major,  N = 128     (dW of pass 2)
+//   mode 2: A K-major,  B MN-major, N = 128     (O of pass 1)
+//   mode 3: A K-major,  B K-major,  N = 256
+//   mode 4: A from TMEM, B K-major,  N = 128     (S of pass 1)
+//   mode 5: A from TMEM, B MN-major, N = 128     (O of pass 1, dW of pass 2)
+// =====================================================================
+__global__ void __launch_bounds__(128, 1) k_tc_bench(int mode, int iters, long long *out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint64_t *bar = (uint64_t *)(smem_raw + 4 * 32768);
+  uint32_t *slot = (uint32_t *)(bar + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < 4 * 32768 / 4; k += blockDim.x) ((uint32_t *)smem_raw)[k] = 0x3c003c00u;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc(slot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *slot;
+  if (warp == 0 && mode >= 6) {
+    // warp-converged issue (all lanes), elect inside the asm
+    const uint32_t aA = smem_u32(smem_raw), aB = aA + 65536;
+    const uint64_t dA = sdesc(aA, 16, 1024), dB = sdesc(aB, 16, 1024);
+    const uint32_t id = idesc_bf16(128, 128, 0, 0);
+    const long long t0 = clock64();
+    if (mode == 6)
+      for (int it = 0; it < iters; ++it) mma_grp_ss_kk_8(tmem, dA, dB, id, it > 0);
+    else
+      for (int it = 0; it < iters; ++it) mma_grp_ts_k_8(tmem, tmem + 256, dB, id, it > 0);
+    mma_commit_w(bar);
+    mbar_wait(bar, 0);
+    if (lane == 0) out[0] = clock64() - t0;
+  } else if (warp == 0 && lane == 0) {
+    const uint32_t aA = smem_u32(smem_raw), aB = aA + 65536;
+    const uint32_t id = mode == 1 ? idesc_bf16(128, 128, 1, 0)
+                        : (mode == 2 || mode == 5) ? idesc_bf16(128, 128, 0, 1)
+                        : mode == 3 ? idesc_bf16(128, 256, 0, 0) : idesc_bf16(128, 128, 0, 0);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t a = mode == 1 ? desc_mn(aA, kk) : desc_k(aA, kk);
+        const uint64_t b = (mode == 2 || mode == 5) ? desc_mn(aB, kk) : desc_k(aB, kk);
+        if (mode >= 4)
+          mma_bf16_ts(tmem, tmem + 256 + 8 * kk, b, id, (it | kk) ? 1u : 0u);
+        else
+          mma_bf16(tmem, a, b, id, (it | kk) ? 1u : 0u);
+      }
+    }
+    mma_commit(bar);
+    mbar_wait(bar, 0);
+    out[0] = clock64() - t0;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// self-test of the TMEM-A ("TS") MMA (tests only), one CTA, 128 threads:
+//   thread r writes row r of A (bf16) into TMEM columns [256, 320) packed,
+//   and row r of P = bf16(A/4) likewise into [320, 384);
+//   V = A_tmem . B^T (B K-major)   -> TMEM cols [0, 128)
+//   U = P_tmem . B   (B MN-major)  -> TMEM cols [128, 256)
+__global__ void __launch_bounds__(128, 1)
+    k_tc_selftest2(const __grid_constant__ CUtensorMap mapB, const __nv_bfloat16 *__restrict__ A,
+                   float *__restrict__ V, float *__restrict__ U) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sB = smem_raw;
+  uint64_t *bars = (uint64_t *)(sB + 32768);
+  uint64_t *ld_full = bars, *mma_done = bars + 1;
+  uint32_t *slot = (uint32_t *)(bars + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(ld_full, 1); mbar_init(mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(slot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *slot;
+  const int row = warp * 32 + lane;
+  const uint32_t tl = tmem + ((uint32_t)(warp * 32) << 16);
+  // rows of A and P into TMEM (two bf16 per column, even k in the low half)
+  for (int ch = 0; ch < 2; ++ch) {
+    uint32_t ra[32], rp[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int k = 64 * ch + 2 * c;
+      const float a0 = __bfloat162float(A[row * 128 + k]), a1 = __bfloat162float(A[row * 128 + k + 1]);
+      ra[c] = pack_bf16x2(a0, a1);
+      rp[c] = pack_bf16x2(a0 * 0.25f, a1 * 0.25f);
+    }
+    AS_TMEM_ST32(tl + 256 + 32 * ch, ra);
+    AS_TMEM_ST32(tl + 320 + 32 * ch, rp);
+  }
+  tmem_wait_st();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(ld_full, 32768);
+    for (int a = 0; a < 2; ++a) tma_load_2d(&mapB, ld_full, sB + a * ATOM_BYTES, a * 64, 0);
+    mbar_wait(ld_full, 0);
+    fence_after();
+    const uint32_t aB = smem_u32(sB);
+    for (int kk = 0; kk < 8; ++kk)
+      mma_bf16_ts(tmem, tmem + 256 + 8 * kk, desc_k(aB, kk), idesc_bf16(128, 128, 0, 0), kk > 0);
+    for (int kk = 0; kk < 8; ++kk)
+      mma_bf16_ts(tmem + 128, tmem + 320 + 8 * kk, desc_mn(aB, kk), idesc_bf16(128, 128, 0, 1), kk > 0);
+    mma_commit(mma_done);
+  }
+  mbar_wait(mma_done, 0);
+  fence_after();
+  for (int ch = 0; ch < 4; ++ch) {
+    uint32_t r[32];
+    AS_TMEM_LD32(tl + ch * 32, r);
+    AS_TMEM_WAIT_LD(r);
+    for (int k = 0; k < 32; ++k) V[row * 128 + ch * 32 + k] = __uint_as_float(r[k]);
+    AS_TMEM_LD32(tl + 128 + ch * 32, r);
+    AS_TMEM_WAIT_LD(r);
+    for (int k = 0; k < 32; ++k) U[row * 128 + ch * 32 + k] = __uint_as_float(r[k]);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
 }  // namespace tc
 
 // =====================================================================
@@ -724,6 +1019,7 @@ static int make_map(CUtensorMap *m, const void *base, long long rows, int cols) 
 
 struct TcPlan {
   CUtensorMap mapH, mapW;
+  const void *Hb;
   int h, b_max, bpad, n_cblocks, num_sms, max_splits;
   long long C;
 };
@@ -739,6 +1035,7 @@ int tc_splits(int h, int b_max, long long C, int num_sms) {
 int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const void *Hb,
                  const void *W2b) {
   plan->h = h;
+  plan->Hb = Hb;
   plan->b_max = b_max;
   plan->bpad = (b_max + tc::BM - 1) / tc::BM * tc::BM;
   plan->C = C;
@@ -769,32 +1066,76 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2,
                        float *pm, float *pl, float *pO) {
   if (p->h == 128)
-    tc::k_out_fwd<128><<<p->num_sms, 192, tc::FwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pm, pl, pO);
+    tc::k_out_fwd<128><<<p->num_sms, tc::FwdCfg<128>::THREADS, tc::FwdCfg<128>::SMEM, s>>>(
+        p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
+        p->max_splits, p->bpad, pm, pl, pO);
   else
-    tc::k_out_fwd<256><<<p->num_sms, 192, tc::FwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pm, pl, pO);
+    tc::k_out_fwd<256><<<p->num_sms, tc::FwdCfg<256>::THREADS, tc::FwdCfg<256>::SMEM, s>>>(
+        p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
+        p->max_splits, p->bpad, pm, pl, pO);
 }
 
+// number of pass-1 partial slots for a batch of B rows (2 per CTA split)
 int tc_fwd_splits_host(const TcPlan *p, int B) {
-  return tc::fwd_splits(B, p->n_cblocks, p->num_sms, p->max_splits);
+  return 2 * tc::fwd_splits(B, p->n_cblocks, p->num_sms, p->max_splits);
 }
 
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lse2,
-                       const float *b2_in, const int32_t *cls_seg, const int32_t *lseg_ptr,
-                       const int32_t *lrow, const int64_t *lab_ptr, const float *Hf, float *W2T,
-                       float *b2, __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2,
-                       float *db2_tmp) {
-  (void)b2_in; (void)db2_tmp;
+                       const int32_t *cls_seg, const int32_t *lseg_ptr, const int32_t *lrow,
+                       const float *lw, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
+                       float *dbg_dW2T, float *dbg_db2) {
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
-    tc::k_out_bwd<128><<<grid, 192, tc::BwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, lse2, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lab_ptr,
-        Hf, W2T, b2, W2b, lr, dbg_dW2T, dbg_db2);
+    tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
+        p->mapH, p->mapW, desc, lse2, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        b2, W2b, lr, dbg_dW2T, dbg_db2);
   else
-    tc::k_out_bwd<256><<<grid, 192, tc::BwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, lse2, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lab_ptr,
-        Hf, W2T, b2, W2b, lr, dbg_dW2T, dbg_db2);
+    tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
+        p->mapH, p->mapW, desc, lse2, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        b2, W2b, lr, dbg_dW2T, dbg_db2);
+}
+
+int tc_trace_dump(long long *out, int max_events) {
+#ifdef AS_TRACE
+  int n[4] = {0, 0, 0, 0};
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(n, tc::g_trace_n, sizeof(n));
+  static long long buf[4][4096][3];
+  cudaMemcpyFromSymbol(buf, tc::g_trace, sizeof(buf));
+  int k = 0;
+  for (int r = 0; r < 4; ++r)
+    for (int i = 0; i < n[r] && k < max_events; ++i, ++k) {
+      out[3 * k] = buf[r][i][0];
+      out[3 * k + 1] = buf[r][i][1];
+      out[3 * k + 2] = buf[r][i][2];
+    }
+  const int z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(tc::g_trace_n, z, sizeof(z));
+  return k;
+#else
+  (void)out; (void)max_events;
+  return 0;
+#endif
+}
+
+int tc_selftest2(const void *A, const void *B, float *V, float *U, cudaStream_t s) {
+  CUtensorMap mB;
+  if (make_map(&mB, B, 128, 128) != 0) return -1;
+  const int smem = 32768 + 1024;
+  cudaFuncSetAttribute(tc::k_tc_selftest2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tc::k_tc_selftest2<<<1, 128, smem, s>>>(mB, (const __nv_bfloat16 *)A, V, U);
+  return 0;
+}
+
+int tc_bench(int mode, int iters, long long *cycles_host) {
+  long long *d = nullptr;
+  cudaMalloc(&d, 8);
+  const int smem = 4 * 32768 + 1024;
+  cudaFuncSetAttribute(tc::k_tc_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tc::k_tc_bench<<<1, 128, smem>>>(mode, iters, d);
+  const cudaError_t e = cudaMemcpy(cycles_host, d, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? 0 : -1;
 }
 
 // test hook: A, B bf16 [128][128] device; S, O, T fp32 [128][128] device

@@ -82,6 +82,19 @@ def test_tc_selftest_descriptors(gpu_lib):
     assert rel_err(T.cpu().numpy(), (Af.T @ P.T).cpu().numpy()) < 1e-5
 
 
+def test_tc_selftest_tmem_a_operand(gpu_lib):
+    import torch
+    from paper_2110_07029_b200.api import tc_selftest2
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn(128, 128, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(128, 128, device="cuda", generator=g).to(torch.bfloat16)
+    V, U = tc_selftest2(A, B)
+    Af, Bf = A.double(), B.double()
+    assert rel_err(V.cpu().numpy(), (Af @ Bf.T).cpu().numpy()) < 1e-5
+    P = (A.float() * 0.25).to(torch.bfloat16).double()
+    assert rel_err(U.cpu().numpy(), (P @ Bf).cpu().numpy()) < 1e-5
+
+
 CASES = [
     # d, C, h, n, B (rows of the batch), b_max
     (2000, 1000, 128, 600, 200, 256),    # ragged: 2 row tiles (72 rows in the 2nd), C % 128 = 104
