@@ -65,7 +65,7 @@ struct as_ctx {
   float *lw;
   float *Hf;
   __nv_bfloat16 *Hb;
-  float *dA, *lse2, *zsum, *labW, *lossr, *loss;
+  float *dA, *lse2, *lsep, *zsum, *labW, *lossr, *loss;
   float *pm, *pl, *pO;
   float *Z, *dH, *dW2, *splitk_tmp;
   float *dbg_dW2, *dbg_db2, *dbg_dW1, *dbg_db1;
@@ -88,6 +88,9 @@ struct as_ctx {
   const float *ds_val;
   int64_t ds_n;
   ncclComm_t comm;
+  // side stream for the batch transposes (overlap with SpMM / pass 1)
+  cudaStream_t side;
+  cudaEvent_t ev_fork, ev_join;
   // live profiling (as_profile)
   bool prof_on;
   std::vector<cudaEvent_t> ev_pool;
@@ -180,6 +183,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(2 * (size_t)D.bpad * D.h); if (x) x->Hb = (__nv_bfloat16 *)p;
   p = P(4 * (size_t)D.b_max * D.h); if (x) x->dA = (float *)p;
   p = P(4 * (size_t)D.bpad); if (x) x->lse2 = (float *)p;
+  p = P(4 * (size_t)D.bpad); if (x) x->lsep = (float *)p;
   p = P(4 * (size_t)D.b_max); if (x) x->zsum = (float *)p;
   p = P(4 * (size_t)D.b_max * D.h); if (x) x->labW = (float *)p;
   p = P(4 * (size_t)D.b_max); if (x) x->lossr = (float *)p;
@@ -227,15 +231,15 @@ cudaEvent_t get_event(as_ctx *x) {
   cudaEventCreate(&e);
   return e;
 }
-inline void ph_begin(as_ctx *x, int ph) {
+inline void ph_begin(as_ctx *x, int ph, cudaStream_t s = nullptr) {
   if (!x->prof_on) return;
   x->ph_start[ph] = get_event(x);
-  cudaEventRecord(x->ph_start[ph], x->stream);
+  cudaEventRecord(x->ph_start[ph], s ? s : x->stream);
 }
-inline void ph_end(as_ctx *x, int ph) {
+inline void ph_end(as_ctx *x, int ph, cudaStream_t s = nullptr) {
   if (!x->prof_on) return;
   cudaEvent_t e = get_event(x);
-  cudaEventRecord(e, x->stream);
+  cudaEventRecord(e, s ? s : x->stream);
   x->pending.push_back({ph, x->ph_start[ph], e});
 }
 // kernels launched by the transpose of a key space with `bits` bits
@@ -336,6 +340,9 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
     rc = cuda_check(x, cudaMemsetAsync(x->cls_seg, 0xFF, 4 * D.C, x->stream), "memset");
   }
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->Hb, 0, 2 * (size_t)D.bpad * D.h, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking), "side stream");
+  if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming), "event");
+  if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming), "event");
   // pinned double-buffered staging for host batches
   x->pin_bytes = 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
   for (int i = 0; i < 2 && !rc; ++i) {
@@ -371,6 +378,9 @@ int as_destroy(as_ctx *x) {
     if (x->pin_ev[i]) cudaEventDestroy(x->pin_ev[i]);
   }
   if (x->comm) ncclCommDestroy(x->comm);
+  if (x->side) { cudaStreamSynchronize(x->side); cudaStreamDestroy(x->side); }
+  if (x->ev_fork) cudaEventDestroy(x->ev_fork);
+  if (x->ev_join) cudaEventDestroy(x->ev_join);
   for (auto &p : x->pending) { x->ev_pool.push_back(p.a); x->ev_pool.push_back(p.b); }
   for (auto e : x->ev_pool) cudaEventDestroy(e);
   free(x->plan);
@@ -506,18 +516,23 @@ int as_train_step(as_ctx *x, float *loss_out) {
   const bool dbg = (x->cfg.flags & AS_FLAG_DEBUG_GRADS) != 0;
   float *W1 = x->w, *b1 = x->w + D.d * D.h, *W2T = b1 + D.h, *b2 = W2T + D.C * D.h;
 
-  // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2)
-  ph_begin(x, AS_PH_TRANSPOSE);
+  // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2) on
+  // the side stream, concurrent with a4/a5; joined before a6 and a7
+  cudaStream_t ss = x->side;
+  cudaEventRecord(x->ev_fork, s);
+  cudaStreamWaitEvent(ss, x->ev_fork, 0);
+  ph_begin(x, AS_PH_TRANSPOSE, ss);
   x->launches += n_transpose_launches(key_bits(D.d)) + n_transpose_launches(key_bits(D.C)) + 2;
-  as::launch_transpose(s, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
+  as::launch_transpose(ss, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->fseg_id,
                        x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val);
-  as::launch_transpose(s, x->lab_ptr, x->lab, rows, &d->nlab, D.lab_cap, key_bits(D.C), x->sk0,
+  as::launch_transpose(ss, x->lab_ptr, x->lab, rows, &d->nlab, D.lab_cap, key_bits(D.C), x->sk0,
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->lseg_id,
                        x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr);
-  as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
-  as::launch_label_weights(s, d, D.lab_cap, x->lseg_row, x->lab_ptr, x->lw);
-  ph_end(x, AS_PH_TRANSPOSE);
+  as::launch_class_map(ss, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
+  as::launch_label_weights(ss, d, D.lab_cap, x->lseg_row, x->lab_ptr, x->lw);
+  ph_end(x, AS_PH_TRANSPOSE, ss);
+  cudaEventRecord(x->ev_join, ss);
   // a4: SpMM forward
   ph_begin(x, AS_PH_SPMM);
   x->launches += 1;
@@ -534,13 +549,15 @@ int as_train_step(as_ctx *x, float *loss_out) {
     // label terms of the loss and of dH (R3)
     as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
-                            x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lse2, x->lossr, x->dA);
+                            x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lse2, x->lsep, x->lossr,
+                            x->dA);
     as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
     ph_end(x, AS_PH_COMBINE);
+    cudaStreamWaitEvent(s, x->ev_join, 0);   // label transpose ready
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
     ph_begin(x, AS_PH_OUT_BWD);
     x->launches += 1;
-    as::launch_out_bwd_tc(s, x->plan, d, x->lse2, x->cls_seg, x->lseg_ptr, x->lseg_row, x->lw,
+    as::launch_out_bwd_tc(s, x->plan, d, x->lsep, x->cls_seg, x->lseg_ptr, x->lseg_row, x->lw,
                           W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
                           dbg ? x->dbg_db2 : nullptr);
     ph_end(x, AS_PH_OUT_BWD);
@@ -555,6 +572,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
     as::launch_row_lse(s, d, D.b_max, (int)C, x->Z, x->lse2);
     as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2);
     ph_end(x, AS_PH_OUT_FWD);
+    cudaStreamWaitEvent(s, x->ev_join, 0);   // transposes ready
     ph_begin(x, AS_PH_OUT_BWD);
     x->launches += (D.splitk > 1 ? 2 : 1) + 1 + 1 + 2 + 1 + (dbg ? 0 : 0);
     as::launch_gemm_f32(s, D.b_max, D.h, (int)C, x->Z, C, 1, W2T, D.h, 1, x->dH, D.h, nullptr,
@@ -805,7 +823,7 @@ int as_trace_dump(int64_t *out, int32_t max_events) {
 }
 
 int as_tc_bench(int32_t mode, int32_t iters, int64_t *cycles) {
-  if (!cycles || mode < 0 || mode > 7 || iters < 1) return as_fail(AS_E_INVALID, "bad arguments");
+  if (!cycles || mode < 0 || mode > 10 || iters < 1) return as_fail(AS_E_INVALID, "bad arguments");
   long long c = 0;
   if (as::tc_bench(mode, iters, &c) != 0) return as_fail(AS_E_CUDA, "tc_bench failed");
   *cycles = c;

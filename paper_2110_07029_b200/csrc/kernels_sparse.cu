@@ -525,11 +525,14 @@ __global__ void k_combine_bf16(const StepDesc *__restrict__ desc, int h, int bpa
                                const float *__restrict__ pm, const float *__restrict__ pl,
                                const float *__restrict__ pO, const float *__restrict__ labW,
                                const float *__restrict__ zsum, const float *__restrict__ Hf,
-                               float *__restrict__ lse2, float *__restrict__ lossr,
-                               float *__restrict__ dA) {
+                               float *__restrict__ lse2, float *__restrict__ lsep,
+                               float *__restrict__ lossr, float *__restrict__ dA) {
   const int r = blockIdx.x, j = threadIdx.x;
   const int B = desc->rows;
-  if (r >= B) return;
+  if (r >= B) {                       // padding rows of the last tile: p = 2^-inf = 0
+    if (j == 0) lsep[r] = INFINITY;
+    return;
+  }
   float M = -FLT_MAX;
   for (int s = 0; s < splits; ++s) M = fmaxf(M, pm[(size_t)s * bpad + r]);
   float l = 0.f, o = 0.f;
@@ -545,6 +548,7 @@ __global__ void k_combine_bf16(const StepDesc *__restrict__ desc, int h, int bpa
   dA[(size_t)r * h + j] = Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
   if (j == 0) {
     lse2[r] = L2;
+    lsep[r] = L2 + log2f((float)B);   // pass 2: p / B = 2^(s log2e - lsep)
     lossr[r] = L2 * 0.69314718055994531f - zsum[r];
   }
 }
@@ -552,9 +556,9 @@ __global__ void k_combine_bf16(const StepDesc *__restrict__ desc, int h, int bpa
 void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max, int bpad,
                          int splits, const float *pm, const float *pl, const float *pO,
                          const float *labW, const float *zsum, const float *Hf, float *lse2,
-                         float *lossr, float *dA) {
-  k_combine_bf16<<<b_max, h, 0, s>>>(desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lossr,
-                                     dA);
+                         float *lsep, float *lossr, float *dA) {
+  k_combine_bf16<<<bpad, h, 0, s>>>(desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lsep,
+                                    lossr, dA);
 }
 
 // =====================================================================

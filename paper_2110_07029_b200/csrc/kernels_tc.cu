@@ -440,67 +440,79 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 
 template <int H>
 struct BwdCfg {
-  static constexpr int NW = H == 128 ? 2 : 1;     // W2T block buffers
-  static constexpr int NSH = H == 128 ? 4 : 2;    // H tile stages (TMA latency off the chain)
-  static constexpr int NDW = H == 128 ? 2 : 1;    // dW2T accumulators in TMEM
+  static constexpr int NSH = H == 128 ? 4 : 2;    // H tile stages (128 rows each)
+  static constexpr int NSB = H == 128 ? 4 : 2;    // S^T unit buffers (64 rows = 64 columns)
+  static constexpr int NWT = H == 128 ? 2 : 1;    // W2T blocks resident in TMEM (A operand)
+  static constexpr int WCOLS = H / 2;             // TMEM columns of one W2T block (bf16 pairs)
   static constexpr int TILE = BM * H * 2;
   static constexpr int THREADS = 14 * 32;
-  static constexpr int TSTAGE = BM * 36 * 4;      // update-warp transpose stage (16-B rows)
-  static constexpr int SMEM = NW * TILE + NSH * TILE + TSTAGE + 4 * BM * 4 /*lse*/ +
-                              2 * BM * 4 /*db2*/ + 256 /*barriers*/;
+  static constexpr bool FULLSTAGE = H == 128;     // whole dW2T block staged in smem
+  static constexpr int SROW = FULLSTAGE ? H + 4 : 36;   // staging row (floats, 16-B aligned)
+  static constexpr int TSTAGE = BM * SROW * 4;
+  static constexpr int SMEM = NSH * TILE + TSTAGE + 2 * BM * 4 /*db2*/ + 512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
+  static_assert(NSB * 64 + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
 };
 
 // =====================================================================
-// pass 2 (v3: G^T lives in TMEM)
-//   warps 0-7   softmax: two warpgroups ping-pong over the S^T tiles (WG g takes
-//               tiles t with t % 2 == g, i.e. S buffer g); thread = class (TMEM
-//               lane).  G^T = softmax^T / B is written back into TMEM over the
+// pass 2 (v6: W2T block and G^T in TMEM)
+// Work of a CTA: its class blocks cb = blockIdx.x + k * gridDim.x; every block
+// is swept by NU = 2 * RT units of 64 batch rows.  Global unit counter gu.
+//   warps 0-7   softmax: two warpgroups, WG g takes the units gu % 2 == g;
+//               thread = class (TMEM lane).  G^T = softmax^T / B - T^T
+//               (label term folded in, R3) is written back into TMEM over the
 //               S^T columns it came from.
-//   warps 8-11  update: dW2T (lane = class) -> smem transpose -> fused SGD of
-//               W2T and the bf16 shadow (coalesced); db2, b2.
-// The label term of R3 (-1/(k_r B) at the row's labels) is folded into G^T by
-// the softmax threads, so the MMA produces the complete gradient.
-//   warp 12     TMA producer (W2T block, H row tiles)
-//   warp 13     MMA issuer + TMEM owner:
-//                 S^T_t  = W2T_blk . H_t^T          (SS, TMEM cols 128*b)
-//                 dW2T  += G^T_t . H_t              (A = G^T from TMEM, B MN-major)
+//   warps 8-11  update: (a) load the W2T block (bf16 shadow) of block kb+NWT
+//               into TMEM; (b) dW2T (lane = class) -> smem staging -> fused SGD
+//               of W2T and the bf16 shadow (128-bit, coalesced); db2, b2.
+//   warp 12     TMA producer (H row tiles of 128 rows)
+//   warp 13     MMA issuer (warp-converged) + TMEM owner, S running NSB units
+//               ahead of dW across block boundaries:
+//                 S^T_u  = W2T_blk . H_u^T   (A = W2T_blk from TMEM, N = 64)
+//                 dW2T  += G^T_u . H_u       (A = G^T from TMEM, B MN-major;
+//                                             fixed unit order: deterministic)
+// TMEM: S^T units at 64*b; W2T blocks at 64*NSB (+WCOLS each); dW2T last.
 // =====================================================================
 template <int H>
 __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
-              const StepDesc *__restrict__ desc, const float *__restrict__ lse2, int C,
+              const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
               int n_cblocks, const int32_t *__restrict__ cls_seg,
               const int32_t *__restrict__ lseg_ptr, const int32_t *__restrict__ lrow,
               const float *__restrict__ lw, float *__restrict__ W2T, float *__restrict__ b2,
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
               float *__restrict__ dbg_db2) {
+  (void)mapW;
   using Cfg = BwdCfg<H>;
-  constexpr int NW = Cfg::NW, NSH = Cfg::NSH, NDW = Cfg::NDW, TILE = Cfg::TILE;
+  constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
+  constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
+  constexpr bool FULLSTAGE = Cfg::FULLSTAGE;
+  constexpr uint32_t COL_W = NSB * 64, COL_DW = NSB * 64 + NWT * WCOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *sW = smem_raw;
-  uint8_t *sHt = sW + NW * TILE;
-  float *sT = (float *)(sHt + NSH * TILE);      // [128][36] transpose stage
-  float *sL = sT + BM * 36;                     // [2 WG][2][128] lse of the WG's tiles
-  float *sDB = sL + 4 * BM;                     // [2][128] db2 partials of the two WGs
+  uint8_t *sHt = smem_raw;
+  float *sT = (float *)(sHt + NSH * TILE);      // dW2T staging [128][SROW]
+  float *sDB = sT + BM * SROW;                  // [2][128] db2 partials of the two WGs
   uint64_t *bars = (uint64_t *)(sDB + 2 * BM);
-  uint64_t *w_full = bars, *w_empty = w_full + NW, *h_full = w_empty + NW, *h_empty = h_full + NSH,
-           *s_full = h_empty + NSH, *p_full = s_full + 2, *dw_full = p_full + 2,
-           *dw_empty = dw_full + NDW, *db_full = dw_empty + NDW, *db_empty = db_full + 1;
+  uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + NSB,
+           *wt_full = p_full + NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
+           *db_full = dw_empty + 1, *db_empty = db_full + 1;
   uint32_t *tmem_slot = (uint32_t *)(db_empty + 1);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
 
   const int B = desc->rows;
-  const int RT = (B + BM - 1) / BM;
-  const float invB = 1.0f / (float)B;
+  const int RT = (B + BM - 1) / BM;               // 128-row H tiles
+  const int NU = 2 * RT;                          // 64-row units per class block
+  const int NB = blockIdx.x < n_cblocks ? (n_cblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int NT = NB * NU;                         // units of this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = 12, kMmaWarp = 13;   // highest ids: scheduler priority
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NW; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
     for (int i = 0; i < NSH; ++i) { mbar_init(&h_full[i], 1); mbar_init(&h_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
-    for (int i = 0; i < NDW; ++i) { mbar_init(&dw_full[i], 1); mbar_init(&dw_empty[i], 4); }
+    for (int i = 0; i < NSB; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+    for (int i = 0; i < NWT; ++i) mbar_init(&wt_full[i], 4);
+    mbar_init(dw_full, 1);
+    mbar_init(dw_empty, 4);
     mbar_init(db_full, 8);
     mbar_init(db_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -512,15 +524,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kProdWarp) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer (H tiles)
       TRACE_INIT;
-      int kb = 0, it = 0;
-      for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
-        const int wb = kb % NW;
-        if (kb >= NW) mbar_wait(&w_empty[wb], ((kb / NW) - 1) & 1);
-        mbar_expect_tx(&w_full[wb], TILE);
-        for (int a = 0; a < H / 64; ++a)
-          tma_load_2d(&mapW, &w_full[wb], sW + wb * TILE + a * ATOM_BYTES, a * 64, cb * BM);
+      int it = 0;
+      for (int kb = 0; kb < NB; ++kb)
         for (int t = 0; t < RT; ++t, ++it) {
           const int st = it % NSH;
           if (it >= NSH) mbar_wait(&h_empty[st], ((it / NSH) - 1) & 1);
@@ -529,215 +536,261 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           for (int a = 0; a < H / 64; ++a)
             tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
         }
-      }
     }
   } else if (warp == kMmaWarp) {
     {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
-      constexpr uint32_t idS = idesc_bf16(BM, BM, 0, 0);   // S^T = W2T_blk . H_t^T
-      constexpr uint32_t idW = idesc_bf16(BM, H, 0, 1);    // dW2T += G^T . H_t
-      const uint32_t aW = smem_u32(sW), aH = smem_u32(sHt);
-      int kb = 0, it = 0, sj = 0;
+      constexpr uint32_t idS = idesc_bf16(BM, 64, 0, 0);   // S^T_u = W2T_blk . H_u^T
+      constexpr uint32_t idW = idesc_bf16(BM, H, 0, 1);    // dW2T += G^T_u . H_u
+      const uint32_t aH = smem_u32(sHt);
       TRACE_INIT;
-      auto do_dw = [&](int t, int st, int sjt) {
-        const int b = sjt & 1, db = kb % NDW;
-        TRACE(0, lane == 0, 1, t);
-        mbar_wait(&p_full[b], (sjt >> 1) & 1);
-        TRACE(0, lane == 0, 2, t);
-        if (t == 0 && kb >= NDW) mbar_wait(&dw_empty[db], ((kb / NDW) - 1) & 1);
+      auto issue_S = [&](int gu) {
+        const int kb = gu / NU, v = gu - kb * NU, t = v >> 1, hh = v & 1;
+        const int it = kb * RT + t, st = it % NSH, b = gu % NSB, wb = kb % NWT;
+        if (v == 0) mbar_wait(&wt_full[wb], (kb / NWT) & 1);
+        if (hh == 0) mbar_wait(&h_full[st], (it / NSH) & 1);
+        TRACE(0, lane == 0, 5, v);
         fence_after();
-        mma_grp_ts_mn_8(tmem + 2 * BM + db * BM, tmem + b * BM,
-                        sdesc(aH + st * TILE, ATOM_BYTES, 1024), idW, t > 0 ? 1u : 0u);
-        mma_commit_w(&h_empty[st]);
+        // buffer b was last read (G^T of unit gu - NSB) by a dW issued earlier by
+        // this warp: tcgen05.mma executes in issue order
+        const uint64_t dB = sdesc(aH + st * TILE + hh * 8192, 16, 1024);
+        if constexpr (H == 128)
+          mma_grp_ts_k_8(tmem + b * 64, tmem + COL_W + wb * WCOLS, dB, idS, 0u);
+        else
+          mma_grp_ts_k_16(tmem + b * 64, tmem + COL_W + wb * WCOLS, dB, idS, 0u);
+        mma_commit_w(&s_full[b]);
       };
-      for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
-        const int wb = kb % NW;
-        mbar_wait(&w_full[wb], (kb / NW) & 1);
-        const uint64_t dW = sdesc(aW + wb * TILE, 16, 1024);
-        int st_prev = 0;
-        for (int t = 0; t < RT; ++t, ++it) {
-          const int st = it % NSH, b = sj & 1;
-          TRACE(0, lane == 0, 3, t);
-          mbar_wait(&h_full[st], (it / NSH) & 1);
-          TRACE(0, lane == 0, 5, t);
-          fence_after();
-          // S^T_t overwrites buffer b: the previous user (dW of tile t-2, which
-          // read its G^T there) was issued earlier by this warp (in order).
-          if constexpr (H == 128)
-            mma_grp_ss_kk_8(tmem + b * BM, dW, sdesc(aH + st * TILE, 16, 1024), idS, 0u);
-          else
-            mma_grp_ss_kk_16(tmem + b * BM, dW, sdesc(aH + st * TILE, 16, 1024), idS, 0u);
-          mma_commit_w(&s_full[b]);
-          ++sj;
-          if (t == RT - 1) mma_commit_w(&w_empty[wb]);
-          if (t > 0) do_dw(t - 1, st_prev, sj - 2);
-          st_prev = st;
-        }
-        do_dw(RT - 1, st_prev, sj - 1);
-        mma_commit_w(&dw_full[kb % NDW]);
+      auto do_dw = [&](int gu) {
+        const int kb = gu / NU, v = gu - kb * NU, t = v >> 1, hh = v & 1;
+        const int it = kb * RT + t, st = it % NSH, b = gu % NSB;
+        TRACE(0, lane == 0, 1, v);
+        mbar_wait(&p_full[b], (gu / NSB) & 1);
+        TRACE(0, lane == 0, 2, v);
+        if (v == 0 && kb >= 1) mbar_wait(dw_empty, (kb - 1) & 1);
+        fence_after();
+        mma_grp_ts_mn_4(tmem + COL_DW, tmem + b * 64, sdesc(aH + st * TILE + hh * 8192, ATOM_BYTES, 1024),
+                        idW, v > 0 ? 1u : 0u);
+        if (hh == 1) mma_commit_w(&h_empty[st]);
+        if (v == NU - 1) mma_commit_w(dw_full);
+      };
+      for (int gu = 0; gu < NT && gu < NSB; ++gu) issue_S(gu);
+      for (int gu = 0; gu < NT; ++gu) {
+        do_dw(gu);
+        const int nx = gu + NSB;
+        // with a single TMEM W2T buffer the look-ahead may not cross into the next
+        // block (its W2T is loaded only after this block's last dW completes)
+        if (nx < NT && (NWT > 1 || nx / NU == gu / NU)) issue_S(nx);
+        if (NWT == 1 && gu % NU == NU - 1)
+          for (int k = 0; k < NSB && gu + 1 + k < NT; ++k) issue_S(gu + 1 + k);
       }
     }
-  } else if (warp < 8) {  // ---------------- softmax warpgroups (ping-pong over tiles)
-    const int g = warp >> 2;                  // WG g takes the tiles with sj % 2 == g (S buffer g)
+  } else if (warp < 8) {  // ---------------- softmax warpgroups (units gu % 2 == g)
+    const int g = warp >> 2;
     const int q = warp & 3;
-    const int i = q * 32 + lane;              // class inside the block (TMEM lane) == loader index
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + g * BM;
-    const float log2B = __log2f((float)B);
-    int kb = 0, sj = 0;
+    const int i = q * 32 + lane;              // class inside the block (TMEM lane)
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     TRACE_INIT;
-    // lse prefetch (log2 units, 1/B folded in): thread i owns row i of the WG's next tile
-    float nxt = 0.f;
-    {
-      const int t0 = g < RT ? g : (g - RT) % RT;   // first tile index this WG will see
-      const int r = t0 * BM + i;
-      nxt = r < B ? lse2[r] + log2B : INFINITY;
-    }
-    for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
-      const int c = cb * BM + i;
-      const bool cvalid = c < C;
-      const float b2c = cvalid ? b2[c] * LOG2E : -INFINITY;   // invalid class -> p = 0
-      float db2 = 0.f;
-      int lc = 0, le = 0, lnr = 0x7fffffff;
-      float lnw = 0.f;
-      if (cvalid) {
-        const int sg = cls_seg[c];
+    // per-class label range of the next block, prefetched one block ahead
+    auto seg_of = [&](int kb_) -> int {
+      const int c = (blockIdx.x + kb_ * gridDim.x) * BM + i;
+      return (kb_ < NB && c < C) ? cls_seg[c] : -1;
+    };
+    int nseg = seg_of(0);
+    int kb_cur = -1, lc = 0, le = 0, lnr = 0x7fffffff;
+    float lnw = 0.f, b2c = 0.f, db2 = 0.f;
+    for (int gu = g; gu < NT; gu += 2) {
+      const int kb = gu / NU, v = gu - kb * NU;
+      if (kb != kb_cur) {                     // new class block: per-class state
+        kb_cur = kb;
+        const int c = (blockIdx.x + kb * gridDim.x) * BM + i;
+        b2c = c < C ? b2[c] * LOG2E : -INFINITY;   // invalid class -> p = 0
+        db2 = 0.f;
+        lc = 0; le = 0; lnr = 0x7fffffff; lnw = 0.f;
+        const int sg = nseg;
+        nseg = seg_of(kb + 1);
         if (sg >= 0) {
           lc = lseg_ptr[sg]; le = lseg_ptr[sg + 1];
           lnr = lrow[lc]; lnw = lw[lc];
         }
       }
-      for (int t = 0; t < RT; ++t, ++sj) {
-        if ((sj & 1) != g) continue;
-        float *myL = sL + (g * 2 + ((sj >> 1) & 1)) * BM;   // double-buffered per WG
-        myL[i] = nxt;
-        {  // prefetch the lse of this WG's next tile (global tile counter sj + 2)
-          int tn = t + 2, cbn = cb;
-          if (tn >= RT) { tn -= RT; cbn += gridDim.x; if (tn >= RT) tn %= RT; }
-          const int r = tn * BM + i;
-          nxt = (cbn < n_cblocks && r < B) ? lse2[r] + log2B : INFINITY;
+      const int b = gu % NSB;
+      TRACE(1, threadIdx.x == 0, 6, v);
+      mbar_wait(&s_full[b], (gu / NSB) & 1);
+      TRACE(1, threadIdx.x == 0, 7, v);
+      fence_after();
+      uint32_t r0[32], r1[32];
+      AS_TMEM_LD32(tl + b * 64, r0);
+      AS_TMEM_LD32(tl + b * 64 + 32, r1);
+      // lse' = LSE_r * log2e + log2 B of the unit's 64 rows (broadcast, L1-resident)
+      const float4 *lq = reinterpret_cast<const float4 *>(lsep + 64 * v);
+      AS_TMEM_WAIT_LD(r0);
+      AS_TMEM_WAIT_LD(r1);
+      float vv[64];
+#pragma unroll
+      for (int k4 = 0; k4 < 16; ++k4) {
+        const float4 l4 = __ldg(lq + k4);
+        const float lk[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int k = 4 * k4 + m;
+          const uint32_t x = k < 32 ? r0[k] : r1[k - 32];
+          vv[k] = ex2(fmaf(__uint_as_float(x), LOG2E, b2c) - lk[m]);
         }
-        named_bar(1 + g, 128);
-        TRACE(1, threadIdx.x == 0, 6, t);
-        mbar_wait(&s_full[g], (sj >> 1) & 1);
-        TRACE(1, threadIdx.x == 0, 7, t);
-        fence_after();
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {        // two halves of 64 rows
-          uint32_t r0[32], r1[32];
-          AS_TMEM_LD32(tl + 64 * hh, r0);
-          AS_TMEM_LD32(tl + 64 * hh + 32, r1);
-          AS_TMEM_WAIT_LD(r0);
-          AS_TMEM_WAIT_LD(r1);
-          const float *ls = myL + 64 * hh;
-          float v[64];
-#pragma unroll
-          for (int k = 0; k < 64; ++k) {
-            const uint32_t x = k < 32 ? r0[k] : r1[k - 32];
-            v[k] = ex2(fmaf(__uint_as_float(x), LOG2E, b2c) - ls[k]);
-          }
-          const int base = t * BM + 64 * hh;
-          while (lnr < base + 64) {             // rare: labels of class c in these rows
-            if (lnr >= base) {
-              const int kk = lnr - base;
-#pragma unroll
-              for (int k = 0; k < 64; ++k)
-                if (k == kk) v[k] -= lnw;
-            }
-            ++lc;
-            lnr = lc < le ? lrow[lc] : 0x7fffffff;
-            lnw = lc < le ? lw[lc] : 0.f;
-          }
-          uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
-#pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            db2 += v[2 * u] + v[2 * u + 1];
-            pk[u] = pack_bf16x2(v[2 * u], v[2 * u + 1]);
-          }
-          // G^T rows 64hh.. into columns [32hh, 32hh + 32) of this S buffer (consumed)
-          AS_TMEM_ST32(tl + 32 * hh, pk);
-        }
-        TRACE(1, threadIdx.x == 0, 8, t);
-        tmem_wait_st();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[g]);
       }
-      // db2 partial of this WG for class i -> update warps
-      if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
-      sDB[g * BM + i] = db2;
+      const int base = 64 * v;
+      while (lnr < base + 64) {               // rare: labels of this class in these rows
+        if (lnr >= base) {
+          const int kk = lnr - base;
+#pragma unroll
+          for (int k = 0; k < 64; ++k)
+            if (k == kk) vv[k] -= lnw;
+        }
+        ++lc;
+        lnr = lc < le ? lrow[lc] : 0x7fffffff;
+        lnw = lc < le ? lw[lc] : 0.f;
+      }
+      uint32_t pk[32];                        // 64 bf16 of G^T, packed in pairs
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        db2 += vv[2 * u] + vv[2 * u + 1];
+        pk[u] = pack_bf16x2(vv[2 * u], vv[2 * u + 1]);
+      }
+      AS_TMEM_ST32(tl + b * 64, pk);          // G^T over the consumed S^T columns
+      TRACE(1, threadIdx.x == 0, 8, v);
+      tmem_wait_st();
+      fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(db_full);
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
+        if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
+        sDB[g * BM + i] = db2;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(db_full);
+      }
     }
   } else if (warp < 12) {  // ---------------- update warps
     const int q = warp & 3;
-    const int i = q * 32 + lane;              // thread = class (TMEM lane) for the loads
+    const int i = q * 32 + lane;              // thread = class (TMEM lane)
     const int ut = threadIdx.x - 256;         // 0..127
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int NCH = H / 32;               // 32-column chunks of dW2T
-    // transposed phase: warp q owns classes 32q..32q+31; per instruction the
-    // warp covers 4 classes (lane / 8) x 32 hidden units (4 per lane, 128-bit)
     const int sub = lane >> 3, hq = (lane & 7) * 4;
-    int kb = 0;
     TRACE_INIT;
-    float4 wn[8];
-    auto load_w = [&](int cb_, int ch_) {
+    // W2T block (bf16 shadow, row of class i) -> TMEM A-operand columns of buffer wb
+    auto load_wt = [&](int kb_) {
+      const int wb = kb_ % NWT;
+      const int cls = (blockIdx.x + kb_ * gridDim.x) * BM + i;
+      const uint4 *src = reinterpret_cast<const uint4 *>(W2b + (size_t)(cls < C ? cls : 0) * H);
+#pragma unroll 1
+      for (int part = 0; part < H / 64; ++part) {
+        uint32_t r[32];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const int cls = cb_ * BM + q * 32 + 4 * m + sub;
-        wn[m] = cls < C ? *reinterpret_cast<const float4 *>(W2T + (size_t)cls * H + ch_ * 32 + hq)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int v4 = 0; v4 < 8; ++v4) {
+          uint4 x = src[part * 8 + v4];
+          if (cls >= C) x = make_uint4(0u, 0u, 0u, 0u);
+          r[4 * v4] = x.x; r[4 * v4 + 1] = x.y; r[4 * v4 + 2] = x.z; r[4 * v4 + 3] = x.w;
+        }
+        AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 32 * part, r);
       }
+      tmem_wait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wt_full[wb]);
     };
-    if (blockIdx.x < n_cblocks) load_w(blockIdx.x, 0);
-    for (int cb = blockIdx.x; cb < n_cblocks; cb += gridDim.x, ++kb) {
-      const int db = kb % NDW;
+    for (int kb = 0; kb < NB && kb < NWT; ++kb) load_wt(kb);
+    for (int kb = 0; kb < NB; ++kb) {
+      const int cb = blockIdx.x + kb * gridDim.x;
       TRACE(3, ut == 0, 11, kb);
-      mbar_wait(&dw_full[db], (kb / NDW) & 1);
+      mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
+      if constexpr (FULLSTAGE) {
+        // (1) whole dW2T block: TMEM -> smem staging, then release the accumulator
 #pragma unroll 1
-      for (int ch = 0; ch < NCH; ++ch) {
-        uint32_t r[32];
-        AS_TMEM_LD32(tl + 2 * BM + db * BM + ch * 32, r);
-        AS_TMEM_WAIT_LD(r);
-        if (ch == NCH - 1) {
-          fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&dw_empty[db]);   // TMEM fully read
+        for (int ch = 0; ch < NCH; ++ch) {
+          uint32_t r[32];
+          AS_TMEM_LD32(tl + COL_DW + ch * 32, r);
+          AS_TMEM_WAIT_LD(r);
+#pragma unroll
+          for (int k = 0; k < 32; k += 4)
+            *reinterpret_cast<float4 *>(sT + i * SROW + ch * 32 + k) =
+                make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]),
+                            __uint_as_float(r[k + 2]), __uint_as_float(r[k + 3]));
         }
-        named_bar(3, 128);                              // previous chunk's reads done
-#pragma unroll
-        for (int k = 0; k < 32; k += 4)
-          *reinterpret_cast<float4 *>(sT + i * 36 + k) =
-              make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]), __uint_as_float(r[k + 2]),
-                          __uint_as_float(r[k + 3]));
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dw_empty);
+        // (2) the W2T block two ahead into the TMEM buffer just freed by block kb
+        if (kb + NWT < NB) load_wt(kb + NWT);
         named_bar(3, 128);
-        float4 w[8];
+        // (3) fused SGD, coalesced: warp q -> classes 32q..32q+31, 4 per instruction
+#pragma unroll 1
+        for (int ch = 0; ch < NCH; ++ch) {
+          float4 w[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) w[m] = wn[m];
-        // prefetch the next chunk (or chunk 0 of the next block) before storing
-        if (ch + 1 < NCH) load_w(cb, ch + 1);
-        else if (cb + (int)gridDim.x < n_cblocks) load_w(cb + gridDim.x, 0);
+          for (int m = 0; m < 8; ++m) {
+            const int cls = cb * BM + q * 32 + 4 * m + sub;
+            w[m] = cls < C ? *reinterpret_cast<const float4 *>(W2T + (size_t)cls * H + ch * 32 + hq)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int cl = q * 32 + 4 * m + sub;          // class inside the block
-          const int cls = cb * BM + cl;
-          if (cls < C) {
-            const float4 g = *reinterpret_cast<const float4 *>(sT + cl * 36 + hq);
-            float4 nw;
-            nw.x = w[m].x - lr * g.x; nw.y = w[m].y - lr * g.y;
-            nw.z = w[m].z - lr * g.z; nw.w = w[m].w - lr * g.w;
-            const size_t idx = (size_t)cls * H + ch * 32 + hq;
-            *reinterpret_cast<float4 *>(W2T + idx) = nw;
-            *reinterpret_cast<uint2 *>(W2b + idx) = make_uint2(pack_bf16x2(nw.x, nw.y),
-                                                               pack_bf16x2(nw.z, nw.w));
-            if (dbg_dW2T) *reinterpret_cast<float4 *>(dbg_dW2T + idx) = g;
+          for (int m = 0; m < 8; ++m) {
+            const int cl = q * 32 + 4 * m + sub;
+            const int cls = cb * BM + cl;
+            if (cls < C) {
+              const float4 gv = *reinterpret_cast<const float4 *>(sT + cl * SROW + ch * 32 + hq);
+              float4 nw;
+              nw.x = w[m].x - lr * gv.x; nw.y = w[m].y - lr * gv.y;
+              nw.z = w[m].z - lr * gv.z; nw.w = w[m].w - lr * gv.w;
+              const size_t idx = (size_t)cls * H + ch * 32 + hq;
+              *reinterpret_cast<float4 *>(W2T + idx) = nw;
+              *reinterpret_cast<uint2 *>(W2b + idx) = make_uint2(pack_bf16x2(nw.x, nw.y),
+                                                                 pack_bf16x2(nw.z, nw.w));
+              if (dbg_dW2T) *reinterpret_cast<float4 *>(dbg_dW2T + idx) = gv;
+            }
           }
         }
+        named_bar(3, 128);                    // staging reads done before the next block
+      } else {
+        // chunked staging (h = 256): the accumulator is released after the last chunk
+#pragma unroll 1
+        for (int ch = 0; ch < NCH; ++ch) {
+          uint32_t r[32];
+          AS_TMEM_LD32(tl + COL_DW + ch * 32, r);
+          AS_TMEM_WAIT_LD(r);
+          if (ch == NCH - 1) {
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dw_empty);
+          }
+          named_bar(3, 128);
+#pragma unroll
+          for (int k = 0; k < 32; k += 4)
+            *reinterpret_cast<float4 *>(sT + i * SROW + k) =
+                make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]),
+                            __uint_as_float(r[k + 2]), __uint_as_float(r[k + 3]));
+          named_bar(3, 128);
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int cl = q * 32 + 4 * m + sub;
+            const int cls = cb * BM + cl;
+            if (cls < C) {
+              const float4 gv = *reinterpret_cast<const float4 *>(sT + cl * SROW + hq);
+              const size_t idx = (size_t)cls * H + ch * 32 + hq;
+              float4 nw = *reinterpret_cast<const float4 *>(W2T + idx);
+              nw.x -= lr * gv.x; nw.y -= lr * gv.y; nw.z -= lr * gv.z; nw.w -= lr * gv.w;
+              *reinterpret_cast<float4 *>(W2T + idx) = nw;
+              *reinterpret_cast<uint2 *>(W2b + idx) = make_uint2(pack_bf16x2(nw.x, nw.y),
+                                                                 pack_bf16x2(nw.z, nw.w));
+              if (dbg_dW2T) *reinterpret_cast<float4 *>(dbg_dW2T + idx) = gv;
+            }
+          }
+        }
+        if (kb + NWT < NB) load_wt(kb + NWT);
       }
-      // db2 (thread ut = class ut of the block), label term, SGD on b2
+      // db2 (thread ut = class ut of the block; label term already in G), SGD on b2
       TRACE(3, ut == 0, 13, kb);
       mbar_wait(db_full, kb & 1);
-      float dsum = sDB[ut] + sDB[BM + ut];
+      const float dsum = sDB[ut] + sDB[BM + ut];
       named_bar(3, 128);
       if (lane == 0) mbar_arrive(db_empty);
       const int c = cb * BM + ut;
@@ -878,8 +931,27 @@ __global__ void __launch_bounds__(128, 1) k_tc_bench(int mode, int iters, long l
     const long long t0 = clock64();
     if (mode == 6)
       for (int it = 0; it < iters; ++it) mma_grp_ss_kk_8(tmem, dA, dB, id, it > 0);
-    else
+    else if (mode == 7)
       for (int it = 0; it < iters; ++it) mma_grp_ts_k_8(tmem, tmem + 256, dB, id, it > 0);
+    else if (mode == 8)   // S unit of pass 2: TS, B K-major, N = 64 (x2 per group)
+      for (int it = 0; it < iters; ++it) {
+        mma_grp_ts_k_8(tmem, tmem + 256, dB, idesc_bf16(128, 64, 0, 0), it > 0);
+        mma_grp_ts_k_8(tmem + 64, tmem + 256, dB + 512, idesc_bf16(128, 64, 0, 0), it > 0);
+      }
+    else if (mode == 9)   // dW unit of pass 2: TS, B MN-major, N = 128, K = 64 (x2 per group)
+      for (int it = 0; it < iters; ++it) {
+        const uint64_t dBm = sdesc(aB, ATOM_BYTES, 1024);
+        mma_grp_ts_mn_4(tmem + 128, tmem + 256, dBm, idesc_bf16(128, 128, 0, 1), it > 0);
+        mma_grp_ts_mn_4(tmem + 128, tmem + 288, dBm + 512, idesc_bf16(128, 128, 0, 1), 1u);
+      }
+    else   // mode 10: both of the above (one 128-row tile of pass 2)
+      for (int it = 0; it < iters; ++it) {
+        const uint64_t dBm = sdesc(aB, ATOM_BYTES, 1024);
+        mma_grp_ts_k_8(tmem, tmem + 256, dB, idesc_bf16(128, 64, 0, 0), it > 0);
+        mma_grp_ts_mn_4(tmem + 128, tmem + 320, dBm, idesc_bf16(128, 128, 0, 1), it > 0);
+        mma_grp_ts_k_8(tmem + 64, tmem + 256, dB + 512, idesc_bf16(128, 64, 0, 0), it > 0);
+        mma_grp_ts_mn_4(tmem + 128, tmem + 384, dBm + 512, idesc_bf16(128, 128, 0, 1), 1u);
+      }
     mma_commit_w(bar);
     mbar_wait(bar, 0);
     if (lane == 0) out[0] = clock64() - t0;
@@ -1080,18 +1152,18 @@ int tc_fwd_splits_host(const TcPlan *p, int B) {
   return 2 * tc::fwd_splits(B, p->n_cblocks, p->num_sms, p->max_splits);
 }
 
-void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lse2,
+void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lsep,
                        const int32_t *cls_seg, const int32_t *lseg_ptr, const int32_t *lrow,
                        const float *lw, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
                        float *dbg_dW2T, float *dbg_db2) {
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, lse2, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
   else
     tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, lse2, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
 }
 
