@@ -59,7 +59,8 @@ struct as_ctx {
   StepDesc *desc;
   uint32_t *sk0, *sv0, *sk1, *sv1, *hist;
   int32_t *rowid, *flags, *scan_tmp;
-  int32_t *fseg_id, *fseg_ptr, *fseg_row, *long_list;
+  int32_t *fseg_id, *fseg_ptr, *fseg_row, *long_list, *fseg_of, *rid;
+  float *seg_part;
   float *fseg_val;
   int32_t *lseg_id, *lseg_ptr, *lseg_row, *cls_seg;
   float *lw;
@@ -174,6 +175,9 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_row = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_val = (float *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->long_list = (int32_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_of = (int32_t *)p;
+  p = P(4 * (size_t)D.nnz_cap); if (x) x->rid = (int32_t *)p;
+  p = P(4 * 2 * (size_t)D.h * ((size_t)D.nnz_cap / 16 + 1)); if (x) x->seg_part = (float *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.lab_cap + 1)); if (x) x->lseg_ptr = (int32_t *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_row = (int32_t *)p;
@@ -525,18 +529,19 @@ int as_train_step(as_ctx *x, float *loss_out) {
   x->launches += n_transpose_launches(key_bits(D.d)) + n_transpose_launches(key_bits(D.C)) + 2;
   as::launch_transpose(ss, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->fseg_id,
-                       x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val);
+                       x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val, x->fseg_of);
   as::launch_transpose(ss, x->lab_ptr, x->lab, rows, &d->nlab, D.lab_cap, key_bits(D.C), x->sk0,
                        x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->lseg_id,
-                       x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr);
+                       x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr, nullptr);
   as::launch_class_map(ss, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
   as::launch_label_weights(ss, d, D.lab_cap, x->lseg_row, x->lab_ptr, x->lw);
   ph_end(x, AS_PH_TRANSPOSE, ss);
   cudaEventRecord(x->ev_join, ss);
   // a4: SpMM forward
   ph_begin(x, AS_PH_SPMM);
-  x->launches += 1;
-  as::launch_spmm(s, D.h, d, D.bpad, x->row_ptr, x->col, x->val, W1, b1, x->Hf, x->Hb);
+  x->launches += 3;
+  as::launch_spmm_chunked(s, D.h, d, rows, D.bpad, D.nnz_cap, x->row_ptr, x->col, x->val, x->rid, W1,
+                          b1, x->Hf, x->Hb, x->seg_part);
   ph_end(x, AS_PH_SPMM);
   if (x->cfg.precision == AS_BF16) {
     // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
@@ -589,8 +594,8 @@ int as_train_step(as_ctx *x, float *loss_out) {
   // a7: first-layer gradient (deterministic segmented reduction) + SGD
   ph_begin(x, AS_PH_DW1);
   x->launches += 2 + 1 + 1;
-  as::launch_dw1_sgd(s, D.h, d, D.nnz_cap, x->fseg_id, x->fseg_ptr, x->fseg_row, x->fseg_val, x->dA,
-                     W1, lr, x->long_list, dbg ? x->dbg_dW1 : nullptr);
+  as::launch_dw1_chunked(s, D.h, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
+                         x->fseg_val, x->dA, W1, lr, x->seg_part, dbg ? x->dbg_dW1 : nullptr);
   as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 0);
   as::launch_loss_mean(s, d, x->lossr, x->loss);
   ph_end(x, AS_PH_DW1);

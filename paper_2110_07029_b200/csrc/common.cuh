@@ -50,13 +50,22 @@ void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, in
                       const int *n_dev, int cap, int key_bits, uint32_t *k0, uint32_t *v0,
                       uint32_t *k1, uint32_t *v1, uint32_t *hist, int32_t *rowid, int32_t *flags,
                       int32_t *scan_tmp, int32_t *seg_id, int32_t *seg_ptr, int32_t *seg_row,
-                      int *nseg_dev, const float *val_in, float *seg_val);
+                      int *nseg_dev, const float *val_in, float *seg_val, int32_t *seg_of);
 void launch_class_map(cudaStream_t s, const int32_t *lseg_id, const int *V_dev, int cap,
                       int32_t *cls_seg, int value_is_index);
 // SpMM forward (step a4)
 void launch_spmm(cudaStream_t s, int h, const StepDesc *desc, int bpad, const int64_t *row_ptr,
                  const int32_t *col, const float *val, const float *W1, const float *b1, float *Hf,
                  __nv_bfloat16 *Hb);
+// load-balanced chunked segmented gather-reduce (kernels_segmm.cu)
+void launch_spmm_chunked(cudaStream_t s, int h, const StepDesc *desc, int rows, int bpad, int nnz_cap,
+                         const int64_t *row_ptr, const int32_t *col, const float *val, int32_t *rid,
+                         const float *W1, const float *b1, float *Hf, __nv_bfloat16 *Hb,
+                         float *part);
+void launch_dw1_chunked(cudaStream_t s, int h, StepDesc *desc, int nnz_cap, const int32_t *seg_id,
+                        const int32_t *seg_of, const int32_t *seg_ptr, const int32_t *seg_row,
+                        const float *seg_val, const float *dA, float *W1, float lr, float *part,
+                        float *dbg_dW1);
 // label terms of loss and dH (steps a5)
 void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                         const int64_t *lab_ptr, const int32_t *lab, const float *Hf,

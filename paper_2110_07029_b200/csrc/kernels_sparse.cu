@@ -307,7 +307,7 @@ __global__ void k_seg_flags(const uint32_t *__restrict__ kf, const uint32_t *__r
 __global__ void k_seg_write(const uint32_t *__restrict__ kf, const int32_t *__restrict__ flags,
                             const int32_t *__restrict__ idx, const int *__restrict__ n_dev,
                             int32_t *__restrict__ seg_id, int32_t *__restrict__ seg_ptr,
-                            int *__restrict__ nseg) {
+                            int *__restrict__ nseg, int32_t *__restrict__ seg_of) {
   const int n = *n_dev;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (n == 0) {
@@ -322,6 +322,7 @@ __global__ void k_seg_write(const uint32_t *__restrict__ kf, const int32_t *__re
     seg_id[idx[j]] = (int32_t)kf[j];
     seg_ptr[idx[j]] = j;
   }
+  if (seg_of) seg_of[j] = idx[j] + flags[j] - 1;   // segment of entry j
   if (j == n - 1) {
     const int U = idx[j] + flags[j];
     seg_ptr[U] = n;
@@ -333,7 +334,7 @@ void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, in
                       const int *n_dev, int cap, int key_bits, uint32_t *k0, uint32_t *v0,
                       uint32_t *k1, uint32_t *v1, uint32_t *hist, int32_t *rowid, int32_t *flags,
                       int32_t *scan_tmp, int32_t *seg_id, int32_t *seg_ptr, int32_t *seg_row,
-                      int *nseg_dev, const float *val_in, float *seg_val) {
+                      int *nseg_dev, const float *val_in, float *seg_val, int32_t *seg_of) {
   const int nb = ceil_div(cap > 0 ? cap : 1, kSortTile);
   k_rowid<<<ceil_div((long long)rows * 32, 256), 256, 0, s>>>(ptr, key, rows, rowid, k0, v0);
   uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
@@ -349,7 +350,7 @@ void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, in
   int32_t *idx = scan_tmp;
   int32_t *totals = scan_tmp + (cap > 0 ? cap : 1);
   scan_exclusive(s, flags, idx, totals, n_dev, cap);
-  k_seg_write<<<g, 256, 0, s>>>(ki, flags, idx, n_dev, seg_id, seg_ptr, nseg_dev);
+  k_seg_write<<<g, 256, 0, s>>>(ki, flags, idx, n_dev, seg_id, seg_ptr, nseg_dev, seg_of);
 }
 
 // lw[u] = 1 / (k_r B) for label entry u of the label-sorted batch (R3)
@@ -521,32 +522,41 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // dA_r = dH_r * [A_r > 0]  (R3, R4).  One CTA (h threads) per row.  Partial
 // layout: pm, pl [split][bpad]; pO [split][h][bpad] (coalesced TC epilogue).
 // =====================================================================
-__global__ void k_combine_bf16(const StepDesc *__restrict__ desc, int h, int bpad, int splits,
-                               const float *__restrict__ pm, const float *__restrict__ pl,
-                               const float *__restrict__ pO, const float *__restrict__ labW,
-                               const float *__restrict__ zsum, const float *__restrict__ Hf,
-                               float *__restrict__ lse2, float *__restrict__ lsep,
-                               float *__restrict__ lossr, float *__restrict__ dA) {
-  const int r = blockIdx.x, j = threadIdx.x;
+__global__ void __launch_bounds__(256) k_combine_bf16(
+    const StepDesc *__restrict__ desc, int h, int bpad, int splits, const float *__restrict__ pm,
+    const float *__restrict__ pl, const float *__restrict__ pO, const float *__restrict__ labW,
+    const float *__restrict__ zsum, const float *__restrict__ Hf, float *__restrict__ lse2,
+    float *__restrict__ lsep, float *__restrict__ lossr, float *__restrict__ dA) {
+  // CTA = 32 rows x 16 columns (8 groups of 2); partial reads coalesced over rows
+  const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
   const int B = desc->rows;
-  if (r >= B) {                       // padding rows of the last tile: p = 2^-inf = 0
-    if (j == 0) lsep[r] = INFINITY;
+  if (blockIdx.x * 32 >= B) {         // a CTA of padding rows only
+    const int r = blockIdx.x * 32 + rx;
+    if (jy == 0 && r < bpad && blockIdx.y == 0) lsep[r] = INFINITY;
     return;
   }
+  const bool live = blockIdx.x * 32 + rx < B;
+  const int r = live ? blockIdx.x * 32 + rx : B - 1;   // padding lanes shadow a live row
+  if (!live && jy == 0 && blockIdx.y == 0) lsep[blockIdx.x * 32 + rx] = INFINITY;
+  extern __shared__ float sc[];             // [splits][32] per-slot scales of the rows
   float M = -FLT_MAX;
   for (int s = 0; s < splits; ++s) M = fmaxf(M, pm[(size_t)s * bpad + r]);
-  float l = 0.f, o = 0.f;
-  for (int s = 0; s < splits; ++s) {
+  for (int s = jy; s < splits; s += 8) {
     const float ms = pm[(size_t)s * bpad + r];
-    const float sc = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
-    l = fmaf(pl[(size_t)s * bpad + r], sc, l);
-    o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc, o);
+    sc[s * 32 + rx] = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
   }
-  const float L2 = M + log2f(l);
-  const float invB = 1.0f / (float)B;
-  const float dh = (o / l - labW[(size_t)r * h + j]) * invB;
-  dA[(size_t)r * h + j] = Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
-  if (j == 0) {
+  __syncthreads();
+  float l = 0.f;
+  for (int s = 0; s < splits; ++s) l = fmaf(pl[(size_t)s * bpad + r], sc[s * 32 + rx], l);
+  const float invB = 1.0f / (float)B, invl = 1.0f / l;
+  for (int j = blockIdx.y * 16 + jy; j < h && j < blockIdx.y * 16 + 16; j += 8) {
+    float o = 0.f;
+    for (int s = 0; s < splits; ++s) o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc[s * 32 + rx], o);
+    const float dh = (o * invl - labW[(size_t)r * h + j]) * invB;
+    if (live) dA[(size_t)r * h + j] = Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
+  }
+  if (jy == 0 && live && blockIdx.y == 0) {
+    const float L2 = M + log2f(l);
     lse2[r] = L2;
     lsep[r] = L2 + log2f((float)B);   // pass 2: p / B = 2^(s log2e - lsep)
     lossr[r] = L2 * 0.69314718055994531f - zsum[r];
@@ -557,8 +567,8 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          int splits, const float *pm, const float *pl, const float *pO,
                          const float *labW, const float *zsum, const float *Hf, float *lse2,
                          float *lsep, float *lossr, float *dA) {
-  k_combine_bf16<<<bpad, h, 0, s>>>(desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lsep,
-                                    lossr, dA);
+  k_combine_bf16<<<dim3(ceil_div(bpad, 32), h / 16), 256, (size_t)splits * 32 * 4, s>>>(
+      desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lsep, lossr, dA);
 }
 
 // =====================================================================
@@ -566,21 +576,30 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // order), param[c] -= lr * g_c.  Used for db1 (X = dA) and, in the fp32
 // mode, db2 (X = dZ).  Deterministic.
 // =====================================================================
-__global__ void k_colsum_sgd(const StepDesc *__restrict__ desc, int ncols,
-                             const float *__restrict__ X, long long ldx, float *__restrict__ param,
-                             float lr, float *__restrict__ grad_out) {
-  __shared__ float red[8][33];
+__global__ void __launch_bounds__(1024) k_colsum_sgd(const StepDesc *__restrict__ desc, int ncols,
+                                                     const float *__restrict__ X, long long ldx,
+                                                     float *__restrict__ param, float lr,
+                                                     float *__restrict__ grad_out) {
+  __shared__ float red[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int B = desc->rows;
-  float acc = 0.f;
-  if (c < ncols)
-    for (int r = threadIdx.y; r < B; r += 8) acc += X[(size_t)r * ldx + c];
-  red[threadIdx.y][threadIdx.x] = acc;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (c < ncols) {
+    int r = threadIdx.y;
+    for (; r + 96 < B; r += 128) {
+      a0 += X[(size_t)r * ldx + c];
+      a1 += X[(size_t)(r + 32) * ldx + c];
+      a2 += X[(size_t)(r + 64) * ldx + c];
+      a3 += X[(size_t)(r + 96) * ldx + c];
+    }
+    for (; r < B; r += 32) a0 += X[(size_t)r * ldx + c];
+  }
+  red[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (threadIdx.y == 0 && c < ncols) {
-    float g = red[0][threadIdx.x];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) g += red[q][threadIdx.x];
+    float g = 0.f;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) g += red[q][threadIdx.x];
     param[c] -= lr * g;
     if (grad_out) grad_out[c] = g;
   }
@@ -589,8 +608,8 @@ __global__ void k_colsum_sgd(const StepDesc *__restrict__ desc, int ncols,
 void launch_colsum_sgd(cudaStream_t s, const StepDesc *desc, int n_rows_cap, int ncols,
                        const float *X, long long ldx, float *param, float lr, float *grad_out) {
   (void)n_rows_cap;
-  k_colsum_sgd<<<ceil_div(ncols, 32), dim3(32, 8), 0, s>>>(desc, ncols, X, ldx, param, lr,
-                                                            grad_out);
+  k_colsum_sgd<<<ceil_div(ncols, 32), dim3(32, 32), 0, s>>>(desc, ncols, X, ldx, param, lr,
+                                                             grad_out);
 }
 
 // =====================================================================

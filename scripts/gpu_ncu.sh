@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
 export ADASGD_NO_BUILD=1
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_out_ -s 4 -c 2 -o gpurun_out/prof_v3 -f python scripts/probe_full.py amazon670k 60000 > gpurun_out/ncu_v3.log 2>&1; echo "rc=$?"
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 200 -c 150 --csv --log-file gpurun_out/launches_probe.csv python scripts/probe_full.py amazon670k 60000 > gpurun_out/ncu_probe.log 2>&1; echo "rc=$?"
