@@ -315,9 +315,19 @@ def main():
         peak_t = 0.0
     spmm_bytes = (4 * cfg.h + 8) * cfg.avg_nnz * my_samples + 8 * my_samples + 4 * cfg.h * my_samples
     spmm_gbs = spmm_bytes / (ph_ms[2] / 1e3) / 1e9 if ph_ms[2] > 0 else 0.0
+    traffic, traffic_src = None, None
+    try:                       # dram bytes per launch from the committed `ncu --set full` capture
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+        ks = ["k_out_fwd<%d>" % cfg.h, "k_out_bwd<%d>" % cfg.h]
+        if args.config == "amazon670k" and all(k in tr for k in ks):
+            traffic = sum(tr[k]["dram_bytes"] for k in ks)
+            traffic_src = "profiles/ncu_traffic.json (%s; pass1+pass2 per SGD step)" % tr[ks[0]]["report"]
+    except (OSError, ValueError):
+        pass
     roof = {"bound": "tensor", "kernel": "out_fwd+out_bwd (tcgen05 passes 1+2, one launch each per SGD step)",
             "achieved": tflops_alg, "peak": peak_t, "unit": "TFLOP/s",
-            "frac": tflops_alg / peak_t if peak_t else None, "traffic": None,
+            "frac": tflops_alg / peak_t if peak_t else None, "traffic": traffic, "traffic_source": traffic_src,
+            "bytes_alg_per_step": float(cfg.C * cfg.h * (2 + 2 + 4 + 4 + 2)),  # W2T bf16 read x2, fp32 RMW, bf16 write
             "flops_per_launch_alg": 6.0 * cfg.h * cfg.C * cfg.b_max,
             "issued_frac": (fl_iss / t_out / 1e12) / peak_t if (peak_t and t_out) else None,
             "peak_kind": "%s bf16_tflops_sustained (kernel timed inside a long step)" % pk_kind,
