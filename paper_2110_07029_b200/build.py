@@ -27,18 +27,22 @@ def _needs_build():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False, jobs=5, trace=False):
+def build(force=False, verbose=False, jobs=5, trace=False, variant=None, defines=()):
+    """variant: experiment build libadasgd_x_<variant>.so with extra -D defines
+    (tools only; the product library is always the plain build)."""
     out = OUT_TRACE if trace else OUT
-    if not force and not trace and not _needs_build():
+    if variant:
+        out = os.path.join(HERE, "libadasgd_x_%s.so" % variant)
+    if not force and not trace and not variant and not _needs_build():
         return OUT
-    objdir = os.path.join(HERE, "build_trace" if trace else "build")
+    objdir = os.path.join(HERE, "build_x_" + variant if variant else ("build_trace" if trace else "build"))
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         objs.append(obj)
-        cmd = [NVCC] + ARCH + FLAGS + (["-DAS_TRACE"] if trace else []) + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + ARCH + FLAGS + (["-DAS_TRACE"] if trace else []) + ["-D" + d for d in defines] + ["-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         else:
@@ -60,4 +64,8 @@ def build(force=False, verbose=False, jobs=5, trace=False):
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))
+    if "--variant" in sys.argv:      # --variant NAME DEF1,DEF2
+        i = sys.argv.index("--variant")
+        print(build(variant=sys.argv[i + 1], defines=[d for d in sys.argv[i + 2].split(",") if d]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

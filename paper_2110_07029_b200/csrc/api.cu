@@ -828,7 +828,7 @@ int as_trace_dump(int64_t *out, int32_t max_events) {
 }
 
 int as_tc_bench(int32_t mode, int32_t iters, int64_t *cycles) {
-  if (!cycles || mode < 0 || mode > 10 || iters < 1) return as_fail(AS_E_INVALID, "bad arguments");
+  if (!cycles || mode < 0 || mode > 14 || iters < 1) return as_fail(AS_E_INVALID, "bad arguments");
   long long c = 0;
   if (as::tc_bench(mode, iters, &c) != 0) return as_fail(AS_E_CUDA, "tc_bench failed");
   *cycles = c;

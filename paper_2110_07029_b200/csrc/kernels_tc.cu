@@ -166,6 +166,39 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100): one issue slot per pair
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t v;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(lo), "f"(hi));
+  return v;
+}
+__device__ __forceinline__ void f2split(uint64_t v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// Experiment switches (scripts/x_probe.sh builds; never set in the product
+// library): AS_X_NOEXP replaces ex2 by a move, AS_X_NOSOFT skips the softmax
+// TMEM work, AS_X_NOMMA1 / AS_X_NOMMA2 skip the first / second GEMM of a pass,
+// AS_X_NOTMA reuses the first operand stages, AS_X_NOUPD skips pass 2's SGD.
+#ifdef AS_X_NOEXP
+#define XEX2(v) (v)
+#else
+#define XEX2(v) ex2(v)
+#endif
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -204,8 +237,8 @@ template <int H>
 struct FwdCfg {
   static constexpr int NST = H == 128 ? 4 : 2;    // W stages
   static constexpr int TILE = BM * H * 2;         // bytes of a 128 x H bf16 tile
-  static constexpr int THREADS = 10 * 32;
-  static constexpr int SMEM = TILE /*H*/ + NST * TILE + 2 * 2 * BM * 4 /*b2*/ + 256;
+  static constexpr int THREADS = 12 * 32;        // 3 warpgroups (setmaxnreg granularity)
+  static constexpr int SMEM = TILE /*H*/ + NST * TILE + 2 * 2 * BM * 4 /*b2*/ + 64 /*b2 max*/ + 256;
   static_assert(SMEM <= 232448, "pass-1 shared memory exceeds 227 KB");
   static_assert(H == 128 || H == 256, "h");
 };
@@ -246,7 +279,8 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   uint8_t *sH = smem_raw;
   uint8_t *sW = smem_raw + TILE;
   float *sB2 = (float *)(sW + NST * TILE);          // [2 WG][2][128]
-  uint64_t *bars = (uint64_t *)(sB2 + 4 * BM);
+  float *sBmax = sB2 + 4 * BM;                       // [2 WG][2][4 warps] block max of b2
+  uint64_t *bars = (uint64_t *)(sBmax + 16);
   uint64_t *h_full = bars, *w_full = bars + 1, *w_empty = w_full + NST, *s_full = w_empty + NST,
            *p_full = s_full + 2, *o_fin = p_full + 2, *o_done = o_fin + 1;
   uint32_t *tmem_slot = (uint32_t *)(o_done + 1);
@@ -260,7 +294,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   const int cb0 = (int)((long long)sp * n_cblocks / splits);
   const int nloc = (int)((long long)(sp + 1) * n_cblocks / splits) - cb0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kProdWarp = 8, kMmaWarp = 9;   // highest ids: scheduler priority
+  constexpr int kProdWarp = 10, kMmaWarp = 11;  // highest ids: scheduler priority; 8-9 idle
 
   if (threadIdx.x == 0) {
     mbar_init(h_full, 1);
@@ -275,20 +309,31 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  // registers: the launch gives every warp 168 (3 warps per SM sub-partition);
+  // warpgroup 2 (producer, MMA, 2 idle warps) hands its share to the softmax
+  // warpgroups, which keep a whole 128-column S row in registers.  Each role
+  // branch adjusts its own budget (setmaxnreg is warpgroup-collective).
+#define AS_REG_DEC() asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory")
+#define AS_REG_INC() asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory")
 
   if (warp == kProdWarp) {
+    AS_REG_DEC();
     if (lane == 0) {  // ---------------- TMA producer
       mbar_expect_tx(h_full, TILE);
       for (int a = 0; a < H / 64; ++a) tma_load_2d(&mapH, h_full, sH + a * ATOM_BYTES, a * 64, rt * BM);
       for (int j = 0; j < nloc; ++j) {
         const int st = j % NST;
         if (j >= NST) mbar_wait(&w_empty[st], ((j / NST) - 1) & 1);
+#ifdef AS_X_NOTMA
+        if (j >= NST) { mbar_arrive(&w_full[st]); continue; }
+#endif
         mbar_expect_tx(&w_full[st], TILE);
         for (int a = 0; a < H / 64; ++a)
           tma_load_2d(&mapW, &w_full[st], sW + st * TILE + a * ATOM_BYTES, a * 64, (cb0 + j) * BM);
       }
     }
   } else if (warp == kMmaWarp) {
+    AS_REG_DEC();
     {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
       constexpr uint32_t idS = idesc_bf16(BM, BM, 0, 0);
       constexpr uint32_t idO = idesc_bf16(BM, H, 0, 1);
@@ -302,10 +347,12 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
         fence_after();
         // S_j overwrites buffer b; O of block j-2 (the last reader of P_{j-2}
         // there) was issued earlier by this warp: tcgen05.mma executes in order.
+#ifndef AS_X_NOMMA1
         if constexpr (H == 128)
           mma_grp_ss_kk_8(tmem + b * BM, dH, sdesc(aW + st * TILE, 16, 1024), idS, 0u);
         else
           mma_grp_ss_kk_16(tmem + b * BM, dH, sdesc(aW + st * TILE, 16, 1024), idS, 0u);
+#endif
         mma_commit_w(&s_full[b]);
       };
       if (nloc > 0) issue_S(0);
@@ -315,8 +362,10 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
         const int g = NWG == 2 ? b : 0;
         mbar_wait(&p_full[b], (j >> 1) & 1);
         fence_after();
+#ifndef AS_X_NOMMA2
         mma_grp_ts_mn_8(tmem + 2 * BM + g * BM, tmem + b * BM, sdesc(aW + st * TILE, ATOM_BYTES, 1024),
                         idO, j >= NWG ? 1u : 0u);
+#endif
         mma_commit_w(&w_empty[st]);
         if (NWG == 1) mma_commit_w(o_done);     // single WG: O_{j} before the rescale at j+1
         if (j + 2 < nloc) issue_S(j + 2);
@@ -324,6 +373,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       mma_commit_w(o_fin);
     }
   } else if (warp < 4 * NWG) {  // ---------------- softmax warpgroups (thread = row)
+    AS_REG_INC();
     const int g = warp >> 2;
     const int q = warp & 3;
     const int row = q * 32 + lane;            // TMEM lane == tile row == loader index
@@ -337,27 +387,41 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       const int b = j & 1;
       float *myB2 = sB2 + (g * 2 + (jj & 1)) * BM;
       myB2[row] = b2n;
+      float wm = b2n;                         // max of b2 (log2 units) over the block
+#pragma unroll
+      for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+      if (lane == 0) sBmax[(g * 2 + (jj & 1)) * 4 + q] = wm;
       if (j + NWG < nloc) {
         const int c = (cb0 + j + NWG) * BM + row;
         b2n = c < C ? b2[c] * LOG2E : -INFINITY;
       }
       named_bar(1 + g, 128);
+      const float *bmx = sBmax + (g * 2 + (jj & 1)) * 4;
+      const float bmax = fmaxf(fmaxf(bmx[0], bmx[1]), fmaxf(bmx[2], bmx[3]));
       // s_full(j) also implies that the O MMA of this WG's previous block (issued
       // before S_j) completed: O is stable and the P region of buffer b is free.
       mbar_wait(&s_full[b], (j >> 1) & 1);
       fence_after();
       const uint32_t tS = tlq + b * BM;
       const float *bb = myB2;
-      // pass A: block max (log2 units)
-      float mx = -FLT_MAX;
+#ifndef AS_X_NOSOFT
+      // the whole S row of this block in registers (one TMEM read)
+      uint32_t r[BM];
 #pragma unroll
-      for (int ch = 0; ch < BM / 32; ++ch) {
-        uint32_t r[32];
-        AS_TMEM_LD32(tS + ch * 32, r);
-        AS_TMEM_WAIT_LD(r);
+      for (int ch = 0; ch < BM / 32; ++ch) AS_TMEM_LD32(tS + ch * 32, (r + ch * 32));
 #pragma unroll
-        for (int k = 0; k < 32; ++k) mx = fmaxf(mx, fmaf(__uint_as_float(r[k]), LOG2E, bb[ch * 32 + k]));
-      }
+      for (int ch = 0; ch < BM / 32; ++ch) AS_TMEM_WAIT_LD((r + ch * 32));
+      // reference value for the exponentials: max_k(s_k) log2e + max_k(b2_k) is an
+      // upper bound of the block max of s_k log2e + b2_k (exact when b2 is flat;
+      // only the scaling of the partial sums depends on it, R-readings DESIGN 3)
+      float mt[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mt[k] = __uint_as_float(r[k]);
+#pragma unroll
+      for (int k = 8; k < BM; ++k) mt[k & 7] = fmaxf(mt[k & 7], __uint_as_float(r[k]));
+      const float mx = fmaf(fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
+                                  fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7]))),
+                            LOG2E, bmax);
       float m_new = m_used;
       if (mx > m_used + 8.f) m_new = mx;   // lazy rescale: p <= 2^8 otherwise
       if (NWG == 1 && jj > 0) {               // single WG: O of block j-1 must be done
@@ -373,34 +437,41 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       if (jj > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
         for (int ch = 0; ch < H / 32; ++ch) {
-          uint32_t r[32];
-          AS_TMEM_LD32(tO + ch * 32, r);
-          AS_TMEM_WAIT_LD(r);
+          uint32_t ro[32];
+          AS_TMEM_LD32(tO + ch * 32, ro);
+          AS_TMEM_WAIT_LD(ro);
 #pragma unroll
-          for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * sc);
-          AS_TMEM_ST32(tO + ch * 32, r);
+          for (int k = 0; k < 32; ++k) ro[k] = __float_as_uint(__uint_as_float(ro[k]) * sc);
+          AS_TMEM_ST32(tO + ch * 32, ro);
         }
       }
-      // pass B: P = 2^(s - m) chunk by chunk, packed bf16 written over the S
-      // columns already consumed (chunk ch -> columns [16ch, 16ch + 16))
-      float rs = 0.f;
+      // P = 2^(s log2e + b2 - m) with packed fp32x2 FMA/ADD, bf16 pairs written
+      // over S (chunk ch -> columns [16ch, 16ch + 16), all of S already read)
+      const uint64_t l2e2 = f2(LOG2E, LOG2E), negm2 = f2(-m_new, -m_new);
+      uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
       for (int ch = 0; ch < BM / 32; ++ch) {
-        uint32_t r[32];
-        AS_TMEM_LD32(tS + ch * 32, r);
-        AS_TMEM_WAIT_LD(r);
         uint32_t pk[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          const float p0 = ex2(fmaf(__uint_as_float(r[2 * u]), LOG2E, bb[ch * 32 + 2 * u]) - m_new);
-          const float p1 = ex2(fmaf(__uint_as_float(r[2 * u + 1]), LOG2E, bb[ch * 32 + 2 * u + 1]) - m_new);
-          rs += p0 + p1;
+          const int k = ch * 32 + 2 * u;
+          const float2 bv = *reinterpret_cast<const float2 *>(bb + k);
+          uint64_t x = ffma2(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), l2e2, f2(bv.x, bv.y));
+          x = fadd2(x, negm2);
+          float x0, x1;
+          f2split(x, x0, x1);
+          const float p0 = XEX2(x0), p1 = XEX2(x1);
+          acc[u & 3] = fadd2(acc[u & 3], f2(p0, p1));
           pk[u] = pack_bf16x2(p0, p1);
         }
         AS_TMEM_ST16(tS + ch * 16, pk);
       }
-      l += rs;
+      acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+      float s0, s1;
+      f2split(acc[0], s0, s1);
+      l += s0 + s1;
       tmem_wait_st();
+#endif
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
@@ -425,12 +496,15 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     pm[slot * bpad + grow] = m_used;
     pl[slot * bpad + grow] = l;
   } else if (NWG == 1 && warp < 8) {          // h = 256: idle second WG fills its empty slot
+    AS_REG_INC();
     const int q = warp & 3;
     const int grow = rt * BM + q * 32 + lane;
     const size_t slot = (size_t)sp * 2 + 1;
     for (int k = 0; k < H; ++k) pO[(slot * H + k) * bpad + grow] = 0.f;
     pm[slot * bpad + grow] = -FLT_MAX;
     pl[slot * bpad + grow] = 0.f;
+  } else {                                    // warps 8-9: idle
+    AS_REG_DEC();
   }
   fence_before();
   __syncthreads();
@@ -532,6 +606,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           const int st = it % NSH;
           if (it >= NSH) mbar_wait(&h_empty[st], ((it / NSH) - 1) & 1);
           TRACE(2, true, 10, t);
+#ifdef AS_X_NOTMA
+          if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
+#endif
           mbar_expect_tx(&h_full[st], TILE);
           for (int a = 0; a < H / 64; ++a)
             tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
@@ -546,6 +623,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       auto issue_S = [&](int gu) {
         const int kb = gu / NU, v = gu - kb * NU, t = v >> 1, hh = v & 1;
         const int it = kb * RT + t, st = it % NSH, b = gu % NSB, wb = kb % NWT;
+        TRACE(0, lane == 0, 15, v);
         if (v == 0) mbar_wait(&wt_full[wb], (kb / NWT) & 1);
         if (hh == 0) mbar_wait(&h_full[st], (it / NSH) & 1);
         TRACE(0, lane == 0, 5, v);
@@ -553,10 +631,12 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         // buffer b was last read (G^T of unit gu - NSB) by a dW issued earlier by
         // this warp: tcgen05.mma executes in issue order
         const uint64_t dB = sdesc(aH + st * TILE + hh * 8192, 16, 1024);
+#ifndef AS_X_NOMMA1
         if constexpr (H == 128)
           mma_grp_ts_k_8(tmem + b * 64, tmem + COL_W + wb * WCOLS, dB, idS, 0u);
         else
           mma_grp_ts_k_16(tmem + b * 64, tmem + COL_W + wb * WCOLS, dB, idS, 0u);
+#endif
         mma_commit_w(&s_full[b]);
       };
       auto do_dw = [&](int gu) {
@@ -565,10 +645,14 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         TRACE(0, lane == 0, 1, v);
         mbar_wait(&p_full[b], (gu / NSB) & 1);
         TRACE(0, lane == 0, 2, v);
+        TRACE(0, lane == 0 && v == 0, 3, v);
         if (v == 0 && kb >= 1) mbar_wait(dw_empty, (kb - 1) & 1);
+        TRACE(0, lane == 0 && v == 0, 4, v);
         fence_after();
+#ifndef AS_X_NOMMA2
         mma_grp_ts_mn_4(tmem + COL_DW, tmem + b * 64, sdesc(aH + st * TILE + hh * 8192, ATOM_BYTES, 1024),
                         idW, v > 0 ? 1u : 0u);
+#endif
         if (hh == 1) mma_commit_w(&h_empty[st]);
         if (v == NU - 1) mma_commit_w(dw_full);
       };
@@ -617,6 +701,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       mbar_wait(&s_full[b], (gu / NSB) & 1);
       TRACE(1, threadIdx.x == 0, 7, v);
       fence_after();
+#ifndef AS_X_NOSOFT
       uint32_t r0[32], r1[32];
       AS_TMEM_LD32(tl + b * 64, r0);
       AS_TMEM_LD32(tl + b * 64 + 32, r1);
@@ -625,15 +710,20 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       AS_TMEM_WAIT_LD(r0);
       AS_TMEM_WAIT_LD(r1);
       float vv[64];
+      const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
 #pragma unroll
       for (int k4 = 0; k4 < 16; ++k4) {
         const float4 l4 = __ldg(lq + k4);
-        const float lk[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int k = 4 * k4 + m;
-          const uint32_t x = k < 32 ? r0[k] : r1[k - 32];
-          vv[k] = ex2(fmaf(__uint_as_float(x), LOG2E, b2c) - lk[m]);
+        for (int m = 0; m < 2; ++m) {         // packed: x = s log2e + b2 - lse'
+          const int k = 4 * k4 + 2 * m;
+          const uint32_t xa = k < 32 ? r0[k] : r1[k - 32], xb = k < 32 ? r0[k + 1] : r1[k - 31];
+          uint64_t x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
+          x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
+          float x0, x1;
+          f2split(x, x0, x1);
+          vv[k] = XEX2(x0);
+          vv[k + 1] = XEX2(x1);
         }
       }
       const int base = 64 * v;
@@ -649,14 +739,21 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         lnw = lc < le ? lw[lc] : 0.f;
       }
       uint32_t pk[32];                        // 64 bf16 of G^T, packed in pairs
+      uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
-        db2 += vv[2 * u] + vv[2 * u + 1];
+        dacc[u & 3] = fadd2(dacc[u & 3], f2(vv[2 * u], vv[2 * u + 1]));
         pk[u] = pack_bf16x2(vv[2 * u], vv[2 * u + 1]);
+      }
+      {
+        float d0, d1;
+        f2split(fadd2(fadd2(dacc[0], dacc[1]), fadd2(dacc[2], dacc[3])), d0, d1);
+        db2 += d0 + d1;
       }
       AS_TMEM_ST32(tl + b * 64, pk);          // G^T over the consumed S^T columns
       TRACE(1, threadIdx.x == 0, 8, v);
       tmem_wait_st();
+#endif
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
@@ -723,8 +820,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         if (kb + NWT < NB) load_wt(kb + NWT);
         named_bar(3, 128);
         // (3) fused SGD, coalesced: warp q -> classes 32q..32q+31, 4 per instruction
+#ifdef AS_X_NOUPD
+        constexpr int NCH_UPD = 0;
+#else
+        constexpr int NCH_UPD = NCH;
+#endif
 #pragma unroll 1
-        for (int ch = 0; ch < NCH; ++ch) {
+        for (int ch = 0; ch < NCH_UPD; ++ch) {
           float4 w[8];
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
@@ -943,6 +1045,25 @@ __global__ void __launch_bounds__(128, 1) k_tc_bench(int mode, int iters, long l
         const uint64_t dBm = sdesc(aB, ATOM_BYTES, 1024);
         mma_grp_ts_mn_4(tmem + 128, tmem + 256, dBm, idesc_bf16(128, 128, 0, 1), it > 0);
         mma_grp_ts_mn_4(tmem + 128, tmem + 288, dBm + 512, idesc_bf16(128, 128, 0, 1), 1u);
+      }
+    else if (mode == 11 || mode == 12)
+      // pass-2 order: dW(u) reads G^T from buffer u % 4, then S(u + 4) is written
+      // to buffer u % 4 (mode 11: adjacent WAR on TMEM) or to buffer (u + 2) % 4
+      // (mode 12); per iteration two 64-row units
+      for (int it = 0; it < 2 * iters; ++it) {
+        const uint64_t dBm = sdesc(aB, ATOM_BYTES, 1024);
+        const uint32_t rb = (it & 3) * 64, wb = mode == 11 ? rb : ((it + 2) & 3) * 64;
+        mma_grp_ts_mn_4(tmem + 384, tmem + rb, dBm, idesc_bf16(128, 128, 0, 1), it > 0);
+        mma_grp_ts_k_8(tmem + wb, tmem + 256, dB, idesc_bf16(128, 64, 0, 0), 0u);
+      }
+    else if (mode == 13 || mode == 14)
+      // pass-1 order: O(j) reads P from buffer j % 2, then S(j + 2) is written to
+      // buffer j % 2 (mode 13) / a third buffer (mode 14); per iteration one block
+      for (int it = 0; it < iters; ++it) {
+        const uint64_t dBm = sdesc(aB, ATOM_BYTES, 1024);
+        const uint32_t rb = (it & 1) * 128, wb = mode == 13 ? rb : 256;
+        mma_grp_ts_mn_8(tmem + 384, tmem + rb, dBm, idesc_bf16(128, 128, 0, 1), it > 0);
+        mma_grp_ss_kk_8(tmem + wb, dA, dB, idesc_bf16(128, 128, 0, 0), 0u);
       }
     else   // mode 10: both of the above (one 128-row tile of pass 2)
       for (int it = 0; it < iters; ++it) {
