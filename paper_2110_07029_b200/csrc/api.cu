@@ -34,6 +34,7 @@ struct Layout {
 struct Dims {
   long long d, C, P;
   int h, b_max, bpad, nnz_cap, lab_cap, sort_cap, max_splits, splitk;
+  int bw, tr_tiles;   // transpose bitmap words per key, scan tiles
 };
 
 int key_bits(long long n) {
@@ -57,9 +58,12 @@ struct as_ctx {
   int32_t *col, *lab;
   float *val;
   StepDesc *desc;
-  uint32_t *sk0, *sv0, *sk1, *sv1, *hist;
-  int32_t *rowid, *flags, *scan_tmp;
-  int32_t *fseg_id, *fseg_ptr, *fseg_row, *long_list, *fseg_of, *rid;
+  // dense per-key transpose state (idle between steps: counts 0, bitmaps 0)
+  int32_t *fcnt, *fsidx, *lcnt;
+  uint32_t *fbits, *lbits;
+  unsigned long long *tile_state;
+  int *ticket, *arrive;
+  int32_t *fseg_id, *fseg_ptr, *fseg_row, *fseg_of, *rid, *lrid;
   float *seg_part;
   float *fseg_val;
   int32_t *lseg_id, *lseg_ptr, *lseg_row, *cls_seg;
@@ -135,7 +139,9 @@ Dims dims_of(const as_config *c) {
   D.bpad = (c->b_max + 127) / 128 * 128;
   D.nnz_cap = c->b_max * c->max_row_nnz;
   D.lab_cap = c->b_max * c->max_row_labels;
-  D.sort_cap = std::max(D.nnz_cap, D.lab_cap);
+  D.sort_cap = std::max(std::max(D.nnz_cap, D.lab_cap), D.bpad);
+  D.bw = (c->b_max + 127) / 128 * 4;          // bitmap words per key (16-B rows)
+  D.tr_tiles = (D.d + 8191) / 8192 + (D.C + 8191) / 8192;
   D.max_splits = 2 * as::tc_splits(D.h, D.b_max, D.C, 160);  // partial slots (2 per pass-1 CTA)
   D.splitk = (int)std::min<long long>(64, std::max<long long>(1, D.C / 4096));
   return D;
@@ -162,22 +168,22 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.nnz_cap); if (x) x->val = (float *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lab = (int32_t *)p;
   p = P(sizeof(StepDesc)); if (x) x->desc = (StepDesc *)p;
-  p = P(4 * S); if (x) x->sk0 = (uint32_t *)p;
-  p = P(4 * S); if (x) x->sv0 = (uint32_t *)p;
-  p = P(4 * S); if (x) x->sk1 = (uint32_t *)p;
-  p = P(4 * S); if (x) x->sv1 = (uint32_t *)p;
-  p = P(4 * 256 * (S / as::kSortTile + 1)); if (x) x->hist = (uint32_t *)p;
-  p = P(4 * S); if (x) x->rowid = (int32_t *)p;
-  p = P(4 * S); if (x) x->flags = (int32_t *)p;
-  p = P(4 * (S + S / as::kScanTile + 2)); if (x) x->scan_tmp = (int32_t *)p;
+  p = P(4 * (size_t)D.d); if (x) x->fcnt = (int32_t *)p;
+  p = P(4 * (size_t)D.d); if (x) x->fsidx = (int32_t *)p;
+  p = P(4 * (size_t)D.d * D.bw); if (x) x->fbits = (uint32_t *)p;
+  p = P(4 * (size_t)D.C); if (x) x->lcnt = (int32_t *)p;
+  p = P(4 * (size_t)D.C * D.bw); if (x) x->lbits = (uint32_t *)p;
+  p = P(8 * (size_t)D.tr_tiles); if (x) x->tile_state = (unsigned long long *)p;
+  p = P(16); if (x) x->ticket = (int *)p;
+  p = P(4 * S); if (x) x->arrive = (int *)p;
+  p = P(4 * (size_t)D.lab_cap); if (x) x->lrid = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.nnz_cap + 1)); if (x) x->fseg_ptr = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_row = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_val = (float *)p;
-  p = P(4 * (size_t)D.nnz_cap); if (x) x->long_list = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_of = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->rid = (int32_t *)p;
-  p = P(4 * 2 * (size_t)D.h * ((size_t)D.nnz_cap / 16 + 1)); if (x) x->seg_part = (float *)p;
+  p = P(4 * 2 * (size_t)D.h * ((size_t)D.sort_cap * D.h / 2048 + 2)); if (x) x->seg_part = (float *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.lab_cap + 1)); if (x) x->lseg_ptr = (int32_t *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_row = (int32_t *)p;
@@ -291,6 +297,22 @@ int validate_csr(const as_ctx *x, int64_t rows, const int64_t *row_ptr, const in
   return AS_OK;
 }
 
+as::TrArgs tr_args(as_ctx *x) {
+  const Dims &D = x->D;
+  as::TrArgs a{};
+  a.desc = x->desc;
+  a.nnz_cap = (int)D.nnz_cap; a.lab_cap = (int)D.lab_cap; a.d = (int)D.d; a.C = (int)D.C; a.W = D.bw;
+  a.col = x->col; a.rid = x->rid; a.val = x->val;
+  a.fcnt = x->fcnt; a.fsidx = x->fsidx; a.fbits = x->fbits;
+  a.fseg_id = x->fseg_id; a.fseg_ptr = x->fseg_ptr; a.fseg_row = x->fseg_row; a.fseg_of = x->fseg_of;
+  a.fseg_val = x->fseg_val;
+  a.lab = x->lab; a.lrid = x->lrid; a.lab_ptr = x->lab_ptr;
+  a.lcnt = x->lcnt; a.cls_seg = x->cls_seg; a.lbits = x->lbits;
+  a.lseg_id = x->lseg_id; a.lseg_ptr = x->lseg_ptr; a.lseg_row = x->lseg_row; a.lw = x->lw;
+  a.tile_state = x->tile_state; a.ticket = x->ticket;
+  return a;
+}
+
 }  // namespace
 
 extern "C" {
@@ -343,6 +365,14 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
     as::launch_f32_to_bf16(x->stream, x->w + D.d * D.h + D.h, x->w2b, D.C * D.h);
     rc = cuda_check(x, cudaMemsetAsync(x->cls_seg, 0xFF, 4 * D.C, x->stream), "memset");
   }
+  // idle transpose / combine state (returned to idle by every step)
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->fcnt, 0, 4 * (size_t)D.d, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->fbits, 0, 4 * (size_t)D.d * D.bw, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->lcnt, 0, 4 * (size_t)D.C, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->lbits, 0, 4 * (size_t)D.C * D.bw, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->tile_state, 0, 8 * (size_t)D.tr_tiles, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->ticket, 0, 16, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->arrive, 0, 4 * (size_t)D.sort_cap, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->Hb, 0, 2 * (size_t)D.bpad * D.h, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking), "side stream");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming), "event");
@@ -355,7 +385,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   }
   if (!rc && cfg->precision == AS_BF16) {
     x->plan = (as::TcPlan *)malloc(as::tc_plan_bytes());
-    if (as::tc_plan_init(x->plan, D.h, D.b_max, D.C, x->num_sms, x->Hb, x->w2b) != 0)
+    if (as::tc_plan_init(x->plan, D.h, D.b_max, D.C, x->num_sms, x->Hb, x->w2b, x->w + D.d * D.h + D.h) != 0)
       rc = as_fail(AS_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
   }
   if (!rc && cfg->world > 1 && cfg->nccl_unique_id) {
@@ -431,6 +461,8 @@ int as_load_batch_csr(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int
   if (nnz) cudaMemcpyAsync(x->val, vv, 4 * nnz, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(x->lab, ll, 4 * L, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(x->desc, dd, sizeof(StepDesc), cudaMemcpyHostToDevice, s);
+  x->launches += 1;
+  as::launch_entry_rows(s, x->row_ptr, x->lab_ptr, rows, x->rid, x->lrid);
   ph_end(x, AS_PH_BATCH);
   rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], s), "batch H2D");
   if (rc) return rc;
@@ -497,10 +529,10 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
   if (pos < 0) return as_fail(AS_E_INVALID, "pos < 0");
   ph_begin(x, AS_PH_BATCH);
-  x->launches += 3;
+  x->launches += 2;
   as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
                           x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
-                          x->lab, x->ids, x->desc, x->D.nnz_cap, x->D.lab_cap);
+                          x->lab, x->ids, x->rid, x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
   ph_end(x, AS_PH_BATCH);
   const int rc = cuda_check(x, cudaSuccess, "gather batch");
   if (rc) return rc;
@@ -526,22 +558,16 @@ int as_train_step(as_ctx *x, float *loss_out) {
   cudaEventRecord(x->ev_fork, s);
   cudaStreamWaitEvent(ss, x->ev_fork, 0);
   ph_begin(x, AS_PH_TRANSPOSE, ss);
-  x->launches += n_transpose_launches(key_bits(D.d)) + n_transpose_launches(key_bits(D.C)) + 2;
-  as::launch_transpose(ss, x->row_ptr, x->col, rows, &d->nnz, D.nnz_cap, key_bits(D.d), x->sk0,
-                       x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->fseg_id,
-                       x->fseg_ptr, x->fseg_row, &d->U, x->val, x->fseg_val, x->fseg_of);
-  as::launch_transpose(ss, x->lab_ptr, x->lab, rows, &d->nlab, D.lab_cap, key_bits(D.C), x->sk0,
-                       x->sv0, x->sk1, x->sv1, x->hist, x->rowid, x->flags, x->scan_tmp, x->lseg_id,
-                       x->lseg_ptr, x->lseg_row, &d->V, nullptr, nullptr, nullptr);
-  as::launch_class_map(ss, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 1);
-  as::launch_label_weights(ss, d, D.lab_cap, x->lseg_row, x->lab_ptr, x->lw);
+  const as::TrArgs tr = tr_args(x);
+  x->launches += 3;
+  as::launch_transposes(ss, tr);
   ph_end(x, AS_PH_TRANSPOSE, ss);
   cudaEventRecord(x->ev_join, ss);
   // a4: SpMM forward
   ph_begin(x, AS_PH_SPMM);
-  x->launches += 3;
-  as::launch_spmm_chunked(s, D.h, d, rows, D.bpad, D.nnz_cap, x->row_ptr, x->col, x->val, x->rid, W1,
-                          b1, x->Hf, x->Hb, x->seg_part);
+  x->launches += 1;
+  as::launch_spmm_chunked(s, D.h, x->num_sms, d, D.bpad, D.nnz_cap, x->row_ptr, x->col, x->val, x->rid, W1, b1,
+                          x->Hf, x->Hb, x->seg_part, x->arrive);
   ph_end(x, AS_PH_SPMM);
   if (x->cfg.precision == AS_BF16) {
     // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
@@ -593,11 +619,11 @@ int as_train_step(as_ctx *x, float *loss_out) {
   }
   // a7: first-layer gradient (deterministic segmented reduction) + SGD
   ph_begin(x, AS_PH_DW1);
-  x->launches += 2 + 1 + 1;
-  as::launch_dw1_chunked(s, D.h, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
-                         x->fseg_val, x->dA, W1, lr, x->seg_part, dbg ? x->dbg_dW1 : nullptr);
-  as::launch_class_map(s, x->lseg_id, &d->V, D.lab_cap, x->cls_seg, 0);
-  as::launch_loss_mean(s, d, x->lossr, x->loss);
+  x->launches += 2;
+  as::launch_dw1_chunked(s, D.h, x->num_sms, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
+                         x->fseg_val, x->dA, W1, lr, x->seg_part, x->arrive,
+                         dbg ? x->dbg_dW1 : nullptr);
+  as::launch_step_tail(s, tr, x->num_sms, x->lossr, x->loss);
   ph_end(x, AS_PH_DW1);
   int rc = cuda_check(x, cudaSuccess, "train step launch");
   if (rc) return rc;

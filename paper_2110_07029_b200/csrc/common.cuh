@@ -37,6 +37,31 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+__device__ __forceinline__ int ceil_div_dev(int a, int b) { return (a + b - 1) / b; }
+
+// Arguments of the batch transposes (step a3, kernels_transpose.cu).  Dense
+// per-key state lives in the arena and is idle (0 / -1) between steps.
+struct TrArgs {
+  StepDesc *desc;
+  int nnz_cap, lab_cap, d, C, W;              // W = 32-bit bitmap words per key
+  // feature side (CSR entries -> feature-sorted)
+  const int32_t *col, *rid;
+  const float *val;
+  int32_t *fcnt, *fsidx;
+  uint32_t *fbits;
+  int32_t *fseg_id, *fseg_ptr, *fseg_row, *fseg_of;
+  float *fseg_val;
+  // label side (label entries -> label-sorted)
+  const int32_t *lab, *lrid;
+  const int64_t *lab_ptr;
+  int32_t *lcnt, *cls_seg;
+  uint32_t *lbits;
+  int32_t *lseg_id, *lseg_ptr, *lseg_row;
+  float *lw;
+  // single-pass scan state
+  unsigned long long *tile_state;
+  int *ticket;
+};
 
 // ---------------------------------------------------------------- launchers
 // batch construction (step a2)
@@ -44,13 +69,18 @@ void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_
                          const float *ds_val, const int64_t *ds_lab_ptr, const int32_t *ds_lab,
                          const int64_t *order, int64_t n, int64_t pos, int rows,
                          int64_t *row_ptr, int32_t *col, float *val, int64_t *lab_ptr,
-                         int32_t *lab, int64_t *ids, StepDesc *desc, int nnz_cap, int lab_cap);
+                         int32_t *lab, int64_t *ids, int32_t *rid, int32_t *lrid, StepDesc *desc,
+                         int nnz_cap, int lab_cap);
 // batch transposes (step a3)
 void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, int rows,
                       const int *n_dev, int cap, int key_bits, uint32_t *k0, uint32_t *v0,
                       uint32_t *k1, uint32_t *v1, uint32_t *hist, int32_t *rowid, int32_t *flags,
                       int32_t *scan_tmp, int32_t *seg_id, int32_t *seg_ptr, int32_t *seg_row,
                       int *nseg_dev, const float *val_in, float *seg_val, int32_t *seg_of);
+void launch_entry_rows(cudaStream_t s, const int64_t *row_ptr, const int64_t *lab_ptr, int rows,
+                       int32_t *rid, int32_t *lrid);
+void launch_transposes(cudaStream_t s, const TrArgs &a);
+void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss);
 void launch_class_map(cudaStream_t s, const int32_t *lseg_id, const int *V_dev, int cap,
                       int32_t *cls_seg, int value_is_index);
 // SpMM forward (step a4)
@@ -58,14 +88,14 @@ void launch_spmm(cudaStream_t s, int h, const StepDesc *desc, int bpad, const in
                  const int32_t *col, const float *val, const float *W1, const float *b1, float *Hf,
                  __nv_bfloat16 *Hb);
 // load-balanced chunked segmented gather-reduce (kernels_segmm.cu)
-void launch_spmm_chunked(cudaStream_t s, int h, const StepDesc *desc, int rows, int bpad, int nnz_cap,
-                         const int64_t *row_ptr, const int32_t *col, const float *val, int32_t *rid,
-                         const float *W1, const float *b1, float *Hf, __nv_bfloat16 *Hb,
-                         float *part);
-void launch_dw1_chunked(cudaStream_t s, int h, StepDesc *desc, int nnz_cap, const int32_t *seg_id,
+void launch_spmm_chunked(cudaStream_t s, int h, int num_sms, const StepDesc *desc, int bpad, int nnz_cap,
+                         const int64_t *row_ptr, const int32_t *col, const float *val,
+                         const int32_t *rid, const float *W1, const float *b1, float *Hf,
+                         __nv_bfloat16 *Hb, float *part, int *arrive);
+void launch_dw1_chunked(cudaStream_t s, int h, int num_sms, StepDesc *desc, int nnz_cap, const int32_t *seg_id,
                         const int32_t *seg_of, const int32_t *seg_ptr, const int32_t *seg_row,
                         const float *seg_val, const float *dA, float *W1, float lr, float *part,
-                        float *dbg_dW1);
+                        int *arrive, float *dbg_dW1);
 // label terms of loss and dH (steps a5)
 void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                         const int64_t *lab_ptr, const int32_t *lab, const float *Hf,
@@ -115,7 +145,7 @@ void launch_f32_to_bf16(cudaStream_t s, const float *src, __nv_bfloat16 *dst, lo
 struct TcPlan;
 size_t tc_plan_bytes();
 int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const void *Hb,
-                 const void *W2b);
+                 const void *W2b, const void *W2T);
 int tc_splits(int h, int b_max, long long C, int num_sms);
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
                        const float *b2, float *pm, float *pl, float *pO);

@@ -99,47 +99,56 @@ static void scan_exclusive(cudaStream_t s, const int32_t *in, int32_t *out, int3
 // Step a2 on the device: gather `rows` samples of the resident dataset at
 // stream positions [pos, pos+rows) (R10 order) into a rebased batch CSR.
 // =====================================================================
-__global__ void k_gather_count(const int64_t *__restrict__ rp, const int64_t *__restrict__ lp,
-                               const int64_t *__restrict__ order, int64_t n, int64_t pos,
-                               int rows, int64_t *__restrict__ row_ptr,
-                               int64_t *__restrict__ lab_ptr, int64_t *__restrict__ ids) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int64_t p = (pos + r) % n;
-  const int64_t id = order ? order[p] : p;
-  ids[r] = id;
-  row_ptr[r + 1] = rp[id + 1] - rp[id];
-  lab_ptr[r + 1] = lp[id + 1] - lp[id];
-}
-
-__global__ void __launch_bounds__(1024) k_gather_scan(int rows, int64_t *__restrict__ row_ptr,
+// one CTA: stream position -> dataset id, row / label lengths, their scans
+// (rebased row_ptr / lab_ptr) and the step descriptor
+__global__ void __launch_bounds__(1024) k_gather_scan(const int64_t *__restrict__ rp,
+                                                      const int64_t *__restrict__ lp,
+                                                      const int64_t *__restrict__ order, int64_t n,
+                                                      int64_t pos, int rows,
+                                                      int64_t *__restrict__ row_ptr,
                                                       int64_t *__restrict__ lab_ptr,
+                                                      int64_t *__restrict__ ids,
                                                       StepDesc *__restrict__ desc, int nnz_cap,
                                                       int lab_cap) {
-  __shared__ long long bufa[1024], bufb[1024];
+  __shared__ long long wa[32], wb[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   long long ca = 0, cb = 0;
   for (int c = 0; c < rows; c += 1024) {
     const int i = c + threadIdx.x;
-    const long long a = i < rows ? row_ptr[i + 1] : 0, b = i < rows ? lab_ptr[i + 1] : 0;
-    bufa[threadIdx.x] = a;
-    bufb[threadIdx.x] = b;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-      const long long ya = threadIdx.x >= o ? bufa[threadIdx.x - o] : 0;
-      const long long yb = threadIdx.x >= o ? bufb[threadIdx.x - o] : 0;
-      __syncthreads();
-      bufa[threadIdx.x] += ya;
-      bufb[threadIdx.x] += yb;
-      __syncthreads();
-    }
+    long long a = 0, b = 0;
     if (i < rows) {
-      row_ptr[i + 1] = ca + bufa[threadIdx.x];
-      lab_ptr[i + 1] = cb + bufb[threadIdx.x];
+      const int64_t p = (pos + i) % n;
+      const int64_t id = order ? order[p] : p;
+      ids[i] = id;
+      a = rp[id + 1] - rp[id];
+      b = lp[id + 1] - lp[id];
     }
-    const long long la = bufa[1023], lb = bufb[1023];
+    long long ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long ya = __shfl_up_sync(0xffffffffu, ia, o), yb = __shfl_up_sync(0xffffffffu, ib, o);
+      if (lane >= o) { ia += ya; ib += yb; }
+    }
+    if (lane == 31) { wa[w] = ia; wb[w] = ib; }
     __syncthreads();
-    ca += la;
-    cb += lb;
+    if (w == 0) {
+      long long xa = wa[lane], xb = wb[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+        if (lane >= o) { xa += ya; xb += yb; }
+      }
+      wa[lane] = xa; wb[lane] = xb;
+    }
+    __syncthreads();
+    if (i < rows) {
+      row_ptr[i + 1] = ca + (w > 0 ? wa[w - 1] : 0) + ia;
+      lab_ptr[i + 1] = cb + (w > 0 ? wb[w - 1] : 0) + ib;
+    }
+    const long long ta = wa[31], tb = wb[31];
+    __syncthreads();
+    ca += ta;
+    cb += tb;
   }
   if (threadIdx.x == 0) {
     row_ptr[0] = 0;
@@ -154,12 +163,14 @@ __global__ void __launch_bounds__(1024) k_gather_scan(int rows, int64_t *__restr
   }
 }
 
+// one CTA per batch row: copy its entries and write the entry -> row maps
 __global__ void k_gather_copy(const int64_t *__restrict__ rp, const int32_t *__restrict__ dcol,
                               const float *__restrict__ dval, const int64_t *__restrict__ lp,
                               const int32_t *__restrict__ dlab, const int64_t *__restrict__ ids,
                               const int64_t *__restrict__ row_ptr,
                               const int64_t *__restrict__ lab_ptr, int32_t *__restrict__ col,
                               float *__restrict__ val, int32_t *__restrict__ lab,
+                              int32_t *__restrict__ rid, int32_t *__restrict__ lrid,
                               const StepDesc *__restrict__ desc) {
   if (desc->err) return;
   const int r = blockIdx.x;
@@ -168,21 +179,25 @@ __global__ void k_gather_copy(const int64_t *__restrict__ rp, const int32_t *__r
   for (int64_t j = threadIdx.x; j < n0; j += blockDim.x) {
     col[d0 + j] = dcol[s0 + j];
     val[d0 + j] = dval[s0 + j];
+    rid[d0 + j] = r;
   }
   const int64_t s1 = lp[id], n1 = lp[id + 1] - s1, d1 = lab_ptr[r];
-  for (int64_t j = threadIdx.x; j < n1; j += blockDim.x) lab[d1 + j] = dlab[s1 + j];
+  for (int64_t j = threadIdx.x; j < n1; j += blockDim.x) {
+    lab[d1 + j] = dlab[s1 + j];
+    lrid[d1 + j] = r;
+  }
 }
 
 void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_t *ds_col,
                          const float *ds_val, const int64_t *ds_lab_ptr, const int32_t *ds_lab,
                          const int64_t *order, int64_t n, int64_t pos, int rows,
                          int64_t *row_ptr, int32_t *col, float *val, int64_t *lab_ptr,
-                         int32_t *lab, int64_t *ids, StepDesc *desc, int nnz_cap, int lab_cap) {
-  k_gather_count<<<ceil_div(rows, 256), 256, 0, s>>>(ds_row_ptr, ds_lab_ptr, order, n, pos, rows,
-                                                      row_ptr, lab_ptr, ids);
-  k_gather_scan<<<1, 1024, 0, s>>>(rows, row_ptr, lab_ptr, desc, nnz_cap, lab_cap);
+                         int32_t *lab, int64_t *ids, int32_t *rid, int32_t *lrid, StepDesc *desc,
+                         int nnz_cap, int lab_cap) {
+  k_gather_scan<<<1, 1024, 0, s>>>(ds_row_ptr, ds_lab_ptr, order, n, pos, rows, row_ptr, lab_ptr, ids,
+                                   desc, nnz_cap, lab_cap);
   k_gather_copy<<<rows, 128, 0, s>>>(ds_row_ptr, ds_col, ds_val, ds_lab_ptr, ds_lab, ids, row_ptr,
-                                     lab_ptr, col, val, lab, desc);
+                                     lab_ptr, col, val, lab, rid, lrid, desc);
 }
 
 // =====================================================================

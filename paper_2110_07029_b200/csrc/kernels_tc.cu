@@ -84,6 +84,23 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *ba
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   (uint64_t)map),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -519,11 +536,16 @@ struct BwdCfg {
   static constexpr int NWT = H == 128 ? 2 : 1;    // W2T blocks resident in TMEM (A operand)
   static constexpr int WCOLS = H / 2;             // TMEM columns of one W2T block (bf16 pairs)
   static constexpr int TILE = BM * H * 2;
-  static constexpr int THREADS = 14 * 32;
-  static constexpr bool FULLSTAGE = H == 128;     // whole dW2T block staged in smem
-  static constexpr int SROW = FULLSTAGE ? H + 4 : 36;   // staging row (floats, 16-B aligned)
-  static constexpr int TSTAGE = BM * SROW * 4;
-  static constexpr int SMEM = NSH * TILE + TSTAGE + 2 * BM * 4 /*db2*/ + 512 /*barriers*/;
+  static constexpr int THREADS = 16 * 32;        // 4 warpgroups (setmaxnreg granularity)
+  // h = 128: the fp32 W2T block (4 swizzled 32-column boxes) is TMA-loaded one
+  // block ahead, updated in shared memory from the TMEM dW2T accumulator and
+  // TMA-stored; the bf16 shadow is written from registers.
+  // h = 256: chunked register path through a small staging tile.
+  static constexpr bool TMAUPD = H == 128;
+  static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
+  static constexpr int TSTAGE = TMAUPD ? BM * H * 4 : BM * SROW * 4;
+  static constexpr int SMEM = NSH * TILE + TSTAGE + NSH * BM * 4 /*lse' ring*/ + 2 * BM * 4 /*db2*/ +
+                              512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
   static_assert(NSB * 64 + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
 };
@@ -550,27 +572,27 @@ struct BwdCfg {
 template <int H>
 __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
-              const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
+              const __grid_constant__ CUtensorMap mapWf, const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
               int n_cblocks, const int32_t *__restrict__ cls_seg,
               const int32_t *__restrict__ lseg_ptr, const int32_t *__restrict__ lrow,
               const float *__restrict__ lw, float *__restrict__ W2T, float *__restrict__ b2,
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
               float *__restrict__ dbg_db2) {
-  (void)mapW;
   using Cfg = BwdCfg<H>;
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
   constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
-  constexpr bool FULLSTAGE = Cfg::FULLSTAGE;
+  constexpr bool TMAUPD = Cfg::TMAUPD;
   constexpr uint32_t COL_W = NSB * 64, COL_DW = NSB * 64 + NWT * WCOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sHt = smem_raw;
-  float *sT = (float *)(sHt + NSH * TILE);      // dW2T staging [128][SROW]
-  float *sDB = sT + BM * SROW;                  // [2][128] db2 partials of the two WGs
+  float *sT = (float *)(sHt + NSH * TILE);      // h = 128: W2T fp32 block; else dW2T staging
+  float *sL = (float *)((uint8_t *)sT + Cfg::TSTAGE);    // lse' of the rows of each H stage
+  float *sDB = sL + NSH * BM;                   // [2][128] db2 partials of the two WGs
   uint64_t *bars = (uint64_t *)(sDB + 2 * BM);
   uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + NSB,
            *wt_full = p_full + NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
-           *db_full = dw_empty + 1, *db_empty = db_full + 1;
-  uint32_t *tmem_slot = (uint32_t *)(db_empty + 1);
+           *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1;
+  uint32_t *tmem_slot = (uint32_t *)(wf_full + 1);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
 
   const int B = desc->rows;
@@ -589,6 +611,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     mbar_init(dw_empty, 4);
     mbar_init(db_full, 8);
     mbar_init(db_empty, 4);
+    mbar_init(wf_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
@@ -597,7 +620,14 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // registers: 128 per thread at launch; warpgroup 3 (producer, MMA, 2 idle
+  // warps) drops to 40 and the two softmax warpgroups rise to 168 (a whole
+  // 64-column S^T unit plus its lse' values in registers); the update
+  // warpgroup keeps 128.
+#define AS_REG_DEC2() asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory")
+#define AS_REG_INC2() asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory")
   if (warp == kProdWarp) {
+    AS_REG_DEC2();
     if (lane == 0) {  // ---------------- TMA producer (H tiles)
       TRACE_INIT;
       int it = 0;
@@ -609,65 +639,83 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #ifdef AS_X_NOTMA
           if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
 #endif
-          mbar_expect_tx(&h_full[st], TILE);
+          mbar_expect_tx(&h_full[st], TILE + BM * 4);
           for (int a = 0; a < H / 64; ++a)
             tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
+          bulk_load_1d(sL + st * BM, lsep + t * BM, BM * 4, &h_full[st]);
         }
     }
   } else if (warp == kMmaWarp) {
+    AS_REG_DEC2();
     {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
       constexpr uint32_t idS = idesc_bf16(BM, 64, 0, 0);   // S^T_u = W2T_blk . H_u^T
       constexpr uint32_t idW = idesc_bf16(BM, H, 0, 1);    // dW2T += G^T_u . H_u
       const uint32_t aH = smem_u32(sHt);
       TRACE_INIT;
-      auto issue_S = [&](int gu) {
-        const int kb = gu / NU, v = gu - kb * NU, t = v >> 1, hh = v & 1;
-        const int it = kb * RT + t, st = it % NSH, b = gu % NSB, wb = kb % NWT;
-        TRACE(0, lane == 0, 15, v);
-        if (v == 0) mbar_wait(&wt_full[wb], (kb / NWT) & 1);
-        if (hh == 0) mbar_wait(&h_full[st], (it / NSH) & 1);
-        TRACE(0, lane == 0, 5, v);
+      // unit cursors with incremental indices and barrier phases: no integer
+      // division on this warp's per-unit path (the uniform datapath is slow
+      // and a division would queue on the MUFU behind the softmax exps)
+      struct Cur {
+        int kb, v, st, b, wb;
+        uint32_t hph, bph, wph;
+      };
+      auto advance = [&](Cur &c) {
+        ++c.v;
+        if ((c.v & 1) == 0) { if (++c.st == NSH) { c.st = 0; c.hph ^= 1u; } }
+        if (c.v == NU) { c.v = 0; ++c.kb; if (++c.wb == NWT) { c.wb = 0; c.wph ^= 1u; } }
+        if (++c.b == NSB) { c.b = 0; c.bph ^= 1u; }
+      };
+      auto issue_S = [&](const Cur &c) {
+        TRACE(0, lane == 0, 15, c.v);
+        if (c.v == 0) mbar_wait(&wt_full[c.wb], c.wph);
+        if ((c.v & 1) == 0) mbar_wait(&h_full[c.st], c.hph);
+        TRACE(0, lane == 0, 5, c.v);
         fence_after();
         // buffer b was last read (G^T of unit gu - NSB) by a dW issued earlier by
         // this warp: tcgen05.mma executes in issue order
-        const uint64_t dB = sdesc(aH + st * TILE + hh * 8192, 16, 1024);
-#ifndef AS_X_NOMMA1
+        const uint64_t dB = sdesc(aH + c.st * TILE + (c.v & 1) * 8192, 16, 1024);
+#if defined(AS_X_SSS)
+        mma_grp_ss_kk_8(tmem + c.b * 64, sdesc(aH + ((c.st + 1) % NSH) * TILE, 16, 1024), dB, idS, 0u);
+#elif !defined(AS_X_NOMMA1)
         if constexpr (H == 128)
-          mma_grp_ts_k_8(tmem + b * 64, tmem + COL_W + wb * WCOLS, dB, idS, 0u);
+          mma_grp_ts_k_8(tmem + c.b * 64, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
         else
-          mma_grp_ts_k_16(tmem + b * 64, tmem + COL_W + wb * WCOLS, dB, idS, 0u);
+          mma_grp_ts_k_16(tmem + c.b * 64, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
 #endif
-        mma_commit_w(&s_full[b]);
+        mma_commit_w(&s_full[c.b]);
       };
-      auto do_dw = [&](int gu) {
-        const int kb = gu / NU, v = gu - kb * NU, t = v >> 1, hh = v & 1;
-        const int it = kb * RT + t, st = it % NSH, b = gu % NSB;
-        TRACE(0, lane == 0, 1, v);
-        mbar_wait(&p_full[b], (gu / NSB) & 1);
-        TRACE(0, lane == 0, 2, v);
-        TRACE(0, lane == 0 && v == 0, 3, v);
-        if (v == 0 && kb >= 1) mbar_wait(dw_empty, (kb - 1) & 1);
-        TRACE(0, lane == 0 && v == 0, 4, v);
+      uint32_t dwe_ph = 0u;                   // dw_empty phase of the previous block
+      auto do_dw = [&](const Cur &c) {
+        TRACE(0, lane == 0, 1, c.v);
+        mbar_wait(&p_full[c.b], c.bph);
+        TRACE(0, lane == 0, 2, c.v);
+        if (c.v == 0 && c.kb >= 1) { mbar_wait(dw_empty, dwe_ph); dwe_ph ^= 1u; }
         fence_after();
 #ifndef AS_X_NOMMA2
-        mma_grp_ts_mn_4(tmem + COL_DW, tmem + b * 64, sdesc(aH + st * TILE + hh * 8192, ATOM_BYTES, 1024),
-                        idW, v > 0 ? 1u : 0u);
+        mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * 64,
+                        sdesc(aH + c.st * TILE + (c.v & 1) * 8192, ATOM_BYTES, 1024), idW,
+                        c.v > 0 ? 1u : 0u);
 #endif
-        if (hh == 1) mma_commit_w(&h_empty[st]);
-        if (v == NU - 1) mma_commit_w(dw_full);
+        if (c.v & 1) mma_commit_w(&h_empty[c.st]);
+        if (c.v == NU - 1) mma_commit_w(dw_full);
       };
-      for (int gu = 0; gu < NT && gu < NSB; ++gu) issue_S(gu);
+      Cur cs{0, 0, 0, 0, 0, 0u, 0u, 0u}, cd{0, 0, 0, 0, 0, 0u, 0u, 0u};
+      int ns = 0;                             // S units issued
+      for (; ns < NT && ns < NSB; ++ns) { issue_S(cs); advance(cs); }
       for (int gu = 0; gu < NT; ++gu) {
-        do_dw(gu);
-        const int nx = gu + NSB;
-        // with a single TMEM W2T buffer the look-ahead may not cross into the next
-        // block (its W2T is loaded only after this block's last dW completes)
-        if (nx < NT && (NWT > 1 || nx / NU == gu / NU)) issue_S(nx);
-        if (NWT == 1 && gu % NU == NU - 1)
-          for (int k = 0; k < NSB && gu + 1 + k < NT; ++k) issue_S(gu + 1 + k);
+        do_dw(cd);
+        // S runs NSB units ahead; with a single TMEM W2T buffer the look-ahead
+        // may not cross into the next block before this block's last dW
+        while (ns < NT && ns <= gu + NSB && (NWT > 1 || cs.kb == cd.kb || cd.v == NU - 1)) {
+          issue_S(cs);
+          advance(cs);
+          ++ns;
+        }
+        advance(cd);
       }
     }
   } else if (warp < 8) {  // ---------------- softmax warpgroups (units gu % 2 == g)
+    AS_REG_INC2();
     const int g = warp >> 2;
     const int q = warp & 3;
     const int i = q * 32 + lane;              // class inside the block (TMEM lane)
@@ -681,8 +729,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     int nseg = seg_of(0);
     int kb_cur = -1, lc = 0, le = 0, lnr = 0x7fffffff;
     float lnw = 0.f, b2c = 0.f, db2 = 0.f;
+    int kb = 0, v = g, lst = 0, sb = g;      // unit cursor: block, unit, lse' stage, S buffer
+    uint32_t sph = 0u;
     for (int gu = g; gu < NT; gu += 2) {
-      const int kb = gu / NU, v = gu - kb * NU;
       if (kb != kb_cur) {                     // new class block: per-class state
         kb_cur = kb;
         const int c = (blockIdx.x + kb * gridDim.x) * BM + i;
@@ -696,9 +745,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           lnr = lrow[lc]; lnw = lw[lc];
         }
       }
-      const int b = gu % NSB;
+      const int b = sb;
       TRACE(1, threadIdx.x == 0, 6, v);
-      mbar_wait(&s_full[b], (gu / NSB) & 1);
+      mbar_wait(&s_full[b], sph);
       TRACE(1, threadIdx.x == 0, 7, v);
       fence_after();
 #ifndef AS_X_NOSOFT
@@ -706,14 +755,14 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       AS_TMEM_LD32(tl + b * 64, r0);
       AS_TMEM_LD32(tl + b * 64 + 32, r1);
       // lse' = LSE_r * log2e + log2 B of the unit's 64 rows (broadcast, L1-resident)
-      const float4 *lq = reinterpret_cast<const float4 *>(lsep + 64 * v);
+      const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v & 1) * 64);
       AS_TMEM_WAIT_LD(r0);
       AS_TMEM_WAIT_LD(r1);
       float vv[64];
       const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
 #pragma unroll
       for (int k4 = 0; k4 < 16; ++k4) {
-        const float4 l4 = __ldg(lq + k4);
+        const float4 l4 = lq[k4];
 #pragma unroll
         for (int m = 0; m < 2; ++m) {         // packed: x = s log2e + b2 - lse'
           const int k = 4 * k4 + 2 * m;
@@ -763,6 +812,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(db_full);
       }
+      v += 2;                                 // next unit of this WG
+      if (v >= NU) { v -= NU; ++kb; }
+      if (++lst == NSH) lst = 0;
+      sb += 2;
+      if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
     }
   } else if (warp < 12) {  // ---------------- update warps
     const int q = warp & 3;
@@ -778,21 +832,28 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       const int cls = (blockIdx.x + kb_ * gridDim.x) * BM + i;
       const uint4 *src = reinterpret_cast<const uint4 *>(W2b + (size_t)(cls < C ? cls : 0) * H);
 #pragma unroll 1
-      for (int part = 0; part < H / 64; ++part) {
-        uint32_t r[32];
+      for (int half = 0; half < H / 128; ++half) {
+        uint32_t r[64];                       // 128 bf16 of the row: every load in flight
 #pragma unroll
-        for (int v4 = 0; v4 < 8; ++v4) {
-          uint4 x = src[part * 8 + v4];
+        for (int v4 = 0; v4 < 16; ++v4) {
+          uint4 x = src[half * 16 + v4];
           if (cls >= C) x = make_uint4(0u, 0u, 0u, 0u);
           r[4 * v4] = x.x; r[4 * v4 + 1] = x.y; r[4 * v4 + 2] = x.z; r[4 * v4 + 3] = x.w;
         }
-        AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 32 * part, r);
+        AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 64 * half, r);
+        AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 64 * half + 32, (r + 32));
       }
       tmem_wait_st();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&wt_full[wb]);
     };
+    if constexpr (TMAUPD) {                   // fp32 W2T of the first block
+      if (ut == 0 && NB > 0) {
+        mbar_expect_tx(wf_full, BM * H * 4);
+        for (int c = 0; c < 4; ++c) tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, c * 32, blockIdx.x * BM);
+      }
+    }
     for (int kb = 0; kb < NB && kb < NWT; ++kb) load_wt(kb);
     for (int kb = 0; kb < NB; ++kb) {
       const int cb = blockIdx.x + kb * gridDim.x;
@@ -800,58 +861,72 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
-      if constexpr (FULLSTAGE) {
-        // (1) whole dW2T block: TMEM -> smem staging, then release the accumulator
+      if constexpr (TMAUPD) {
+        // fused SGD of the block from the TMEM accumulator (lane i = class i)
+        // and the TMA-loaded fp32 block: W2T -= lr dW2T in place (swizzled
+        // 32-column boxes, conflict-free), bf16 shadow into its staging boxes
+        mbar_wait(wf_full, kb & 1);
+        const uint32_t sw = (uint32_t)(i & 7);
+        const uint32_t aWf = smem_u32(sT) + i * 128;
+        const int cls_i = cb * BM + i;
 #pragma unroll 1
         for (int ch = 0; ch < NCH; ++ch) {
           uint32_t r[32];
           AS_TMEM_LD32(tl + COL_DW + ch * 32, r);
           AS_TMEM_WAIT_LD(r);
+          if (ch == NCH - 1) {                  // accumulator free for block kb+1
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dw_empty);
+          }
+#ifndef AS_X_NOUPD
 #pragma unroll
-          for (int k = 0; k < 32; k += 4)
-            *reinterpret_cast<float4 *>(sT + i * SROW + ch * 32 + k) =
-                make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]),
-                            __uint_as_float(r[k + 2]), __uint_as_float(r[k + 3]));
-        }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dw_empty);
-        // (2) the W2T block two ahead into the TMEM buffer just freed by block kb
-        if (kb + NWT < NB) load_wt(kb + NWT);
-        named_bar(3, 128);
-        // (3) fused SGD, coalesced: warp q -> classes 32q..32q+31, 4 per instruction
-#ifdef AS_X_NOUPD
-        constexpr int NCH_UPD = 0;
-#else
-        constexpr int NCH_UPD = NCH;
+          for (int g = 0; g < 8; g += 2) {
+            float4 w0, w1;
+            const uint32_t a0 = aWf + ch * 16384 + (((uint32_t)g ^ sw) << 4);
+            const uint32_t a1 = aWf + ch * 16384 + (((uint32_t)(g + 1) ^ sw) << 4);
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(w0.x), "=f"(w0.y), "=f"(w0.z), "=f"(w0.w) : "r"(a0));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(w1.x), "=f"(w1.y), "=f"(w1.z), "=f"(w1.w) : "r"(a1));
+            w0.x -= lr * __uint_as_float(r[4 * g]);     w0.y -= lr * __uint_as_float(r[4 * g + 1]);
+            w0.z -= lr * __uint_as_float(r[4 * g + 2]); w0.w -= lr * __uint_as_float(r[4 * g + 3]);
+            w1.x -= lr * __uint_as_float(r[4 * g + 4]); w1.y -= lr * __uint_as_float(r[4 * g + 5]);
+            w1.z -= lr * __uint_as_float(r[4 * g + 6]); w1.w -= lr * __uint_as_float(r[4 * g + 7]);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a0), "f"(w0.x), "f"(w0.y),
+                         "f"(w0.z), "f"(w0.w) : "memory");
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a1), "f"(w1.x), "f"(w1.y),
+                         "f"(w1.z), "f"(w1.w) : "memory");
+            if (cls_i < C)                    // bf16 shadow: 8 columns, one 16-byte store
+              *reinterpret_cast<uint4 *>(W2b + (size_t)cls_i * H + ch * 32 + 4 * g) =
+                  make_uint4(pack_bf16x2(w0.x, w0.y), pack_bf16x2(w0.z, w0.w), pack_bf16x2(w1.x, w1.y),
+                             pack_bf16x2(w1.z, w1.w));
+          }
 #endif
-#pragma unroll 1
-        for (int ch = 0; ch < NCH_UPD; ++ch) {
-          float4 w[8];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const int cls = cb * BM + q * 32 + 4 * m + sub;
-            w[m] = cls < C ? *reinterpret_cast<const float4 *>(W2T + (size_t)cls * H + ch * 32 + hq)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const int cl = q * 32 + 4 * m + sub;
-            const int cls = cb * BM + cl;
-            if (cls < C) {
-              const float4 gv = *reinterpret_cast<const float4 *>(sT + cl * SROW + ch * 32 + hq);
-              float4 nw;
-              nw.x = w[m].x - lr * gv.x; nw.y = w[m].y - lr * gv.y;
-              nw.z = w[m].z - lr * gv.z; nw.w = w[m].w - lr * gv.w;
-              const size_t idx = (size_t)cls * H + ch * 32 + hq;
-              *reinterpret_cast<float4 *>(W2T + idx) = nw;
-              *reinterpret_cast<uint2 *>(W2b + idx) = make_uint2(pack_bf16x2(nw.x, nw.y),
-                                                                 pack_bf16x2(nw.z, nw.w));
-              if (dbg_dW2T) *reinterpret_cast<float4 *>(dbg_dW2T + idx) = gv;
-            }
+          if (dbg_dW2T) {
+            const int cls = cb * BM + i;
+            if (cls < C)
+              for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls * H + ch * 32 + k] = __uint_as_float(r[k]);
           }
         }
-        named_bar(3, 128);                    // staging reads done before the next block
+        // (2) the W2T block two ahead into the TMEM buffer freed by block kb
+        if (kb + NWT < NB) load_wt(kb + NWT);
+        // (3) TMA store of the updated block, then the next block's fp32 W2T
+        //     into the same buffer once the store has read it
+        fence_proxy_async();
+        named_bar(3, 128);
+        if (ut == 0) {
+#ifndef AS_X_NOUPD
+          for (int c = 0; c < 4; ++c) tma_store_2d(&mapWf, (uint8_t *)sT + c * 16384, c * 32, cb * BM);
+          bulk_commit();
+          bulk_wait_read0();
+#endif
+          if (kb + 1 < NB) {
+            mbar_expect_tx(wf_full, BM * H * 4);
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, c * 32, (cb + gridDim.x) * BM);
+          }
+        }
       } else {
         // chunked staging (h = 256): the accumulator is released after the last chunk
 #pragma unroll 1
@@ -902,6 +977,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       }
       TRACE(3, ut == 0, 14, kb);
     }
+    if (TMAUPD && ut == 0) bulk_wait0();      // stores complete before the grid ends
+  } else {                                    // warps 14-15: idle
+    AS_REG_DEC2();
   }
   fence_before();
   __syncthreads();
@@ -1211,7 +1289,7 @@ static int make_map(CUtensorMap *m, const void *base, long long rows, int cols) 
 }
 
 struct TcPlan {
-  CUtensorMap mapH, mapW;
+  CUtensorMap mapH, mapW, mapWf;
   const void *Hb;
   int h, b_max, bpad, n_cblocks, num_sms, max_splits;
   long long C;
@@ -1225,8 +1303,22 @@ int tc_splits(int h, int b_max, long long C, int num_sms) {
   return num_sms < ncb ? num_sms : ncb;   // capacity of the partial buffers
 }
 
+// fp32 row-major [rows][cols] with a {32, 128} box (128-byte rows) and 128-byte swizzle
+static int make_map_f32(CUtensorMap *m, const void *base, long long rows, int cols) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const void *Hb,
-                 const void *W2b) {
+                 const void *W2b, const void *W2T) {
   plan->h = h;
   plan->Hb = Hb;
   plan->b_max = b_max;
@@ -1237,6 +1329,7 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
   plan->max_splits = tc_splits(h, b_max, C, plan->num_sms);
   if (make_map(&plan->mapH, Hb, plan->bpad, h) != 0) return -1;
   if (make_map(&plan->mapW, W2b, C, h) != 0) return -1;
+  if (make_map_f32(&plan->mapWf, W2T, C, h) != 0) return -1;
   static bool attr_done[2] = {false, false};
   const int hi = h == 128 ? 0 : 1;
   if (!attr_done[hi]) {
@@ -1280,11 +1373,11 @@ void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
   else
     tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
 }
 
