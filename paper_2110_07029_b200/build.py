@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
          "-I", CSRC, "--expt-relaxed-constexpr"]
-SOURCES = ["api.cu", "kernels_sparse.cu", "kernels_segmm.cu", "kernels_dense.cu", "kernels_tc.cu",
+SOURCES = ["api.cu", "kernels_sparse.cu", "kernels_segmm.cu", "kernels_dense.cu", "kernels_tc.cu", "kernels_transpose.cu",
            "sched.cpp"]
 
 
