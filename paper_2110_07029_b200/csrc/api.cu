@@ -67,6 +67,7 @@ struct as_ctx {
   float *seg_part;
   float *fseg_val;
   int32_t *lseg_id, *lseg_ptr, *lseg_row, *cls_seg;
+  int4 *cls_lab;
   float *lw;
   float *Hf;
   __nv_bfloat16 *Hb;
@@ -189,6 +190,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_row = (int32_t *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lw = (float *)p;
   p = P(4 * D.C); if (x) x->cls_seg = (int32_t *)p;
+  p = P(16 * D.C); if (x) x->cls_lab = (int4 *)p;
   p = P(4 * (size_t)D.bpad * D.h); if (x) x->Hf = (float *)p;
   p = P(2 * (size_t)D.bpad * D.h); if (x) x->Hb = (__nv_bfloat16 *)p;
   p = P(4 * (size_t)D.b_max * D.h); if (x) x->dA = (float *)p;
@@ -307,7 +309,7 @@ as::TrArgs tr_args(as_ctx *x) {
   a.fseg_id = x->fseg_id; a.fseg_ptr = x->fseg_ptr; a.fseg_row = x->fseg_row; a.fseg_of = x->fseg_of;
   a.fseg_val = x->fseg_val;
   a.lab = x->lab; a.lrid = x->lrid; a.lab_ptr = x->lab_ptr;
-  a.lcnt = x->lcnt; a.cls_seg = x->cls_seg; a.lbits = x->lbits;
+  a.lcnt = x->lcnt; a.cls_seg = x->cls_seg; a.cls_lab = x->cls_lab; a.lbits = x->lbits;
   a.lseg_id = x->lseg_id; a.lseg_ptr = x->lseg_ptr; a.lseg_row = x->lseg_row; a.lw = x->lw;
   a.tile_state = x->tile_state; a.ticket = x->ticket;
   return a;
@@ -367,6 +369,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   }
   // idle transpose / combine state (returned to idle by every step)
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->fcnt, 0, 4 * (size_t)D.d, x->stream), "memset");
+  if (!rc) as::launch_fill_int4(x->stream, x->cls_lab, D.C, 0, 0, 0x7fffffff, 0);
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->fbits, 0, 4 * (size_t)D.d * D.bw, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->lcnt, 0, 4 * (size_t)D.C, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->lbits, 0, 4 * (size_t)D.C * D.bw, x->stream), "memset");
@@ -588,7 +591,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
     ph_begin(x, AS_PH_OUT_BWD);
     x->launches += 1;
-    as::launch_out_bwd_tc(s, x->plan, d, x->lsep, x->cls_seg, x->lseg_ptr, x->lseg_row, x->lw,
+    as::launch_out_bwd_tc(s, x->plan, d, x->lsep, x->cls_lab, x->lseg_ptr, x->lseg_row, x->lw,
                           W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
                           dbg ? x->dbg_db2 : nullptr);
     ph_end(x, AS_PH_OUT_BWD);

@@ -55,6 +55,7 @@ struct TrArgs {
   const int32_t *lab, *lrid;
   const int64_t *lab_ptr;
   int32_t *lcnt, *cls_seg;
+  int4 *cls_lab;                              // per class {first, end, first row, first weight}
   uint32_t *lbits;
   int32_t *lseg_id, *lseg_ptr, *lseg_row;
   float *lw;
@@ -80,6 +81,7 @@ void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, in
 void launch_entry_rows(cudaStream_t s, const int64_t *row_ptr, const int64_t *lab_ptr, int rows,
                        int32_t *rid, int32_t *lrid);
 void launch_transposes(cudaStream_t s, const TrArgs &a);
+void launch_fill_int4(cudaStream_t s, int4 *p, long long n, int x, int y, int z, int w);
 void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss);
 void launch_class_map(cudaStream_t s, const int32_t *lseg_id, const int *V_dev, int cap,
                       int32_t *cls_seg, int value_is_index);
@@ -158,7 +160,7 @@ void launch_gemm_f32_kdev(cudaStream_t s, int M, int N, int K, const float *A, l
                           long long sak, const float *B, long long sbk, long long sbn, float *Cm,
                           long long ldc, const int *K_dev);
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
-                       const float *lsep, const int32_t *cls_seg, const int32_t *lseg_ptr,
+                       const float *lsep, const int4 *cls_lab, const int32_t *lseg_ptr,
                        const int32_t *lrow, const float *lw, float *W2T, float *b2,
                        __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2);
 // per label entry of the label-sorted batch: lw[u] = 1 / (k_r B), r = lrow[u]  (R3)

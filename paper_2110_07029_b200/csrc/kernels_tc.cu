@@ -563,7 +563,9 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 template <int H>
 struct BwdCfg {
   static constexpr int NSH = H == 128 ? 4 : 2;    // H tile stages (128 rows each)
-  static constexpr int NSB = H == 128 ? 4 : 2;    // S^T unit buffers (64 rows = 64 columns)
+  static constexpr int UNIT = H == 128 ? 128 : 64; // batch rows per unit = S^T columns per buffer
+  static constexpr int HPT = 128 / UNIT;          // units per 128-row H tile
+  static constexpr int NSB = 2;                   // S^T unit buffers
   static constexpr int NWT = H == 128 ? 2 : 1;    // W2T blocks resident in TMEM (A operand)
   static constexpr int WCOLS = H / 2;             // TMEM columns of one W2T block (bf16 pairs)
   static constexpr int TILE = BM * H * 2;
@@ -578,7 +580,7 @@ struct BwdCfg {
   static constexpr int SMEM = NSH * TILE + TSTAGE + NSH * BM * 4 /*lse' ring*/ + 2 * BM * 4 /*db2*/ +
                               512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
-  static_assert(NSB * 64 + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
+  static_assert(NSB * UNIT + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
 };
 
 // =====================================================================
@@ -604,16 +606,17 @@ template <int H>
 __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
               const __grid_constant__ CUtensorMap mapWf, const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
-              int n_cblocks, const int32_t *__restrict__ cls_seg,
+              int n_cblocks, const int4 *__restrict__ cls_lab,
               const int32_t *__restrict__ lseg_ptr, const int32_t *__restrict__ lrow,
               const float *__restrict__ lw, float *__restrict__ W2T, float *__restrict__ b2,
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
               float *__restrict__ dbg_db2) {
   using Cfg = BwdCfg<H>;
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
+  constexpr int UNIT = Cfg::UNIT, HPT = Cfg::HPT;
   constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
   constexpr bool TMAUPD = Cfg::TMAUPD;
-  constexpr uint32_t COL_W = NSB * 64, COL_DW = NSB * 64 + NWT * WCOLS;
+  constexpr uint32_t COL_W = NSB * UNIT, COL_DW = NSB * UNIT + NWT * WCOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sHt = smem_raw;
   float *sT = (float *)(sHt + NSH * TILE);      // h = 128: W2T fp32 block; else dW2T staging
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 
   const int B = desc->rows;
   const int RT = (B + BM - 1) / BM;               // 128-row H tiles
-  const int NU = 2 * RT;                          // 64-row units per class block
+  const int NU = HPT * RT;                        // units per class block
   const int NB = blockIdx.x < n_cblocks ? (n_cblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int NT = NB * NU;                         // units of this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   } else if (warp == kMmaWarp) {
     AS_REG_DEC2();
     {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
-      constexpr uint32_t idS = idesc_bf16(BM, 64, 0, 0);   // S^T_u = W2T_blk . H_u^T
+      constexpr uint32_t idS = idesc_bf16(BM, UNIT, 0, 0); // S^T_u = W2T_blk . H_u^T
       constexpr uint32_t idW = idesc_bf16(BM, H, 0, 1);    // dW2T += G^T_u . H_u
       const uint32_t aH = smem_u32(sHt);
       TRACE_INIT;
@@ -687,31 +690,29 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       // division on this warp's per-unit path (the uniform datapath is slow
       // and a division would queue on the MUFU behind the softmax exps)
       struct Cur {
-        int kb, v, st, b, wb;
+        int kb, v, st, b, wb, hh;
         uint32_t hph, bph, wph;
       };
       auto advance = [&](Cur &c) {
         ++c.v;
-        if ((c.v & 1) == 0) { if (++c.st == NSH) { c.st = 0; c.hph ^= 1u; } }
+        if (++c.hh == HPT) { c.hh = 0; if (++c.st == NSH) { c.st = 0; c.hph ^= 1u; } }
         if (c.v == NU) { c.v = 0; ++c.kb; if (++c.wb == NWT) { c.wb = 0; c.wph ^= 1u; } }
         if (++c.b == NSB) { c.b = 0; c.bph ^= 1u; }
       };
       auto issue_S = [&](const Cur &c) {
         TRACE(0, lane == 0, 15, c.v);
         if (c.v == 0) mbar_wait(&wt_full[c.wb], c.wph);
-        if ((c.v & 1) == 0) mbar_wait(&h_full[c.st], c.hph);
+        if (c.hh == 0) mbar_wait(&h_full[c.st], c.hph);
         TRACE(0, lane == 0, 5, c.v);
         fence_after();
         // buffer b was last read (G^T of unit gu - NSB) by a dW issued earlier by
         // this warp: tcgen05.mma executes in issue order
-        const uint64_t dB = sdesc(aH + c.st * TILE + (c.v & 1) * 8192, 16, 1024);
-#if defined(AS_X_SSS)
-        mma_grp_ss_kk_8(tmem + c.b * 64, sdesc(aH + ((c.st + 1) % NSH) * TILE, 16, 1024), dB, idS, 0u);
-#elif !defined(AS_X_NOMMA1)
+        const uint64_t dB = sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), 16, 1024);
+#ifndef AS_X_NOMMA1
         if constexpr (H == 128)
-          mma_grp_ts_k_8(tmem + c.b * 64, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
+          mma_grp_ts_k_8(tmem + c.b * UNIT, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
         else
-          mma_grp_ts_k_16(tmem + c.b * 64, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
+          mma_grp_ts_k_16(tmem + c.b * UNIT, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
 #endif
         mma_commit_w(&s_full[c.b]);
       };
@@ -723,14 +724,18 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         if (c.v == 0 && c.kb >= 1) { mbar_wait(dw_empty, dwe_ph); dwe_ph ^= 1u; }
         fence_after();
 #ifndef AS_X_NOMMA2
-        mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * 64,
-                        sdesc(aH + c.st * TILE + (c.v & 1) * 8192, ATOM_BYTES, 1024), idW,
-                        c.v > 0 ? 1u : 0u);
+        if constexpr (UNIT == 128)
+          mma_grp_ts_mn_8(tmem + COL_DW, tmem + c.b * UNIT, sdesc(aH + c.st * TILE, ATOM_BYTES, 1024), idW,
+                          c.v > 0 ? 1u : 0u);
+        else
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * UNIT,
+                          sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), ATOM_BYTES, 1024), idW,
+                          c.v > 0 ? 1u : 0u);
 #endif
-        if (c.v & 1) mma_commit_w(&h_empty[c.st]);
+        if (c.hh == HPT - 1) mma_commit_w(&h_empty[c.st]);
         if (c.v == NU - 1) mma_commit_w(dw_full);
       };
-      Cur cs{0, 0, 0, 0, 0, 0u, 0u, 0u}, cd{0, 0, 0, 0, 0, 0u, 0u, 0u};
+      Cur cs{0, 0, 0, 0, 0, 0, 0u, 0u, 0u}, cd{0, 0, 0, 0, 0, 0, 0u, 0u, 0u};
       int ns = 0;                             // S units issued
       for (; ns < NT && ns < NSB; ++ns) { issue_S(cs); advance(cs); }
       for (int gu = 0; gu < NT; ++gu) {
@@ -752,29 +757,28 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     const int i = q * 32 + lane;              // class inside the block (TMEM lane)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     TRACE_INIT;
-    // per-class label range of the next block, prefetched one block ahead
-    auto seg_of = [&](int kb_) -> int {
+    // per-class state of the next block (b2 and the class's label range with
+    // its first label, one 16-byte load from the transposes' cls_lab),
+    // prefetched one block ahead: a block change has no dependent loads
+    struct ClsState { float b2c; int4 cl; };
+    auto cls_state = [&](int kb_) -> ClsState {
+      ClsState st{-INFINITY, make_int4(0, 0, 0x7fffffff, 0)};
       const int c = (blockIdx.x + kb_ * gridDim.x) * BM + i;
-      return (kb_ < NB && c < C) ? cls_seg[c] : -1;
+      if (kb_ < NB && c < C) { st.b2c = b2[c] * LOG2E; st.cl = cls_lab[c]; }
+      return st;                              // invalid class: b2 = -inf -> p = 0
     };
-    int nseg = seg_of(0);
+    ClsState nxt = cls_state(0);
     int kb_cur = -1, lc = 0, le = 0, lnr = 0x7fffffff;
     float lnw = 0.f, b2c = 0.f, db2 = 0.f;
-    int kb = 0, v = g, lst = 0, sb = g;      // unit cursor: block, unit, lse' stage, S buffer
+    int kb = 0, v = g, lst = g / HPT, sb = g; // unit cursor: block, unit, lse' stage, S buffer
     uint32_t sph = 0u;
     for (int gu = g; gu < NT; gu += 2) {
       if (kb != kb_cur) {                     // new class block: per-class state
         kb_cur = kb;
-        const int c = (blockIdx.x + kb * gridDim.x) * BM + i;
-        b2c = c < C ? b2[c] * LOG2E : -INFINITY;   // invalid class -> p = 0
+        b2c = nxt.b2c;
+        lc = nxt.cl.x; le = nxt.cl.y; lnr = nxt.cl.z; lnw = __int_as_float(nxt.cl.w);
         db2 = 0.f;
-        lc = 0; le = 0; lnr = 0x7fffffff; lnw = 0.f;
-        const int sg = nseg;
-        nseg = seg_of(kb + 1);
-        if (sg >= 0) {
-          lc = lseg_ptr[sg]; le = lseg_ptr[sg + 1];
-          lnr = lrow[lc]; lnw = lw[lc];
-        }
+        nxt = cls_state(kb + 1);
       }
       const int b = sb;
       TRACE(1, threadIdx.x == 0, 6, v);
@@ -782,59 +786,63 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       TRACE(1, threadIdx.x == 0, 7, v);
       fence_after();
 #ifndef AS_X_NOSOFT
-      uint32_t r0[32], r1[32];
-      AS_TMEM_LD32(tl + b * 64, r0);
-      AS_TMEM_LD32(tl + b * 64 + 32, r1);
-      // lse' = LSE_r * log2e + log2 B of the unit's 64 rows (broadcast, L1-resident)
-      const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v & 1) * 64);
-      AS_TMEM_WAIT_LD(r0);
-      AS_TMEM_WAIT_LD(r1);
-      float vv[64];
-      const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
+#pragma unroll 1
+      for (int half = 0; half < UNIT / 64; ++half) {   // 64 rows of the unit at a time
+        uint32_t r0[32], r1[32];
+        AS_TMEM_LD32(tl + b * UNIT + half * 64, r0);
+        AS_TMEM_LD32(tl + b * UNIT + half * 64 + 32, r1);
+        // lse' = LSE_r * log2e + log2 B of these 64 rows (smem broadcast)
+        const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v % HPT) * UNIT + half * 64);
+        AS_TMEM_WAIT_LD(r0);
+        AS_TMEM_WAIT_LD(r1);
+        float vv[64];
+        const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
 #pragma unroll
-      for (int k4 = 0; k4 < 16; ++k4) {
-        const float4 l4 = lq[k4];
+        for (int k4 = 0; k4 < 16; ++k4) {
+          const float4 l4 = lq[k4];
 #pragma unroll
-        for (int m = 0; m < 2; ++m) {         // packed: x = s log2e + b2 - lse'
-          const int k = 4 * k4 + 2 * m;
-          const uint32_t xa = k < 32 ? r0[k] : r1[k - 32], xb = k < 32 ? r0[k + 1] : r1[k - 31];
-          uint64_t x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
-          x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
-          if ((2 * k4 + m) % AS_EMU_MOD == AS_EMU_MOD - 1) {
-            ex2_emu2(x, vv[k], vv[k + 1]);
-          } else {
-            float x0, x1;
-            f2split(x, x0, x1);
-            vv[k] = XEX2(x0);
-            vv[k + 1] = XEX2(x1);
+          for (int m = 0; m < 2; ++m) {       // packed: x = s log2e + b2 - lse'
+            const int k = 4 * k4 + 2 * m;
+            const uint32_t xa = k < 32 ? r0[k] : r1[k - 32], xb = k < 32 ? r0[k + 1] : r1[k - 31];
+            uint64_t x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
+            x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
+            if ((2 * k4 + m) % AS_EMU_MOD == AS_EMU_MOD - 1) {
+              ex2_emu2(x, vv[k], vv[k + 1]);
+            } else {
+              float x0, x1;
+              f2split(x, x0, x1);
+              vv[k] = XEX2(x0);
+              vv[k + 1] = XEX2(x1);
+            }
           }
         }
-      }
-      const int base = 64 * v;
-      while (lnr < base + 64) {               // rare: labels of this class in these rows
-        if (lnr >= base) {
-          const int kk = lnr - base;
+        const int base = UNIT * v + 64 * half;
+        while (lnr < base + 64) {             // rare: labels of this class in these rows
+          if (lnr >= base) {
+            const int kk = lnr - base;
 #pragma unroll
-          for (int k = 0; k < 64; ++k)
-            if (k == kk) vv[k] -= lnw;
+            for (int k = 0; k < 64; ++k)
+              if (k == kk) vv[k] -= lnw;
+          }
+          ++lc;
+          lnr = lc < le ? lrow[lc] : 0x7fffffff;
+          lnw = lc < le ? lw[lc] : 0.f;
         }
-        ++lc;
-        lnr = lc < le ? lrow[lc] : 0x7fffffff;
-        lnw = lc < le ? lw[lc] : 0.f;
-      }
-      uint32_t pk[32];                        // 64 bf16 of G^T, packed in pairs
-      uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
+        uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        dacc[u & 3] = fadd2(dacc[u & 3], f2(vv[2 * u], vv[2 * u + 1]));
-        pk[u] = pack_bf16x2(vv[2 * u], vv[2 * u + 1]);
+        for (int u = 0; u < 32; ++u) {
+          dacc[u & 3] = fadd2(dacc[u & 3], f2(vv[2 * u], vv[2 * u + 1]));
+          pk[u] = pack_bf16x2(vv[2 * u], vv[2 * u + 1]);
+        }
+        {
+          float d0, d1;
+          f2split(fadd2(fadd2(dacc[0], dacc[1]), fadd2(dacc[2], dacc[3])), d0, d1);
+          db2 += d0 + d1;
+        }
+        // G^T over S^T columns already consumed (cols [32 half, 32 half + 32))
+        AS_TMEM_ST32(tl + b * UNIT + half * 32, pk);
       }
-      {
-        float d0, d1;
-        f2split(fadd2(fadd2(dacc[0], dacc[1]), fadd2(dacc[2], dacc[3])), d0, d1);
-        db2 += d0 + d1;
-      }
-      AS_TMEM_ST32(tl + b * 64, pk);          // G^T over the consumed S^T columns
       TRACE(1, threadIdx.x == 0, 8, v);
       tmem_wait_st();
 #endif
@@ -844,12 +852,17 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
         if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
         sDB[g * BM + i] = db2;
+        if (NU == 1) sDB[(1 - g) * BM + i] = 0.f;   // one unit per block: the other WG has none
         __syncwarp();
-        if (lane == 0) mbar_arrive(db_full);
+        if (lane == 0) {
+          mbar_arrive(db_full);
+          if (NU == 1) mbar_arrive(db_full);
+        }
       }
       v += 2;                                 // next unit of this WG
       if (v >= NU) { v -= NU; ++kb; }
-      if (++lst == NSH) lst = 0;
+      lst += 2 / HPT;                         // its H stage
+      if (lst >= NSH) lst -= NSH;
       sb += 2;
       if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
     }
@@ -1402,17 +1415,17 @@ int tc_fwd_splits_host(const TcPlan *p, int B) {
 }
 
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lsep,
-                       const int32_t *cls_seg, const int32_t *lseg_ptr, const int32_t *lrow,
+                       const int4 *cls_lab, const int32_t *lseg_ptr, const int32_t *lrow,
                        const float *lw, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
                        float *dbg_dW2T, float *dbg_db2) {
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lseg_ptr, lrow, lw, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
   else
     tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_seg, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lseg_ptr, lrow, lw, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
 }
 

@@ -196,10 +196,14 @@ __global__ void __launch_bounds__(256) k_tr_place(TrArgs a) {
   } else if (t - nnz < nlab) {
     const int j = t - nnz;
     const int c = a.lab[j], r = a.lrid[j];
-    const int pos = a.lcnt[c] + rank_below(a.lbits + (size_t)c * a.W, r);
+    const int first = a.lcnt[c];
+    const int pos = first + rank_below(a.lbits + (size_t)c * a.W, r);
     a.lseg_row[pos] = r;
     // 1 / (k_r B): the label weight of the uniform multi-label target (R3)
-    a.lw[pos] = (1.0f / (float)d->rows) / (float)(a.lab_ptr[r + 1] - a.lab_ptr[r]);
+    const float wgt = (1.0f / (float)d->rows) / (float)(a.lab_ptr[r + 1] - a.lab_ptr[r]);
+    a.lw[pos] = wgt;
+    if (pos == first)                       // the class's label range for pass 2 in one load
+      a.cls_lab[c] = make_int4(first, a.lseg_ptr[a.cls_seg[c] + 1], r, __float_as_int(wgt));
   }
 }
 
@@ -245,6 +249,7 @@ __global__ void __launch_bounds__(256) k_step_tail(TrArgs a, const float *__rest
       const int c = a.lab[j], r = a.lrid[j];
       a.lcnt[c] = 0;
       a.cls_seg[c] = -1;
+      a.cls_lab[c] = make_int4(0, 0, 0x7fffffff, 0);
       a.lbits[(size_t)c * a.W + (r >> 5)] = 0u;
     }
   }
@@ -254,4 +259,14 @@ void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float 
   k_step_tail<<<2 * num_sms, 256, 0, s>>>(a, lossr, loss);
 }
 
+}  // namespace as
+
+namespace as {
+__global__ void k_fill_int4(int4 *p, long long n, int4 v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+void launch_fill_int4(cudaStream_t s, int4 *p, long long n, int x, int y, int z, int w) {
+  k_fill_int4<<<1024, 256, 0, s>>>(p, n, make_int4(x, y, z, w));
+}
 }  // namespace as
