@@ -795,6 +795,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v % HPT) * UNIT + half * 64);
         AS_TMEM_WAIT_LD(r0);
         AS_TMEM_WAIT_LD(r1);
+#ifdef AS_X_EARLYP
+        if (half == UNIT / 64 - 1) { fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&p_full[b]); }
+#endif
         float vv[64];
         const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
 #pragma unroll
@@ -848,7 +851,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #endif
       fence_before();
       __syncwarp();
+#ifndef AS_X_EARLYP
       if (lane == 0) mbar_arrive(&p_full[b]);
+#endif
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
         if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
         sDB[g * BM + i] = db2;
