@@ -188,7 +188,9 @@ def main():
     p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
     log("dataset + init generated")
     nccl_id = driver.broadcast_nccl_id(dist, rank, device=dev) if world > 1 else None
-    stream = torch.cuda.Stream(dev)
+    # high priority: the step's critical path (SpMM, passes 1/2) wins SMs over the
+    # library's low-priority side stream (batch transposes)
+    stream = torch.cuda.Stream(dev, priority=-1)
     lr0 = 0.1
     rep = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta, megabatch=cfg.megabatch,
                   max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),

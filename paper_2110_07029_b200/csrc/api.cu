@@ -377,7 +377,11 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->ticket, 0, 16, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->arrive, 0, 4 * (size_t)D.sort_cap, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->Hb, 0, 2 * (size_t)D.bpad * D.h, x->stream), "memset");
-  if (!rc) rc = cuda_check(x, cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking), "side stream");
+  // side stream at the lowest priority: the transposes fill SMs the critical
+  // path (SpMM, pass 1 on the caller's stream) leaves idle
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->side, cudaStreamNonBlocking, prio_lo), "side stream");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming), "event");
   // pinned double-buffered staging for host batches

@@ -13,7 +13,7 @@ cfg = synthgen.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "amazon670k"]
 ds = synthgen.make_dataset(cfg, n=40000)
 p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
 rep = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, max_row_nnz=int(np.diff(ds.row_ptr).max()),
-              max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=0.01, precision="bf16")
+              max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=0.01, precision="bf16", stream=torch.cuda.Stream(priority=-1))
 rep.upload_dataset(ds)
 for k in range(3):
     rep.load_batch_stream(k * 1024, 1024); rep.train_step(False)
