@@ -184,7 +184,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_val = (float *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_of = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->rid = (int32_t *)p;
-  p = P(4 * 2 * (size_t)D.h * ((size_t)D.sort_cap * D.h / 2048 + 2)); if (x) x->seg_part = (float *)p;
+  p = P(4 * 2 * (size_t)D.h * (std::max<size_t>((size_t)D.sort_cap * D.h / 2048, 1024) + 2)); if (x) x->seg_part = (float *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.lab_cap + 1)); if (x) x->lseg_ptr = (int32_t *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_row = (int32_t *)p;

@@ -175,6 +175,38 @@ def test_one_step_parity(gpu_lib, case, precision, tol):
     assert np.all(dnew["W1"][untouched] == 0)                  # untouched rows bit-identical
 
 
+@pytest.mark.parametrize("h,B,avg_nnz,d", [(128, 64, 400.0, 3000), (256, 96, 250.0, 2000), (128, 1, 600.0, 5000),
+                                            (128, 700, 3.0, 900)])
+def test_sparse_long_segments(gpu_lib, h, B, avg_nnz, d):
+    """SpMM rows and dW1 feature segments far longer than one CTA's entry range
+    (every segment crosses warp and CTA ranges: the ordered shared-memory and
+    last-arriver combines), plus many very short rows; fp32, twice for
+    bit-identical results (deterministic sum order)."""
+    cfg = _cfg(d, 300, h, 4 * B + 8, max(B, 8), avg_nnz=avg_nnz, seed=5)
+    ds = synthgen.make_dataset(cfg, n=cfg.n)
+    p = _params(cfg)
+    sub = ds.rows(np.arange(B) + 3)
+    ref = om.gradients_chunked(sub, otrain.unpack(p, d, cfg.C, h), chunk=64)
+    keys = np.unique(sub.col)
+    outs = []
+    for _ in range(2):
+        rep = _replica(cfg, p, ds, "fp32", lr=0.5)
+        rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+        rep.train_step(want_loss=True)
+        H = _f32(rep.debug_get(0, 4 * B * h)).reshape(B, h)
+        assert_close("H", H, ref["H"], 1e-5)
+        dW1 = _f32(rep.debug_get(7, 4 * len(keys) * h)).reshape(len(keys), h)
+        assert_close("dW1", dW1, ref["dW1"][keys], 1e-4)
+        new = rep.get_params()
+        dnew = otrain.unpack(new.astype(np.float64) - p.astype(np.float64), d, cfg.C, h)
+        assert_close("W1 update", dnew["W1"][keys], -0.5 * ref["dW1"][keys], 1e-3)
+        untouched = np.setdiff1d(np.arange(d), keys)
+        assert np.all(dnew["W1"][untouched] == 0)
+        outs.append((H.copy(), new.copy()))
+        rep.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
 @pytest.mark.parametrize("h", [128, 256])
 def test_bf16_online_softmax_rescale_paths(gpu_lib, h):
     """b2 ramps up over the classes and the rows differ in scale, so the lazy
