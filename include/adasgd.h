@@ -140,6 +140,24 @@ int as_load_batch_stream(as_ctx *ctx, int64_t pos, int32_t rows);
  * the batch (R3); non-NULL forces a stream synchronisation. */
 int as_train_step(as_ctx *ctx, float *loss_out);
 
+/* ---- top-1 evaluation -----------------------------------------
+ * P:228 "We measure the top-1 accuracy – corresponding to the class with the
+ * highest probability – on the testing dataset after processing every
+ * megabatch."  Forward pass of `rows` HOST CSR samples (same layout, validation
+ * and ownership as as_load_batch_csr; rows in [1, b_max]) through this
+ * replica's current model (right after as_merge that is the global model,
+ * P:187): H = ReLU(X W1 + b1), z = H W2T^T + b2, top1_r = argmax_c z_rc with
+ * the lowest class id on ties (R21; softmax is monotone).  AS_BF16: z from the
+ * bf16 H and W2T shadow on the tensor cores (fp32 accumulate); AS_FP32: fp32
+ * SIMT logits.  Outputs (host, nullable): top1_out[rows] (int32 class ids),
+ * hits_out = number of rows whose top-1 class is one of their labels.
+ * Overwrites the loaded training batch (call as_load_batch_* again before
+ * as_train_step).  Synchronises the stream. */
+int as_eval_top1(as_ctx *ctx, int32_t rows, const int64_t *row_ptr,
+                 const int32_t *col, const float *val,
+                 const int64_t *lab_ptr, const int32_t *lab,
+                 int32_t *top1_out, int64_t *hits_out);
+
 /* ---- merge (steps a9-a13, Alg. 2) ------------------------------------
  * Collective over all `world` ranks, called with identical u[world] (updates
  * since the last merge) and b[world] (batch sizes in force during the

@@ -140,3 +140,47 @@ def gradients_chunked(batch, params, chunk=64):
     np.add.at(dW1, np.asarray(batch.col, np.int64), np.asarray(batch.val, np.float64)[:, None] * dA[rid])
     return {"A": A, "H": H, "LSE": LSE, "loss": float(np.mean(LSE - label_term)), "dA": dA,
             "db1": dA.sum(axis=0), "dW1": dW1, "dW2T": dW2T, "db2": db2}
+
+
+def bf16_round(x):
+    """Round fp32 values to bfloat16 (round to nearest even), returned as fp64.
+    Used only where an integer decision (an argmax) is taken in the kernel's
+    operand precision (task rule: both sides decide in the same precision)."""
+    x32 = np.ascontiguousarray(np.asarray(x, np.float32))
+    u = x32.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def top1(batch, params, operands="fp64", chunk=256):
+    """Top-1 prediction and hits ("top-1 accuracy – corresponding to the
+    class with the highest probability"; softmax is monotone, so the class
+    with the largest logit z_rc).  Ties -> lowest class id (reading R21); a hit
+    when that class is one of the row's labels.
+
+    operands="bf16" rounds h_r and W2T to bfloat16 before the product (the
+    tensor-core path's operands; the products are still summed in fp64), so the
+    argmax is decided in the kernel's operand precision.
+
+    Returns (top1[B] int64, hits int, zmax[B] fp64, Z-accessor) where
+    Z-accessor(r, c) gives the logit used for the decision (for near-tie checks)."""
+    W1, b1, W2T, b2 = (np.asarray(params[k], np.float64) for k in ("W1", "b1", "W2T", "b2"))
+    H = np.maximum(spmm(batch.row_ptr, batch.col, batch.val, W1, b1), 0.0)
+    if operands == "bf16":
+        H = bf16_round(H.astype(np.float32))
+        W2T = bf16_round(np.asarray(params["W2T"], np.float32))
+    B = H.shape[0]
+    top = np.empty(B, np.int64)
+    zmax = np.empty(B, np.float64)
+    for r0 in range(0, B, chunk):
+        Z = H[r0:r0 + chunk] @ W2T.T + b2
+        top[r0:r0 + chunk] = np.argmax(Z, axis=1)          # numpy: first (lowest) index on ties
+        zmax[r0:r0 + chunk] = Z[np.arange(Z.shape[0]), top[r0:r0 + chunk]]
+    hits = 0
+    for r in range(B):
+        s, e = int(batch.lab_ptr[r]), int(batch.lab_ptr[r + 1])
+        hits += int(top[r] in set(int(y) for y in batch.lab[s:e]))
+
+    def logit(r, c):
+        return float(H[r] @ W2T[c] + b2[c])
+    return top, hits, zmax, logit

@@ -29,6 +29,7 @@ EXPORTS = [
     "as_set_params", "as_debug_get", "as_tc_selftest", "as_sched_route_replay", "as_sched_alg1",
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
     "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
+    "as_eval_top1",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -85,6 +86,7 @@ def load():
         "as_init": [P(Config), P(F), P(VP)],
         "as_destroy": [VP],
         "as_load_batch_csr": [VP, I32, P(I64), P(I32), P(F), P(I64), P(I32)],
+        "as_eval_top1": [VP, I32, P(I64), P(I32), P(F), P(I64), P(I32), P(I32), P(I64)],
         "as_dataset_bytes": [I64, I64, I64, P(C.c_size_t)],
         "as_dataset_upload": [VP, VP, C.c_size_t, I64, P(I64), P(I32), P(F), P(I64), P(I32), P(I64)],
         "as_load_batch_stream": [VP, I64, I32],

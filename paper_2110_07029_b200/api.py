@@ -69,6 +69,32 @@ class Replica:
                                            L.ptr(vl, C.c_float), L.ptr(lp, C.c_int64),
                                            L.ptr(lb, C.c_int32)))
 
+    def eval_top1(self, rows, row_ptr, col, val, lab_ptr, lab):
+        """as_eval_top1: (top1 class ids [rows] int32, hits) of the current model."""
+        rp, cl, vl = L.as_np(row_ptr, np.int64), L.as_np(col, np.int32), L.as_np(val, np.float32)
+        lp, lb = L.as_np(lab_ptr, np.int64), L.as_np(lab, np.int32)
+        top1 = np.empty(int(rows), np.int32)
+        hits = C.c_int64()
+        L.check(self.lib.as_eval_top1(self.ctx, int(rows), L.ptr(rp, C.c_int64), L.ptr(cl, C.c_int32),
+                                      L.ptr(vl, C.c_float), L.ptr(lp, C.c_int64), L.ptr(lb, C.c_int32),
+                                      L.ptr(top1, C.c_int32), C.byref(hits)))
+        return top1, int(hits.value)
+
+    def evaluate(self, ds, batch=None):
+        """Top-1 accuracy of the current model over a whole CSR dataset, in
+        batches of at most b_max rows (the paper's per-mega-batch test metric)."""
+        b = int(batch or self.cfg.b_max)
+        n = len(ds.row_ptr) - 1
+        hits = 0
+        for a in range(0, n, b):
+            r = min(b, n - a)
+            c0, c1 = ds.row_ptr[a], ds.row_ptr[a + r]
+            l0, l1 = ds.lab_ptr[a], ds.lab_ptr[a + r]
+            _, h = self.eval_top1(r, ds.row_ptr[a:a + r + 1] - c0, ds.col[c0:c1], ds.val[c0:c1],
+                                  ds.lab_ptr[a:a + r + 1] - l0, ds.lab[l0:l1])
+            hits += h
+        return hits / max(n, 1)
+
     def upload_dataset(self, ds, order=None):
         torch = _torch()
         rp, cl, vl = L.as_np(ds.row_ptr, np.int64), L.as_np(ds.col, np.int32), L.as_np(ds.val, np.float32)

@@ -73,6 +73,8 @@ struct as_ctx {
   __nv_bfloat16 *Hb;
   float *dA, *lse2, *lsep, *zsum, *labW, *lossr, *loss;
   float *pm, *pl, *pO;
+  int32_t *top1;              // top-1 evaluation (NEXT f1)
+  unsigned long long *hits;
   float *Z, *dH, *dW2, *splitk_tmp;
   float *dbg_dW2, *dbg_db2, *dbg_dW1, *dbg_db1;
   double *norm_part, *norm_dev, *norms_all;
@@ -200,9 +202,11 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.b_max * D.h); if (x) x->labW = (float *)p;
   p = P(4 * (size_t)D.b_max); if (x) x->lossr = (float *)p;
   p = P(4); if (x) x->loss = (float *)p;
+  p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pm = (float *)p;
+  p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pl = (float *)p;
+  p = P(4 * (size_t)D.bpad); if (x) x->top1 = (int32_t *)p;
+  p = P(8); if (x) x->hits = (unsigned long long *)p;
   if (bf16) {
-    p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pm = (float *)p;
-    p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pl = (float *)p;
     p = P(4 * (size_t)D.max_splits * D.bpad * D.h); if (x) x->pO = (float *)p;
   } else {
     p = P(4 * (size_t)D.b_max * D.C); if (x) x->Z = (float *)p;
@@ -429,11 +433,10 @@ int as_destroy(as_ctx *x) {
   return AS_OK;
 }
 
-int as_load_batch_csr(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t *col,
-                      const float *val, const int64_t *lab_ptr, const int32_t *lab) {
-  AS_GUARD(x);
-  const int bi = x->b_all[x->cfg.rank];
-  if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
+// validate a host CSR batch and stage it (pinned, double-buffered) onto the
+// device batch buffers; shared by as_load_batch_csr and as_eval_top1
+static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t *col, const float *val,
+                       const int64_t *lab_ptr, const int32_t *lab) {
   int64_t nnz = 0, L = 0;
   int rc = validate_csr(x, rows, row_ptr, col, val, lab_ptr, lab, &nnz, &L);
   if (rc) return rc;
@@ -474,7 +477,56 @@ int as_load_batch_csr(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int
   rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], s), "batch H2D");
   if (rc) return rc;
   x->loaded_rows = rows;
+  return AS_OK;
+}
+
+int as_load_batch_csr(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t *col,
+                      const float *val, const int64_t *lab_ptr, const int32_t *lab) {
+  AS_GUARD(x);
+  const int bi = x->b_all[x->cfg.rank];
+  if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
+  const int rc = stage_batch(x, rows, row_ptr, col, val, lab_ptr, lab);
+  if (rc) return rc;
   x->has_batch = true;
+  return AS_OK;
+}
+
+int as_eval_top1(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t *col, const float *val,
+                 const int64_t *lab_ptr, const int32_t *lab, int32_t *top1_out, int64_t *hits_out) {
+  AS_GUARD(x);
+  if (rows < 1 || rows > x->cfg.b_max) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_max=%d]", rows, x->cfg.b_max);
+  int rc = stage_batch(x, rows, row_ptr, col, val, lab_ptr, lab);
+  if (rc) return rc;
+  x->has_batch = false;                     // the batch buffers now hold the evaluation rows
+  const Dims &D = x->D;
+  cudaStream_t s = x->stream;
+  StepDesc *d = x->desc;
+  const float *W1 = x->w, *b1 = x->w + D.d * D.h, *W2T = b1 + D.h, *b2 = W2T + D.C * D.h;
+  // forward: H = ReLU(X W1 + b1) (a4), then the row argmax of z = H W2T^T + b2
+  x->launches += 3;
+  as::launch_spmm_chunked(s, D.h, x->num_sms, d, D.bpad, D.nnz_cap, x->row_ptr, x->col, x->val, x->rid,
+                          W1, b1, x->Hf, x->Hb, x->seg_part, x->arrive);
+  int slots = 1;
+  if (x->cfg.precision == AS_BF16) {
+    as::launch_out_top1_tc(s, x->plan, d, b2, x->pm, (int *)x->pl);
+    slots = as::tc_fwd_splits_host(x->plan, rows);
+  } else {
+    x->launches += 1;
+    as::launch_gemm_f32(s, D.b_max, (int)D.C, D.h, x->Hf, D.h, 1, W2T, 1, D.h, x->Z, D.C, b2, 1, nullptr,
+                        &d->rows);
+    as::launch_row_argmax_f32(s, d, D.b_max, (int)D.C, x->Z, x->pm, (int *)x->pl);
+  }
+  cudaMemsetAsync(x->hits, 0, 8, s);
+  as::launch_top1_combine(s, d, slots, D.bpad, x->pm, (const int *)x->pl, x->lab_ptr, x->lab, x->top1,
+                          x->hits);
+  rc = cuda_check(x, cudaSuccess, "eval launch");
+  if (rc) return rc;
+  if (top1_out) cudaMemcpyAsync(top1_out, x->top1, 4 * (size_t)rows, cudaMemcpyDeviceToHost, s);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, x->hits, 8, cudaMemcpyDeviceToHost, s);
+  rc = cuda_check(x, cudaStreamSynchronize(s), "eval");
+  if (rc) return rc;
+  if (hits_out) *hits_out = (int64_t)h;
   return AS_OK;
 }
 
@@ -562,26 +614,34 @@ int as_train_step(as_ctx *x, float *loss_out) {
   // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2) on
   // the side stream, concurrent with a4/a5; joined before a6 and a7
   cudaStream_t ss = x->side;
-  cudaEventRecord(x->ev_fork, s);
-  cudaStreamWaitEvent(ss, x->ev_fork, 0);
-  ph_begin(x, AS_PH_TRANSPOSE, ss);
   const as::TrArgs tr = tr_args(x);
-  x->launches += 3;
-  as::launch_transposes(ss, tr);
-  ph_end(x, AS_PH_TRANSPOSE, ss);
-  cudaEventRecord(x->ev_join, ss);
+  auto fork_transposes = [&]() {
+    cudaEventRecord(x->ev_fork, s);
+    cudaStreamWaitEvent(ss, x->ev_fork, 0);
+    ph_begin(x, AS_PH_TRANSPOSE, ss);
+    x->launches += 3;
+    as::launch_transposes(ss, tr);
+    ph_end(x, AS_PH_TRANSPOSE, ss);
+    cudaEventRecord(x->ev_join, ss);
+  };
+#ifndef AS_X_FORK
+#define AS_X_FORK 0
+#endif
+  if (AS_X_FORK == 0) fork_transposes();
   // a4: SpMM forward
   ph_begin(x, AS_PH_SPMM);
   x->launches += 1;
   as::launch_spmm_chunked(s, D.h, x->num_sms, d, D.bpad, D.nnz_cap, x->row_ptr, x->col, x->val, x->rid, W1, b1,
                           x->Hf, x->Hb, x->seg_part, x->arrive);
   ph_end(x, AS_PH_SPMM);
+  if (AS_X_FORK == 1) fork_transposes();
   if (x->cfg.precision == AS_BF16) {
     // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
     ph_begin(x, AS_PH_OUT_FWD);
     x->launches += 1;
     as::launch_out_fwd_tc(s, x->plan, d, b2, x->pm, x->pl, x->pO);
     ph_end(x, AS_PH_OUT_FWD);
+    if (AS_X_FORK == 2) fork_transposes();
     ph_begin(x, AS_PH_COMBINE);
     x->launches += 3;
     // label terms of the loss and of dH (R3)
@@ -601,6 +661,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
     ph_end(x, AS_PH_OUT_BWD);
   } else {
     // fp32 parity mode: logits materialised
+    if (AS_X_FORK == 2) fork_transposes();
     const long long C = D.C;
     ph_begin(x, AS_PH_OUT_FWD);
     x->launches += 1 + 1 + 1 + 2;

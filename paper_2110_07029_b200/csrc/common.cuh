@@ -152,6 +152,14 @@ int tc_splits(int h, int b_max, long long C, int num_sms);
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
                        const float *b2, float *pm, float *pl, float *pO);
 int tc_fwd_splits_host(const TcPlan *plan, int B);
+// top-1 evaluation (NEXT f1): per-split (max, argmax) partials, then the ordered combine
+void launch_out_top1_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc, const float *b2,
+                        float *pmax, int *pidx);
+void launch_row_argmax_f32(cudaStream_t s, const StepDesc *desc, int b_max, int C, const float *Z, float *pmax,
+                           int *pidx);
+void launch_top1_combine(cudaStream_t s, const StepDesc *desc, int slots, int bpad, const float *pmax,
+                         const int *pidx, const int64_t *lab_ptr, const int32_t *lab, int32_t *top1,
+                         unsigned long long *hits);
 int tc_bench(int mode, int iters, long long *cycles_host);
 int tc_selftest2(const void *A, const void *B, float *V, float *U, cudaStream_t s);
 int tc_trace_dump(long long *out, int max_events);

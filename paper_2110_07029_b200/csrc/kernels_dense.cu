@@ -147,6 +147,67 @@ void launch_row_lse(cudaStream_t s, const StepDesc *desc, int b_max, int C, cons
   k_row_lse<<<b_max, 256, 0, s>>>(desc, C, Z, lse2);
 }
 
+// top-1 evaluation, fp32 mode: per row max_c z_c with the lowest c on ties
+// (R21) over the materialised logits; one partial slot
+__global__ void __launch_bounds__(256) k_row_argmax(const StepDesc *__restrict__ desc, int C,
+                                                    const float *__restrict__ Z, float *__restrict__ pmax,
+                                                    int *__restrict__ pidx) {
+  __shared__ float rv[256];
+  __shared__ int ri[256];
+  const int r = blockIdx.x;
+  if (r >= desc->rows) return;
+  const float *z = Z + (size_t)r * C;
+  float m = -INFINITY;
+  int mi = 0x7fffffff;
+  for (int c = threadIdx.x; c < C; c += 256)
+    if (z[c] > m) { m = z[c]; mi = c; }        // ascending c per thread
+  rv[threadIdx.x] = m; ri[threadIdx.x] = mi;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const float v = rv[threadIdx.x + o];
+      const int i = ri[threadIdx.x + o];
+      if (v > rv[threadIdx.x] || (v == rv[threadIdx.x] && i < ri[threadIdx.x])) {
+        rv[threadIdx.x] = v; ri[threadIdx.x] = i;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { pmax[r] = rv[0]; pidx[r] = ri[0]; }
+}
+
+void launch_row_argmax_f32(cudaStream_t s, const StepDesc *desc, int b_max, int C, const float *Z, float *pmax,
+                           int *pidx) {
+  k_row_argmax<<<b_max, 256, 0, s>>>(desc, C, Z, pmax, pidx);
+}
+
+// ordered combine of the (max, argmax) slots; a hit when the top-1 class is
+// one of the row's labels; integer hit count
+__global__ void k_top1_combine(const StepDesc *__restrict__ desc, int slots, int bpad,
+                               const float *__restrict__ pmax, const int *__restrict__ pidx,
+                               const int64_t *__restrict__ lab_ptr, const int32_t *__restrict__ lab,
+                               int32_t *__restrict__ top1, unsigned long long *__restrict__ hits) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= desc->rows) return;
+  float m = -INFINITY;
+  int mi = 0x7fffffff;
+  for (int sl = 0; sl < slots; ++sl) {
+    const float v = pmax[(size_t)sl * bpad + r];
+    const int i = pidx[(size_t)sl * bpad + r];
+    if (v > m || (v == m && i < mi)) { m = v; mi = i; }
+  }
+  top1[r] = mi;
+  int hit = 0;
+  for (int64_t j = lab_ptr[r]; j < lab_ptr[r + 1]; ++j) hit |= lab[j] == mi;
+  if (hit) atomicAdd(hits, 1ull);
+}
+
+void launch_top1_combine(cudaStream_t s, const StepDesc *desc, int slots, int bpad, const float *pmax,
+                         const int *pidx, const int64_t *lab_ptr, const int32_t *lab, int32_t *top1,
+                         unsigned long long *hits) {
+  k_top1_combine<<<(bpad + 127) / 128, 128, 0, s>>>(desc, slots, bpad, pmax, pidx, lab_ptr, lab, top1, hits);
+}
+
 // dZ = (softmax(z_r) - T_r)/B in place (R3)
 __global__ void k_softmax(const StepDesc *__restrict__ desc, int C, float *__restrict__ Z,
                           const float *__restrict__ lse2) {

@@ -347,19 +347,33 @@ __global__ void __launch_bounds__(SegCfg<H, MODE>::NW * 32, 1)
     }
     return m;
   };
+  // gathers of group k (need only the source rows: one metadata round trip);
+  // MODE 1's W1 prefetch follows in issue_w1 once the segment bounds are in
   auto issue = [&](int k, const Meta &m) {
     if (k >= ngr) return;
     const int st = k % NST;
     uint8_t *buf = ring + st * Cfg::STAGE;
     const int e0 = wb + k * GE, cnt = min(GE, we - e0);
-    // MODE 1: W1 row of each segment finalised inside this warp range at this entry
-    const bool pre = MODE == 1 && lane < cnt && m.s1 == e0 + lane + 1 && m.s0 >= wb && m.s1 <= we;
-    const int npre = __popc(__ballot_sync(0xffffffffu, pre));
     fence_proxy_async_seg();
-    if (lane == 0) sb_expect(&full[st], (uint32_t)(cnt + npre) * ROW);
+    if (lane == 0) {
+      if (MODE == 0) sb_expect(&full[st], (uint32_t)cnt * ROW);
+      else asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(sm32(&full[st])),
+                        "r"((uint32_t)cnt * ROW) : "memory");
+    }
     __syncwarp();
     if (lane < cnt) sb_copy(buf + lane * ROW, S + (size_t)m.idx * (H / 4), ROW, &full[st]);
-    if (MODE == 1 && pre) sb_copy(buf + (GE + lane) * ROW, a.W1 + (size_t)m.key * H, ROW, &full[st]);
+  };
+  auto issue_w1 = [&](int k, const Meta &m) {   // MODE 1: the stage's arrival
+    if (MODE != 1 || k >= ngr) return;
+    const int st = k % NST;
+    uint8_t *buf = ring + st * Cfg::STAGE;
+    const int e0 = wb + k * GE, cnt = min(GE, we - e0);
+    // W1 row of each segment finalised inside this warp range at this entry
+    const bool pre = lane < cnt && m.s1 == e0 + lane + 1 && m.s0 >= wb && m.s1 <= we;
+    const int npre = __popc(__ballot_sync(0xffffffffu, pre));
+    if (lane == 0) sb_expect(&full[st], (uint32_t)npre * ROW);
+    __syncwarp();
+    if (pre) sb_copy(buf + (GE + lane) * ROW, a.W1 + (size_t)m.key * H, ROW, &full[st]);
   };
 
   // prologue: metadata of groups 0..NST, rows of groups 0..NST-1 in flight
@@ -368,6 +382,8 @@ __global__ void __launch_bounds__(SegCfg<H, MODE>::NW * 32, 1)
   for (int i = 0; i <= NST; ++i) mq[i] = load_meta(i);
 #pragma unroll
   for (int i = 0; i < NST; ++i) issue(i, mq[i]);
+#pragma unroll
+  for (int i = 0; i < NST; ++i) issue_w1(i, mq[i]);
 
   if (MODE == 0) {
     // rows no entry covers (empty rows: H = ReLU(b1); zero padding rows of the
@@ -389,10 +405,22 @@ __global__ void __launch_bounds__(SegCfg<H, MODE>::NW * 32, 1)
   float4 acc[V];
 #pragma unroll
   for (int q = 0; q < V; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int fsg = 0, fs0 = 0, fs1 = 0, lsg = 0, ls0 = 0, ls1 = 0;   // first / last segment of the range
 #pragma unroll 1
   for (int k = 0; k < ngr; ++k) {
     const int st = k % NST;
     const Meta m = mq[0];
+    if (k == 0) {
+      fsg = __shfl_sync(0xffffffffu, m.sg, 0);
+      fs0 = __shfl_sync(0xffffffffu, m.s0, 0);
+      fs1 = __shfl_sync(0xffffffffu, m.s1, 0);
+    }
+    if (k == ngr - 1) {
+      const int lu = we - 1 - (wb + k * GE);
+      lsg = __shfl_sync(0xffffffffu, m.sg, lu);
+      ls0 = __shfl_sync(0xffffffffu, m.s0, lu);
+      ls1 = __shfl_sync(0xffffffffu, m.s1, lu);
+    }
     sb_wait(&full[st], (uint32_t)((k / NST) & 1));
     const float4 *rows = reinterpret_cast<const float4 *>(ring + st * Cfg::STAGE);
     const int e0 = wb + k * GE, cnt = min(GE, we - e0);
@@ -430,6 +458,7 @@ __global__ void __launch_bounds__(SegCfg<H, MODE>::NW * 32, 1)
 #pragma unroll
     for (int i = 0; i < NST; ++i) mq[i] = mq[i + 1];
     issue(k + NST, mq[NST - 1]);
+    issue_w1(k + NST, mq[NST - 1]);
     mq[NST] = load_meta(k + NST + 1);
   }
   __syncthreads();
@@ -441,9 +470,8 @@ __global__ void __launch_bounds__(SegCfg<H, MODE>::NW * 32, 1)
   if (c < G && we > wb) {
 #pragma unroll 1
     for (int task = 0; task < 2; ++task) {
-      const int e = task == 0 ? wb : we - 1;
-      const int sg = seg_of[e];
-      const int s0 = (int)seg_ptr[sg], s1 = (int)seg_ptr[sg + 1];
+      const int sg = task == 0 ? fsg : lsg;
+      const int s0 = task == 0 ? fs0 : ls0, s1 = task == 0 ? fs1 : ls1;
       bool mine;
       if (task == 0) mine = s0 < wb && (s1 <= we || we == ce);
       else mine = s0 >= wb && s1 > ce && we == ce;

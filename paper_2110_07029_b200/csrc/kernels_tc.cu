@@ -1304,6 +1304,139 @@ __global__ void __launch_bounds__(128, 1)
   fence_after();
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
+
+// =====================================================================
+// top-1 evaluation ("top-1 accuracy –
+// corresponding to the class with the highest probability"): the forward
+// logits z = H W2T^T + b2 of a 128-row tile against this CTA's class blocks
+// and, per row, max_c z_c with the LOWEST class id on ties (R21; softmax is
+// monotone, so no exponentials).  Same split of the class range as pass 1;
+// partial slot (sp, g) = 2 sp + g holds (max, argmax) of WG g's blocks.
+//   warps 0-7  two epilogue warpgroups, WG g takes the blocks j % 2 == g and
+//              reads S_j from TMEM buffer g (thread = row = TMEM lane)
+//   warp 8     TMA producer (H tile once, W2T class blocks through a ring)
+//   warp 9     MMA issuer: S_j = H . W2T_blk^T into buffer j % 2
+// =====================================================================
+template <int H>
+struct Top1Cfg {
+  static constexpr int NST = H == 128 ? 4 : 2;
+  static constexpr int TILE = BM * H * 2;
+  static constexpr int THREADS = 10 * 32;
+  static constexpr int SMEM = TILE + NST * TILE + 2 * BM * 4 /*b2 of the current block per WG*/ + 256;
+  static_assert(SMEM <= 232448, "top-1 shared memory exceeds 227 KB");
+};
+
+template <int H>
+__global__ void __launch_bounds__(Top1Cfg<H>::THREADS, 1)
+    k_out_top1(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
+               const StepDesc *__restrict__ desc, const float *__restrict__ b2, int C, int n_cblocks,
+               int max_splits, int bpad, float *__restrict__ pmax, int *__restrict__ pidx) {
+  using Cfg = Top1Cfg<H>;
+  constexpr int NST = Cfg::NST, TILE = Cfg::TILE;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sH = smem_raw;
+  uint8_t *sW = smem_raw + TILE;
+  float *sB2 = (float *)(sW + NST * TILE);          // [2 WG][128]
+  uint64_t *bars = (uint64_t *)(sB2 + 2 * BM);
+  uint64_t *h_full = bars, *w_full = bars + 1, *w_empty = w_full + NST, *s_full = w_empty + NST,
+           *s_empty = s_full + 2;
+  uint32_t *tmem_slot = (uint32_t *)(s_empty + 2);
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+
+  const int B = desc->rows;
+  const int RT = (B + BM - 1) / BM;
+  const int splits = fwd_splits(B, n_cblocks, gridDim.x, max_splits);
+  const int rt = blockIdx.x / splits, sp = blockIdx.x % splits;
+  if (rt >= RT) return;
+  const int cb0 = (int)((long long)sp * n_cblocks / splits);
+  const int nloc = (int)((long long)(sp + 1) * n_cblocks / splits) - cb0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kProdWarp = 8, kMmaWarp = 9;
+
+  if (threadIdx.x == 0) {
+    mbar_init(h_full, 1);
+    for (int i = 0; i < NST; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 256);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      mbar_expect_tx(h_full, TILE);
+      for (int a = 0; a < H / 64; ++a) tma_load_2d(&mapH, h_full, sH + a * ATOM_BYTES, a * 64, rt * BM);
+      for (int j = 0; j < nloc; ++j) {
+        const int st = j % NST;
+        if (j >= NST) mbar_wait(&w_empty[st], ((j / NST) - 1) & 1);
+        mbar_expect_tx(&w_full[st], TILE);
+        for (int a = 0; a < H / 64; ++a)
+          tma_load_2d(&mapW, &w_full[st], sW + st * TILE + a * ATOM_BYTES, a * 64, (cb0 + j) * BM);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    constexpr uint32_t idS = idesc_bf16(BM, BM, 0, 0);
+    const uint32_t aH = smem_u32(sH), aW = smem_u32(sW);
+    mbar_wait(h_full, 0);
+    fence_after();
+    const uint64_t dH = sdesc(aH, 16, 1024);
+    for (int j = 0; j < nloc; ++j) {
+      const int st = j % NST, b = j & 1;
+      if (j >= 2) mbar_wait(&s_empty[b], ((j >> 1) - 1) & 1);
+      mbar_wait(&w_full[st], (j / NST) & 1);
+      fence_after();
+      if constexpr (H == 128)
+        mma_grp_ss_kk_8(tmem + b * BM, dH, sdesc(aW + st * TILE, 16, 1024), idS, 0u);
+      else
+        mma_grp_ss_kk_16(tmem + b * BM, dH, sdesc(aW + st * TILE, 16, 1024), idS, 0u);
+      mma_commit_w(&s_full[b]);
+      mma_commit_w(&w_empty[st]);
+    }
+  } else {  // ---------------- epilogue warpgroups (thread = row)
+    const int g = warp >> 2, q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t tS = tmem + ((uint32_t)(q * 32) << 16) + g * BM;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    int jj = 0;
+    for (int j = g; j < nloc; j += 2, ++jj) {
+      const int c0 = (cb0 + j) * BM;
+      float *myB2 = sB2 + g * BM;
+      named_bar(1 + g, 128);                  // previous block's b2 reads are done
+      myB2[row] = c0 + row < C ? b2[c0 + row] : -INFINITY;   // class past C: never selected
+      named_bar(1 + g, 128);
+      mbar_wait(&s_full[g], jj & 1);
+      fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < BM / 32; ++ch) {
+        uint32_t r[32];
+        AS_TMEM_LD32(tS + ch * 32, r);
+        AS_TMEM_WAIT_LD(r);
+        if (ch == BM / 32 - 1) {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[g]);
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float z = __uint_as_float(r[k]) + myB2[ch * 32 + k];
+          if (z > best) { best = z; bi = c0 + ch * 32 + k; }   // ascending c: lowest id on ties
+        }
+      }
+    }
+    const size_t slot = (size_t)sp * 2 + g;
+    const int grow = rt * BM + row;
+    pmax[slot * bpad + grow] = best;
+    pidx[slot * bpad + grow] = bi;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == kMmaWarp) tmem_dealloc(tmem, 256);
+}
 }  // namespace tc
 
 // =====================================================================
@@ -1391,11 +1524,15 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
                            tc::FwdCfg<128>::SMEM);
       cudaFuncSetAttribute(tc::k_out_bwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::BwdCfg<128>::SMEM);
+      cudaFuncSetAttribute(tc::k_out_top1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc::Top1Cfg<128>::SMEM);
     } else {
       cudaFuncSetAttribute(tc::k_out_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::FwdCfg<256>::SMEM);
       cudaFuncSetAttribute(tc::k_out_bwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::BwdCfg<256>::SMEM);
+      cudaFuncSetAttribute(tc::k_out_top1<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc::Top1Cfg<256>::SMEM);
     }
     attr_done[hi] = true;
   }
@@ -1412,6 +1549,16 @@ void launch_out_fwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
     tc::k_out_fwd<256><<<p->num_sms, tc::FwdCfg<256>::THREADS, tc::FwdCfg<256>::SMEM, s>>>(
         p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
         p->max_splits, p->bpad, pm, pl, pO);
+}
+
+void launch_out_top1_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2, float *pmax,
+                        int *pidx) {
+  if (p->h == 128)
+    tc::k_out_top1<128><<<p->num_sms, tc::Top1Cfg<128>::THREADS, tc::Top1Cfg<128>::SMEM, s>>>(
+        p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pmax, pidx);
+  else
+    tc::k_out_top1<256><<<p->num_sms, tc::Top1Cfg<256>::THREADS, tc::Top1Cfg<256>::SMEM, s>>>(
+        p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pmax, pidx);
 }
 
 // number of pass-1 partial slots for a batch of B rows (2 per CTA split)

@@ -18,6 +18,13 @@ rep.upload_dataset(ds)
 for k in range(3):
     rep.load_batch_stream(k * 1024, 1024); rep.train_step(False)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(rep.stream)
+for k in range(30):
+    rep.load_batch_stream(k * 1024, 1024); rep.train_step(False)
+e1.record(rep.stream)
+torch.cuda.synchronize()
+step_ms = e0.elapsed_time(e1) / 30
 rep.lib.as_profile(rep.ctx, 1)
 for k in range(30):
     rep.load_batch_stream(k * 1024, 1024); rep.train_step(False)
@@ -25,4 +32,4 @@ torch.cuda.synchronize()
 ms = (C.c_double * 8)(); calls = (C.c_int64 * 8)(); nl = C.c_int64()
 rep.lib.as_profile_read(rep.ctx, ms, calls, C.byref(nl))
 print("%-40s" % os.path.basename(os.environ.get("ADASGD_LIB", "libadasgd.so")),
-      " ".join("%s=%.4f" % (L.AS_PH_NAMES[i], ms[i] / max(1, calls[i])) for i in range(7)), flush=True)
+      "step=%.4f" % step_ms, " ".join("%s=%.4f" % (L.AS_PH_NAMES[i], ms[i] / max(1, calls[i])) for i in range(7)), flush=True)

@@ -375,3 +375,69 @@ def test_full_size_amazon670k_sampled(gpu_lib):
     keys = np.unique(sub.col)
     dW1 = _f32(rep.debug_get(7, 4 * len(keys) * 128)).reshape(len(keys), 128)
     assert_close("dW1", dW1, ref["dW1"][keys], tol)
+
+
+# ---------------------------------------------------------------- top-1 evaluation (NEXT f1)
+TOP1_CASES = [
+    (2000, 1000, 128, 600, 200, 256),     # ragged row tile, C % 128 = 104
+    (3000, 700, 256, 400, 130, 192),      # h = 256
+    (4000, 30000, 128, 1200, 1024, 1024), # many class blocks per split
+    (500, 50, 128, 64, 1, 64),            # a single row, C < 128
+]
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", TOP1_CASES)
+def test_eval_top1_parity(gpu_lib, case, precision):
+    """as_eval_top1 vs oracle.model.top1 with the decision taken in the kernel's
+    operand precision (bf16 operands for the tensor-core path).  The argmax is
+    unique except at near-ties: a differing row must be a near-tie of the
+    oracle's logits (both classes valid); hits agree up to those rows.  The
+    training state is untouched (a following step matches the oracle)."""
+    d, C, h, n, B, b_max = case
+    cfg = _cfg(d, C, h, n, b_max, seed=hash(case) % 89)
+    ds = synthgen.make_dataset(cfg, n=n)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, precision, lr=0.5, debug=False)
+    sub = ds.rows(np.arange(B) + 11)
+    top, hits = rep.eval_top1(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    prm = otrain.unpack(p, d, C, h)
+    otop, ohits, zmax, logit = om.top1(sub, prm, operands="bf16" if precision == "bf16" else "fp64")
+    diff = np.nonzero(top != otop)[0]
+    assert len(diff) <= max(1, B // 50), (len(diff), B)
+    for r in diff:
+        assert 0 <= top[r] < C
+        assert zmax[r] - logit(r, int(top[r])) <= 1e-4 * (1.0 + abs(zmax[r])), r
+    assert abs(hits - ohits) <= len(diff)
+    # the training batch path is unaffected by the evaluation
+    tr = ds.rows(np.arange(B))
+    rep.load_batch_csr(B, tr.row_ptr, tr.col, tr.val, tr.lab_ptr, tr.lab)
+    loss = rep.train_step(want_loss=True)
+    ref = om.gradients_chunked(tr, prm, chunk=64)
+    assert abs(loss - ref["loss"]) <= (2e-2 if precision == "bf16" else 1e-4) * abs(ref["loss"])
+    rep.close()
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_eval_top1_ties_lowest_class_across_splits(gpu_lib, precision):
+    """W2T = 0: z = b2 exactly on both paths; the maximum is repeated at class
+    5 and at class 29000 (different class blocks and pass-1 splits): the
+    lowest id must win on every row (R21), bit-exact."""
+    d, C, h, B = 3000, 30000, 128, 300
+    cfg = _cfg(d, C, h, 400, 512, seed=2)
+    ds = synthgen.make_dataset(cfg, n=400)
+    p = _params(cfg)
+    lay = synthgen.param_layout(d, C, h)
+    o, shp = lay["W2T"]
+    p[o:o + shp[0] * shp[1]] = 0.0
+    o, _ = lay["b2"]
+    b2 = np.linspace(-1, 1, C).astype(np.float32)
+    b2[5] = b2[29000] = 3.0
+    p[o:o + C] = b2
+    rep = _replica(cfg, p, ds, precision, debug=False)
+    sub = ds.rows(np.arange(B))
+    top, hits = rep.eval_top1(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    assert np.all(top == 5)
+    otop, ohits, _, _ = om.top1(sub, otrain.unpack(p, d, C, h))
+    assert np.all(otop == 5) and hits == ohits
+    rep.close()

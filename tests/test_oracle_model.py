@@ -141,3 +141,46 @@ def test_chunked_gradients_equal_plain():
     np.testing.assert_allclose(gc["LSE"], f["LSE"], rtol=1e-14)
     for k, kc in (("W1", "dW1"), ("W2T", "dW2T"), ("b2", "db2"), ("b1", "db1"), ("dA", "dA")):
         np.testing.assert_allclose(gc[kc], g[k], rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- top-1 (NEXT f1)
+def test_top1_vs_torch_argmax_and_label_hits():
+    """P:228 top-1 = class of highest probability; pinned to torch softmax +
+    argmax on the densified batch (library routine) and a direct hit count."""
+    ds, p = _tiny(seed=4, n=30, d=50, C=40, h=8)
+    prm = otrain.unpack(p, ds.d, ds.C, 8)
+    X, _ = _dense_x(ds)
+    t = {k: torch.tensor(np.asarray(v, np.float64)) for k, v in prm.items()}
+    prob = torch.softmax(torch.relu(torch.tensor(X) @ t["W1"] + t["b1"]) @ t["W2T"].T + t["b2"], dim=1)
+    want = torch.argmax(prob, dim=1).numpy()
+    top, hits, zmax, logit = om.top1(ds, prm)
+    assert np.array_equal(top, want)
+    h = sum(int(want[r] in set(ds.lab[ds.lab_ptr[r]:ds.lab_ptr[r + 1]].tolist())) for r in range(ds.n))
+    assert hits == h
+    assert all(abs(zmax[r] - logit(r, int(top[r]))) < 1e-12 for r in range(ds.n))
+
+
+def test_top1_closed_form_zero_output_weights_ties_lowest_id():
+    """W2T = 0: z_r = b2 for every row, so top-1 = argmax b2; with the maximum
+    repeated at classes 3 and 7 the lowest id (3) wins (reading R21)."""
+    ds, p = _tiny(seed=6, n=20, d=30, C=12, h=8)
+    prm = otrain.unpack(p, ds.d, ds.C, 8)
+    prm["W2T"] = np.zeros_like(prm["W2T"])
+    b2 = np.linspace(-1.0, 0.5, ds.C).astype(np.float32)
+    b2[3] = b2[7] = 2.0
+    prm["b2"] = b2
+    for ops in ("fp64", "bf16"):
+        top, hits, _, _ = om.top1(ds, prm, operands=ops)
+        assert np.all(top == 3)
+        assert hits == sum(int(3 in ds.lab[ds.lab_ptr[r]:ds.lab_ptr[r + 1]]) for r in range(ds.n))
+
+
+def test_bf16_round_matches_torch_bfloat16():
+    """bf16_round (round to nearest even) vs torch's float32 -> bfloat16 cast,
+    including exact halfway cases and signed zeros."""
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.normal(0, 3, 5000), rng.normal(0, 1e-3, 1000)]).astype(np.float32)
+    half = np.array([0x3F808000, 0x3F818000, 0xBF808000, 0x00000000, 0x80000000], np.uint32).view(np.float32)
+    x = np.concatenate([x, half])
+    want = torch.tensor(x).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(om.bf16_round(x), want)
