@@ -83,7 +83,20 @@ typedef struct {
   size_t workspace_bytes;
   void *stream;           /* cudaStream_t borrowed from the caller             */
   int32_t device;         /* CUDA device ordinal of this replica               */
+  int32_t algo;           /* AS_ALGO_* merge rule (0 = the paper's Adaptive SGD) */
 } as_config;
+
+/* Merge rules (as_config.algo).  AS_ALGO_ADAPTIVE: Alg. 2 normalized,
+ * perturbed weights.  The comparison methods of P:215-217 use
+ * alpha_i = 1/N with no perturbation and no norm computation:
+ * AS_ALGO_ELASTIC  elastic model averaging / K-step averaging (Fig. 3),
+ *                  statically partitioned equal batches (as_sched_route_static)
+ * AS_ALGO_SYNC     gradient aggregation / synchronous SGD (Fig. 2):
+ *                  the same average after one batch per replica (mega-batch
+ *                  = N batches), which equals the averaged-gradient step.
+ * gamma is applied as configured in every mode (the caller sets 0 for plain
+ * averaging).  Routing and Alg. 1 are host-side choices of the caller. */
+enum { AS_ALGO_ADAPTIVE = 0, AS_ALGO_ELASTIC = 1, AS_ALGO_SYNC = 2 };
 
 /* Bytes of device workspace the ctx needs for cfg (validates cfg). */
 int as_workspace_size(const as_config *cfg, size_t *bytes);
@@ -263,6 +276,17 @@ typedef struct {
   int32_t rows;         /* rows of this batch (last one may be truncated, R8)  */
   int64_t start;        /* offset inside the mega-batch                         */
 } as_route;
+
+/* Static routing of one mega-batch for the comparison methods (P:71, P:215:
+ * "multi-GPU SGD algorithms that do not consider heterogeneity"): batch k
+ * covers samples [k*b0, k*b0 + b0) (last one truncated, R8) and goes to
+ * replica k mod N regardless of speed (b[] must be all equal, = b0).  The
+ * replay clocks are advanced exactly as in as_sched_route_replay so that the
+ * straggler cost (max_i clocks_out[i]) is comparable.  Same arguments. */
+int as_sched_route_static(int32_t N, const as_cost_model *cost, const int32_t *b,
+                          int64_t M, const int64_t *nnz_prefix, as_route *out_log,
+                          int64_t max_log, int64_t *n_log, int32_t *u_out,
+                          int64_t *clocks_out);
 
 /* Replay routing of one mega-batch (next batch to the GPU that frees
  * first; R8 ties -> lowest id, truncated last batch; R9 integer clocks).

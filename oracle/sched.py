@@ -62,6 +62,31 @@ def route_replay(costs, b, M, nnz_of):
     return log, u, t
 
 
+def route_static(costs, b, M, nnz_of):
+    """Static partitioning of the comparison methods that "do not consider
+    heterogeneity": elastic model averaging (Fig. 3) and gradient
+    aggregation (Fig. 2) give every GPU the same batches regardless of
+    speed - batch k of the mega-batch goes to GPU k mod N, all batches of the
+    same size (the last one truncated, R8).  Clocks advance with the same cost
+    models as route_replay so the straggler time max_i t_i is comparable."""
+    N = len(costs)
+    assert all(x == b[0] for x in b), "static partitioning uses equal batch sizes"
+    t = [0] * N
+    u = [0] * N
+    log = []
+    assigned = 0
+    k = 0
+    while assigned < M:
+        i = k % N
+        rows = min(b[0], M - assigned)
+        log.append((i, assigned, rows))
+        t[i] += batch_cost(costs[i], rows, nnz_of(assigned, rows))
+        u[i] += 1
+        assigned += rows
+        k += 1
+    return log, u, t
+
+
 # --------------------------------------------------------------------------
 # Algorithm 1 "Batch Size Scaling" (P:117-137), reading R11/R23 for the
 # rounding of beta*(u_i - mu) and the bound check, and the linear scaling rule

@@ -34,6 +34,11 @@ class RunConfig:
     delta: float = 0.1
     pert_thr: float = 0.1
     world: int = 2
+    # "adaptive" (the paper's method) or the comparison methods of P:215:
+    # "elastic" (elastic model averaging, Fig. 3) and "sync" (gradient
+    # aggregation, Fig. 2; callers set M = N * b_max): static equal
+    # batches, alpha_i = 1/N, no perturbation, no batch scaling
+    algo: str = "adaptive"
 
 
 def unpack(p, d, C, h):
@@ -80,18 +85,25 @@ def run(dataset, init, cfg: RunConfig, costs, total_samples, order=None, log_ste
             ids = ocsr.stream_ids(_pos + start, rows, dataset.n, order)
             return int(np.sum(rp[ids + 1] - rp[ids]))
 
-        log, u, clocks = osched.route_replay(costs, b, Mm, nnz_of)
+        if cfg.algo == "adaptive":
+            log, u, clocks = osched.route_replay(costs, b, Mm, nnz_of)
+        else:
+            log, u, clocks = osched.route_static(costs, b, Mm, nnz_of)
         losses = []
         for (i, start, rows) in log:
             bt = batch_of(dataset, ocsr.stream_ids(pos + start, rows, dataset.n, order))
             new, loss, _ = omodel.sgd_step(bt, unpack(replicas[i], cfg.d, cfg.C, cfg.h), lr[i])
             replicas[i] = pack(new)
             losses.append(loss)
-        norms = [omerge.replica_norm(w) for w in replicas]
-        alpha, pert = osched.alg2(u, b, norms, cfg.delta, cfg.pert_thr)
+        if cfg.algo == "adaptive":
+            norms = [omerge.replica_norm(w) for w in replicas]
+            alpha, pert = osched.alg2(u, b, norms, cfg.delta, cfg.pert_thr)
+        else:                                              # plain model average
+            norms, alpha, pert = None, [1.0 / N] * N, False
         b_used, lr_used = list(b), list(lr)
         wbar, wbar_p = omerge.merge(replicas, alpha, wbar, wbar_p, cfg.gamma)
-        b, lr = osched.alg1(u, b, cfg.beta, cfg.b_min, cfg.b_max, cfg.lr0)
+        if cfg.algo == "adaptive":
+            b, lr = osched.alg1(u, b, cfg.beta, cfg.b_min, cfg.b_max, cfg.lr0)
         records.append({"log": log, "u": u, "clocks": clocks, "b": b_used, "lr": lr_used,
                         "norms": norms, "alpha": alpha, "perturbed": pert,
                         "b_next": list(b), "lr_next": list(lr), "losses": losses,

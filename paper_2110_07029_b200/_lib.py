@@ -16,6 +16,8 @@ LIB_PATH = os.environ.get("ADASGD_LIB", os.path.join(HERE, "libadasgd.so"))
 
 AS_OK, AS_E_INVALID, AS_E_CUDA, AS_E_NCCL, AS_E_OOM, AS_E_STATE = 0, -1, -2, -3, -4, -5
 AS_FP32, AS_BF16 = 0, 1
+AS_ALGO_ADAPTIVE, AS_ALGO_ELASTIC, AS_ALGO_SYNC = 0, 1, 2
+ALGOS = {"adaptive": AS_ALGO_ADAPTIVE, "elastic": AS_ALGO_ELASTIC, "sync": AS_ALGO_SYNC}
 AS_FLAG_DEBUG_GRADS = 1
 AS_PARAMS_REPLICA, AS_PARAMS_GLOBAL, AS_PARAMS_GLOBAL_PREV = 0, 1, 2
 (AS_DBG_H, AS_DBG_LSE, AS_DBG_LOSS, AS_DBG_DA, AS_DBG_DB1, AS_DBG_DW2T, AS_DBG_DB2, AS_DBG_DW1,
@@ -29,7 +31,7 @@ EXPORTS = [
     "as_set_params", "as_debug_get", "as_tc_selftest", "as_sched_route_replay", "as_sched_alg1",
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
     "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
-    "as_eval_top1",
+    "as_eval_top1", "as_sched_route_static",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -48,7 +50,7 @@ class Config(C.Structure):
         ("gamma", C.c_double), ("delta", C.c_double), ("pert_thr", C.c_double),
         ("precision", C.c_int32), ("flags", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-        ("stream", C.c_void_p), ("device", C.c_int32),
+        ("stream", C.c_void_p), ("device", C.c_int32), ("algo", C.c_int32),
     ]
 
 
@@ -99,6 +101,8 @@ def load():
         "as_debug_get": [VP, I32, VP, C.c_size_t, P(C.c_size_t)],
         "as_tc_selftest": [VP, VP, P(F), P(F), P(F)],
         "as_sched_route_replay": [I32, P(CostModel), P(I32), I64, P(I64), P(Route), I64, P(I64),
+                                  P(I32), P(I64)],
+        "as_sched_route_static": [I32, P(CostModel), P(I32), I64, P(I64), P(Route), I64, P(I64),
                                   P(I32), P(I64)],
         "as_sched_alg1": [I32, P(I32), P(I32), I32, I32, I32, D, P(I32), P(F)],
         "as_sched_alg2": [I32, P(I32), P(I32), P(D), D, D, P(D), P(I32)],

@@ -26,7 +26,7 @@ class Replica:
     def __init__(self, d, C_labels, h, b_max, init_params, *, b_min=None, beta=None, megabatch=None,
                  max_row_nnz=1024, max_row_labels=64, lr0=0.1, gamma=0.9, delta=0.1, pert_thr=0.1,
                  precision="bf16", rank=0, world=1, nccl_id=None, device=0, stream=None,
-                 debug_grads=False):
+                 debug_grads=False, algo="adaptive"):
         torch = _torch()
         self.lib = L.load()
         b_min = b_max // 8 if b_min is None else b_min
@@ -37,6 +37,7 @@ class Replica:
         cfg = L.Config()
         cfg.n_features, cfg.n_labels, cfg.hidden = d, C_labels, h
         cfg.b_max, cfg.b_min, cfg.beta, cfg.megabatch = b_max, max(b_min, 1), beta, megabatch
+        cfg.algo = L.ALGOS[algo]
         cfg.max_row_nnz, cfg.max_row_labels = max_row_nnz, max_row_labels
         cfg.lr0, cfg.gamma, cfg.delta, cfg.pert_thr = lr0, gamma, delta, pert_thr
         cfg.precision = L.AS_BF16 if precision == "bf16" else L.AS_FP32

@@ -124,6 +124,7 @@ int validate_cfg(const as_config *c) {
   if ((long long)c->b_max * c->max_row_nnz >= (1ll << 31) ||
       (long long)c->b_max * c->max_row_labels >= (1ll << 31))
     return as_fail(AS_E_INVALID, "batch capacity exceeds 2^31 entries");
+  if (c->algo < AS_ALGO_ADAPTIVE || c->algo > AS_ALGO_SYNC) return as_fail(AS_E_INVALID, "unknown algo %d", c->algo);
   if (c->precision != AS_FP32 && c->precision != AS_BF16)
     return as_fail(AS_E_INVALID, "precision must be AS_FP32 or AS_BF16");
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
@@ -624,8 +625,11 @@ int as_train_step(as_ctx *x, float *loss_out) {
     ph_end(x, AS_PH_TRANSPOSE, ss);
     cudaEventRecord(x->ev_join, ss);
   };
+  // fork point of the transposes (experiment switch): 1 = after the SpMM, so
+  // the latency-bound SpMM runs alone and the transposes fill the SMs pass 1
+  // has not claimed yet and the combine kernels
 #ifndef AS_X_FORK
-#define AS_X_FORK 0
+#define AS_X_FORK 1
 #endif
   if (AS_X_FORK == 0) fork_transposes();
   // a4: SpMM forward
@@ -723,24 +727,31 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
     return as_fail(AS_E_STATE, "as_merge needs an NCCL ctx (use as_group_merge in local-group mode)");
   const Dims &D = x->D;
   cudaStream_t s = x->stream;
-  // a9: replica norm
   ph_begin(x, AS_PH_MERGE);
-  x->launches += 4;
-  as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
-  if (N > 1) {
-    const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
-    if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r)); }
-  } else {
-    cudaMemcpyAsync(x->norms_all, x->norm_dev, 8, cudaMemcpyDeviceToDevice, s);
-  }
   std::vector<double> norms(N), alpha(N);
-  int rc = cuda_check(x, cudaMemcpyAsync(norms.data(), x->norms_all, 8 * N, cudaMemcpyDeviceToHost, s), "norms D2H");
-  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "norms");
-  if (rc) return rc;
-  // a10: merge weights (host, identical on all ranks)
   int32_t pert = 0;
-  rc = as_sched_alg2(N, u, b, norms.data(), x->cfg.delta, x->cfg.pert_thr, alpha.data(), &pert);
-  if (rc) return rc;
+  int rc = AS_OK;
+  if (x->cfg.algo == AS_ALGO_ADAPTIVE) {
+    // a9: replica norm
+    x->launches += 2;
+    as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
+    if (N > 1) {
+      const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
+      if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r)); }
+    } else {
+      cudaMemcpyAsync(x->norms_all, x->norm_dev, 8, cudaMemcpyDeviceToDevice, s);
+    }
+    rc = cuda_check(x, cudaMemcpyAsync(norms.data(), x->norms_all, 8 * N, cudaMemcpyDeviceToHost, s), "norms D2H");
+    if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "norms");
+    if (rc) return rc;
+    // a10: merge weights (host, identical on all ranks)
+    rc = as_sched_alg2(N, u, b, norms.data(), x->cfg.delta, x->cfg.pert_thr, alpha.data(), &pert);
+    if (rc) return rc;
+  } else {
+    // comparison methods: plain average, no norms
+    for (int i = 0; i < N; ++i) alpha[i] = 1.0 / N;
+  }
+  x->launches += 2;
   // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset
   as::launch_scale(s, x->w, D.P, (float)alpha[x->cfg.rank]);
   if (N > 1) {
@@ -770,17 +781,22 @@ int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32
   as_ctx *x0 = ctxs[0];
   const Dims &D = x0->D;
   std::vector<double> norms(n), alpha(n);
-  for (int i = 0; i < n; ++i) {
-    as_ctx *x = ctxs[i];
-    cudaSetDevice(x->cfg.device);
-    as::launch_sumsq(x->stream, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
-    int rc = cuda_check(x, cudaMemcpyAsync(&norms[i], x->norm_dev, 8, cudaMemcpyDeviceToHost, x->stream), "norm");
-    if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "norm sync");
-    if (rc) return rc;
-  }
   int32_t pert = 0;
-  int rc = as_sched_alg2(n, u, b, norms.data(), x0->cfg.delta, x0->cfg.pert_thr, alpha.data(), &pert);
-  if (rc) return rc;
+  int rc = AS_OK;
+  if (x0->cfg.algo == AS_ALGO_ADAPTIVE) {
+    for (int i = 0; i < n; ++i) {
+      as_ctx *x = ctxs[i];
+      cudaSetDevice(x->cfg.device);
+      as::launch_sumsq(x->stream, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
+      rc = cuda_check(x, cudaMemcpyAsync(&norms[i], x->norm_dev, 8, cudaMemcpyDeviceToHost, x->stream), "norm");
+      if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "norm sync");
+      if (rc) return rc;
+    }
+    rc = as_sched_alg2(n, u, b, norms.data(), x0->cfg.delta, x0->cfg.pert_thr, alpha.data(), &pert);
+    if (rc) return rc;
+  } else {
+    for (int i = 0; i < n; ++i) alpha[i] = 1.0 / n;
+  }
   std::vector<float> af(n);
   std::vector<const float *> reps(n);
   for (int i = 0; i < n; ++i) { af[i] = (float)alpha[i]; reps[i] = ctxs[i]->w; }

@@ -60,6 +60,44 @@ int as_sched_route_replay(int32_t N, const as_cost_model *cost, const int32_t *b
   return AS_OK;
 }
 
+// Static partitioning of the comparison methods (Fig. 3): batch k
+// -> replica k mod N, equal batch sizes; the clocks replay the same cost
+// models so that the straggler time max_i t_i can be compared with P:105's
+// dynamic routing.
+int as_sched_route_static(int32_t N, const as_cost_model *cost, const int32_t *b,
+                          int64_t M, const int64_t *nnz_prefix, as_route *out_log,
+                          int64_t max_log, int64_t *n_log, int32_t *u_out,
+                          int64_t *clocks_out) {
+  if (N < 1 || !cost || !b || M < 0 || !nnz_prefix || !out_log || !n_log || !u_out ||
+      !clocks_out)
+    return as_fail(AS_E_INVALID, "as_sched_route_static: bad arguments");
+  for (int i = 0; i < N; ++i) {
+    if (b[i] < 1 || b[i] != b[0]) return as_fail(AS_E_INVALID, "as_sched_route_static: b must be equal and >= 1");
+    if (cost[i].den <= 0 || cost[i].num < 0 || cost[i].c0 < 0 || cost[i].c_row < 0 ||
+        cost[i].c_nnz < 0)
+      return as_fail(AS_E_INVALID, "as_sched_route_static: bad cost model %d", i);
+    u_out[i] = 0;
+    clocks_out[i] = 0;
+  }
+  int64_t assigned = 0, k = 0;
+  while (assigned < M) {
+    const int i = (int)(k % N);
+    const int64_t rows = b[0] < M - assigned ? b[0] : M - assigned;
+    if (k >= max_log) return as_fail(AS_E_INVALID, "as_sched_route_static: log too small");
+    const int64_t nnz = nnz_prefix[assigned + rows] - nnz_prefix[assigned];
+    const as_cost_model &c = cost[i];
+    clocks_out[i] += ((c.c0 + c.c_row * rows + c.c_nnz * nnz) * c.num) / c.den;
+    out_log[k].replica = i;
+    out_log[k].rows = (int32_t)rows;
+    out_log[k].start = assigned;
+    ++k;
+    u_out[i] += 1;
+    assigned += rows;
+  }
+  *n_log = k;
+  return AS_OK;
+}
+
 // Algorithm 1 "Batch Size Scaling".  mu = sum(u)/N (line 1).
 // beta*(u_i - mu) = beta*D_i/N with the exact integer D_i = N*u_i - sum(u);
 // R11 rounds it half away from zero and checks the bound on the rounded

@@ -25,8 +25,12 @@ def stream_nnz_prefix(row_ptr, n, pos, M, order=None):
 class ReplayState:
     """Host scheduler state shared (identically) by every rank."""
 
-    def __init__(self, world, b_max, b_min, beta, lr0, costs):
+    def __init__(self, world, b_max, b_min, beta, lr0, costs, algo="adaptive"):
+        """algo: "adaptive" (P:105 dynamic routing + Alg. 1) or a comparison
+        method of P:215 ("elastic", "sync": static equal batches, no scaling;
+        the replicas' as_config.algo must match)."""
         self.world, self.b_max, self.b_min, self.beta, self.lr0 = world, b_max, b_min, beta, lr0
+        self.algo = algo
         self.costs = [tuple(int(v) for v in (c.c0, c.c_row, c.c_nnz, c.num, c.den)) if hasattr(c, "c0")
                       else tuple(c) for c in costs]
         self.b = [b_max] * world
@@ -34,11 +38,12 @@ class ReplayState:
 
     def route(self, row_ptr, n, pos, M, order=None):
         pre = stream_nnz_prefix(row_ptr, n, pos, M, order)
-        return sched.route_replay(self.costs, self.b, M, pre)
+        return sched.route_replay(self.costs, self.b, M, pre, static=self.algo != "adaptive")
 
     def rescale(self, u):
         b_used = list(self.b)
-        self.b, self.lr = sched.alg1(u, self.b, self.beta, self.b_min, self.b_max, self.lr0)
+        if self.algo == "adaptive":
+            self.b, self.lr = sched.alg1(u, self.b, self.beta, self.b_min, self.b_max, self.lr0)
         return b_used
 
 

@@ -10,9 +10,10 @@ import numpy as np
 from . import _lib as L
 
 
-def route_replay(costs, b, M, nnz_prefix):
+def route_replay(costs, b, M, nnz_prefix, static=False):
     """costs: sequence of (c0, c_row, c_nnz, num, den); b: batch sizes;
-    nnz_prefix: int64[M+1].  Returns (log [(replica, start, rows)], u, clocks)."""
+    nnz_prefix: int64[M+1].  Returns (log [(replica, start, rows)], u, clocks).
+    static=True: as_sched_route_static (batch k -> replica k mod N)."""
     lib = L.load()
     N = len(b)
     cm = (L.CostModel * N)(*[L.CostModel(*[int(v) for v in c]) for c in costs])
@@ -24,8 +25,9 @@ def route_replay(costs, b, M, nnz_prefix):
     nlog = C.c_int64()
     u = np.zeros(N, np.int32)
     clk = np.zeros(N, np.int64)
-    L.check(lib.as_sched_route_replay(N, cm, L.ptr(bb, C.c_int32), int(M), L.ptr(pre, C.c_int64), log, cap,
-                                      C.byref(nlog), L.ptr(u, C.c_int32), L.ptr(clk, C.c_int64)))
+    fn = lib.as_sched_route_static if static else lib.as_sched_route_replay
+    L.check(fn(N, cm, L.ptr(bb, C.c_int32), int(M), L.ptr(pre, C.c_int64), log, cap,
+               C.byref(nlog), L.ptr(u, C.c_int32), L.ptr(clk, C.c_int64)))
     return [(log[k].replica, int(log[k].start), log[k].rows) for k in range(nlog.value)], u.tolist(), clk.tolist()
 
 

@@ -71,6 +71,27 @@ def test_routing_bit_exact_vs_oracle(N, M, data):
     assert log == olog and u == ou and t == ot
 
 
+def test_routing_static_golden_cpp():
+    for case in json.load(open(os.path.join(GOLD, "routing_static_cases.json")))["cases"]:
+        log, u, t = psched.route_replay(case["costs"], case["b"], case["M"], [0] * (case["M"] + 1), static=True)
+        assert [list(x) for x in log] == case["log"] and u == case["u"] and t == case["clocks"]
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 8), st.integers(1, 500), st.integers(1, 64), st.data())
+def test_routing_static_bit_exact_vs_oracle(N, M, b0, data):
+    costs = [(data.draw(st.integers(0, 10**6)), data.draw(st.integers(0, 10**5)),
+              data.draw(st.integers(0, 10**3)), data.draw(st.integers(1, 140)), data.draw(st.integers(1, 100)))
+             for _ in range(N)]
+    nnz = np.array([data.draw(st.integers(1, 50)) for _ in range(M)], np.int64)
+    pre = np.zeros(M + 1, np.int64); pre[1:] = np.cumsum(nnz)
+    log, u, t = psched.route_replay(costs, [b0] * N, M, pre, static=True)
+    olog, ou, ot = osched.route_static([synthgen.CostModel(*c) for c in costs], [b0] * N, M,
+                                       lambda s, r: int(pre[s + r] - pre[s]))
+    assert log == olog and u == ou and t == ot
+    assert sum(r for (_, _, r) in log) == M
+
+
 def test_alg1_golden_cpp():
     for case in json.load(open(os.path.join(GOLD, "alg1_cases.json")))["cases"]:
         b, lr = psched.alg1(case["u"], case["b"], case["beta"], case["b_min"], case["b_max"], 0.1)

@@ -351,6 +351,38 @@ def test_end_to_end_tiny_two_replicas_replay(gpu_lib):
     assert_close("wbar after 4 merges", reps[0].get_params(1), owbar, 1e-4)
 
 
+@pytest.mark.parametrize("algo,M", [("elastic", 1024), ("sync", 128)])
+def test_end_to_end_tiny_comparison_methods(gpu_lib, algo, M):
+    """the comparison methods of P:215 under the same
+    heterogeneous replay as T5: static equal batches (batch k -> replica k mod
+    N), alpha = 1/N, no perturbation, no batch scaling.  "sync" merges after
+    one batch per replica (M = N b_max).  Routing bit-exact, b_i
+    trajectories constant, the global model matches the oracle."""
+    from paper_2110_07029_b200 import driver
+    from paper_2110_07029_b200.api import Replica
+    cfg = synthgen.CONFIGS["tiny"]
+    ds = synthgen.make_dataset(cfg)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    costs = synthgen.make_cost_models(2, hetero=True)
+    lr0, gamma = 0.5, 0.0
+    reps = [Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta, megabatch=M,
+                    max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
+                    lr0=lr0, gamma=gamma, precision="fp32", rank=rank, world=2, algo=algo) for rank in range(2)]
+    st = driver.ReplayState(2, cfg.b_max, cfg.b_min, cfg.beta, lr0, costs, algo=algo)
+    total = 1024
+    recs = driver.run_local(reps, ds, st, total)
+    ocfg = otrain.RunConfig(d=cfg.d, C=cfg.C, h=cfg.h, b_max=cfg.b_max, b_min=cfg.b_min, beta=cfg.beta,
+                            M=M, lr0=lr0, gamma=gamma, world=2, algo=algo)
+    orecs, owbar = otrain.run(ds, p, ocfg, costs, total)
+    assert len(recs) == len(orecs) == total // M
+    for g, o in zip(recs, orecs):
+        assert [tuple(x) for x in g["log"]] == [tuple(x) for x in o["log"]]
+        assert g["u"] == o["u"] == [M // (2 * cfg.b_max)] * 2
+        assert g["b"] == o["b"] == [cfg.b_max] * 2 and g["b_next"] == [cfg.b_max] * 2
+        assert g["alpha"] == o["alpha"] == [0.5, 0.5] and not g["perturbed"]
+    assert_close("wbar", reps[0].get_params(1), owbar, 1e-4)
+
+
 @pytest.mark.slow
 def test_full_size_amazon670k_sampled(gpu_lib):
     """Amazon-670K shape at b = 1024 in the bench's launch configuration

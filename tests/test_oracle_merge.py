@@ -124,3 +124,53 @@ def test_samples_conserved_over_run():
     recs, _ = otrain.run(ds, p, cfg, costs, 100)
     assert sum(sum(r for _, _, r in rec["log"]) for rec in recs) == 100
     assert [sum(r for _, _, r in rec["log"]) for rec in recs] == [30, 30, 30, 10]
+
+
+# ------------------------------------------------ comparison methods (NEXT f2)
+def test_sync_mode_is_sgd_on_union_batch_under_heterogeneous_speeds():
+    """algo="sync" (gradient aggregation, Fig. 2): M = N b, so every
+    merge follows exactly one batch per replica regardless of the replay
+    speeds; with gamma = 0 every merge equals ONE mini-batch SGD step on the
+    union batch ("gradient and model averaging are equivalent in this
+    case").  A 32% slowdown does not change the result (static routing)."""
+    ds, p = _setup(n=72)
+    N, b, lr = 3, 8, 0.4
+    cfg = _cfg(world=N, b_max=b, b_min=1, M=N * b, gamma=0.0, lr0=lr, algo="sync", pert_thr=1e9)
+    costs = [synthgen.CostModel(5, 10, 1, 1, 1), synthgen.CostModel(5, 10, 1, 132, 100),
+             synthgen.CostModel(5, 10, 1, 116, 100)]
+    recs, wbar = otrain.run(ds, p, cfg, costs, 72)
+    w = p.copy()
+    for s in range(0, 72, N * b):
+        union = otrain.batch_of(ds, ocsr.stream_ids(s, N * b, ds.n))
+        new, _, _ = om.sgd_step(union, otrain.unpack(w, D, C, H), lr)
+        w = otrain.pack(new)
+    for r in recs:
+        assert r["u"] == [1] * N and r["alpha"] == [1.0 / N] * N and not r["perturbed"]
+        assert r["b_next"] == [b] * N
+    np.testing.assert_allclose(wbar, w, rtol=0, atol=2e-6)
+
+
+def test_elastic_equals_adaptive_at_equal_speeds():
+    """With equal row-only costs dynamic routing is round-robin, Alg. 1 leaves
+    b unchanged, Alg. 2 gives 1/N with no perturbation (R14): the paper's method
+    reduces to elastic model averaging; the whole runs are identical."""
+    ds, p = _setup(n=64)
+    kw = dict(world=2, b_max=8, b_min=1, M=32, gamma=0.9, lr0=0.5)
+    costs = [synthgen.CostModel(0, 10, 0, 1, 1)] * 2
+    ra, wa = otrain.run(ds, p, _cfg(algo="adaptive", **kw), costs, 64)
+    re, we = otrain.run(ds, p, _cfg(algo="elastic", **kw), costs, 64)
+    for a, e in zip(ra, re):
+        assert a["log"] == e["log"] and a["u"] == e["u"] and a["alpha"] == e["alpha"]
+    assert np.array_equal(wa, we)
+
+
+def test_elastic_static_split_ignores_speed():
+    """Under a 32% slowdown the elastic split keeps equal batch counts (the
+    straggler problem) while adaptive routing gives the fast GPU more."""
+    ds, p = _setup(n=64)
+    kw = dict(world=2, b_max=4, b_min=1, beta=1, M=64, gamma=0.0, lr0=0.5)
+    costs = [synthgen.CostModel(0, 10, 0, 1, 1), synthgen.CostModel(0, 10, 0, 132, 100)]
+    re, _ = otrain.run(ds, p, _cfg(algo="elastic", **kw), costs, 64)
+    ra, _ = otrain.run(ds, p, _cfg(algo="adaptive", **kw), costs, 64)
+    assert re[0]["u"] == [8, 8] and max(re[0]["clocks"]) == 8 * (40 * 132 // 100)
+    assert ra[0]["u"][0] > ra[0]["u"][1] and max(ra[0]["clocks"]) < max(re[0]["clocks"])

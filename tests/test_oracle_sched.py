@@ -146,3 +146,12 @@ def test_stream_ids_and_batch_csr():
     ref = ds.rows(ids)
     assert np.array_equal(rp, ref.row_ptr) and np.array_equal(col, ref.col)
     assert np.array_equal(lp, ref.lab_ptr) and np.array_equal(lab, ref.lab)
+
+
+def test_routing_static_golden():
+    """as hand-worked in tests/golden/routing_static_cases.json (P:71, P:215, R26)."""
+    cases = json.load(open(os.path.join(GOLD, "routing_static_cases.json")))["cases"]
+    for c in cases:
+        costs = [synthgen.CostModel(*x) for x in c["costs"]]
+        log, u, t = osched.route_static(costs, c["b"], c["M"], lambda s, r: 0)
+        assert [list(x) for x in log] == c["log"] and u == c["u"] and t == c["clocks"]
