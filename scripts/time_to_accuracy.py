@@ -1,0 +1,74 @@
+"""Synthetic time-to-accuracy harness (the paper's
+methodology: top-1 accuracy on the test set after every mega-batch).
+
+Adaptive SGD vs the comparison methods (R26: elastic model averaging, gradient
+aggregation) on ONE GPU holding N replicas (local-group merge), under the same
+heterogeneous replay (per-replica slowdowns 1.00-1.32).  Time axis = the
+replayed makespan (sum over mega-batches of max_i t_i, the straggler-bound
+wall time the replay models) plus the measured device time.  The data are a
+planted-signal synthetic XML set (synthgen.make_planted_dataset): accuracy
+numbers here say nothing about the paper's datasets.
+
+    python scripts/time_to_accuracy.py [N] [megabatches] > gpurun_out/tta.jsonl
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import synthgen
+from paper_2110_07029_b200 import driver
+from paper_2110_07029_b200.api import Replica, group_merge
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+MB = int(sys.argv[2]) if len(sys.argv) > 2 else 12
+cfg = synthgen.XMLConfig("tta", 20000, 2000, 48000, 30.0, 3.0, 128, 256, 1, 77)
+full = synthgen.make_planted_dataset(cfg)
+train = full.rows(np.arange(40000))
+test = full.rows(np.arange(40000, 48000))
+p0 = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+costs = synthgen.make_cost_models(N, hetero=True)
+lr0 = float(sys.argv[3]) if len(sys.argv) > 3 else 0.5
+ALGOS = sys.argv[4].split(",") if len(sys.argv) > 4 else ["adaptive", "elastic", "sync"]
+b_max, b_min = cfg.b_max, cfg.b_max // 8
+for algo in ALGOS:
+    M = N * b_max if algo == "sync" else 20 * b_max       # sync: one batch per replica per merge
+    gamma = 0.9 if algo == "adaptive" else 0.0
+    reps = [Replica(cfg.d, cfg.C, cfg.h, b_max, p0, b_min=b_min, beta=b_min // 2, megabatch=M,
+                    max_row_nnz=int(np.diff(full.row_ptr).max()), max_row_labels=int(np.diff(full.lab_ptr).max()),
+                    lr0=lr0, gamma=gamma, precision="bf16", rank=i, world=N, algo=algo) for i in range(N)]
+    st = driver.ReplayState(N, b_max, b_min, b_min // 2, lr0, costs, algo=algo)
+    for r in reps:
+        r.upload_dataset(train)
+    n = len(train.row_ptr) - 1
+    sim_ps, gpu_s, seen = 0, 0.0, 0
+    total = MB * 20 * b_max                                # same samples for every method
+    while seen < total:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pos = seen % n
+        log, u, clocks = st.route(train.row_ptr, n, pos, M)
+        for (i, start, rows) in log:
+            reps[i].load_batch_stream(pos + start, rows)
+            reps[i].train_step(False)
+        b_used = list(st.b)
+        group_merge(reps, u, b_used)
+        st.rescale(u)
+        for r in reps:
+            r.set_batch_sizes(st.b, st.lr)
+        torch.cuda.synchronize()
+        gpu_s += time.perf_counter() - t0
+        sim_ps += max(clocks)
+        seen += M
+        if seen % (20 * b_max) and seen < total:
+            continue
+        acc = reps[0].evaluate(test)                   # replicas restart from wbar
+        print(json.dumps({"algo": algo, "lr0": lr0, "samples": seen, "replay_s": sim_ps * 1e-12, "gpu_s": round(gpu_s, 4),
+                          "top1": acc, "u": u, "b": b_used}), flush=True)
+    for r in reps:
+        r.close()
+    torch.cuda.empty_cache()

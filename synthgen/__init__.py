@@ -184,6 +184,37 @@ def make_dataset(cfg: XMLConfig, n: int | None = None, seed: int | None = None) 
     return CSRDataset(cfg.d, cfg.C, row_ptr, col, val, lab_ptr, lab)
 
 
+def make_planted_dataset(cfg: XMLConfig, n: int | None = None, seed: int | None = None, signal: float = 0.6,
+                         proto: int = 6) -> CSRDataset:
+    """Like make_dataset, but with a learnable label signal (for the synthetic
+    time-to-accuracy harness only; the paper's data are real): class
+    c owns `proto` fixed prototype features, and about `signal` of a row's
+    features are drawn from the prototypes of its labels (the rest is the
+    Zipf noise of make_dataset).  Labels are drawn exactly as in make_dataset."""
+    n = cfg.n if n is None else int(n)
+    rng = np.random.default_rng((cfg.seed if seed is None else seed) ^ 0xA11CE)
+    base = make_dataset(cfg, n=n, seed=(cfg.seed if seed is None else seed))
+    protos = rng.integers(0, cfg.d, size=(cfg.C, proto))
+    rp, cols = [0], []
+    for r in range(n):
+        noise = base.col[base.row_ptr[r]:base.row_ptr[r + 1]]
+        labs = base.lab[base.lab_ptr[r]:base.lab_ptr[r + 1]]
+        k = max(1, int(round(signal * len(noise))))
+        sig = protos[labs].ravel()
+        sig = sig[rng.integers(0, len(sig), size=k)]
+        keep = noise[: max(0, len(noise) - k)]
+        row = np.unique(np.concatenate([sig, keep]).astype(np.int32))
+        cols.append(row)
+        rp.append(rp[-1] + len(row))
+    col = np.concatenate(cols).astype(np.int32)
+    row_ptr = np.asarray(rp, np.int64)
+    val = (1.0 - rng.random(len(col))).astype(np.float64)
+    rid = np.repeat(np.arange(n), np.diff(row_ptr))
+    ss = np.bincount(rid, weights=val * val, minlength=n)
+    val = (val / np.sqrt(ss)[rid]).astype(np.float32)
+    return CSRDataset(cfg.d, cfg.C, row_ptr, col, val, base.lab_ptr.copy(), base.lab.copy())
+
+
 def param_layout(d: int, C: int, h: int) -> dict:
     """Offsets (in floats) of the packed parameter vector [W1 | b1 | W2T | b2]
     (reading R2).  W1 is [d][h], W2T is [C][h] (label-major)."""
