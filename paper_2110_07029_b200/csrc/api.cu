@@ -73,6 +73,8 @@ struct as_ctx {
   __nv_bfloat16 *Hb;
   float *dA, *lse2, *lsep, *zsum, *labW, *lossr, *loss;
   float *pm, *pl, *pO;
+  float *db1p;                // db1 partials of the fused combine
+  int *db1cnt;
   int32_t *top1;              // top-1 evaluation (NEXT f1)
   unsigned long long *hits;
   float *Z, *dH, *dW2, *splitk_tmp;
@@ -206,6 +208,8 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pm = (float *)p;
   p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pl = (float *)p;
   p = P(4 * (size_t)D.bpad); if (x) x->top1 = (int32_t *)p;
+  p = P(4 * (size_t)(D.bpad / 32 + 1) * D.h); if (x) x->db1p = (float *)p;
+  p = P(4 * (size_t)D.h); if (x) x->db1cnt = (int *)p;
   p = P(8); if (x) x->hits = (unsigned long long *)p;
   if (bf16) {
     p = P(4 * (size_t)D.max_splits * D.bpad * D.h); if (x) x->pO = (float *)p;
@@ -380,6 +384,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->lbits, 0, 4 * (size_t)D.C * D.bw, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->tile_state, 0, 8 * (size_t)D.tr_tiles, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->ticket, 0, 16, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->db1cnt, 0, 4 * (size_t)D.h, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->arrive, 0, 4 * (size_t)D.sort_cap, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->Hb, 0, 2 * (size_t)D.bpad * D.h, x->stream), "memset");
   // side stream at the lowest priority: the transposes fill SMs the critical
@@ -647,13 +652,13 @@ int as_train_step(as_ctx *x, float *loss_out) {
     ph_end(x, AS_PH_OUT_FWD);
     if (AS_X_FORK == 2) fork_transposes();
     ph_begin(x, AS_PH_COMBINE);
-    x->launches += 3;
-    // label terms of the loss and of dH (R3)
+    x->launches += 2;
+    // label terms of the loss and of dH (R3), then the split combine -> LSE,
+    // loss, dA, and db1 with b1's SGD fused (ordered last-arriver column sums)
     as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
                             x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lse2, x->lsep, x->lossr,
-                            x->dA);
-    as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
+                            x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr);
     ph_end(x, AS_PH_COMBINE);
     cudaStreamWaitEvent(s, x->ev_join, 0);   // label transpose ready
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2

@@ -105,8 +105,9 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // combine of the bf16 pass-1 partials -> LSE, loss rows, dA (steps a5)
 void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max, int bpad,
                          int splits, const float *pm, const float *pl, const float *pO,
-                         const float *labW, const float *zsum, const float *Hf, float *lse2,
-                         float *lsep, float *lossr, float *dA);
+                         const float *labW, const float *zsum, const float *Hf, float *lse2, float *lsep,
+                         float *lossr, float *dA, float *db1p, int *db1cnt, float *b1, float lr,
+                         float *dbg_db1);
 // fp32 (SIMT) output layer (steps a5/a6 in parity mode)
 void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
                      long long sak, const float *B, long long sbk, long long sbn, float *Cm,

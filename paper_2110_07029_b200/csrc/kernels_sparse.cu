@@ -501,16 +501,30 @@ __global__ void k_label_terms(const StepDesc *__restrict__ desc, const int64_t *
     lw[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float zs = 0.f;
-  for (int64_t j = s; j < e; ++j) {
-    const int y = lab[j];
-    float d = 0.f;
+  // labels 4 at a time: all four W2T rows (and b2 values) in flight at once
+  for (int64_t j0 = s; j0 < e; j0 += 4) {
+    float4 w[4][V];
+    float bb[4];
 #pragma unroll
-    for (int q = 0; q < V; ++q) {
-      const float4 w = reinterpret_cast<const float4 *>(W2T + (size_t)y * H)[lane + 32 * q];
-      d = fmaf(hr[q].x, w.x, fmaf(hr[q].y, w.y, fmaf(hr[q].z, w.z, fmaf(hr[q].w, w.w, d))));
-      lw[q].x += w.x; lw[q].y += w.y; lw[q].z += w.z; lw[q].w += w.w;
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = j0 + u < e;
+      const int y = ok ? lab[j0 + u] : 0;
+      bb[u] = ok ? b2[y] : 0.f;
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+        w[u][q] = ok ? reinterpret_cast<const float4 *>(W2T + (size_t)y * H)[lane + 32 * q]
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    zs += warp_sum(d) + b2[y];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float d = 0.f;
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        d = fmaf(hr[q].x, w[u][q].x, fmaf(hr[q].y, w[u][q].y, fmaf(hr[q].z, w[u][q].z, fmaf(hr[q].w, w[u][q].w, d))));
+        lw[q].x += w[u][q].x; lw[q].y += w[u][q].y; lw[q].z += w[u][q].z; lw[q].w += w[u][q].w;
+      }
+      zs += warp_sum(d) + bb[u];
+    }
   }
   if (lane == 0) zsum[r] = zs * inv_k;
 #pragma unroll
@@ -541,7 +555,8 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     const StepDesc *__restrict__ desc, int h, int bpad, int splits, const float *__restrict__ pm,
     const float *__restrict__ pl, const float *__restrict__ pO, const float *__restrict__ labW,
     const float *__restrict__ zsum, const float *__restrict__ Hf, float *__restrict__ lse2,
-    float *__restrict__ lsep, float *__restrict__ lossr, float *__restrict__ dA) {
+    float *__restrict__ lsep, float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
+    int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1) {
   // CTA = 32 rows x 16 columns (8 groups of 2); partial reads coalesced over rows
   const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
   const int B = desc->rows;
@@ -564,11 +579,38 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   float l = 0.f;
   for (int s = 0; s < splits; ++s) l = fmaf(pl[(size_t)s * bpad + r], sc[s * 32 + rx], l);
   const float invB = 1.0f / (float)B, invl = 1.0f / l;
+  __shared__ float cs[16][33];                // dA of this CTA's rows x columns (db1 partial)
   for (int j = blockIdx.y * 16 + jy; j < h && j < blockIdx.y * 16 + 16; j += 8) {
     float o = 0.f;
     for (int s = 0; s < splits; ++s) o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc[s * 32 + rx], o);
     const float dh = (o * invl - labW[(size_t)r * h + j]) * invB;
-    if (live) dA[(size_t)r * h + j] = Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
+    const float da = live && Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
+    if (live) dA[(size_t)r * h + j] = da;
+    cs[j - blockIdx.y * 16][rx] = da;
+  }
+  // db1 = sum_r dA_r (step a5), fused: per-CTA column sums over its 32 rows in
+  // row order, then the last row block to arrive for this column group adds
+  // the partials in row-block order and applies b1 -= lr db1 (deterministic)
+  __syncthreads();
+  const int nrb = (B + 31) / 32;
+  if (threadIdx.x < 16) {
+    float g = 0.f;
+    for (int k = 0; k < 32; ++k) g += cs[threadIdx.x][k];
+    db1p[(size_t)blockIdx.x * h + blockIdx.y * 16 + threadIdx.x] = g;
+    __threadfence();
+  }
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = atomicAdd(&db1cnt[blockIdx.y], 1) == nrb - 1;
+  __syncthreads();
+  if (last && threadIdx.x < 16) {
+    __threadfence();
+    const int c = blockIdx.y * 16 + threadIdx.x;
+    float g = 0.f;
+    for (int k = 0; k < nrb; ++k) g += __ldcg(db1p + (size_t)k * h + c);
+    b1[c] -= lr * g;
+    if (dbg_db1) dbg_db1[c] = g;
+    if (threadIdx.x == 0) db1cnt[blockIdx.y] = 0;
   }
   if (jy == 0 && live && blockIdx.y == 0) {
     const float L2 = M + log2f(l);
@@ -580,10 +622,11 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
 
 void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max, int bpad,
                          int splits, const float *pm, const float *pl, const float *pO,
-                         const float *labW, const float *zsum, const float *Hf, float *lse2,
-                         float *lsep, float *lossr, float *dA) {
+                         const float *labW, const float *zsum, const float *Hf, float *lse2, float *lsep,
+                         float *lossr, float *dA, float *db1p, int *db1cnt, float *b1, float lr,
+                         float *dbg_db1) {
   k_combine_bf16<<<dim3(ceil_div(bpad, 32), h / 16), 256, (size_t)splits * 32 * 4, s>>>(
-      desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lsep, lossr, dA);
+      desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lsep, lossr, dA, db1p, db1cnt, b1, lr, dbg_db1);
 }
 
 // =====================================================================
