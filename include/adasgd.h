@@ -51,9 +51,15 @@ enum { AS_FP32 = 0, AS_BF16 = 1 };
 
 /* ---- flags --------------------------------------------------------------- */
 enum {
-  AS_FLAG_DEBUG_GRADS = 1 /* keep every gradient of the last step in device
-                             memory for as_debug_get (tests only)            */
+  AS_FLAG_DEBUG_GRADS = 1, /* keep every gradient of the last step in device
+                              memory for as_debug_get (tests only)            */
+  AS_FLAG_NORM_UB = 2      /* as_merge (AS_ALGO_ADAPTIVE): Alg. 2 line 5 uses
+                              u_i b_i / sum(u b) instead of u_i / sum(u), the
+                              alternative of P:175                             */
 };
+
+/* Alg. 2 line-5 normalisation (as_sched_alg2_ex). */
+enum { AS_NORM_UPDATES = 0, AS_NORM_UB = 1 };
 
 typedef struct as_ctx as_ctx; /* opaque */
 
@@ -308,6 +314,20 @@ int as_sched_alg1(int32_t N, const int32_t *u, const int32_t *b, int32_t beta,
 int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b,
                   const double *norms, double delta, double pert_thr,
                   double *alpha_out, int32_t *perturbed_out);
+
+/* as_sched_alg2 with the line-5 normalisation selectable: AS_NORM_UPDATES
+ * (Alg. 2 as printed) or AS_NORM_UB ("normalize based on the product
+ * between the number of updates and the batch size").  Same outputs. */
+int as_sched_alg2_ex(int32_t N, const int32_t *u, const int32_t *b, const double *norms,
+                     double delta, double pert_thr, int32_t norm_mode, double *alpha_out,
+                     int32_t *perturbed_out);
+
+/* Fit one replica's replay cost model (R9) to a live trace of n >= 3 batches
+ * (rows_k, nnz_k, measured time ps_k in picoseconds; host arrays): least
+ * squares of ps = c0 + c_row rows + c_nnz nnz, integer-rounded, >= 0,
+ * num = den = 1.  AS_E_INVALID when the design is singular. */
+int as_sched_fit_cost(int64_t n, const int32_t *rows, const int64_t *nnz, const int64_t *ps,
+                      as_cost_model *out);
 
 /* Fisher-Yates permutation of [0, n) driven by SplitMix64(seed) (R10). */
 int as_sched_permutation(int64_t n, uint64_t seed, int64_t *out);

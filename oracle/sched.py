@@ -5,6 +5,8 @@ doubles, written out in the paper's order and notation.
 """
 from __future__ import annotations
 
+import numpy as np
+
 MASK64 = (1 << 64) - 1
 
 
@@ -117,14 +119,20 @@ def _f32(x):
 # R13 (exact equality), R14 (lexicographic argmax/argmin of (u_i, b_i), skip
 # when identical), R15 (strict <), R16 (no renormalisation).
 # --------------------------------------------------------------------------
-def alg2(u, b, norms, delta, pert_thr):
+def alg2(u, b, norms, delta, pert_thr, norm="u"):
+    """norm="ub": line 5 normalises by u_i b_i instead ("an alternative
+    for later stages is to normalize based on the product between the number
+    of updates and the batch size")."""
     N = len(u)
     if all(x == u[0] for x in u):                 # line 2
         sb = float(sum(b))
         alpha = [float(bi) / sb for bi in b]      # line 3
-    else:
+    elif norm == "u":
         su = float(sum(u))
         alpha = [float(ui) / su for ui in u]      # line 5
+    else:
+        sub = float(sum(ui * bi for ui, bi in zip(u, b)))
+        alpha = [float(ui * bi) / sub for ui, bi in zip(u, b)]
     perturbed = 0
     if all(nrm < pert_thr for nrm in norms):      # line 7
         keys = [(u[i], b[i]) for i in range(N)]
@@ -135,3 +143,13 @@ def alg2(u, b, norms, delta, pert_thr):
             alpha[s] = alpha[s] * (1.0 - delta)
             perturbed = 1
     return alpha, perturbed
+
+
+def fit_cost(rows, nnz, ps):
+    """Replay cost model from a live trace (reading R9): least
+    squares of ps = c0 + c_row rows + c_nnz nnz (numpy lstsq), rounded to the
+    nearest integer and clamped at 0; num = den = 1."""
+    X = np.stack([np.ones(len(rows)), np.asarray(rows, np.float64), np.asarray(nnz, np.float64)], axis=1)
+    coef, *_ = np.linalg.lstsq(X, np.asarray(ps, np.float64), rcond=None)
+    c = [max(0, int(np.rint(v))) for v in coef]
+    return (c[0], c[1], c[2], 1, 1)

@@ -18,7 +18,8 @@ AS_OK, AS_E_INVALID, AS_E_CUDA, AS_E_NCCL, AS_E_OOM, AS_E_STATE = 0, -1, -2, -3,
 AS_FP32, AS_BF16 = 0, 1
 AS_ALGO_ADAPTIVE, AS_ALGO_ELASTIC, AS_ALGO_SYNC = 0, 1, 2
 ALGOS = {"adaptive": AS_ALGO_ADAPTIVE, "elastic": AS_ALGO_ELASTIC, "sync": AS_ALGO_SYNC}
-AS_FLAG_DEBUG_GRADS = 1
+AS_FLAG_DEBUG_GRADS, AS_FLAG_NORM_UB = 1, 2
+AS_NORM_UPDATES, AS_NORM_UB = 0, 1
 AS_PARAMS_REPLICA, AS_PARAMS_GLOBAL, AS_PARAMS_GLOBAL_PREV = 0, 1, 2
 (AS_DBG_H, AS_DBG_LSE, AS_DBG_LOSS, AS_DBG_DA, AS_DBG_DB1, AS_DBG_DW2T, AS_DBG_DB2, AS_DBG_DW1,
  AS_DBG_FSEG, AS_DBG_LSEG, AS_DBG_BATCH, AS_DBG_LOGITS) = range(12)
@@ -31,7 +32,7 @@ EXPORTS = [
     "as_set_params", "as_debug_get", "as_tc_selftest", "as_sched_route_replay", "as_sched_alg1",
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
     "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
-    "as_eval_top1", "as_sched_route_static",
+    "as_eval_top1", "as_sched_route_static", "as_sched_alg2_ex", "as_sched_fit_cost",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -106,6 +107,8 @@ def load():
                                   P(I32), P(I64)],
         "as_sched_alg1": [I32, P(I32), P(I32), I32, I32, I32, D, P(I32), P(F)],
         "as_sched_alg2": [I32, P(I32), P(I32), P(D), D, D, P(D), P(I32)],
+        "as_sched_alg2_ex": [I32, P(I32), P(I32), P(D), D, D, I32, P(D), P(I32)],
+        "as_sched_fit_cost": [I64, P(I32), P(I64), P(I64), P(CostModel)],
         "as_sched_permutation": [I64, C.c_uint64, P(I64)],
         "as_live_open": [C.c_char_p, I32, P(VP)],
         "as_live_claim": [VP, I64, I32, P(I64), P(I32)],

@@ -750,7 +750,8 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
     if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "norms");
     if (rc) return rc;
     // a10: merge weights (host, identical on all ranks)
-    rc = as_sched_alg2(N, u, b, norms.data(), x->cfg.delta, x->cfg.pert_thr, alpha.data(), &pert);
+    rc = as_sched_alg2_ex(N, u, b, norms.data(), x->cfg.delta, x->cfg.pert_thr,
+                          (x->cfg.flags & AS_FLAG_NORM_UB) ? AS_NORM_UB : AS_NORM_UPDATES, alpha.data(), &pert);
     if (rc) return rc;
   } else {
     // comparison methods: plain average, no norms
@@ -797,7 +798,8 @@ int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32
       if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "norm sync");
       if (rc) return rc;
     }
-    rc = as_sched_alg2(n, u, b, norms.data(), x0->cfg.delta, x0->cfg.pert_thr, alpha.data(), &pert);
+    rc = as_sched_alg2_ex(n, u, b, norms.data(), x0->cfg.delta, x0->cfg.pert_thr,
+                          (x0->cfg.flags & AS_FLAG_NORM_UB) ? AS_NORM_UB : AS_NORM_UPDATES, alpha.data(), &pert);
     if (rc) return rc;
   } else {
     for (int i = 0; i < n; ++i) alpha[i] = 1.0 / n;

@@ -1,6 +1,7 @@
 // Host scheduler of Adaptive SGD: replay routing, Alg. 1, Alg. 2 weights,
 // stream permutation and the live shared cursor.  Pure host code; the device
 // never sees it.  P:N = PAPER.md line N, Rk = DESIGN.md reading k.
+#include <cmath>
 #include <cerrno>
 #include <cstdio>
 #include <cstdlib>
@@ -131,7 +132,16 @@ int as_sched_alg1(int32_t N, const int32_t *u, const int32_t *b, int32_t beta,
 int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b, const double *norms,
                   double delta, double pert_thr, double *alpha_out,
                   int32_t *perturbed_out) {
-  if (N < 1 || !u || !b || !norms || !alpha_out)
+  return as_sched_alg2_ex(N, u, b, norms, delta, pert_thr, AS_NORM_UPDATES, alpha_out, perturbed_out);
+}
+
+// norm_mode AS_NORM_UB: line 5 uses u_i b_i / sum(u b) -- "an alternative for
+// later stages is to normalize based on the product between the number of
+// updates and the batch size".
+int as_sched_alg2_ex(int32_t N, const int32_t *u, const int32_t *b, const double *norms,
+                     double delta, double pert_thr, int32_t norm_mode, double *alpha_out,
+                     int32_t *perturbed_out) {
+  if (N < 1 || !u || !b || !norms || !alpha_out || (norm_mode != AS_NORM_UPDATES && norm_mode != AS_NORM_UB))
     return as_fail(AS_E_INVALID, "as_sched_alg2: bad arguments");
   bool all_equal = true;
   for (int i = 1; i < N; ++i)
@@ -141,10 +151,15 @@ int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b, const double *n
     for (int i = 0; i < N; ++i) sb += b[i];
     if (sb <= 0) return as_fail(AS_E_INVALID, "as_sched_alg2: sum(b) == 0");
     for (int i = 0; i < N; ++i) alpha_out[i] = (double)b[i] / (double)sb;
-  } else {  // line 5: alpha_i = u_i / sum(u)
+  } else if (norm_mode == AS_NORM_UPDATES) {  // line 5: alpha_i = u_i / sum(u)
     int64_t su = 0;
     for (int i = 0; i < N; ++i) su += u[i];
     for (int i = 0; i < N; ++i) alpha_out[i] = (double)u[i] / (double)su;
+  } else {  // P:175 variant: alpha_i = u_i b_i / sum(u b)
+    int64_t sub = 0;
+    for (int i = 0; i < N; ++i) sub += (int64_t)u[i] * b[i];
+    if (sub <= 0) return as_fail(AS_E_INVALID, "as_sched_alg2: sum(u b) == 0");
+    for (int i = 0; i < N; ++i) alpha_out[i] = (double)((int64_t)u[i] * b[i]) / (double)sub;
   }
   int32_t pert = 0;
   bool regular = true;  // line 7
@@ -239,3 +254,44 @@ int as_live_close(as_live *lv, int32_t unlink_segment) {
 }
 
 }  // extern "C"
+
+// Replay cost model from a live trace ("relative processing speed",
+// P:193 the scheduler records per-batch times; reading R9): least-squares fit
+// of t_k = c0 + c_row rows_k + c_nnz nnz_k (picoseconds) over n recorded
+// batches of one replica, normal equations in long double, coefficients
+// rounded to the nearest integer and clamped at 0; num = den = 1.
+int as_sched_fit_cost(int64_t n, const int32_t *rows, const int64_t *nnz, const int64_t *ps,
+                      as_cost_model *out) {
+  if (n < 3 || !rows || !nnz || !ps || !out) return as_fail(AS_E_INVALID, "as_sched_fit_cost: bad arguments");
+  long double A[3][4] = {{0}};
+  for (int64_t k = 0; k < n; ++k) {
+    const long double x[3] = {1.0L, (long double)rows[k], (long double)nnz[k]};
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) A[i][j] += x[i] * x[j];
+      A[i][3] += x[i] * (long double)ps[k];
+    }
+  }
+  for (int c = 0; c < 3; ++c) {  // Gauss-Jordan with partial pivoting
+    int p = c;
+    for (int i = c + 1; i < 3; ++i)
+      if (fabsl(A[i][c]) > fabsl(A[p][c])) p = i;
+    if (fabsl(A[p][c]) < 1e-30L) return as_fail(AS_E_INVALID, "as_sched_fit_cost: singular (rows / nnz collinear)");
+    for (int j = 0; j < 4; ++j) { const long double t = A[c][j]; A[c][j] = A[p][j]; A[p][j] = t; }
+    for (int i = 0; i < 3; ++i) {
+      if (i == c) continue;
+      const long double f = A[i][c] / A[c][c];
+      for (int j = c; j < 4; ++j) A[i][j] -= f * A[c][j];
+    }
+  }
+  int64_t co[3];
+  for (int i = 0; i < 3; ++i) {
+    const long double v = A[i][3] / A[i][i];
+    co[i] = v <= 0.0L ? 0 : (int64_t)llroundl(v);
+  }
+  out->c0 = co[0];
+  out->c_row = co[1];
+  out->c_nnz = co[2];
+  out->num = 1;
+  out->den = 1;
+  return AS_OK;
+}

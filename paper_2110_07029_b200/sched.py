@@ -42,15 +42,28 @@ def alg1(u, b, beta, b_min, b_max, lr0):
     return bo.tolist(), [float(x) for x in lo]
 
 
-def alg2(u, b, norms, delta, pert_thr):
+def alg2(u, b, norms, delta, pert_thr, norm="u"):
+    """norm: "u" (Alg. 2 line 5 as printed) or "ub" (the P:175 alternative)."""
     lib = L.load()
     N = len(u)
     uu, bb, nn = L.as_np(u, np.int32), L.as_np(b, np.int32), L.as_np(norms, np.float64)
     a = np.zeros(N, np.float64)
     p = C.c_int32()
-    L.check(lib.as_sched_alg2(N, L.ptr(uu, C.c_int32), L.ptr(bb, C.c_int32), L.ptr(nn, C.c_double),
-                              float(delta), float(pert_thr), L.ptr(a, C.c_double), C.byref(p)))
+    L.check(lib.as_sched_alg2_ex(N, L.ptr(uu, C.c_int32), L.ptr(bb, C.c_int32), L.ptr(nn, C.c_double),
+                                 float(delta), float(pert_thr), L.AS_NORM_UB if norm == "ub" else L.AS_NORM_UPDATES,
+                                 L.ptr(a, C.c_double), C.byref(p)))
     return a.tolist(), p.value
+
+
+def fit_cost(rows, nnz, ps):
+    """as_sched_fit_cost: replay cost model (c0, c_row, c_nnz, 1, 1) of one
+    replica from a live trace of (rows, nnz, picoseconds) per batch."""
+    lib = L.load()
+    r, z, t = L.as_np(rows, np.int32), L.as_np(nnz, np.int64), L.as_np(ps, np.int64)
+    out = L.CostModel()
+    L.check(lib.as_sched_fit_cost(len(r), L.ptr(r, C.c_int32), L.ptr(z, C.c_int64), L.ptr(t, C.c_int64),
+                                  C.byref(out)))
+    return (out.c0, out.c_row, out.c_nnz, out.num, out.den)
 
 
 def permutation(n, seed):

@@ -92,6 +92,30 @@ def test_routing_static_bit_exact_vs_oracle(N, M, b0, data):
     assert sum(r for (_, _, r) in log) == M
 
 
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 8), st.data())
+def test_alg2_ub_bit_exact_vs_oracle(N, data):
+    u = [data.draw(st.integers(0, 40)) for _ in range(N)]
+    if sum(u) == 0:
+        u[0] = 1
+    b = [data.draw(st.integers(1, 1024)) for _ in range(N)]
+    norms = [data.draw(st.floats(0.0, 0.2)) for _ in range(N)]
+    a, p = psched.alg2(u, b, norms, 0.1, 0.1, norm="ub")
+    oa, op = osched.alg2(u, b, norms, 0.1, 0.1, norm="ub")
+    assert a == oa and p == op
+
+
+def test_fit_cost_cpp_vs_oracle():
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        n = int(rng.integers(3, 60))
+        rows = rng.integers(1, 1025, n)
+        nnz = rng.integers(1, 80_000, n)
+        c = (int(rng.integers(0, 10**7)), int(rng.integers(0, 10**5)), int(rng.integers(0, 10**3)))
+        t = c[0] + c[1] * rows + c[2] * nnz
+        assert psched.fit_cost(rows, nnz, t) == osched.fit_cost(rows, nnz, t) == c + (1, 1)
+
+
 def test_alg1_golden_cpp():
     for case in json.load(open(os.path.join(GOLD, "alg1_cases.json")))["cases"]:
         b, lr = psched.alg1(case["u"], case["b"], case["beta"], case["b_min"], case["b_max"], 0.1)

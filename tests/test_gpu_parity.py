@@ -319,6 +319,31 @@ def test_group_merge_parity(gpu_lib, precision):
     assert_close("wbar2", reps[0].get_params(1), wbar2, 1e-5)
 
 
+def test_group_merge_ub_normalisation(gpu_lib):
+    """AS_FLAG_NORM_UB (P:175 alternative: alpha_i ~ u_i b_i): alpha bit-exact
+    with oracle.sched.alg2(norm="ub"), merged model within 1e-5."""
+    from paper_2110_07029_b200.api import Replica, group_merge
+    cfg = _cfg(1000, 500, 128, 200, 64)
+    ds = synthgen.make_dataset(cfg, n=200)
+    p = _params(cfg)
+    b = [64, 48, 32]
+    reps = [Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=8, max_row_nnz=int(np.diff(ds.row_ptr).max()),
+                    max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=0.5, precision="fp32", rank=i, world=3,
+                    merge_norm="ub") for i in range(3)]
+    for i, r in enumerate(reps):
+        r.set_batch_sizes(b, [0.5, 0.375, 0.25])
+        for k in range(i + 1):
+            sub = ds.rows(np.arange(b[i] // 2) + 40 * i + 8 * k)
+            r.load_batch_csr(b[i] // 2, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+            r.train_step()
+    ws = [r.get_params() for r in reps]
+    alpha, pert = group_merge(reps, [1, 2, 3], b)
+    oa, op = osched.alg2([1, 2, 3], b, [omerge.replica_norm(w) for w in ws], 0.1, 0.1, norm="ub")
+    assert list(alpha) == oa and pert == op
+    wbar, _ = omerge.merge(ws, oa, p, p, 0.9)
+    assert_close("wbar", reps[0].get_params(1), wbar, 1e-5)
+
+
 def test_end_to_end_tiny_two_replicas_replay(gpu_lib):
     """T5: config 'tiny' (BASELINE.json configs[0]): 2 replicas, replay with a
     32% slowdown, 1 epoch, 4 merges, fp32 mode.  Routing, b_i, lr_i and alpha

@@ -155,3 +155,28 @@ def test_routing_static_golden():
         costs = [synthgen.CostModel(*x) for x in c["costs"]]
         log, u, t = osched.route_static(costs, c["b"], c["M"], lambda s, r: 0)
         assert [list(x) for x in log] == c["log"] and u == c["u"] and t == c["clocks"]
+
+
+def test_alg2_ub_normalisation_hand_worked():
+    """P:175 variant (u_i b_i normalisation), hand-worked: u = (5, 3), b = (64, 60)
+    -> u b = (320, 180), alpha = (0.64, 0.36); all norms regular -> perturbed
+    (0.704, 0.324), sum = 1 + delta (0.64 - 0.36) = 1.028 (R16).  Equal u keeps
+    line 3 (b normalisation) in both modes."""
+    a, p = osched.alg2([5, 3], [64, 60], [0.0, 0.0], 0.1, 0.1, norm="ub")
+    assert p == 1
+    assert [Fraction(x).limit_denominator(10**6) for x in a] == [Fraction(704, 1000), Fraction(324, 1000)]
+    a0, _ = osched.alg2([5, 3], [64, 60], [1.0, 1.0], 0.1, 0.1, norm="ub")
+    assert [Fraction(x).limit_denominator(10**6) for x in a0] == [Fraction(16, 25), Fraction(9, 25)]
+    assert osched.alg2([4, 4], [64, 48], [1.0, 1.0], 0.1, 0.1, norm="ub") == \
+        osched.alg2([4, 4], [64, 48], [1.0, 1.0], 0.1, 0.1, norm="u")
+
+
+def test_fit_cost_recovers_integer_model():
+    """R9 replay model from a live trace: noiseless times generated by a known
+    integer model are recovered exactly; with +-0.4 ps of noise too."""
+    rng = np.random.default_rng(3)
+    rows = rng.integers(64, 1025, 40)
+    nnz = rows * 70 + rng.integers(-2000, 2000, 40)
+    t = 2_000_000 + 40_000 * rows + 500 * nnz
+    assert osched.fit_cost(rows, nnz, t) == (2_000_000, 40_000, 500, 1, 1)
+    assert osched.fit_cost(rows, nnz, t + rng.uniform(-0.4, 0.4, 40)) == (2_000_000, 40_000, 500, 1, 1)
