@@ -907,14 +907,41 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         for (int c = 0; c < 4; ++c) tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, c * 32, blockIdx.x * BM);
       }
     }
+    // h = 128: the bf16 W2T rows of block kb + NWT are fetched into registers
+    // BEFORE waiting for block kb's accumulator (the HBM latency hides in that
+    // wait) and written into the TMEM buffer block kb's S MMAs have released
+    auto fetch_wt = [&](int kb_, uint32_t (&r)[64]) {
+      const int cls = (blockIdx.x + kb_ * gridDim.x) * BM + i;
+      const uint4 *src = reinterpret_cast<const uint4 *>(W2b + (size_t)(cls < C ? cls : 0) * H);
+#pragma unroll
+      for (int v4 = 0; v4 < 16; ++v4) {
+        uint4 x = src[v4];
+        if (cls >= C) x = make_uint4(0u, 0u, 0u, 0u);
+        r[4 * v4] = x.x; r[4 * v4 + 1] = x.y; r[4 * v4 + 2] = x.z; r[4 * v4 + 3] = x.w;
+      }
+    };
+    auto put_wt = [&](int kb_, uint32_t (&r)[64]) {
+      const int wb = kb_ % NWT;
+      AS_TMEM_ST32(tl + COL_W + wb * WCOLS, r);
+      AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 32, (r + 32));
+      tmem_wait_st();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wt_full[wb]);
+    };
     for (int kb = 0; kb < NB && kb < NWT; ++kb) load_wt(kb);
     for (int kb = 0; kb < NB; ++kb) {
       const int cb = blockIdx.x + kb * gridDim.x;
+      uint32_t wpre[TMAUPD ? 64 : 1];
+      if constexpr (TMAUPD) {
+        if (kb + NWT < NB) fetch_wt(kb + NWT, wpre);
+      }
       TRACE(3, ut == 0, 11, kb);
       mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
       if constexpr (TMAUPD) {
+        if (kb + NWT < NB) put_wt(kb + NWT, wpre);
         // fused SGD of the block from the TMEM accumulator (lane i = class i)
         // and the TMA-loaded fp32 block: W2T -= lr dW2T in place (swizzled
         // 32-column boxes, conflict-free), bf16 shadow into its staging boxes
@@ -962,8 +989,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls * H + ch * 32 + k] = __uint_as_float(r[k]);
           }
         }
-        // (2) the W2T block two ahead into the TMEM buffer freed by block kb
-        if (kb + NWT < NB) load_wt(kb + NWT);
+        // (2) block kb + NWT's W2T already in TMEM (put_wt above)
         // (3) TMA store of the updated block, then the next block's fp32 W2T
         //     into the same buffer once the store has read it
         fence_proxy_async();
