@@ -263,11 +263,16 @@ __device__ __forceinline__ void sb_copy(void *dst, const void *src, uint32_t byt
                ::"r"(sm32(dst)), "l"((uint64_t)src), "r"(bytes), "r"(sm32(bar)) : "memory");
 }
 
+#ifndef AS_SEG1_NW                                   // experiment overrides (MODE 1)
+#define AS_SEG1_NW 6
+#define AS_SEG1_NST 2
+#define AS_SEG1_GE (2048 / H)
+#endif
 template <int H, int MODE>
 struct SegCfg {
-  static constexpr int GE = 2048 / H;                 // entries per group (8 KB of rows)
-  static constexpr int NW = MODE == 0 ? 8 : 6;        // warps per CTA
-  static constexpr int NST = MODE == 0 ? 3 : 2;       // ring stages per warp
+  static constexpr int GE = MODE == 0 ? 2048 / H : AS_SEG1_GE;   // entries per group
+  static constexpr int NW = MODE == 0 ? 8 : AS_SEG1_NW;          // warps per CTA
+  static constexpr int NST = MODE == 0 ? 3 : AS_SEG1_NST;        // ring stages per warp
   static constexpr int ROW = H * 4;                   // bytes per gathered row
   static constexpr int STAGE = GE * ROW * (MODE == 1 ? 2 : 1);   // + prefetched W1 rows (MODE 1)
   static constexpr int SMEM = NW * NST * STAGE + NW * 2 * ROW + NW * NST * 8;

@@ -569,7 +569,10 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   const int r = live ? blockIdx.x * 32 + rx : B - 1;   // padding lanes shadow a live row
   if (!live && jy == 0 && blockIdx.y == 0) lsep[blockIdx.x * 32 + rx] = INFINITY;
   extern __shared__ float sc[];             // [splits][32] per-slot scales of the rows
+  // every slot loop is unrolled 12-wide so a thread keeps 12 partial loads in
+  // flight (the partials are L2-resident right after pass 1)
   float M = -FLT_MAX;
+#pragma unroll 12
   for (int s = 0; s < splits; ++s) M = fmaxf(M, pm[(size_t)s * bpad + r]);
   for (int s = jy; s < splits; s += 8) {
     const float ms = pm[(size_t)s * bpad + r];
@@ -577,11 +580,13 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   }
   __syncthreads();
   float l = 0.f;
+#pragma unroll 12
   for (int s = 0; s < splits; ++s) l = fmaf(pl[(size_t)s * bpad + r], sc[s * 32 + rx], l);
   const float invB = 1.0f / (float)B, invl = 1.0f / l;
   __shared__ float cs[16][33];                // dA of this CTA's rows x columns (db1 partial)
   for (int j = blockIdx.y * 16 + jy; j < h && j < blockIdx.y * 16 + 16; j += 8) {
     float o = 0.f;
+#pragma unroll 12
     for (int s = 0; s < splits; ++s) o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc[s * 32 + rx], o);
     const float dh = (o * invl - labW[(size_t)r * h + j]) * invB;
     const float da = live && Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
