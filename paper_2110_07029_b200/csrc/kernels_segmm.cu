@@ -263,19 +263,28 @@ __device__ __forceinline__ void sb_copy(void *dst, const void *src, uint32_t byt
                ::"r"(sm32(dst)), "l"((uint64_t)src), "r"(bytes), "r"(sm32(bar)) : "memory");
 }
 
-#ifndef AS_SEG1_NW                                   // experiment overrides (MODE 1)
-#define AS_SEG1_NW 6
+// warps per CTA, ring stages per warp, entries per group: measured on B200 at
+// the Amazon-670K shape (scripts/x_probe.sh sweep); h = 256 keeps the
+// 227 KB shared-memory budget.  -D overrides for experiment builds.
+#ifndef AS_SEG1_NW
+#define AS_SEG1_NW (H == 128 ? 16 : 6)
 #define AS_SEG1_NST 2
-#define AS_SEG1_GE (2048 / H)
+#define AS_SEG1_GE (H == 128 ? 6 : 8)
+#endif
+#ifndef AS_SEG0_NW
+#define AS_SEG0_NW (H == 128 ? 16 : 8)
+#define AS_SEG0_NST 3
+#define AS_SEG0_GE 8
 #endif
 template <int H, int MODE>
 struct SegCfg {
-  static constexpr int GE = MODE == 0 ? 2048 / H : AS_SEG1_GE;   // entries per group
-  static constexpr int NW = MODE == 0 ? 8 : AS_SEG1_NW;          // warps per CTA
-  static constexpr int NST = MODE == 0 ? 3 : AS_SEG1_NST;        // ring stages per warp
+  static constexpr int GE = MODE == 0 ? AS_SEG0_GE : AS_SEG1_GE;     // entries per group
+  static constexpr int NW = MODE == 0 ? AS_SEG0_NW : AS_SEG1_NW;     // warps per CTA
+  static constexpr int NST = MODE == 0 ? AS_SEG0_NST : AS_SEG1_NST;  // ring stages per warp
   static constexpr int ROW = H * 4;                   // bytes per gathered row
   static constexpr int STAGE = GE * ROW * (MODE == 1 ? 2 : 1);   // + prefetched W1 rows (MODE 1)
   static constexpr int SMEM = NW * NST * STAGE + NW * 2 * ROW + NW * NST * 8;
+  static_assert(SMEM <= 232448, "segmented gather-reduce shared memory exceeds 227 KB");
 };
 
 // balanced contiguous split of [0, n) into g parts: part c = [c n / g, (c+1) n / g)
