@@ -423,12 +423,17 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     const uint32_t tlq = tmem + ((uint32_t)(q * 32) << 16);
     const uint32_t tO = tlq + 2 * BM + g * BM;
     float m_used = -FLT_MAX, l = 0.f;
-    float b2n = 0.f;                          // prefetched b2 of this WG's next class block
-    if (g < nloc) { const int c = (cb0 + g) * BM + row; b2n = c < C ? b2[c] * LOG2E : -INFINITY; }
+    // prefetched b2 of this WG's next class block: an unconditional load from
+    // a clamped address whose register is first touched one block later (a
+    // select / multiply right after the load would stall on its latency)
+    float b2raw = 0.f;
+    bool b2ok = false;
+    if (g < nloc) { const int c = (cb0 + g) * BM + row; b2ok = c < C; b2raw = b2[b2ok ? c : 0]; }
     int jj = 0;                               // blocks processed by this WG
     for (int j = g; j < nloc; j += NWG, ++jj) {
       const int b = j & 1;
       float *myB2 = sB2 + (g * 2 + (jj & 1)) * BM;
+      const float b2n = b2ok ? b2raw * LOG2E : -INFINITY;
       myB2[row] = b2n;
       float wm = b2n;                         // max of b2 (log2 units) over the block
 #pragma unroll
@@ -436,7 +441,8 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       if (lane == 0) sBmax[(g * 2 + (jj & 1)) * 4 + q] = wm;
       if (j + NWG < nloc) {
         const int c = (cb0 + j + NWG) * BM + row;
-        b2n = c < C ? b2[c] * LOG2E : -INFINITY;
+        b2ok = c < C;
+        b2raw = b2[b2ok ? c : 0];
       }
       named_bar(1 + g, 128);
       const float *bmx = sBmax + (g * 2 + (jj & 1)) * 4;
@@ -760,12 +766,18 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     // per-class state of the next block (b2 and the class's label range with
     // its first label, one 16-byte load from the transposes' cls_lab),
     // prefetched one block ahead: a block change has no dependent loads
-    struct ClsState { float b2c; int4 cl; };
+    // The loads are unconditional (clamped address) and their registers are
+    // not touched until the block change that consumes them: a select or
+    // multiply on a pending load here would stall the warp on HBM latency.
+    struct ClsState { float b2raw; int4 cl; bool ok; };
     auto cls_state = [&](int kb_) -> ClsState {
-      ClsState st{-INFINITY, make_int4(0, 0, 0x7fffffff, 0)};
+      ClsState st;
       const int c = (blockIdx.x + kb_ * gridDim.x) * BM + i;
-      if (kb_ < NB && c < C) { st.b2c = b2[c] * LOG2E; st.cl = cls_lab[c]; }
-      return st;                              // invalid class: b2 = -inf -> p = 0
+      st.ok = kb_ < NB && c < C;
+      const int cc = st.ok ? c : 0;
+      st.b2raw = b2[cc];
+      st.cl = cls_lab[cc];
+      return st;                              // invalid class: b2 = -inf -> p = 0 (at use)
     };
     ClsState nxt = cls_state(0);
     int kb_cur = -1, lc = 0, le = 0, lnr = 0x7fffffff;
@@ -775,8 +787,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     for (int gu = g; gu < NT; gu += 2) {
       if (kb != kb_cur) {                     // new class block: per-class state
         kb_cur = kb;
-        b2c = nxt.b2c;
-        lc = nxt.cl.x; le = nxt.cl.y; lnr = nxt.cl.z; lnw = __int_as_float(nxt.cl.w);
+        b2c = nxt.ok ? nxt.b2raw * LOG2E : -INFINITY;
+        lc = nxt.ok ? nxt.cl.x : 0; le = nxt.ok ? nxt.cl.y : 0;
+        lnr = nxt.ok ? nxt.cl.z : 0x7fffffff; lnw = nxt.ok ? __int_as_float(nxt.cl.w) : 0.f;
         db2 = 0.f;
         nxt = cls_state(kb + 1);
       }
@@ -854,8 +867,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #ifndef AS_X_EARLYP
       if (lane == 0) mbar_arrive(&p_full[b]);
 #endif
+      TRACE(1, threadIdx.x == 0, 9, v);
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
         if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
+        TRACE(1, threadIdx.x == 0, 16, v);
         sDB[g * BM + i] = db2;
         if (NU == 1) sDB[(1 - g) * BM + i] = 0.f;   // one unit per block: the other WG has none
         __syncwarp();
