@@ -74,6 +74,7 @@ struct as_ctx {
   float *dA, *lse2, *lsep, *zsum, *labW, *lossr, *loss;
   float *pm, *pl, *pO;
   float *db1p;                // db1 partials of the fused combine
+  float *wrow;                // per-row label weight 1/(k_r B) for pass 2
   int *db1cnt;
   int32_t *top1;              // top-1 evaluation (NEXT f1)
   unsigned long long *hits;
@@ -209,6 +210,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.max_splits * D.bpad); if (x) x->pl = (float *)p;
   p = P(4 * (size_t)D.bpad); if (x) x->top1 = (int32_t *)p;
   p = P(4 * (size_t)(D.bpad / 32 + 1) * D.h); if (x) x->db1p = (float *)p;
+  p = P(4 * (size_t)D.bpad); if (x) x->wrow = (float *)p;
   p = P(4 * (size_t)D.h); if (x) x->db1cnt = (int *)p;
   p = P(8); if (x) x->hits = (unsigned long long *)p;
   if (bf16) {
@@ -657,14 +659,14 @@ int as_train_step(as_ctx *x, float *loss_out) {
     // loss, dA, and db1 with b1's SGD fused (ordered last-arriver column sums)
     as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
-                            x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lse2, x->lsep, x->lossr,
-                            x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr);
+                            x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lab_ptr, x->lse2, x->lsep, x->wrow,
+                            x->lossr, x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr);
     ph_end(x, AS_PH_COMBINE);
     cudaStreamWaitEvent(s, x->ev_join, 0);   // label transpose ready
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
     ph_begin(x, AS_PH_OUT_BWD);
     x->launches += 1;
-    as::launch_out_bwd_tc(s, x->plan, d, x->lsep, x->cls_lab, x->lseg_ptr, x->lseg_row, x->lw,
+    as::launch_out_bwd_tc(s, x->plan, d, x->lsep, x->cls_lab, x->lbits, D.bw, x->wrow,
                           W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
                           dbg ? x->dbg_db2 : nullptr);
     ph_end(x, AS_PH_OUT_BWD);

@@ -105,9 +105,9 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // combine of the bf16 pass-1 partials -> LSE, loss rows, dA (steps a5)
 void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max, int bpad,
                          int splits, const float *pm, const float *pl, const float *pO,
-                         const float *labW, const float *zsum, const float *Hf, float *lse2, float *lsep,
-                         float *lossr, float *dA, float *db1p, int *db1cnt, float *b1, float lr,
-                         float *dbg_db1);
+                         const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
+                         float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
+                         int *db1cnt, float *b1, float lr, float *dbg_db1);
 // fp32 (SIMT) output layer (steps a5/a6 in parity mode)
 void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
                      long long sak, const float *B, long long sbk, long long sbn, float *Cm,
@@ -169,9 +169,9 @@ void launch_gemm_f32_kdev(cudaStream_t s, int M, int N, int K, const float *A, l
                           long long sak, const float *B, long long sbk, long long sbn, float *Cm,
                           long long ldc, const int *K_dev);
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
-                       const float *lsep, const int4 *cls_lab, const int32_t *lseg_ptr,
-                       const int32_t *lrow, const float *lw, float *W2T, float *b2,
-                       __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2);
+                       const float *lsep, const int4 *cls_lab, const uint32_t *lbits, int lbw,
+                       const float *wrow, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
+                       float *dbg_dW2T, float *dbg_db2);
 // per label entry of the label-sorted batch: lw[u] = 1 / (k_r B), r = lrow[u]  (R3)
 void launch_label_weights(cudaStream_t s, const StepDesc *desc, int cap, const int32_t *lrow,
                           const int64_t *lab_ptr, float *lw);

@@ -554,20 +554,21 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 __global__ void __launch_bounds__(256) k_combine_bf16(
     const StepDesc *__restrict__ desc, int h, int bpad, int splits, const float *__restrict__ pm,
     const float *__restrict__ pl, const float *__restrict__ pO, const float *__restrict__ labW,
-    const float *__restrict__ zsum, const float *__restrict__ Hf, float *__restrict__ lse2,
-    float *__restrict__ lsep, float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
+    const float *__restrict__ zsum, const float *__restrict__ Hf, const int64_t *__restrict__ lab_ptr,
+    float *__restrict__ lse2, float *__restrict__ lsep, float *__restrict__ wrow,
+    float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
     int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1) {
   // CTA = 32 rows x 16 columns (8 groups of 2); partial reads coalesced over rows
   const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
   const int B = desc->rows;
   if (blockIdx.x * 32 >= B) {         // a CTA of padding rows only
     const int r = blockIdx.x * 32 + rx;
-    if (jy == 0 && r < bpad && blockIdx.y == 0) lsep[r] = INFINITY;
+    if (jy == 0 && r < bpad && blockIdx.y == 0) { lsep[r] = INFINITY; wrow[r] = 0.f; }
     return;
   }
   const bool live = blockIdx.x * 32 + rx < B;
   const int r = live ? blockIdx.x * 32 + rx : B - 1;   // padding lanes shadow a live row
-  if (!live && jy == 0 && blockIdx.y == 0) lsep[blockIdx.x * 32 + rx] = INFINITY;
+  if (!live && jy == 0 && blockIdx.y == 0) { lsep[blockIdx.x * 32 + rx] = INFINITY; wrow[blockIdx.x * 32 + rx] = 0.f; }
   extern __shared__ float sc[];             // [splits][32] per-slot scales of the rows
   // every slot loop is unrolled 12-wide so a thread keeps 12 partial loads in
   // flight (the partials are L2-resident right after pass 1)
@@ -621,17 +622,21 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     const float L2 = M + log2f(l);
     lse2[r] = L2;
     lsep[r] = L2 + log2f((float)B);   // pass 2: p / B = 2^(s log2e - lsep)
+    // pass 2's label weight of the row, 1 / (k_r B) (R3), same fp32 operations
+    // as the label transpose's per-entry weights
+    wrow[r] = (1.0f / (float)B) / (float)(lab_ptr[r + 1] - lab_ptr[r]);
     lossr[r] = L2 * 0.69314718055994531f - zsum[r];
   }
 }
 
 void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max, int bpad,
                          int splits, const float *pm, const float *pl, const float *pO,
-                         const float *labW, const float *zsum, const float *Hf, float *lse2, float *lsep,
-                         float *lossr, float *dA, float *db1p, int *db1cnt, float *b1, float lr,
-                         float *dbg_db1) {
+                         const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
+                         float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
+                         int *db1cnt, float *b1, float lr, float *dbg_db1) {
   k_combine_bf16<<<dim3(ceil_div(bpad, 32), h / 16), 256, (size_t)splits * 32 * 4, s>>>(
-      desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lse2, lsep, lossr, dA, db1p, db1cnt, b1, lr, dbg_db1);
+      desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lab_ptr, lse2, lsep, wrow, lossr, dA, db1p, db1cnt, b1,
+      lr, dbg_db1);
 }
 
 // =====================================================================

@@ -583,8 +583,8 @@ struct BwdCfg {
   static constexpr bool TMAUPD = H == 128;
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
   static constexpr int TSTAGE = TMAUPD ? BM * H * 4 : BM * SROW * 4;
-  static constexpr int SMEM = NSH * TILE + TSTAGE + NSH * BM * 4 /*lse' ring*/ + 2 * BM * 4 /*db2*/ +
-                              512 /*barriers*/;
+  static constexpr int SMEM = NSH * TILE + TSTAGE + 2 * NSH * BM * 4 /*lse' and label-weight rings*/ +
+                              2 * BM * 4 /*db2*/ + 512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
   static_assert(NSB * UNIT + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
 };
@@ -613,8 +613,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
               const __grid_constant__ CUtensorMap mapWf, const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
               int n_cblocks, const int4 *__restrict__ cls_lab,
-              const int32_t *__restrict__ lseg_ptr, const int32_t *__restrict__ lrow,
-              const float *__restrict__ lw, float *__restrict__ W2T, float *__restrict__ b2,
+              const uint32_t *__restrict__ lbits, int lbw, const float *__restrict__ wrow,
+              float *__restrict__ W2T, float *__restrict__ b2,
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
               float *__restrict__ dbg_db2) {
   using Cfg = BwdCfg<H>;
@@ -627,7 +627,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   uint8_t *sHt = smem_raw;
   float *sT = (float *)(sHt + NSH * TILE);      // h = 128: W2T fp32 block; else dW2T staging
   float *sL = (float *)((uint8_t *)sT + Cfg::TSTAGE);    // lse' of the rows of each H stage
-  float *sDB = sL + NSH * BM;                   // [2][128] db2 partials of the two WGs
+  float *sWr = sL + NSH * BM;                   // label weight 1/(k_r B) of those rows (R3)
+  float *sDB = sWr + NSH * BM;                  // [2][128] db2 partials of the two WGs
   uint64_t *bars = (uint64_t *)(sDB + 2 * BM);
   uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + NSB,
            *wt_full = p_full + NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
@@ -679,10 +680,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #ifdef AS_X_NOTMA
           if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
 #endif
-          mbar_expect_tx(&h_full[st], TILE + BM * 4);
+          mbar_expect_tx(&h_full[st], TILE + 2 * BM * 4);
           for (int a = 0; a < H / 64; ++a)
             tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
           bulk_load_1d(sL + st * BM, lsep + t * BM, BM * 4, &h_full[st]);
+          bulk_load_1d(sWr + st * BM, wrow + t * BM, BM * 4, &h_full[st]);
         }
     }
   } else if (warp == kMmaWarp) {
@@ -779,21 +781,48 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       st.cl = cls_lab[cc];
       return st;                              // invalid class: b2 = -inf -> p = 0 (at use)
     };
-    ClsState nxt = cls_state(0);
-    int kb_cur = -1, lc = 0, le = 0, lnr = 0x7fffffff;
-    float lnw = 0.f, b2c = 0.f, db2 = 0.f;
+    // NU = 1 (B <= UNIT): block kb's single unit belongs to WG kb % 2, so a WG
+    // walks every other block
+    const int kstep = NU == 1 ? 2 : 1;
+    ClsState nxt = cls_state(NU == 1 ? g : 0);
+    int kb_cur = -1;
+    bool has_lab = false;                     // class i has labels in this batch
+    float b2c = 0.f, db2 = 0.f;
+    // rows of a unit labelled with class i: the class's row bitmap from the
+    // label transpose (k_tr_mark; bit r = row r has label i)
+    auto load_mask = [&](int kb_, int v_, bool has, uint32_t (&m)[UNIT / 32]) {
+#pragma unroll
+      for (int w = 0; w < UNIT / 32; ++w) m[w] = 0u;
+      if (has) {
+        const uint32_t *bits = lbits + (size_t)((blockIdx.x + kb_ * gridDim.x) * BM + i) * lbw + v_ * (UNIT / 32);
+#pragma unroll
+        for (int w = 0; w < UNIT / 32; ++w) m[w] = bits[w];
+      }
+    };
     int kb = 0, v = g, lst = g / HPT, sb = g; // unit cursor: block, unit, lse' stage, S buffer
+    while (NU > 0 && v >= NU) { v -= NU; ++kb; }   // NU = 1: WG 1 starts in block 1
+    uint32_t mk[UNIT / 32], mkn[UNIT / 32];
+    load_mask(kb, v, kb < NB && nxt.ok && nxt.cl.x < nxt.cl.y, mk);
     uint32_t sph = 0u;
     for (int gu = g; gu < NT; gu += 2) {
       if (kb != kb_cur) {                     // new class block: per-class state
         kb_cur = kb;
         b2c = nxt.ok ? nxt.b2raw * LOG2E : -INFINITY;
-        lc = nxt.ok ? nxt.cl.x : 0; le = nxt.ok ? nxt.cl.y : 0;
-        lnr = nxt.ok ? nxt.cl.z : 0x7fffffff; lnw = nxt.ok ? __int_as_float(nxt.cl.w) : 0.f;
+        has_lab = nxt.ok && nxt.cl.x < nxt.cl.y;
         db2 = 0.f;
-        nxt = cls_state(kb + 1);
+        nxt = cls_state(kb + kstep);
       }
       const int b = sb;
+      // the next unit of this WG: its class's row bitmap is prefetched now and
+      // consumed one unit later (the HBM latency hides behind this unit)
+      {
+        int vn = v + 2, kbn = kb;
+        while (vn >= NU) { vn -= NU; ++kbn; }
+        // crossing a block: nxt was loaded at this block's change, >= 1 unit ago
+        // except for NU <= 2 (tiny batches), where the wait is harmless
+        const bool hn = kbn == kb ? has_lab : (kbn < NB && nxt.ok && nxt.cl.x < nxt.cl.y);
+        load_mask(kbn, vn, hn, mkn);
+      }
       TRACE(1, threadIdx.x == 0, 6, v);
       mbar_wait(&s_full[b], sph);
       TRACE(1, threadIdx.x == 0, 7, v);
@@ -832,17 +861,24 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             }
           }
         }
-        const int base = UNIT * v + 64 * half;
-        while (lnr < base + 64) {             // rare: labels of this class in these rows
-          if (lnr >= base) {
-            const int kk = lnr - base;
+        // label term of the uniform multi-label target folded into G (R3, R24):
+        // G_rc = p_rc / B - [c in Y_r] / (k_r B), the weights per row from the
+        // stage's label-weight ring; only warps with a label in these 64 rows
+        {
+          const uint32_t m0 = mk[(2 * half) % (UNIT / 32)], m1 = mk[(2 * half + 1) % (UNIT / 32)];
+          if (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
+            const float4 *wq = reinterpret_cast<const float4 *>(sWr + lst * BM + (v % HPT) * UNIT + half * 64);
 #pragma unroll
-            for (int k = 0; k < 64; ++k)
-              if (k == kk) vv[k] -= lnw;
+            for (int k4 = 0; k4 < 16; ++k4) {
+              const float4 w4 = wq[k4];
+              const uint32_t mw = k4 < 8 ? m0 : m1;
+              const int sh = (4 * k4) & 31;
+              if (mw & (1u << sh)) vv[4 * k4] -= w4.x;
+              if (mw & (2u << sh)) vv[4 * k4 + 1] -= w4.y;
+              if (mw & (4u << sh)) vv[4 * k4 + 2] -= w4.z;
+              if (mw & (8u << sh)) vv[4 * k4 + 3] -= w4.w;
+            }
           }
-          ++lc;
-          lnr = lc < le ? lrow[lc] : 0x7fffffff;
-          lnw = lc < le ? lw[lc] : 0.f;
         }
         uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
         uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
@@ -880,11 +916,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         }
       }
       v += 2;                                 // next unit of this WG
-      if (v >= NU) { v -= NU; ++kb; }
+      while (v >= NU) { v -= NU; ++kb; }
       lst += 2 / HPT;                         // its H stage
       if (lst >= NSH) lst -= NSH;
       sb += 2;
       if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
+#pragma unroll
+      for (int w = 0; w < UNIT / 32; ++w) mk[w] = mkn[w];
     }
   } else if (warp < 12) {  // ---------------- update warps
     const int q = warp & 3;
@@ -1608,17 +1646,16 @@ int tc_fwd_splits_host(const TcPlan *p, int B) {
 }
 
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lsep,
-                       const int4 *cls_lab, const int32_t *lseg_ptr, const int32_t *lrow,
-                       const float *lw, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
-                       float *dbg_dW2T, float *dbg_db2) {
+                       const int4 *cls_lab, const uint32_t *lbits, int lbw, const float *wrow, float *W2T,
+                       float *b2, __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2) {
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
   else
     tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lseg_ptr, lrow, lw, W2T,
+        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
 }
 

@@ -100,6 +100,7 @@ CASES = [
     (2000, 1000, 128, 600, 200, 256),    # ragged: 2 row tiles (72 rows in the 2nd), C % 128 = 104
     (3000, 700, 256, 400, 130, 192),     # h = 256
     (500, 50, 128, 64, 1, 64),           # a single row, C < 128
+    (2000, 900, 128, 300, 100, 128),     # one row tile (pass-2 WGs walk alternate class blocks), 8 blocks
     (1500, 2048, 128, 700, 512, 512),    # exact tiles
     (4000, 30000, 128, 1200, 1024, 1024),  # multi-block pipelines: 13 class blocks per pass-1 CTA
     (3000, 20000, 256, 800, 512, 512),   # h = 256, W ring wraps (2 stages)
