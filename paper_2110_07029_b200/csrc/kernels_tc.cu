@@ -840,57 +840,66 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #ifdef AS_X_EARLYP
         if (half == UNIT / 64 - 1) { fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&p_full[b]); }
 #endif
-        float vv[64];
+        uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
+        uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
         const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
 #pragma unroll
         for (int k4 = 0; k4 < 16; ++k4) {
           const float4 l4 = lq[k4];
 #pragma unroll
           for (int m = 0; m < 2; ++m) {       // packed: x = s log2e + b2 - lse'
-            const int k = 4 * k4 + 2 * m;
+            const int k = 4 * k4 + 2 * m, u = 2 * k4 + m;
             const uint32_t xa = k < 32 ? r0[k] : r1[k - 32], xb = k < 32 ? r0[k + 1] : r1[k - 31];
             uint64_t x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
             x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
-            if ((2 * k4 + m) % AS_EMU_MOD == AS_EMU_MOD - 1) {
-              ex2_emu2(x, vv[k], vv[k + 1]);
+            float e0, e1;
+            if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
+              ex2_emu2(x, e0, e1);
             } else {
               float x0, x1;
               f2split(x, x0, x1);
-              vv[k] = XEX2(x0);
-              vv[k + 1] = XEX2(x1);
+              e0 = XEX2(x0);
+              e1 = XEX2(x1);
             }
+            // p / B straight into the db2 sums and the packed bf16 G^T: no
+            // 64-value array stays live (register pressure)
+            dacc[u & 3] = fadd2(dacc[u & 3], f2(e0, e1));
+            pk[u] = pack_bf16x2(e0, e1);
           }
-        }
-        // label term of the uniform multi-label target folded into G (R3, R24):
-        // G_rc = p_rc / B - [c in Y_r] / (k_r B), the weights per row from the
-        // stage's label-weight ring; only warps with a label in these 64 rows
-        {
-          const uint32_t m0 = mk[(2 * half) % (UNIT / 32)], m1 = mk[(2 * half + 1) % (UNIT / 32)];
-          if (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
-            const float4 *wq = reinterpret_cast<const float4 *>(sWr + lst * BM + (v % HPT) * UNIT + half * 64);
-#pragma unroll
-            for (int k4 = 0; k4 < 16; ++k4) {
-              const float4 w4 = wq[k4];
-              const uint32_t mw = k4 < 8 ? m0 : m1;
-              const int sh = (4 * k4) & 31;
-              if (mw & (1u << sh)) vv[4 * k4] -= w4.x;
-              if (mw & (2u << sh)) vv[4 * k4 + 1] -= w4.y;
-              if (mw & (4u << sh)) vv[4 * k4 + 2] -= w4.z;
-              if (mw & (8u << sh)) vv[4 * k4 + 3] -= w4.w;
-            }
-          }
-        }
-        uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
-        uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          dacc[u & 3] = fadd2(dacc[u & 3], f2(vv[2 * u], vv[2 * u + 1]));
-          pk[u] = pack_bf16x2(vv[2 * u], vv[2 * u + 1]);
         }
         {
           float d0, d1;
           f2split(fadd2(fadd2(dacc[0], dacc[1]), fadd2(dacc[2], dacc[3])), d0, d1);
           db2 += d0 + d1;
+        }
+        // label term of the uniform multi-label target folded into G (R3, R24):
+        // G_rc = bf16(p_rc / B) - [c in Y_r] / (k_r B) (rounded to bf16 again),
+        // db2 -= the same weights; row weights from the stage's label-weight
+        // ring; only warps with a label of one of their classes in these rows
+        {
+          // static register indices (half is a runtime loop counter)
+          uint32_t m0 = mk[0], m1 = mk[1];
+          if constexpr (UNIT == 128) {
+            if (half) { m0 = mk[UNIT / 32 > 2 ? 2 : 0]; m1 = mk[UNIT / 32 > 3 ? 3 : 1]; }
+          }
+#ifdef AS_X_NOLAB
+          if (false)
+#endif
+          if (__any_sync(0xffffffffu, (m0 | m1) != 0u)) {
+            const float4 *wq = reinterpret_cast<const float4 *>(sWr + lst * BM + (v % HPT) * UNIT + half * 64);
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+              const uint32_t mw = u < 16 ? m0 : m1;
+              const uint32_t bits = (mw >> ((2 * u) & 31)) & 3u;
+              if (bits) {
+                const float2 w2 = reinterpret_cast<const float2 *>(wq)[u];
+                float lo = __uint_as_float(pk[u] << 16), hi = __uint_as_float(pk[u] & 0xffff0000u);
+                if (bits & 1u) { lo -= w2.x; db2 -= w2.x; }
+                if (bits & 2u) { hi -= w2.y; db2 -= w2.y; }
+                pk[u] = pack_bf16x2(lo, hi);
+              }
+            }
+          }
         }
         // G^T over S^T columns already consumed (cols [32 half, 32 half + 32))
         AS_TMEM_ST32(tl + b * UNIT + half * 32, pk);
