@@ -110,6 +110,22 @@ __device__ __forceinline__ void fence_after() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// cp.async (LDGSTS) global -> shared, zero-filled beyond src_bytes
+__device__ __forceinline__ void cp_async_16(void *sdst, const void *gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void *sdst, const void *gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void *sdst, const void *gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -584,7 +600,8 @@ struct BwdCfg {
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
   static constexpr int TSTAGE = TMAUPD ? BM * H * 4 : BM * SROW * 4;
   static constexpr int SMEM = NSH * TILE + TSTAGE + 2 * NSH * BM * 4 /*lse' and label-weight rings*/ +
-                              2 * BM * 4 /*db2*/ + 512 /*barriers*/;
+                              2 * BM * 4 /*db2*/ + 2 * 256 * (16 + 16 + 4) /*softmax prefetch slots*/ +
+                              512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
   static_assert(NSB * UNIT + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
 };
@@ -629,7 +646,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   float *sL = (float *)((uint8_t *)sT + Cfg::TSTAGE);    // lse' of the rows of each H stage
   float *sWr = sL + NSH * BM;                   // label weight 1/(k_r B) of those rows (R3)
   float *sDB = sWr + NSH * BM;                  // [2][128] db2 partials of the two WGs
-  uint64_t *bars = (uint64_t *)(sDB + 2 * BM);
+  uint4 *sMk = (uint4 *)(sDB + 2 * BM);          // [2][256] label-row bitmaps (softmax prefetch)
+  int4 *sCl = (int4 *)(sMk + 2 * 256);           // [2][256] cls_lab of the next block
+  float *sB2r = (float *)(sCl + 2 * 256);        // [2][256] b2 of the next block
+  uint64_t *bars = (uint64_t *)(sB2r + 2 * 256);
   uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + NSB,
            *wt_full = p_full + NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
            *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1;
@@ -765,68 +785,85 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     const int i = q * 32 + lane;              // class inside the block (TMEM lane)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     TRACE_INIT;
-    // per-class state of the next block (b2 and the class's label range with
-    // its first label, one 16-byte load from the transposes' cls_lab),
-    // prefetched one block ahead: a block change has no dependent loads
-    // The loads are unconditional (clamped address) and their registers are
-    // not touched until the block change that consumes them: a select or
-    // multiply on a pending load here would stall the warp on HBM latency.
-    struct ClsState { float b2raw; int4 cl; bool ok; };
-    auto cls_state = [&](int kb_) -> ClsState {
-      ClsState st;
-      const int c = (blockIdx.x + kb_ * gridDim.x) * BM + i;
-      st.ok = kb_ < NB && c < C;
-      const int cc = st.ok ? c : 0;
-      st.b2raw = b2[cc];
-      st.cl = cls_lab[cc];
-      return st;                              // invalid class: b2 = -inf -> p = 0 (at use)
+    // Prefetches go global -> shared with cp.async (zero-filled when the class
+    // is out of range or has no label), two slots each, so no register ever
+    // holds a pending load (a move or select of one stalls the warp on HBM):
+    //   * per-class state of a class block (b2, and cls_lab from the label
+    //     transpose) one block ahead, slot = block parity;
+    //   * the class's label-row bitmap of a unit (k_tr_mark; bit r = row r
+    //     has label i) one unit ahead, slot = WG unit parity.
+    const int tix = threadIdx.x;              // 0..255
+    auto cls_ok = [&](int kb_) {
+      return kb_ < NB && (blockIdx.x + kb_ * gridDim.x) * BM + i < C;
+    };
+    auto pf_cls = [&](int kb_) {
+      const bool ok = cls_ok(kb_);
+      const int cc = ok ? (blockIdx.x + kb_ * gridDim.x) * BM + i : 0;
+      const int sl = (kb_ & 1) * 256 + tix;
+      cp_async_16(sCl + sl, cls_lab + cc, ok ? 16u : 0u);
+      cp_async_4(sB2r + sl, b2 + cc, ok ? 4u : 0u);
+    };
+    auto pf_mask = [&](int kb_, int v_, bool has, int slot) {
+      const uint32_t *bits = has ? lbits + (size_t)((blockIdx.x + kb_ * gridDim.x) * BM + i) * lbw + v_ * (UNIT / 32)
+                                 : lbits;
+      if constexpr (UNIT == 128) cp_async_16(sMk + slot * 256 + tix, bits, has ? 16u : 0u);
+      else cp_async_8(sMk + slot * 256 + tix, bits, has ? 8u : 0u);
+    };
+    auto cls_has = [&](int kb_) {             // the block's state must have landed
+      const int4 cl = sCl[(kb_ & 1) * 256 + tix];
+      return cls_ok(kb_) && cl.x < cl.y;
     };
     // NU = 1 (B <= UNIT): block kb's single unit belongs to WG kb % 2, so a WG
     // walks every other block
     const int kstep = NU == 1 ? 2 : 1;
-    ClsState nxt = cls_state(NU == 1 ? g : 0);
     int kb_cur = -1;
     bool has_lab = false;                     // class i has labels in this batch
     float b2c = 0.f, db2 = 0.f;
-    // rows of a unit labelled with class i: the class's row bitmap from the
-    // label transpose (k_tr_mark; bit r = row r has label i)
-    auto load_mask = [&](int kb_, int v_, bool has, uint32_t (&m)[UNIT / 32]) {
-#pragma unroll
-      for (int w = 0; w < UNIT / 32; ++w) m[w] = 0u;
-      if (has) {
-        const uint32_t *bits = lbits + (size_t)((blockIdx.x + kb_ * gridDim.x) * BM + i) * lbw + v_ * (UNIT / 32);
-#pragma unroll
-        for (int w = 0; w < UNIT / 32; ++w) m[w] = bits[w];
-      }
-    };
     int kb = 0, v = g, lst = g / HPT, sb = g; // unit cursor: block, unit, lse' stage, S buffer
     while (NU > 0 && v >= NU) { v -= NU; ++kb; }   // NU = 1: WG 1 starts in block 1
-    uint32_t mk[UNIT / 32], mkn[UNIT / 32];
-    load_mask(kb, v, kb < NB && nxt.ok && nxt.cl.x < nxt.cl.y, mk);
+    pf_cls(kb);
+    cp_async_commit();
+    cp_async_wait<0>();
+    pf_mask(kb, v, cls_has(kb), 0);
+    cp_async_commit();
+    int jj = 0;                               // units of this WG so far
     uint32_t sph = 0u;
-    for (int gu = g; gu < NT; gu += 2) {
+    for (int gu = g; gu < NT; gu += 2, ++jj) {
       if (kb != kb_cur) {                     // new class block: per-class state
         kb_cur = kb;
-        b2c = nxt.ok ? nxt.b2raw * LOG2E : -INFINITY;
-        has_lab = nxt.ok && nxt.cl.x < nxt.cl.y;
+        const bool ok = cls_ok(kb);
+        b2c = ok ? sB2r[(kb & 1) * 256 + tix] * LOG2E : -INFINITY;
+        has_lab = cls_has(kb);
         db2 = 0.f;
-        nxt = cls_state(kb + kstep);
+        pf_cls(kb + kstep);                   // slot (kb + kstep) & 1: read above already
+        cp_async_commit();
       }
       const int b = sb;
-      // the next unit of this WG: its class's row bitmap is prefetched now and
-      // consumed one unit later (the HBM latency hides behind this unit)
+      // the next unit of this WG: its class's row bitmap one unit ahead
       {
         int vn = v + 2, kbn = kb;
         while (vn >= NU) { vn -= NU; ++kbn; }
-        // crossing a block: nxt was loaded at this block's change, >= 1 unit ago
-        // except for NU <= 2 (tiny batches), where the wait is harmless
-        const bool hn = kbn == kb ? has_lab : (kbn < NB && nxt.ok && nxt.cl.x < nxt.cl.y);
-        load_mask(kbn, vn, hn, mkn);
+        bool hn = has_lab;
+        if (kbn != kb) {                      // crossing a block: its state, prefetched at this block's change
+          cp_async_wait<0>();
+          hn = cls_has(kbn);
+        }
+        pf_mask(kbn, vn, hn, (jj + 1) & 1);
+        cp_async_commit();
       }
       TRACE(1, threadIdx.x == 0, 6, v);
       mbar_wait(&s_full[b], sph);
       TRACE(1, threadIdx.x == 0, 7, v);
       fence_after();
+      cp_async_wait<1>();                     // this unit's bitmap (all but the newest group)
+      uint32_t mk[4];
+      if constexpr (UNIT == 128) {
+        const uint4 q4 = sMk[(jj & 1) * 256 + tix];
+        mk[0] = q4.x; mk[1] = q4.y; mk[2] = q4.z; mk[3] = q4.w;
+      } else {
+        const uint2 q2 = *reinterpret_cast<const uint2 *>(sMk + (jj & 1) * 256 + tix);
+        mk[0] = q2.x; mk[1] = q2.y; mk[2] = 0u; mk[3] = 0u;
+      }
 #ifndef AS_X_NOSOFT
 #pragma unroll 1
       for (int half = 0; half < UNIT / 64; ++half) {   // 64 rows of the unit at a time
@@ -879,9 +916,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         {
           // static register indices (half is a runtime loop counter)
           uint32_t m0 = mk[0], m1 = mk[1];
-          if constexpr (UNIT == 128) {
-            if (half) { m0 = mk[UNIT / 32 > 2 ? 2 : 0]; m1 = mk[UNIT / 32 > 3 ? 3 : 1]; }
-          }
+          if (half) { m0 = mk[2]; m1 = mk[3]; }
 #ifdef AS_X_NOLAB
           if (false)
 #endif
@@ -930,8 +965,6 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if (lst >= NSH) lst -= NSH;
       sb += 2;
       if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
-#pragma unroll
-      for (int w = 0; w < UNIT / 32; ++w) mk[w] = mkn[w];
     }
   } else if (warp < 12) {  // ---------------- update warps
     const int q = warp & 3;
