@@ -585,9 +585,15 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 template <int H>
 struct BwdCfg {
   static constexpr int NSH = H == 128 ? 4 : 2;    // H tile stages (128 rows each)
+#ifdef AS_X_U64
+  static constexpr int UNIT = 64;                 // experiment: 64-row units, 4 S^T buffers
+  static constexpr int HPT = 128 / UNIT;
+  static constexpr int NSB = H == 128 ? 4 : 2;
+#else
   static constexpr int UNIT = H == 128 ? 128 : 64; // batch rows per unit = S^T columns per buffer
   static constexpr int HPT = 128 / UNIT;          // units per 128-row H tile
   static constexpr int NSB = 2;                   // S^T unit buffers
+#endif
   static constexpr int NWT = H == 128 ? 2 : 1;    // W2T blocks resident in TMEM (A operand)
   static constexpr int WCOLS = H / 2;             // TMEM columns of one W2T block (bf16 pairs)
   static constexpr int TILE = BM * H * 2;
