@@ -517,7 +517,7 @@ int as_eval_top1(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t 
   int slots = 1;
   if (x->cfg.precision == AS_BF16) {
     as::launch_out_top1_tc(s, x->plan, d, b2, x->pm, (int *)x->pl);
-    slots = as::tc_fwd_splits_host(x->plan, rows);
+    slots = 2 * as::tc_fwd_splits_host(x->plan, rows);   // k_out_top1: one slot per (split, WG)
   } else {
     x->launches += 1;
     as::launch_gemm_f32(s, D.b_max, (int)D.C, D.h, x->Hf, D.h, 1, W2T, 1, D.h, x->Z, D.C, b2, 1, nullptr,

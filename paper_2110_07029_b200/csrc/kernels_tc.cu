@@ -323,7 +323,7 @@ __host__ __device__ inline int fwd_splits(int B, int n_cblocks, int num_ctas, in
 //                S_j   = H . W2T_blk^T        (SS, TMEM buffer j % 2)
 //                O_g  += P_j . W2T_blk        (A = P from TMEM, B MN-major)
 // TMEM: S[2] at columns 0, 128; O[2] at 256, 384 (h = 128; h = 256 uses one
-// WG and O at 256..511).  Partial slot of (CTA split sp, WG g) = 2 sp + g.
+// WG and O at 256..511).  One partial slot per CTA split: WG 1 hands its state to WG 0 in the epilogue.
 // =====================================================================
 template <int H>
 __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
@@ -546,33 +546,64 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
     }
-    // epilogue: the partial slot (sp, g)
+    // epilogue: ONE partial slot per CTA split.  With two warpgroups, WG 1
+    // stages its (m, l, O) in the (now idle) W ring and WG 0 merges the two
+    // online-softmax states before writing: half the partial traffic and
+    // half the combine work of one slot per warpgroup.
     const int grow = rt * BM + row;
-    const size_t slot = (size_t)sp * 2 + g;
-    if (jj > 0) {
-      mbar_wait(o_fin, 0);
-      fence_after();
+    const size_t slot = (size_t)sp;
+    float *sO = reinterpret_cast<float *>(sW);          // [H][128] O of WG 1 (column-major: conflict-free)
+    float *sML = sO + H * BM;                           // [2][128] m, l of WG 1
+    if (NWG == 2 && g == 1) {
+      if (jj > 0) {
+        mbar_wait(o_fin, 0);
+        fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < H / 32; ++ch) {
+          uint32_t r[32];
+          AS_TMEM_LD32(tO + ch * 32, r);
+          AS_TMEM_WAIT_LD(r);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) sO[(ch * 32 + k) * BM + row] = __uint_as_float(r[k]);
+        }
+      }
+      sML[row] = jj > 0 ? m_used : -FLT_MAX;
+      sML[BM + row] = jj > 0 ? l : 0.f;
+    }
+    if (NWG == 2) named_bar(4, 256);
+    if (g == 0) {
+      float m1 = -FLT_MAX, l1 = 0.f;
+      if (NWG == 2) { m1 = sML[row]; l1 = sML[BM + row]; }
+      const float m0 = jj > 0 ? m_used : -FLT_MAX;
+      const float M = fmaxf(m0, m1);
+      const float s0 = m0 == -FLT_MAX ? 0.f : ex2(m0 - M);
+      const float s1 = m1 == -FLT_MAX ? 0.f : ex2(m1 - M);
+      if (jj > 0) {
+        mbar_wait(o_fin, 0);
+        fence_after();
+      }
 #pragma unroll 1
       for (int ch = 0; ch < H / 32; ++ch) {
         uint32_t r[32];
-        AS_TMEM_LD32(tO + ch * 32, r);
-        AS_TMEM_WAIT_LD(r);
+        if (jj > 0) {
+          AS_TMEM_LD32(tO + ch * 32, r);
+          AS_TMEM_WAIT_LD(r);
+        } else {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) pO[(slot * H + ch * 32 + k) * bpad + grow] = __uint_as_float(r[k]);
+          for (int k = 0; k < 32; ++k) r[k] = 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          float o = __uint_as_float(r[k]) * s0;
+          if (NWG == 2 && s1 != 0.f) o = fmaf(sO[(ch * 32 + k) * BM + row], s1, o);
+          pO[(slot * H + ch * 32 + k) * bpad + grow] = o;
+        }
       }
-    } else {
-      for (int k = 0; k < H; ++k) pO[(slot * H + k) * bpad + grow] = 0.f;
+      pm[slot * bpad + grow] = M;
+      pl[slot * bpad + grow] = l * s0 + l1 * s1;
     }
-    pm[slot * bpad + grow] = m_used;
-    pl[slot * bpad + grow] = l;
-  } else if (NWG == 1 && warp < 8) {          // h = 256: idle second WG fills its empty slot
+  } else if (NWG == 1 && warp < 8) {          // h = 256: the second WG is idle
     AS_REG_INC();
-    const int q = warp & 3;
-    const int grow = rt * BM + q * 32 + lane;
-    const size_t slot = (size_t)sp * 2 + 1;
-    for (int k = 0; k < H; ++k) pO[(slot * H + k) * bpad + grow] = 0.f;
-    pm[slot * bpad + grow] = -FLT_MAX;
-    pl[slot * bpad + grow] = 0.f;
   } else {                                    // warps 8-9: idle
     AS_REG_DEC();
   }
@@ -1688,9 +1719,9 @@ void launch_out_top1_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, c
         p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pmax, pidx);
 }
 
-// number of pass-1 partial slots for a batch of B rows (2 per CTA split)
+// number of pass-1 partial slots for a batch of B rows (one per CTA split)
 int tc_fwd_splits_host(const TcPlan *p, int B) {
-  return 2 * tc::fwd_splits(B, p->n_cblocks, p->num_sms, p->max_splits);
+  return tc::fwd_splits(B, p->n_cblocks, p->num_sms, p->max_splits);
 }
 
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lsep,
