@@ -759,12 +759,30 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
     // comparison methods: plain average, no norms
     for (int i = 0; i < N; ++i) alpha[i] = 1.0 / N;
   }
-  x->launches += 2;
-  // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset
-  as::launch_scale(s, x->w, D.P, (float)alpha[x->cfg.rank]);
+  x->launches += 1;                          // momentum (+1 below if a prescale kernel runs)
+  // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset.
+  // N > 1: the prescale rides inside the allreduce (NCCL PreMulSum: every
+  // rank's input multiplied by its own alpha_i as it is reduced), saving an
+  // 8P-byte pass; plain prescale + sum if the op cannot be created.  N = 1:
+  // alpha = b / sum(b) = 1 exactly (Alg. 2 line 3, no perturbation, R14),
+  // so there is nothing to scale unless a caller-forced alpha differs.
+  const float a_me = (float)alpha[x->cfg.rank];
   if (N > 1) {
-    const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, ncclSum, x->comm, s);
+    ncclRedOp_t premul;
+    float a_host = a_me;
+    ncclResult_t r = ncclRedOpCreatePreMulSum(&premul, &a_host, ncclFloat, ncclScalarHostImmediate, x->comm);
+    if (r == ncclSuccess) {
+      r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
+      ncclRedOpDestroy(premul, x->comm);
+    } else {
+      x->launches += 1;
+      as::launch_scale(s, x->w, D.P, a_me);
+      r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, ncclSum, x->comm, s);
+    }
     if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
+  } else if (a_me != 1.0f) {
+    x->launches += 1;
+    as::launch_scale(s, x->w, D.P, a_me);
   }
   as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, D.d * D.h + D.h,
                       D.C * D.h, x->w2b);

@@ -377,6 +377,35 @@ def test_end_to_end_tiny_two_replicas_replay(gpu_lib):
     assert_close("wbar after 4 merges", reps[0].get_params(1), owbar, 1e-4)
 
 
+def test_rank_api_world1_matches_oracle(gpu_lib):
+    """The per-rank public path bench.py times (driver.run_rank: resident
+    dataset, stream batches, as_merge with its N = 1 shortcut) against the
+    oracle's whole run at N = 1: alpha = [1] every merge (Alg. 2 line 3, R14),
+    momentum gamma = 0.9 across 4 merges, global model within 1e-4 (fp32)."""
+    from paper_2110_07029_b200 import driver
+    from paper_2110_07029_b200.api import Replica
+    cfg = synthgen.CONFIGS["tiny"]
+    ds = synthgen.make_dataset(cfg)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    costs = synthgen.make_cost_models(1, hetero=False)
+    lr0, M = 0.5, 256
+    rep = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta, megabatch=M,
+                  max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
+                  lr0=lr0, gamma=0.9, precision="fp32", rank=0, world=1)
+    rep.upload_dataset(ds)
+    st = driver.ReplayState(1, cfg.b_max, cfg.b_min, cfg.beta, lr0, costs)
+    recs = driver.run_rank(rep, ds.row_ptr, ds.n, st, 4 * M, want_alpha=True)
+    ocfg = otrain.RunConfig(d=cfg.d, C=cfg.C, h=cfg.h, b_max=cfg.b_max, b_min=cfg.b_min, beta=cfg.beta,
+                            M=M, lr0=lr0, gamma=0.9, world=1)
+    orecs, owbar = otrain.run(ds, p, ocfg, costs, 4 * M)
+    assert len(recs) == len(orecs) == 4
+    for g, o in zip(recs, orecs):
+        assert list(g["alpha"]) == o["alpha"] == [1.0] and g["perturbed"] == o["perturbed"] == 0
+    assert_close("wbar", rep.get_params(1), owbar, 1e-4)
+    assert np.array_equal(rep.get_params(0), rep.get_params(1))
+    rep.close()
+
+
 @pytest.mark.parametrize("algo,M", [("elastic", 1024), ("sync", 128)])
 def test_end_to_end_tiny_comparison_methods(gpu_lib, algo, M):
     """the comparison methods of P:215 under the same
