@@ -738,7 +738,12 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   std::vector<double> norms(N), alpha(N);
   int32_t pert = 0;
   int rc = AS_OK;
-  if (x->cfg.algo == AS_ALGO_ADAPTIVE) {
+  if (x->cfg.algo == AS_ALGO_ADAPTIVE && N == 1) {
+    // Alg. 2 with one replica: line 3 gives alpha = b / b = 1 and r = s, so
+    // the perturbation is skipped whatever the norm (R14): no norm pass, no
+    // host synchronisation
+    alpha[0] = 1.0;
+  } else if (x->cfg.algo == AS_ALGO_ADAPTIVE) {
     // a9: replica norm
     x->launches += 2;
     as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
