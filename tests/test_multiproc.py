@@ -82,3 +82,60 @@ def test_two_ranks_route_identically_and_share_cursor():
     flat = sorted(x for c in allc for s, r in c for x in range(s, s + r))
     assert flat == list(range(997))                # live cursor conserves samples across processes
     assert nid == bytes(range(128))
+
+
+def _merge_worker(rank, world, port, q):
+    """as_merge's host protocol (a9-a13) with the collectives over gloo: local
+    norm, all-gather of the norms, Alg. 2 on every rank via the C++ scheduler
+    (must agree bit-exactly), all-reduce of alpha_i w_i, momentum."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from oracle import merge as omerge
+        from paper_2110_07029_b200 import sched
+        P = 4099
+        reps = [np.random.default_rng(100 + i).normal(0, 0.01, P).astype(np.float32) for i in range(world)]
+        wbar = np.random.default_rng(7).normal(0, 0.01, P).astype(np.float32)
+        wbar_p = np.random.default_rng(8).normal(0, 0.01, P).astype(np.float32)
+        u, b = [5, 3, 4][:world], [64, 60, 48][:world]
+        out = {}
+        for norm_mode in ("u", "ub"):
+            n_me = torch.tensor([omerge.replica_norm(reps[rank])], dtype=torch.float64)
+            norms = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(norms, n_me)
+            norms = [float(t.item()) for t in norms]
+            alpha, pert = sched.alg2(u, b, norms, 0.1, 0.1, norm=norm_mode)
+            acc = torch.tensor(alpha[rank] * reps[rank].astype(np.float64))
+            dist.all_reduce(acc)
+            merged = (acc.numpy() + 0.9 * (wbar.astype(np.float64) - wbar_p.astype(np.float64))).astype(np.float32)
+            out[norm_mode] = (alpha, pert, merged)
+        allo = [None] * world
+        dist.all_gather_object(allo, out)
+        if rank == 0:
+            q.put((allo, reps, wbar, wbar_p, u, b))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_merge_protocol_matches_oracle():
+    from oracle import merge as omerge
+    from oracle import sched as osched
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_merge_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    allo, reps, wbar, wbar_p, u, b = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for mode in ("u", "ub"):
+        (a0, p0, m0), (a1, p1, m1) = allo[0][mode], allo[1][mode]
+        assert a0 == a1 and p0 == p1                     # Alg. 2 identical on every rank (R13-R16)
+        assert np.array_equal(m0, m1)
+        oa, op = osched.alg2(u, b, [omerge.replica_norm(w) for w in reps], 0.1, 0.1, norm=mode)
+        assert a0 == oa and p0 == op
+        ow, _ = omerge.merge(reps, oa, wbar, wbar_p, 0.9)
+        np.testing.assert_allclose(m0, ow, rtol=0, atol=1e-7)
