@@ -33,14 +33,20 @@ test = full.rows(np.arange(40000, 48000))
 p0 = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
 costs = synthgen.make_cost_models(N, hetero=True)
 lr0 = float(sys.argv[3]) if len(sys.argv) > 3 else 0.5
-ALGOS = sys.argv[4].split(",") if len(sys.argv) > 4 else ["adaptive", "elastic", "sync"]
+ALGOS = sys.argv[4].split(",") if len(sys.argv) > 4 else ["adaptive", "adaptive_np", "elastic", "sync"]
 b_max, b_min = cfg.b_max, cfg.b_max // 8
-for algo in ALGOS:
+for name in ALGOS:
+    # "adaptive_np": Adaptive SGD with the perturbation disabled (pert_thr = 0):
+    # with the literal ||w||_2 / P metric (R15) perturbation fires at every
+    # merge and sum(alpha) = 1 + delta (alpha_r - alpha_s) > 1 inflates the model
+    algo = "adaptive" if name.startswith("adaptive") else name
+    pert_thr = 0.0 if name == "adaptive_np" else 0.1
     M = N * b_max if algo == "sync" else 20 * b_max       # sync: one batch per replica per merge
     gamma = 0.9 if algo == "adaptive" else 0.0
     reps = [Replica(cfg.d, cfg.C, cfg.h, b_max, p0, b_min=b_min, beta=b_min // 2, megabatch=M,
                     max_row_nnz=int(np.diff(full.row_ptr).max()), max_row_labels=int(np.diff(full.lab_ptr).max()),
-                    lr0=lr0, gamma=gamma, precision="bf16", rank=i, world=N, algo=algo) for i in range(N)]
+                    lr0=lr0, gamma=gamma, pert_thr=pert_thr, precision="bf16", rank=i, world=N, algo=algo)
+            for i in range(N)]
     st = driver.ReplayState(N, b_max, b_min, b_min // 2, lr0, costs, algo=algo)
     for r in reps:
         r.upload_dataset(train)
@@ -67,7 +73,7 @@ for algo in ALGOS:
         if seen % (20 * b_max) and seen < total:
             continue
         acc = reps[0].evaluate(test)                   # replicas restart from wbar
-        print(json.dumps({"algo": algo, "lr0": lr0, "samples": seen, "replay_s": sim_ps * 1e-12, "gpu_s": round(gpu_s, 4),
+        print(json.dumps({"algo": name, "lr0": lr0, "samples": seen, "replay_s": sim_ps * 1e-12, "gpu_s": round(gpu_s, 4),
                           "top1": acc, "u": u, "b": b_used}), flush=True)
     for r in reps:
         r.close()
