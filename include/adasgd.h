@@ -53,9 +53,19 @@ enum { AS_FP32 = 0, AS_BF16 = 1 };
 enum {
   AS_FLAG_DEBUG_GRADS = 1, /* keep every gradient of the last step in device
                               memory for as_debug_get (tests only)            */
-  AS_FLAG_NORM_UB = 2      /* as_merge (AS_ALGO_ADAPTIVE): Alg. 2 line 5 uses
+  AS_FLAG_NORM_UB = 2,     /* as_merge (AS_ALGO_ADAPTIVE): Alg. 2 line 5 uses
                               u_i b_i / sum(u b) instead of u_i / sum(u), the
                               alternative of P:175                             */
+  /* bits 2-3: the regularisation metric of Alg. 2 line 7 tested against
+     pert_thr (reading R15; "||w_i||_2/|w|", "L2-norm divided by
+     model dimensionality", in tension with P:276): flags |= metric << 2    */
+  AS_NORM_METRIC_SHIFT = 2
+};
+enum {
+  AS_METRIC_L2_P = 0,       /* ||w||_2 / P   (literal, default)                 */
+  AS_METRIC_L2SQ_P = 1,     /* ||w||_2^2 / P                                    */
+  AS_METRIC_L2_SQRTP = 2,   /* ||w||_2 / sqrt(P)  (RMS of the parameters)       */
+  AS_METRIC_L2 = 3          /* ||w||_2                                          */
 };
 
 /* Alg. 2 line-5 normalisation (as_sched_alg2_ex). */

@@ -7,11 +7,15 @@ from __future__ import annotations
 import numpy as np
 
 
-def replica_norm(w):
+def replica_norm(w, metric="l2/P"):
     """||w_i||_2 / |w| over the packed parameter vector (P:162 Alg. 2 line 7;
-    P:177 "L2-norm divided by model dimensionality"; reading R15), fp64."""
+    P:177 "L2-norm divided by model dimensionality"; reading R15), fp64.
+    metric: "l2/P" (literal, default), "l2^2/P", "l2/sqrt(P)", "l2" -- the
+    readings R15 keeps switchable (P:276 is in tension with the literal one)."""
     w = np.asarray(w, np.float64)
-    return float(np.sqrt(np.sum(w * w)) / w.size)
+    S = float(np.sum(w * w))
+    P = w.size
+    return {"l2/P": np.sqrt(S) / P, "l2^2/P": S / P, "l2/sqrt(P)": np.sqrt(S / P), "l2": np.sqrt(S)}[metric]
 
 
 def merge(replicas, alpha, wbar, wbar_p, gamma):

@@ -20,6 +20,8 @@ AS_ALGO_ADAPTIVE, AS_ALGO_ELASTIC, AS_ALGO_SYNC = 0, 1, 2
 ALGOS = {"adaptive": AS_ALGO_ADAPTIVE, "elastic": AS_ALGO_ELASTIC, "sync": AS_ALGO_SYNC}
 AS_FLAG_DEBUG_GRADS, AS_FLAG_NORM_UB = 1, 2
 AS_NORM_UPDATES, AS_NORM_UB = 0, 1
+AS_NORM_METRIC_SHIFT = 2
+METRICS = {"l2/P": 0, "l2^2/P": 1, "l2/sqrt(P)": 2, "l2": 3}
 AS_PARAMS_REPLICA, AS_PARAMS_GLOBAL, AS_PARAMS_GLOBAL_PREV = 0, 1, 2
 (AS_DBG_H, AS_DBG_LSE, AS_DBG_LOSS, AS_DBG_DA, AS_DBG_DB1, AS_DBG_DW2T, AS_DBG_DB2, AS_DBG_DW1,
  AS_DBG_FSEG, AS_DBG_LSEG, AS_DBG_BATCH, AS_DBG_LOGITS) = range(12)

@@ -26,7 +26,7 @@ class Replica:
     def __init__(self, d, C_labels, h, b_max, init_params, *, b_min=None, beta=None, megabatch=None,
                  max_row_nnz=1024, max_row_labels=64, lr0=0.1, gamma=0.9, delta=0.1, pert_thr=0.1,
                  precision="bf16", rank=0, world=1, nccl_id=None, device=0, stream=None,
-                 debug_grads=False, algo="adaptive", merge_norm="u"):
+                 debug_grads=False, algo="adaptive", merge_norm="u", norm_metric="l2/P"):
         torch = _torch()
         self.lib = L.load()
         b_min = b_max // 8 if b_min is None else b_min
@@ -41,7 +41,8 @@ class Replica:
         cfg.max_row_nnz, cfg.max_row_labels = max_row_nnz, max_row_labels
         cfg.lr0, cfg.gamma, cfg.delta, cfg.pert_thr = lr0, gamma, delta, pert_thr
         cfg.precision = L.AS_BF16 if precision == "bf16" else L.AS_FP32
-        cfg.flags = (L.AS_FLAG_DEBUG_GRADS if debug_grads else 0) | (L.AS_FLAG_NORM_UB if merge_norm == "ub" else 0)
+        cfg.flags = ((L.AS_FLAG_DEBUG_GRADS if debug_grads else 0) | (L.AS_FLAG_NORM_UB if merge_norm == "ub" else 0)
+                     | (L.METRICS[norm_metric] << L.AS_NORM_METRIC_SHIFT))
         cfg.rank, cfg.world, cfg.device = rank, world, device
         self._nccl_buf = None
         if nccl_id is not None:

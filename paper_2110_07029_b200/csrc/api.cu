@@ -746,7 +746,7 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   } else if (x->cfg.algo == AS_ALGO_ADAPTIVE) {
     // a9: replica norm
     x->launches += 2;
-    as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
+    as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev, (x->cfg.flags >> AS_NORM_METRIC_SHIFT) & 3);
     if (N > 1) {
       const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
       if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r)); }
@@ -818,7 +818,7 @@ int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32
     for (int i = 0; i < n; ++i) {
       as_ctx *x = ctxs[i];
       cudaSetDevice(x->cfg.device);
-      as::launch_sumsq(x->stream, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev);
+      as::launch_sumsq(x->stream, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev, (x->cfg.flags >> AS_NORM_METRIC_SHIFT) & 3);
       rc = cuda_check(x, cudaMemcpyAsync(&norms[i], x->norm_dev, 8, cudaMemcpyDeviceToHost, x->stream), "norm");
       if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "norm sync");
       if (rc) return rc;

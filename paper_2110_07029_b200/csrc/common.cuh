@@ -132,7 +132,7 @@ void launch_dw1_sgd(cudaStream_t s, int h, StepDesc *desc, int cap, const int32_
 void launch_loss_mean(cudaStream_t s, const StepDesc *desc, const float *lossr, float *loss);
 // merge (steps a9-a13)
 void launch_sumsq(cudaStream_t s, const float *w, long long P, double *partials, int nblocks,
-                  double *out_norm);
+                  double *out_norm, int metric);
 void launch_scale(cudaStream_t s, float *w, long long P, float alpha);
 void launch_momentum(cudaStream_t s, float *w, float *wbar_p_to_new, const float *wbar,
                      long long P, float gamma, long long w2_off, long long w2_len,

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) k_sumsq(const float *__restrict__ w, long
 }
 
 __global__ void __launch_bounds__(1024) k_sumsq_final(const double *__restrict__ partials, int nb,
-                                                      long long P, double *__restrict__ out) {
+                                                      long long P, int metric, double *__restrict__ out) {
   __shared__ double red[1024];
   double a = 0.0;
   for (int i = threadIdx.x; i < nb; i += 1024) a += partials[i];
@@ -306,14 +306,20 @@ __global__ void __launch_bounds__(1024) k_sumsq_final(const double *__restrict__
     if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = sqrt(red[0]) / (double)P;
+  // R15 regularisation metric: ||w||_2 / P (literal, default), ||w||_2^2 / P,
+  // ||w||_2 / sqrt(P), ||w||_2
+  if (threadIdx.x == 0) {
+    const double S = red[0];
+    *out = metric == 1 ? S / (double)P : metric == 2 ? sqrt(S / (double)P) : metric == 3 ? sqrt(S)
+                                                                                        : sqrt(S) / (double)P;
+  }
 }
 
 void launch_sumsq(cudaStream_t s, const float *w, long long P, double *partials, int nblocks,
-                  double *out_norm) {
+                  double *out_norm, int metric) {
   const long long chunk = (P + nblocks - 1) / nblocks;
   k_sumsq<<<nblocks, 256, 0, s>>>(w, P, chunk, partials);
-  k_sumsq_final<<<1, 1024, 0, s>>>(partials, nblocks, P, out_norm);
+  k_sumsq_final<<<1, 1024, 0, s>>>(partials, nblocks, P, metric, out_norm);
 }
 
 // a11: w_i <- alpha_i w_i

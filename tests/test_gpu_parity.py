@@ -345,6 +345,31 @@ def test_group_merge_ub_normalisation(gpu_lib):
     assert_close("wbar", reps[0].get_params(1), wbar, 1e-5)
 
 
+@pytest.mark.parametrize("metric,thr", [("l2", 1.0), ("l2", 1e6), ("l2/sqrt(P)", 0.05), ("l2^2/P", 1e-3)])
+def test_group_merge_norm_metrics(gpu_lib, metric, thr):
+    """R15's metric switch: the perturbation decision of Alg. 2 line 7 with each
+    metric (thresholds chosen on both sides of the replicas' values) matches the
+    oracle bit-exactly, merged model within 1e-5."""
+    from paper_2110_07029_b200.api import Replica, group_merge
+    cfg = _cfg(1000, 500, 128, 200, 64)
+    ds = synthgen.make_dataset(cfg, n=200)
+    p = _params(cfg)
+    reps = [Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=8, max_row_nnz=int(np.diff(ds.row_ptr).max()),
+                    max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=0.5, precision="fp32", rank=i, world=2,
+                    pert_thr=thr, norm_metric=metric) for i in range(2)]
+    for i, r in enumerate(reps):
+        for k in range(i + 1):
+            sub = ds.rows(np.arange(32) + 40 * i + 8 * k)
+            r.load_batch_csr(32, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+            r.train_step()
+    ws = [r.get_params() for r in reps]
+    alpha, pert = group_merge(reps, [1, 2], [64, 64])
+    oa, op = osched.alg2([1, 2], [64, 64], [omerge.replica_norm(w, metric) for w in ws], 0.1, thr)
+    assert list(alpha) == oa and pert == op
+    wbar, _ = omerge.merge(ws, oa, p, p, 0.9)
+    assert_close("wbar", reps[0].get_params(1), wbar, 1e-5)
+
+
 def test_end_to_end_tiny_two_replicas_replay(gpu_lib):
     """T5: config 'tiny' (BASELINE.json configs[0]): 2 replicas, replay with a
     32% slowdown, 1 epoch, 4 merges, fp32 mode.  Routing, b_i, lr_i and alpha

@@ -174,3 +174,15 @@ def test_elastic_static_split_ignores_speed():
     ra, _ = otrain.run(ds, p, _cfg(algo="adaptive", **kw), costs, 64)
     assert re[0]["u"] == [8, 8] and max(re[0]["clocks"]) == 8 * (40 * 132 // 100)
     assert ra[0]["u"][0] > ra[0]["u"][1] and max(ra[0]["clocks"]) < max(re[0]["clocks"])
+
+
+def test_norm_metrics_closed_form():
+    """R15's switchable regularisation metrics on a constant vector c (P entries):
+    ||w|| = |c| sqrt(P): l2/P = |c|/sqrt(P), l2^2/P = c^2, l2/sqrt(P) = |c|, l2 = |c| sqrt(P)."""
+    P, c = 10_000, -0.3
+    w = np.full(P, c, np.float32)
+    cc = float(np.float32(c))
+    assert abs(omerge.replica_norm(w, "l2/P") - abs(cc) / np.sqrt(P)) < 1e-15
+    assert abs(omerge.replica_norm(w, "l2^2/P") - cc * cc) < 1e-12
+    assert abs(omerge.replica_norm(w, "l2/sqrt(P)") - abs(cc)) < 1e-12
+    assert abs(omerge.replica_norm(w, "l2") - abs(cc) * np.sqrt(P)) < 1e-9
