@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(SegCfg<H, MODE>::NW * 32, 1)
                const int32_t *__restrict__ seg_of, const PtrT *__restrict__ seg_ptr,
                const int32_t *__restrict__ gidx, const float *__restrict__ scale,
                const float *__restrict__ src, float *__restrict__ part, int *__restrict__ arrive, SegArgs a) {
+  griddep_wait();
   using Cfg = SegCfg<H, MODE>;
   constexpr int V = H / 128, GE = Cfg::GE, NW = Cfg::NW, NST = Cfg::NST, ROW = Cfg::ROW;
   extern __shared__ __align__(128) uint8_t seg_smem[];
@@ -547,8 +548,8 @@ static void seg_bulk_launch(cudaStream_t s, int num_sms, const int *n_dev, const
     cudaFuncSetAttribute(k_seg_bulk<H, MODE, PtrT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  k_seg_bulk<H, MODE, PtrT><<<num_sms, Cfg::NW * 32, Cfg::SMEM, s>>>(n_dev, nseg_dev, nseg_pad, seg_of, seg_ptr,
-                                                                     gidx, scale, src, part, arrive, a);
+  launch_pdl(k_seg_bulk<H, MODE, PtrT>, dim3(num_sms), dim3(Cfg::NW * 32), Cfg::SMEM, s, n_dev, nseg_dev,
+             nseg_pad, seg_of, seg_ptr, gidx, scale, src, part, arrive, a);
 }
 
 template <int H, int MODE, typename PtrT>

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(1024) k_gather_scan(const int64_t *__restrict_
                                                       int64_t *__restrict__ ids,
                                                       StepDesc *__restrict__ desc, int nnz_cap,
                                                       int lab_cap) {
+  griddep_wait();
   __shared__ long long wa[32], wb[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   long long ca = 0, cb = 0;
@@ -172,6 +173,7 @@ __global__ void k_gather_copy(const int64_t *__restrict__ rp, const int32_t *__r
                               float *__restrict__ val, int32_t *__restrict__ lab,
                               int32_t *__restrict__ rid, int32_t *__restrict__ lrid,
                               const StepDesc *__restrict__ desc) {
+  griddep_wait();
   if (desc->err) return;
   const int r = blockIdx.x;
   const int64_t id = ids[r];
@@ -194,10 +196,10 @@ void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_
                          int64_t *row_ptr, int32_t *col, float *val, int64_t *lab_ptr,
                          int32_t *lab, int64_t *ids, int32_t *rid, int32_t *lrid, StepDesc *desc,
                          int nnz_cap, int lab_cap) {
-  k_gather_scan<<<1, 1024, 0, s>>>(ds_row_ptr, ds_lab_ptr, order, n, pos, rows, row_ptr, lab_ptr, ids,
-                                   desc, nnz_cap, lab_cap);
-  k_gather_copy<<<rows, 128, 0, s>>>(ds_row_ptr, ds_col, ds_val, ds_lab_ptr, ds_lab, ids, row_ptr,
-                                     lab_ptr, col, val, lab, rid, lrid, desc);
+  launch_pdl(k_gather_scan, dim3(1), dim3(1024), 0, s, ds_row_ptr, ds_lab_ptr, order, n, pos, rows, row_ptr,
+             lab_ptr, ids, desc, nnz_cap, lab_cap);
+  launch_pdl(k_gather_copy, dim3(rows), dim3(128), 0, s, ds_row_ptr, ds_col, ds_val, ds_lab_ptr, ds_lab, ids,
+             row_ptr, lab_ptr, col, val, lab, rid, lrid, desc);
 }
 
 // =====================================================================
@@ -489,6 +491,7 @@ __global__ void k_label_terms(const StepDesc *__restrict__ desc, const int64_t *
                               const int32_t *__restrict__ lab, const float *__restrict__ Hf,
                               const float *__restrict__ W2T, const float *__restrict__ b2,
                               float *__restrict__ zsum, float *__restrict__ labW) {
+  griddep_wait();
   constexpr int V = H / 128;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= desc->rows) return;
@@ -540,9 +543,9 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                         const float *W2T, const float *b2, float *zsum, float *labW) {
   const int g = ceil_div((long long)b_max * 32, 256);
   if (h == 128)
-    k_label_terms<128><<<g, 256, 0, s>>>(desc, lab_ptr, lab, Hf, W2T, b2, zsum, labW);
+    launch_pdl(k_label_terms<128>, dim3(g), dim3(256), 0, s, desc, lab_ptr, lab, Hf, W2T, b2, zsum, labW);
   else
-    k_label_terms<256><<<g, 256, 0, s>>>(desc, lab_ptr, lab, Hf, W2T, b2, zsum, labW);
+    launch_pdl(k_label_terms<256>, dim3(g), dim3(256), 0, s, desc, lab_ptr, lab, Hf, W2T, b2, zsum, labW);
 }
 
 // =====================================================================
@@ -558,6 +561,7 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     float *__restrict__ lse2, float *__restrict__ lsep, float *__restrict__ wrow,
     float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
     int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1) {
+  griddep_wait();
   // CTA = 32 rows x 16 columns (8 groups of 2); partial reads coalesced over rows
   const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
   const int B = desc->rows;
@@ -634,9 +638,9 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
                          float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
                          int *db1cnt, float *b1, float lr, float *dbg_db1) {
-  k_combine_bf16<<<dim3(ceil_div(bpad, 32), h / 16), 256, (size_t)splits * 32 * 4, s>>>(
-      desc, h, bpad, splits, pm, pl, pO, labW, zsum, Hf, lab_ptr, lse2, lsep, wrow, lossr, dA, db1p, db1cnt, b1,
-      lr, dbg_db1);
+  launch_pdl(k_combine_bf16, dim3(ceil_div(bpad, 32), h / 16), dim3(256), (size_t)splits * 32 * 4, s, desc, h,
+             bpad, splits, pm, pl, pO, labW, zsum, Hf, lab_ptr, lse2, lsep, wrow, lossr, dA, db1p, db1cnt, b1, lr,
+             dbg_db1);
 }
 
 // =====================================================================

@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
               const StepDesc *__restrict__ desc, const __nv_bfloat16 *__restrict__ Hb,
               const float *__restrict__ b2, int C, int n_cblocks, int max_splits, int bpad,
               float *__restrict__ pm, float *__restrict__ pl, float *__restrict__ pO) {
+  griddep_wait();
   using Cfg = FwdCfg<H>;
   constexpr int NST = Cfg::NST, TILE = Cfg::TILE;
   constexpr int NWG = H == 128 ? 2 : 1;             // softmax warpgroups (O accumulators)
@@ -671,6 +672,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               float *__restrict__ W2T, float *__restrict__ b2,
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
               float *__restrict__ dbg_db2) {
+  griddep_wait();
   using Cfg = BwdCfg<H>;
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
   constexpr int UNIT = Cfg::UNIT, HPT = Cfg::HPT;
@@ -1700,13 +1702,13 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2,
                        float *pm, float *pl, float *pO) {
   if (p->h == 128)
-    tc::k_out_fwd<128><<<p->num_sms, tc::FwdCfg<128>::THREADS, tc::FwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
-        p->max_splits, p->bpad, pm, pl, pO);
+    launch_pdl(tc::k_out_fwd<128>, dim3(p->num_sms), dim3(tc::FwdCfg<128>::THREADS), tc::FwdCfg<128>::SMEM, s,
+               p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
+               p->max_splits, p->bpad, pm, pl, pO);
   else
-    tc::k_out_fwd<256><<<p->num_sms, tc::FwdCfg<256>::THREADS, tc::FwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
-        p->max_splits, p->bpad, pm, pl, pO);
+    launch_pdl(tc::k_out_fwd<256>, dim3(p->num_sms), dim3(tc::FwdCfg<256>::THREADS), tc::FwdCfg<256>::SMEM, s,
+               p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
+               p->max_splits, p->bpad, pm, pl, pO);
 }
 
 void launch_out_top1_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2, float *pmax,
@@ -1729,6 +1731,7 @@ void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
                        float *b2, __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2) {
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
+    // plain launch: pass 2 follows the wait on the transposes' join event
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
         p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);

@@ -220,6 +220,7 @@ void launch_transposes(cudaStream_t s, const TrArgs &a) {
 // class->segment map -1, scan tiles 0, ticket 0).
 __global__ void __launch_bounds__(256) k_step_tail(TrArgs a, const float *__restrict__ lossr,
                                                    float *__restrict__ loss) {
+  griddep_wait();
   const StepDesc *d = a.desc;
   if (blockIdx.x == 0) {
     __shared__ float red[8];
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(256) k_step_tail(TrArgs a, const float *__rest
 }
 
 void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss) {
-  k_step_tail<<<2 * num_sms, 256, 0, s>>>(a, lossr, loss);
+  launch_pdl(k_step_tail, dim3(2 * num_sms), dim3(256), 0, s, a, lossr, loss);
 }
 
 }  // namespace as
