@@ -101,7 +101,7 @@ struct as_ctx {
   ncclComm_t comm;
   // side stream for the batch transposes (overlap with SpMM / pass 1)
   cudaStream_t side;
-  cudaEvent_t ev_fork, ev_join;
+  cudaEvent_t ev_fork, ev_join, ev_tail;
   // live profiling (as_profile)
   bool prof_on;
   std::vector<cudaEvent_t> ev_pool;
@@ -396,6 +396,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->side, cudaStreamNonBlocking, prio_lo), "side stream");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming), "event");
+  if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_tail, cudaEventDisableTiming), "event");
   // pinned double-buffered staging for host batches
   x->pin_bytes = 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
   for (int i = 0; i < 2 && !rc; ++i) {
@@ -434,6 +435,7 @@ int as_destroy(as_ctx *x) {
   if (x->side) { cudaStreamSynchronize(x->side); cudaStreamDestroy(x->side); }
   if (x->ev_fork) cudaEventDestroy(x->ev_fork);
   if (x->ev_join) cudaEventDestroy(x->ev_join);
+  if (x->ev_tail) cudaEventDestroy(x->ev_tail);
   for (auto &p : x->pending) { x->ev_pool.push_back(p.a); x->ev_pool.push_back(p.b); }
   for (auto e : x->ev_pool) cudaEventDestroy(e);
   free(x->plan);
@@ -698,11 +700,19 @@ int as_train_step(as_ctx *x, float *loss_out) {
   }
   // a7: first-layer gradient (deterministic segmented reduction) + SGD
   ph_begin(x, AS_PH_DW1);
-  x->launches += 2;
+  x->launches += 1;
   as::launch_dw1_chunked(s, D.h, x->num_sms, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
                          x->fseg_val, x->dA, W1, lr, x->seg_part, x->arrive,
                          dbg ? x->dbg_dW1 : nullptr);
-  as::launch_step_tail(s, tr, x->num_sms, x->lossr, x->loss);
+  // transpose state reset on the side stream after the step's last reader
+  cudaEventRecord(x->ev_tail, s);
+  cudaStreamWaitEvent(ss, x->ev_tail, 0);
+  x->launches += 1;
+  as::launch_tr_reset(ss, tr, x->num_sms);
+  if (loss_out || dbg) {
+    x->launches += 1;
+    as::launch_loss_mean(s, d, x->lossr, x->loss);
+  }
   ph_end(x, AS_PH_DW1);
   int rc = cuda_check(x, cudaSuccess, "train step launch");
   if (rc) return rc;

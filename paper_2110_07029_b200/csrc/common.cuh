@@ -107,6 +107,7 @@ void launch_entry_rows(cudaStream_t s, const int64_t *row_ptr, const int64_t *la
 void launch_transposes(cudaStream_t s, const TrArgs &a);
 void launch_fill_int4(cudaStream_t s, int4 *p, long long n, int x, int y, int z, int w);
 void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss);
+void launch_tr_reset(cudaStream_t s, const TrArgs &a, int num_sms);
 void launch_class_map(cudaStream_t s, const int32_t *lseg_id, const int *V_dev, int cap,
                       int32_t *cls_seg, int value_is_index);
 // SpMM forward (step a4)

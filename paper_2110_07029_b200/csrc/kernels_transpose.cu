@@ -146,8 +146,10 @@ __global__ void __launch_bounds__(1024) k_tr_scan(TrArgs a) {
       s_pe = pe; s_ps = ps;
       if (lt == nt - 1) {                          // totals of this key space
         const int E = pe + AE, S = ps + AS;
-        if (lab) { a.lseg_ptr[S] = E; a.desc->V = S; }
-        else { a.fseg_ptr[S] = E; a.desc->U = S; }
+        // segment counts also into ticket[2..3]: the side-stream reset reads them
+        // there while the main stream's next batch rewrites the step descriptor
+        if (lab) { a.lseg_ptr[S] = E; a.desc->V = S; a.ticket[3] = S; }
+        else { a.fseg_ptr[S] = E; a.desc->U = S; a.ticket[2] = S; }
       }
     }
   }
@@ -254,6 +256,40 @@ __global__ void __launch_bounds__(256) k_step_tail(TrArgs a, const float *__rest
       a.lbits[(size_t)c * a.W + (r >> 5)] = 0u;
     }
   }
+}
+
+// The dense per-key transpose state back to idle on the SIDE stream after the
+// step's last reader (dW1), keyed by the step's own segment lists (fseg_id /
+// lseg_id, whole bitmaps) so it does not read the batch arrays the main
+// stream's next batch is already overwriting; the next step's transposes
+// follow it in stream order.
+__global__ void __launch_bounds__(256) k_tr_reset(TrArgs a) {
+  const int U = a.ticket[2], V = a.ticket[3], W = a.W;
+  const int tiles = ceil_div_dev(a.d, kTrTile) + ceil_div_dev(a.C, kTrTile);
+  const long long nf = (long long)U * W, nl = (long long)V * W;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < nf + nl || t < tiles; t += stride) {
+    if (t < tiles) a.tile_state[t] = 0ull;
+    if (t < nf) {
+      const int f = a.fseg_id[t / W];
+      a.fbits[(size_t)f * W + t % W] = 0u;
+      if (t % W == 0) a.fcnt[f] = 0;
+    } else if (t - nf < nl) {
+      const long long j = t - nf;
+      const int c = a.lseg_id[j / W];
+      a.lbits[(size_t)c * W + j % W] = 0u;
+      if (j % W == 0) {
+        a.lcnt[c] = 0;
+        a.cls_seg[c] = -1;
+        a.cls_lab[c] = make_int4(0, 0, 0x7fffffff, 0);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.ticket[0] = 0;
+}
+
+void launch_tr_reset(cudaStream_t s, const TrArgs &a, int num_sms) {
+  k_tr_reset<<<2 * num_sms, 256, 0, s>>>(a);
 }
 
 void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss) {
