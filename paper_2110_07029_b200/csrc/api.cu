@@ -101,7 +101,7 @@ struct as_ctx {
   ncclComm_t comm;
   // side stream for the batch transposes (overlap with SpMM / pass 1)
   cudaStream_t side;
-  cudaEvent_t ev_fork, ev_join, ev_tail;
+  cudaEvent_t ev_fork, ev_join, ev_tail, ev_lab;
   // live profiling (as_profile)
   bool prof_on;
   std::vector<cudaEvent_t> ev_pool;
@@ -397,6 +397,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_tail, cudaEventDisableTiming), "event");
+  if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_lab, cudaEventDisableTiming), "event");
   // pinned double-buffered staging for host batches
   x->pin_bytes = 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
   for (int i = 0; i < 2 && !rc; ++i) {
@@ -436,6 +437,7 @@ int as_destroy(as_ctx *x) {
   if (x->ev_fork) cudaEventDestroy(x->ev_fork);
   if (x->ev_join) cudaEventDestroy(x->ev_join);
   if (x->ev_tail) cudaEventDestroy(x->ev_tail);
+  if (x->ev_lab) cudaEventDestroy(x->ev_lab);
   for (auto &p : x->pending) { x->ev_pool.push_back(p.a); x->ev_pool.push_back(p.b); }
   for (auto e : x->ev_pool) cudaEventDestroy(e);
   free(x->plan);
@@ -629,6 +631,13 @@ int as_train_step(as_ctx *x, float *loss_out) {
     cudaEventRecord(x->ev_fork, s);
     cudaStreamWaitEvent(ss, x->ev_fork, 0);
     ph_begin(x, AS_PH_TRANSPOSE, ss);
+#ifdef AS_X_LABSIDE
+    if (x->cfg.precision == AS_BF16) {        // label terms first on the side stream
+      x->launches += 1;
+      as::launch_label_terms(ss, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
+      cudaEventRecord(x->ev_lab, ss);
+    }
+#endif
     x->launches += 3;
     as::launch_transposes(ss, tr);
     ph_end(x, AS_PH_TRANSPOSE, ss);
@@ -656,10 +665,15 @@ int as_train_step(as_ctx *x, float *loss_out) {
     ph_end(x, AS_PH_OUT_FWD);
     if (AS_X_FORK == 2) fork_transposes();
     ph_begin(x, AS_PH_COMBINE);
-    x->launches += 2;
     // label terms of the loss and of dH (R3), then the split combine -> LSE,
     // loss, dA, and db1 with b1's SGD fused (ordered last-arriver column sums)
+#ifdef AS_X_LABSIDE
+    x->launches += 1;
+    cudaStreamWaitEvent(s, x->ev_lab, 0);
+#else
+    x->launches += 2;
     as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
+#endif
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
                             x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lab_ptr, x->lse2, x->lsep, x->wrow,
                             x->lossr, x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr);
