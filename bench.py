@@ -390,12 +390,17 @@ def main():
     spmm_bytes = (4 * cfg.h + 8) * nnz_prof + 8 * (my_samples + ph_calls[2]) + 4 * cfg.h * my_samples
     spmm_gbs = spmm_bytes / (ph_ms[2] / 1e3) / 1e9 if ph_ms[2] > 0 else 0.0
     traffic, traffic_src = None, None
+    spmm_traffic, spmm_traffic_src = None, None
     try:                       # dram bytes per launch from the committed `ncu --set full` capture
         tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
         ks = ["k_out_fwd<%d>" % cfg.h, "k_out_bwd<%d>" % cfg.h]
         if args.config == "amazon670k" and all(k in tr for k in ks):
             traffic = sum(tr[k]["dram_bytes"] for k in ks)
             traffic_src = "profiles/ncu_traffic.json (%s; pass1+pass2 per SGD step)" % tr[ks[0]]["report"]
+        ksp = "k_seg_bulk<%d, 0, long>" % cfg.h
+        if args.config == "amazon670k" and ksp in tr:
+            spmm_traffic = tr[ksp]["dram_bytes"]
+            spmm_traffic_src = "profiles/ncu_traffic.json (%s; a4 SpMM per launch, cold cache)" % tr[ksp]["report"]
     except (OSError, ValueError):
         pass
     roof = {"bound": "tensor", "kernel": "out_fwd+out_bwd (tcgen05 passes 1+2, one launch each per SGD step)",
@@ -407,7 +412,9 @@ def main():
             "peak_kind": "%s bf16_tflops_sustained (kernel timed inside a long step)" % pk_kind,
             "avg_launch_ms": {"out_fwd": ph_ms[3] / calls_out, "out_bwd": ph_ms[5] / max(1, ph_calls[5])},
             "spmm": {"bound": "hbm", "achieved": spmm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": spmm_gbs / pk["hbm_gbs"], "avg_launch_ms": ph_ms[2] / max(1, ph_calls[2])}}
+                     "frac": spmm_gbs / pk["hbm_gbs"], "avg_launch_ms": ph_ms[2] / max(1, ph_calls[2]),
+                     "bytes_alg_per_launch": spmm_bytes / max(1, ph_calls[2]),
+                     "traffic": spmm_traffic, "traffic_source": spmm_traffic_src}}
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
