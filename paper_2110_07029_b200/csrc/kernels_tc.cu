@@ -689,8 +689,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   int4 *sCl = (int4 *)(sMk + 2 * 256);           // [2][256] cls_lab of the next block
   float *sB2r = (float *)(sCl + 2 * 256);        // [2][256] b2 of the next block
   uint64_t *bars = (uint64_t *)(sB2r + 2 * 256);
+  // p_full[PH b + half]: G^T of one 64-row half of the unit in S^T buffer b is
+  // in TMEM; the dW MMA of that half starts without waiting for the other
+  constexpr int PH = UNIT / 64;
   uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + NSB,
-           *wt_full = p_full + NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
+           *wt_full = p_full + PH * NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
            *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1;
   uint32_t *tmem_slot = (uint32_t *)(wf_full + 1);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
@@ -705,7 +708,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSH; ++i) { mbar_init(&h_full[i], 1); mbar_init(&h_empty[i], 1); }
-    for (int i = 0; i < NSB; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+    for (int i = 0; i < NSB; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < PH * NSB; ++i) mbar_init(&p_full[i], 4);
     for (int i = 0; i < NWT; ++i) mbar_init(&wt_full[i], 4);
     mbar_init(dw_full, 1);
     mbar_init(dw_empty, 4);
@@ -786,18 +790,26 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       uint32_t dwe_ph = 0u;                   // dw_empty phase of the previous block
       auto do_dw = [&](const Cur &c) {
         TRACE(0, lane == 0, 1, c.v);
-        mbar_wait(&p_full[c.b], c.bph);
+        mbar_wait(&p_full[PH * c.b], c.bph);
         TRACE(0, lane == 0, 2, c.v);
         if (c.v == 0 && c.kb >= 1) { mbar_wait(dw_empty, dwe_ph); dwe_ph ^= 1u; }
         fence_after();
 #ifndef AS_X_NOMMA2
-        if constexpr (UNIT == 128)
-          mma_grp_ts_mn_8(tmem + COL_DW, tmem + c.b * UNIT, sdesc(aH + c.st * TILE, ATOM_BYTES, 1024), idW,
+        if constexpr (UNIT == 128) {
+          // rows 0-63 (G^T columns 0-31) while the softmax still works on rows 64-127
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * UNIT, sdesc(aH + c.st * TILE, ATOM_BYTES, 1024), idW,
                           c.v > 0 ? 1u : 0u);
-        else
+          mbar_wait(&p_full[PH * c.b + 1], c.bph);
+          fence_after();
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * UNIT + 32,
+                          sdesc(aH + c.st * TILE + 64 * 128, ATOM_BYTES, 1024), idW, 1u);
+        } else {
           mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * UNIT,
                           sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), ATOM_BYTES, 1024), idW,
                           c.v > 0 ? 1u : 0u);
+        }
+#else
+        if constexpr (UNIT == 128) mbar_wait(&p_full[PH * c.b + 1], c.bph);
 #endif
         if (c.hh == HPT - 1) mma_commit_w(&h_empty[c.st]);
         if (c.v == NU - 1) mma_commit_w(dw_full);
@@ -913,9 +925,6 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v % HPT) * UNIT + half * 64);
         AS_TMEM_WAIT_LD(r0);
         AS_TMEM_WAIT_LD(r1);
-#ifdef AS_X_EARLYP
-        if (half == UNIT / 64 - 1) { fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&p_full[b]); }
-#endif
         uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
         uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
         const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
@@ -975,16 +984,20 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             }
           }
         }
-        // G^T over S^T columns already consumed (cols [32 half, 32 half + 32))
+        // G^T over S^T columns already consumed (cols [32 half, 32 half + 32)),
+        // then this half's dW MMA may start
         AS_TMEM_ST32(tl + b * UNIT + half * 32, pk);
+        tmem_wait_st();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[PH * b + half]);
       }
       TRACE(1, threadIdx.x == 0, 8, v);
-      tmem_wait_st();
-#endif
+#else
       fence_before();
       __syncwarp();
-#ifndef AS_X_EARLYP
-      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (lane == 0)
+        for (int hf = 0; hf < PH; ++hf) mbar_arrive(&p_full[PH * b + hf]);
 #endif
       TRACE(1, threadIdx.x == 0, 9, v);
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
