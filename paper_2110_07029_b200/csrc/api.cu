@@ -266,7 +266,6 @@ inline void ph_end(as_ctx *x, int ph, cudaStream_t s = nullptr) {
   x->pending.push_back({ph, x->ph_start[ph], e});
 }
 // kernels launched by the transpose of a key space with `bits` bits
-inline int n_transpose_launches(int bits) { return 6 + 3 * ((bits + as::kSortBits - 1) / as::kSortBits); }
 
 #define AS_GUARD(x)                                                               \
   do {                                                                            \

@@ -17,15 +17,11 @@ struct StepDesc {
   int32_t nlab;    // labels in the batch
   int32_t U;       // unique features (feature segments)
   int32_t V;       // unique labels (label segments)
-  int32_t n_long;  // long feature segments queued for the block path
+  int32_t n_long;  // (unused, kept for the descriptor layout)
   int32_t err;     // device-side validation error (0 = ok)
   int32_t pad;
 };
 
-constexpr int kLongSeg = 64;     // feature segments longer than this use a block
-constexpr int kScanTile = 4096;  // elements per block in the device scan
-constexpr int kSortTile = 4096;  // elements per block in the radix sort
-constexpr int kSortBits = 8;     // radix digit width
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -96,24 +92,11 @@ void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_
                          int64_t *row_ptr, int32_t *col, float *val, int64_t *lab_ptr,
                          int32_t *lab, int64_t *ids, int32_t *rid, int32_t *lrid, StepDesc *desc,
                          int nnz_cap, int lab_cap);
-// batch transposes (step a3)
-void launch_transpose(cudaStream_t s, const int64_t *ptr, const int32_t *key, int rows,
-                      const int *n_dev, int cap, int key_bits, uint32_t *k0, uint32_t *v0,
-                      uint32_t *k1, uint32_t *v1, uint32_t *hist, int32_t *rowid, int32_t *flags,
-                      int32_t *scan_tmp, int32_t *seg_id, int32_t *seg_ptr, int32_t *seg_row,
-                      int *nseg_dev, const float *val_in, float *seg_val, int32_t *seg_of);
 void launch_entry_rows(cudaStream_t s, const int64_t *row_ptr, const int64_t *lab_ptr, int rows,
                        int32_t *rid, int32_t *lrid);
 void launch_transposes(cudaStream_t s, const TrArgs &a);
 void launch_fill_int4(cudaStream_t s, int4 *p, long long n, int x, int y, int z, int w);
-void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss);
 void launch_tr_reset(cudaStream_t s, const TrArgs &a, int num_sms);
-void launch_class_map(cudaStream_t s, const int32_t *lseg_id, const int *V_dev, int cap,
-                      int32_t *cls_seg, int value_is_index);
-// SpMM forward (step a4)
-void launch_spmm(cudaStream_t s, int h, const StepDesc *desc, int bpad, const int64_t *row_ptr,
-                 const int32_t *col, const float *val, const float *W1, const float *b1, float *Hf,
-                 __nv_bfloat16 *Hb);
 // load-balanced chunked segmented gather-reduce (kernels_segmm.cu)
 void launch_spmm_chunked(cudaStream_t s, int h, int num_sms, const StepDesc *desc, int bpad, int nnz_cap,
                          const int64_t *row_ptr, const int32_t *col, const float *val,
@@ -150,10 +133,6 @@ void launch_colsum_sgd(cudaStream_t s, const StepDesc *desc, int n_rows_cap, int
                        const float *X, long long ldx, float *param, float lr, float *grad_out);
 void launch_sgd_dense(cudaStream_t s, long long n, float *param, const float *grad, float lr,
                       __nv_bfloat16 *shadow);
-// first-layer gradient + SGD (step a7)
-void launch_dw1_sgd(cudaStream_t s, int h, StepDesc *desc, int cap, const int32_t *seg_id,
-                    const int32_t *seg_ptr, const int32_t *seg_row, const float *seg_val,
-                    const float *dA, float *W1, float lr, int32_t *long_list, float *dbg_dW1);
 void launch_loss_mean(cudaStream_t s, const StepDesc *desc, const float *lossr, float *loss);
 // merge (steps a9-a13)
 void launch_sumsq(cudaStream_t s, const float *w, long long P, double *partials, int nblocks,
@@ -197,8 +176,5 @@ void launch_out_bwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
                        const float *lsep, const int4 *cls_lab, const uint32_t *lbits, int lbw,
                        const float *wrow, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
                        float *dbg_dW2T, float *dbg_db2);
-// per label entry of the label-sorted batch: lw[u] = 1 / (k_r B), r = lrow[u]  (R3)
-void launch_label_weights(cudaStream_t s, const StepDesc *desc, int cap, const int32_t *lrow,
-                          const int64_t *lab_ptr, float *lw);
 
 }  // namespace as

@@ -14,8 +14,8 @@
 //               segment-of-entry / label weight 1/(k_r B) arrays
 //
 // The dense per-key state (counts, bitmaps, class->segment map, scan tiles) is
-// returned to its idle value by k_step_tail at the end of the step, touching
-// only the keys of the batch.  Integer-only and bit-exact (pinned against a
+// returned to its idle value by k_tr_reset on the side stream after the
+// step's last reader, touching only the keys of the batch.  Integer-only and bit-exact (pinned against a
 // brute-force rebuild in tests/test_gpu_parity.py::test_transposes_bit_exact).
 #include "common.cuh"
 
@@ -217,47 +217,6 @@ void launch_transposes(cudaStream_t s, const TrArgs &a) {
   k_tr_place<<<ent, 256, 0, s>>>(a);
 }
 
-// End of the step: loss = mean of the per-row losses (block 0), and the dense
-// transpose state of this batch's keys back to idle (counts 0, bitmaps 0,
-// class->segment map -1, scan tiles 0, ticket 0).
-__global__ void __launch_bounds__(256) k_step_tail(TrArgs a, const float *__restrict__ lossr,
-                                                   float *__restrict__ loss) {
-  griddep_wait();
-  const StepDesc *d = a.desc;
-  if (blockIdx.x == 0) {
-    __shared__ float red[8];
-    float v = 0.f;
-    for (int r = threadIdx.x; r < d->rows; r += 256) v += lossr[r];
-    v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float t = 0.f;
-      for (int i = 0; i < 8; ++i) t += red[i];
-      *loss = t / (float)d->rows;
-      *a.ticket = 0;
-    }
-  }
-  const int nnz = min(d->nnz, a.nnz_cap), nlab = min(d->nlab, a.lab_cap);
-  const int tiles = ceil_div_dev(a.d, kTrTile) + ceil_div_dev(a.C, kTrTile);
-  const int stride = gridDim.x * blockDim.x;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nnz + nlab || t < tiles; t += stride) {
-    if (t < tiles) a.tile_state[t] = 0ull;
-    if (t < nnz) {
-      const int f = a.col[t], r = a.rid[t];
-      a.fcnt[f] = 0;
-      a.fbits[(size_t)f * a.W + (r >> 5)] = 0u;
-    } else if (t - nnz < nlab) {
-      const int j = t - nnz;
-      const int c = a.lab[j], r = a.lrid[j];
-      a.lcnt[c] = 0;
-      a.cls_seg[c] = -1;
-      a.cls_lab[c] = make_int4(0, 0, 0x7fffffff, 0);
-      a.lbits[(size_t)c * a.W + (r >> 5)] = 0u;
-    }
-  }
-}
-
 // The dense per-key transpose state back to idle on the SIDE stream after the
 // step's last reader (dW1), keyed by the step's own segment lists (fseg_id /
 // lseg_id, whole bitmaps) so it does not read the batch arrays the main
@@ -292,9 +251,6 @@ void launch_tr_reset(cudaStream_t s, const TrArgs &a, int num_sms) {
   k_tr_reset<<<2 * num_sms, 256, 0, s>>>(a);
 }
 
-void launch_step_tail(cudaStream_t s, const TrArgs &a, int num_sms, const float *lossr, float *loss) {
-  launch_pdl(k_step_tail, dim3(2 * num_sms), dim3(256), 0, s, a, lossr, loss);
-}
 
 }  // namespace as
 
