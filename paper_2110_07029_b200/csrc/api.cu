@@ -101,6 +101,9 @@ struct as_ctx {
   ncclComm_t comm;
   // side stream for the batch transposes (overlap with SpMM / pass 1)
   cudaStream_t side;
+  cudaStream_t comm_s;          // partitioned merge: chunked all-reduce stream
+  cudaEvent_t ev_mg[3];
+  int merge_chunks;             // ADASGD_MERGE_CHUNKS (0 = default)
   cudaEvent_t ev_fork, ev_join, ev_tail, ev_lab;
   // live profiling (as_profile)
   bool prof_on;
@@ -397,6 +400,10 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_tail, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_lab, cudaEventDisableTiming), "event");
+  if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->comm_s, cudaStreamNonBlocking, prio_hi), "comm stream");
+  for (int i = 0; i < 3 && !rc; ++i)
+    rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_mg[i], cudaEventDisableTiming), "event");
+  if (const char *mc = getenv("ADASGD_MERGE_CHUNKS")) x->merge_chunks = atoi(mc) > 0 ? atoi(mc) : 0;
   // pinned double-buffered staging for host batches
   x->pin_bytes = 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
   for (int i = 0; i < 2 && !rc; ++i) {
@@ -437,6 +444,9 @@ int as_destroy(as_ctx *x) {
   if (x->ev_join) cudaEventDestroy(x->ev_join);
   if (x->ev_tail) cudaEventDestroy(x->ev_tail);
   if (x->ev_lab) cudaEventDestroy(x->ev_lab);
+  for (int i = 0; i < 3; ++i)
+    if (x->ev_mg[i]) cudaEventDestroy(x->ev_mg[i]);
+  if (x->comm_s) { cudaStreamSynchronize(x->comm_s); cudaStreamDestroy(x->comm_s); }
   for (auto &p : x->pending) { x->ev_pool.push_back(p.a); x->ev_pool.push_back(p.b); }
   for (auto e : x->ev_pool) cudaEventDestroy(e);
   free(x->plan);
@@ -795,25 +805,57 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   // alpha = b / sum(b) = 1 exactly (Alg. 2 line 3, no perturbation, R14),
   // so there is nothing to scale unless a caller-forced alpha differs.
   const float a_me = (float)alpha[x->cfg.rank];
+  const long long w2_off = D.d * D.h + D.h, w2_len = D.C * D.h;
+  // Partitioned merge ("multi-stream" transfer
+  // overlapping the combine): the all-reduce runs chunk by chunk on the
+  // communication stream and the momentum kernel of chunk c runs on the main
+  // stream as soon as chunk c is reduced, overlapping the reduction of c+1.
+  // ADASGD_MERGE_CHUNKS=k forces k chunks (also at N = 1, without a reduction:
+  // tests the chunk bookkeeping on one GPU); default 8 for N > 1, 1 at N = 1.
+  const int K = x->merge_chunks > 0 ? x->merge_chunks : (N > 1 ? 8 : 1);
+  ncclRedOp_t premul = ncclSum;
+  bool have_premul = false;
   if (N > 1) {
-    ncclRedOp_t premul;
     float a_host = a_me;
-    ncclResult_t r = ncclRedOpCreatePreMulSum(&premul, &a_host, ncclFloat, ncclScalarHostImmediate, x->comm);
-    if (r == ncclSuccess) {
-      r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
-      ncclRedOpDestroy(premul, x->comm);
-    } else {
+    have_premul = ncclRedOpCreatePreMulSum(&premul, &a_host, ncclFloat, ncclScalarHostImmediate, x->comm) ==
+                  ncclSuccess;
+    if (!have_premul) {
       x->launches += 1;
       as::launch_scale(s, x->w, D.P, a_me);
-      r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, ncclSum, x->comm, s);
+      premul = ncclSum;
     }
-    if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
   } else if (a_me != 1.0f) {
     x->launches += 1;
     as::launch_scale(s, x->w, D.P, a_me);
   }
-  as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, D.d * D.h + D.h,
-                      D.C * D.h, x->w2b);
+  if (K == 1) {
+    if (N > 1) {
+      const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
+      if (have_premul) ncclRedOpDestroy(premul, x->comm);
+      if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
+    }
+    as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, w2_off, w2_len, x->w2b);
+  } else {
+    cudaEventRecord(x->ev_mg[0], s);          // training, norms and any prescale are done
+    cudaStreamWaitEvent(x->comm_s, x->ev_mg[0], 0);
+    x->launches += K - 1;
+    for (int c = 0; c < K; ++c) {
+      const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
+      if (N > 1) {
+        const ncclResult_t r = ncclAllReduce(x->w + off, x->w + off, len, ncclFloat, premul, x->comm, x->comm_s);
+        if (r != ncclSuccess) {
+          if (have_premul) ncclRedOpDestroy(premul, x->comm);
+          x->sticky = AS_E_NCCL;
+          return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+        }
+      }
+      cudaEventRecord(x->ev_mg[1 + (c & 1)], x->comm_s);
+      cudaStreamWaitEvent(s, x->ev_mg[1 + (c & 1)], 0);
+      as::launch_momentum(s, x->w + off, x->wbarp + off, x->wbar + off, len, (float)x->cfg.gamma, w2_off - off,
+                          w2_len, x->w2b);
+    }
+    if (have_premul) ncclRedOpDestroy(premul, x->comm);
+  }
   std::swap(x->wbar, x->wbarp);
   ph_end(x, AS_PH_MERGE);
   rc = cuda_check(x, cudaSuccess, "merge launch");

@@ -402,11 +402,16 @@ def test_end_to_end_tiny_two_replicas_replay(gpu_lib):
     assert_close("wbar after 4 merges", reps[0].get_params(1), owbar, 1e-4)
 
 
-def test_rank_api_world1_matches_oracle(gpu_lib):
+@pytest.mark.parametrize("chunks", [None, "7"])
+def test_rank_api_world1_matches_oracle(gpu_lib, chunks, monkeypatch):
     """The per-rank public path bench.py times (driver.run_rank: resident
     dataset, stream batches, as_merge with its N = 1 shortcut) against the
     oracle's whole run at N = 1: alpha = [1] every merge (Alg. 2 line 3, R14),
-    momentum gamma = 0.9 across 4 merges, global model within 1e-4 (fp32)."""
+    momentum gamma = 0.9 across 4 merges, global model within 1e-4 (fp32).
+    chunks="7": the partitioned merge's chunk bookkeeping (7 uneven chunks, the
+    W2T shadow range crossing chunk borders) forced on one GPU."""
+    if chunks:
+        monkeypatch.setenv("ADASGD_MERGE_CHUNKS", chunks)
     from paper_2110_07029_b200 import driver
     from paper_2110_07029_b200.api import Replica
     cfg = synthgen.CONFIGS["tiny"]
