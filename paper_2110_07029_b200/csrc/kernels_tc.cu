@@ -721,6 +721,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   const int NT = NB * NU;                         // units of this CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = 12, kMmaWarp = 13;   // highest ids: scheduler priority
+#ifdef AS_X_SWAPROLES
+  constexpr int kSoftLo = 4, kUpdLo = 0;         // softmax warps above the update warps
+#else
+  constexpr int kSoftLo = 0, kUpdLo = 8;
+#endif
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSH; ++i) { mbar_init(&h_full[i], 1); mbar_init(&h_empty[i], 1); }
@@ -845,9 +850,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         advance(cd);
       }
     }
-  } else if (warp < 8) {  // ---------------- softmax warpgroups (units gu % 2 == g)
+  } else if (warp >= kSoftLo && warp < kSoftLo + 8) {  // ---------------- softmax warpgroups (units gu % 2 == g)
     AS_REG_INC2();
-    const int g = warp >> 2;
+    const int g = (warp - kSoftLo) >> 2;
     const int q = warp & 3;
     const int i = q * 32 + lane;              // class inside the block (TMEM lane)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
@@ -859,7 +864,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     //     transpose) one block ahead, slot = block parity;
     //   * the class's label-row bitmap of a unit (k_tr_mark; bit r = row r
     //     has label i) one unit ahead, slot = WG unit parity.
-    const int tix = threadIdx.x;              // 0..255
+    const int tix = threadIdx.x - kSoftLo * 32;  // 0..255
     auto cls_ok = [&](int kb_) {
       return kb_ < NB && (blockIdx.x + kb_ * gridDim.x) * BM + i < C;
     };
@@ -906,6 +911,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         cp_async_commit();
       }
       const int b = sb;
+      TRACE(1, tix == 0, 18, v);
       // the next unit of this WG: its class's row bitmap one unit ahead
       {
         int vn = v + 2, kbn = kb;
@@ -918,9 +924,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         pf_mask(kbn, vn, hn, (jj + 1) & 1);
         cp_async_commit();
       }
-      TRACE(1, threadIdx.x == 0, 6, v);
+      TRACE(1, tix == 0, 6, v);
       mbar_wait(&s_full[b], sph);
-      TRACE(1, threadIdx.x == 0, 7, v);
+      TRACE(1, tix == 0, 7, v);
       fence_after();
       cp_async_wait<1>();                     // this unit's bitmap (all but the newest group)
       uint32_t mk[4];
@@ -1008,17 +1014,17 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[PH * b + half]);
       }
-      TRACE(1, threadIdx.x == 0, 8, v);
+      TRACE(1, tix == 0, 8, v);
 #else
       fence_before();
       __syncwarp();
       if (lane == 0)
         for (int hf = 0; hf < PH; ++hf) mbar_arrive(&p_full[PH * b + hf]);
 #endif
-      TRACE(1, threadIdx.x == 0, 9, v);
+      TRACE(1, tix == 0, 9, v);
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
         if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
-        TRACE(1, threadIdx.x == 0, 16, v);
+        TRACE(1, tix == 0, 16, v);
         sDB[g * BM + i] = db2;
         if (NU == 1) sDB[(1 - g) * BM + i] = 0.f;   // one unit per block: the other WG has none
         __syncwarp();
@@ -1027,6 +1033,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           if (NU == 1) mbar_arrive(db_full);
         }
       }
+      TRACE(1, tix == 0, 17, v);
       v += 2;                                 // next unit of this WG
       while (v >= NU) { v -= NU; ++kb; }
       lst += 2 / HPT;                         // its H stage
@@ -1034,10 +1041,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       sb += 2;
       if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
     }
-  } else if (warp < 12) {  // ---------------- update warps
+  } else if (warp >= kUpdLo && warp < kUpdLo + 4) {  // ---------------- update warps
     const int q = warp & 3;
     const int i = q * 32 + lane;              // thread = class (TMEM lane)
-    const int ut = threadIdx.x - 256;         // 0..127
+    const int ut = threadIdx.x - kUpdLo * 32;  // 0..127
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     constexpr int NCH = H / 32;               // 32-column chunks of dW2T
     const int sub = lane >> 3, hq = (lane & 7) * 4;
