@@ -343,8 +343,13 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   uint64_t *bars = (uint64_t *)(sBmax + 16);
   // p_full[2 b + half]: P of classes [64 half, 64 half + 64) of the block in S
   // buffer b is in TMEM; the O MMA of that half starts without the other
+#ifdef AS_X_P1Q
+  constexpr int PQ = 4;                             // P signalled per 32-class quarter
+#else
+  constexpr int PQ = 2;                             // P signalled per 64-class half
+#endif
   uint64_t *h_full = bars, *w_full = bars + 1, *w_empty = w_full + NST, *s_full = w_empty + NST,
-           *p_full = s_full + 2, *o_fin = p_full + 4, *o_done = o_fin + 1;
+           *p_full = s_full + 2, *o_fin = p_full + 2 * PQ, *o_done = o_fin + 1;
   uint32_t *tmem_slot = (uint32_t *)(o_done + 1);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
 
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     mbar_init(h_full, 1);
     for (int i = 0; i < NST; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);
+    for (int i = 0; i < 2 * PQ; ++i) mbar_init(&p_full[i], 4);
     mbar_init(o_fin, 1);
     mbar_init(o_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -423,19 +428,22 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       for (int j = 0; j < nloc; ++j) {
         const int st = j % NST, b = j & 1;
         const int g = NWG == 2 ? b : 0;
-        mbar_wait(&p_full[2 * b], (j >> 1) & 1);
-        fence_after();
+        // the O MMA part by part (64 or 32 classes of P) as the softmax finishes them
+#pragma unroll
+        for (int pq = 0; pq < PQ; ++pq) {
+          mbar_wait(&p_full[PQ * b + pq], (j >> 1) & 1);
+          fence_after();
 #ifndef AS_X_NOMMA2
-        // classes 0-63 of the block (P columns 0-31) while the softmax finishes 64-127
-        mma_grp_ts_mn_4(tmem + 2 * BM + g * BM, tmem + b * BM, sdesc(aW + st * TILE, ATOM_BYTES, 1024),
-                        idO, j >= NWG ? 1u : 0u);
+          if constexpr (PQ == 2)
+            mma_grp_ts_mn_4(tmem + 2 * BM + g * BM, tmem + b * BM + 32 * pq,
+                            sdesc(aW + st * TILE + pq * 64 * 128, ATOM_BYTES, 1024), idO,
+                            (j >= NWG || pq > 0) ? 1u : 0u);
+          else
+            mma_grp_ts_mn_2(tmem + 2 * BM + g * BM, tmem + b * BM + 16 * pq,
+                            sdesc(aW + st * TILE + pq * 32 * 128, ATOM_BYTES, 1024), idO,
+                            (j >= NWG || pq > 0) ? 1u : 0u);
 #endif
-        mbar_wait(&p_full[2 * b + 1], (j >> 1) & 1);
-        fence_after();
-#ifndef AS_X_NOMMA2
-        mma_grp_ts_mn_4(tmem + 2 * BM + g * BM, tmem + b * BM + 32,
-                        sdesc(aW + st * TILE + 64 * 128, ATOM_BYTES, 1024), idO, 1u);
-#endif
+        }
         mma_commit_w(&w_empty[st]);
         if (NWG == 1) mma_commit_w(o_done);     // single WG: O_{j} before the rescale at j+1
         if (j + 2 < nloc) issue_S(j + 2);
@@ -546,11 +554,11 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
           pk[u] = pack_bf16x2(p0, p1);
         }
         AS_TMEM_ST16(tS + ch * 16, pk);
-        if (ch & 1) {                          // classes [64 (ch/2), +64) of P are in TMEM
+        if (PQ == 4 || (ch & 1)) {             // this part of P is in TMEM
           tmem_wait_st();
           fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[2 * b + (ch >> 1)]);
+          if (lane == 0) mbar_arrive(&p_full[PQ * b + (PQ == 4 ? ch : (ch >> 1))]);
         }
       }
       acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
@@ -560,7 +568,8 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 #else
       fence_before();
       __syncwarp();
-      if (lane == 0) { mbar_arrive(&p_full[2 * b]); mbar_arrive(&p_full[2 * b + 1]); }
+      if (lane == 0)
+        for (int pq = 0; pq < PQ; ++pq) mbar_arrive(&p_full[PQ * b + pq]);
 #endif
     }
     // epilogue: ONE partial slot per CTA split.  With two warpgroups, WG 1
