@@ -364,7 +364,10 @@ static void seg_bulk_launch(cudaStream_t s, int num_sms, const int *n_dev, const
     cudaFuncSetAttribute(k_seg_bulk<H, MODE, PtrT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  launch_pdl(k_seg_bulk<H, MODE, PtrT>, dim3(num_sms), dim3(Cfg::NW * 32), Cfg::SMEM, s, n_dev, nseg_dev,
+#ifndef AS_SEG_CPS
+#define AS_SEG_CPS 1                            // CTAs per SM (experiment override)
+#endif
+  launch_pdl(k_seg_bulk<H, MODE, PtrT>, dim3(num_sms * AS_SEG_CPS), dim3(Cfg::NW * 32), Cfg::SMEM, s, n_dev, nseg_dev,
              nseg_pad, seg_of, seg_ptr, gidx, scale, src, part, arrive, a);
 }
 
