@@ -494,6 +494,37 @@ def test_full_size_amazon670k_sampled(gpu_lib):
     assert_close("dW1", dW1, ref["dW1"][keys], tol)
 
 
+@pytest.mark.slow
+def test_full_size_amazon670k_top1_sampled(gpu_lib):
+    """Top-1 evaluation at the Amazon-670K shape (670 091 classes, 5236 class
+    blocks over the pass-1 splits) on 1024 rows after one training step: 24
+    sampled rows recomputed by the oracle from the updated parameters with the
+    kernel's bf16 operands; argmax equal or a near-tie, hits consistent."""
+    cfg = synthgen.CONFIGS["amazon670k"]
+    ds = synthgen.make_dataset(cfg, n=20_000)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    rep = _replica(cfg, p, ds, "bf16", lr=0.5, debug=False)
+    rep.upload_dataset(ds)
+    rep.load_batch_stream(0, 1024)
+    rep.train_step(False)
+    ev = ds.rows(np.arange(5000, 6024))
+    top, hits = rep.eval_top1(1024, ev.row_ptr, ev.col, ev.val, ev.lab_ptr, ev.lab)
+    assert top.shape == (1024,) and np.all((top >= 0) & (top < cfg.C))
+    new = otrain.unpack(rep.get_params(), cfg.d, cfg.C, cfg.h)
+    rows = np.random.default_rng(0).choice(1024, 24, replace=False)
+    sub = ds.rows(5000 + rows)
+    otop, _, zmax, logit = om.top1(sub, new, operands="bf16")
+    bad = 0
+    for k, r in enumerate(rows):
+        if top[r] != otop[k]:
+            bad += 1
+            assert zmax[k] - logit(k, int(top[r])) <= 1e-4 * (1.0 + abs(zmax[k])), r
+    assert bad <= 2
+    lab = [set(ev.lab[ev.lab_ptr[r]:ev.lab_ptr[r + 1]].tolist()) for r in range(1024)]
+    assert hits == sum(int(top[r] in lab[r]) for r in range(1024))
+    rep.close()
+
+
 # ---------------------------------------------------------------- top-1 evaluation (NEXT f1)
 TOP1_CASES = [
     (2000, 1000, 128, 600, 200, 256),     # ragged row tile, C % 128 = 104
