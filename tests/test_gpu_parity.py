@@ -589,3 +589,57 @@ def test_eval_top1_ties_lowest_class_across_splits(gpu_lib, precision):
     otop, ohits, _, _ = om.top1(sub, otrain.unpack(p, d, C, h))
     assert np.all(otop == 5) and hits == ohits
     rep.close()
+
+
+def _strip_features(sub, empty_rows):
+    """The batch with the features of `empty_rows` removed (rows with no
+    non-zero feature: H = ReLU(b1), no dW1 contribution)."""
+    keep_rp, cols, vals = [0], [], []
+    for r in range(len(sub.row_ptr) - 1):
+        s, e = sub.row_ptr[r], sub.row_ptr[r + 1]
+        if r not in empty_rows:
+            cols.append(sub.col[s:e]); vals.append(sub.val[s:e])
+        keep_rp.append(keep_rp[-1] + (0 if r in empty_rows else e - s))
+    col = np.concatenate(cols) if cols else np.zeros(0, np.int32)
+    val = np.concatenate(vals) if vals else np.zeros(0, np.float32)
+    return synthgen.CSRDataset(sub.d, sub.C, np.asarray(keep_rp, np.int64), col.astype(np.int32),
+                               val.astype(np.float32), sub.lab_ptr.copy(), sub.lab.copy())
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 2e-2)])
+@pytest.mark.parametrize("which", ["some", "all"])
+def test_empty_feature_rows(gpu_lib, precision, tol, which):
+    """Degenerate rows with no features (first, last, consecutive ones) and a
+    batch with no features at all (nnz = 0: empty SpMM / transposes / dW1):
+    one step against the oracle; W1 untouched when nnz = 0."""
+    d, C, h, B = 2000, 1500, 128, 200
+    cfg = _cfg(d, C, h, 400, 256, seed=9)
+    ds = synthgen.make_dataset(cfg, n=400)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, precision, lr=0.5)
+    sub0 = ds.rows(np.arange(B))
+    empty = set(range(B)) if which == "all" else {0, 1, 2, 77, 78, B - 1}
+    sub = _strip_features(sub0, empty)
+    rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    loss = rep.train_step(want_loss=True)
+    prm = otrain.unpack(p, d, C, h)
+    ref = om.gradients_chunked(sub, prm, chunk=64)
+    H = _f32(rep.debug_get(0, 4 * B * h)).reshape(B, h)
+    assert_close("H", H, ref["H"], 1e-5)
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    assert_close("dA", _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h), ref["dA"], tol)
+    assert_close("dW2T", _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h), ref["dW2T"], tol)
+    new = rep.get_params()
+    dnew = otrain.unpack(new.astype(np.float64) - p.astype(np.float64), d, C, h)
+    keys = np.unique(sub.col)
+    if len(keys):
+        assert_close("W1 update", dnew["W1"][keys], -0.5 * ref["dW1"][keys], max(tol, 1e-3))
+    untouched = np.setdiff1d(np.arange(d), keys)
+    assert np.all(dnew["W1"][untouched] == 0)
+    # the next step on a normal batch still matches (transpose state back to idle)
+    nxt = ds.rows(np.arange(B) + 200)
+    rep.load_batch_csr(B, nxt.row_ptr, nxt.col, nxt.val, nxt.lab_ptr, nxt.lab)
+    loss2 = rep.train_step(want_loss=True)
+    ref2 = om.gradients_chunked(nxt, otrain.unpack(new, d, C, h), chunk=64)
+    assert abs(loss2 - ref2["loss"]) <= tol * abs(ref2["loss"])
+    rep.close()
