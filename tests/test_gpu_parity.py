@@ -643,3 +643,24 @@ def test_empty_feature_rows(gpu_lib, precision, tol, which):
     ref2 = om.gradients_chunked(nxt, otrain.unpack(new, d, C, h), chunk=64)
     assert abs(loss2 - ref2["loss"]) <= tol * abs(ref2["loss"])
     rep.close()
+
+
+@pytest.mark.parametrize("h,C,avg_labels", [(128, 300, 40.0), (256, 200, 25.0), (128, 5000, 75.0)])
+def test_label_heavy_batches(gpu_lib, h, C, avg_labels):
+    """Delicious-like label density (tens of labels per row, Zipf-hot classes
+    labelled in most rows): the pass-2 label term from the row bitmaps and the
+    per-row weights, against the oracle (bf16 bar)."""
+    d, B = 3000, 256
+    cfg = _cfg(d, C, h, 300, 256, avg_labels=avg_labels, seed=21)
+    ds = synthgen.make_dataset(cfg, n=300)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, "bf16", lr=0.5)
+    sub = ds.rows(np.arange(B))
+    rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    loss = rep.train_step(want_loss=True)
+    ref = om.gradients_chunked(sub, otrain.unpack(p, d, C, h), chunk=64)
+    assert abs(loss - ref["loss"]) <= 2e-2 * abs(ref["loss"])
+    assert_close("dW2T", _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h), ref["dW2T"], 2e-2)
+    assert_close("db2", _f32(rep.debug_get(6, 4 * C)), ref["db2"], 2e-2)
+    assert_close("dA", _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h), ref["dA"], 2e-2)
+    rep.close()
