@@ -247,13 +247,21 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   __shared__ int last;
   if (threadIdx.x == 0) last = atomicAdd(&db1cnt[blockIdx.y], 1) == nrb - 1;
   __syncthreads();
-  if (last && threadIdx.x < 16) {
+  if (last) {
+    // every partial in flight at once: warp jy sums columns 2 jy, 2 jy + 1 over
+    // the row blocks (lane k takes blocks k, k + 32, ...; fixed xor tree)
     __threadfence();
-    const int c = blockIdx.y * 16 + threadIdx.x;
-    float g = 0.f;
-    for (int k = 0; k < nrb; ++k) g += __ldcg(db1p + (size_t)k * h + c);
-    b1[c] -= lr * g;
-    if (dbg_db1) dbg_db1[c] = g;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int c = blockIdx.y * 16 + 2 * jy + cc;
+      float g = 0.f;
+      for (int k = rx; k < nrb; k += 32) g += __ldcg(db1p + (size_t)k * h + c);
+      g = warp_sum(g);
+      if (rx == 0) {
+        b1[c] -= lr * g;
+        if (dbg_db1) dbg_db1[c] = g;
+      }
+    }
     if (threadIdx.x == 0) db1cnt[blockIdx.y] = 0;
   }
   if (jy == 0 && live && blockIdx.y == 0) {
