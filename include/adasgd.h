@@ -320,6 +320,22 @@ int as_sched_alg1(int32_t N, const int32_t *u, const int32_t *b, int32_t beta,
                   int32_t b_min, int32_t b_max, double lr0, int32_t *b_out,
                   float *lr_out);
 
+/* Adaptive scaling frequency ("By default, the algorithm is executed
+ * after every mega-batch. However, if stability is achieved or the system
+ * enters an oscillatory state, the frequency at which scaling is performed
+ * can be increased"), reading R27: the policy sets the INTERVAL,
+ * in mega-batches, between two Alg. 1 runs.  Called after an Alg. 1 run with
+ * its input b_prev[N] and output b_next[N] (host).  dir_state[N] (host,
+ * in/out, caller-owned, zero-initialised) carries the sign of each b_i's
+ * previous change.  Stable (no b_i changed) or oscillatory (some b_i reversed
+ * direction, none kept it): *period_out = min(2 * period, p_max); otherwise
+ * 1.  p_max = 1 is the paper's default (every mega-batch).  AS_E_INVALID on
+ * N < 1, null pointers, p_max < 1 or period outside [1, p_max]; no state
+ * change then. */
+int as_sched_scale_period(int32_t N, const int32_t *b_prev, const int32_t *b_next,
+                          int32_t *dir_state, int32_t period, int32_t p_max,
+                          int32_t *period_out);
+
 /* Alg. 2 lines 1-10 with R13-R16. */
 int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b,
                   const double *norms, double delta, double pert_thr,

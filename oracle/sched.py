@@ -109,6 +109,36 @@ def alg1(u, b, beta, b_min, b_max, lr0):
     return b_new, lr_new
 
 
+
+# --------------------------------------------------------------------------
+# Adaptive scaling frequency ("By default, the algorithm is executed
+# after every mega-batch. However, if stability is achieved or the system
+# enters an oscillatory state, the frequency at which scaling is performed can
+# be increased"), reading R27: the quantity adapted is the interval between
+# Alg. 1 runs, in mega-batches.  Written as the two states the sentence names.
+# --------------------------------------------------------------------------
+def scale_period(b_prev, b_next, dir_prev, period, p_max):
+    """Returns (next interval, this run's direction of each b_i)."""
+    directions = []
+    for before, after in zip(b_prev, b_next):
+        if after > before:
+            directions.append(1)
+        elif after < before:
+            directions.append(-1)
+        else:
+            directions.append(0)
+    # "stability is achieved": Alg. 1 left every batch size where it was
+    stable = all(d == 0 for d in directions)
+    # "an oscillatory state": the batch sizes that move now move back (at
+    # least one reverses its previous change, none continues in its direction)
+    reversing = [d != 0 and p != 0 and d != p for d, p in zip(directions, dir_prev)]
+    continuing = [d != 0 and d == p for d, p in zip(directions, dir_prev)]
+    oscillatory = any(reversing) and not any(continuing)
+    if stable or oscillatory:
+        return min(2 * period, p_max), directions
+    return 1, directions
+
+
 def _f32(x):
     import numpy as np
     return np.float32(x)

@@ -39,6 +39,9 @@ class RunConfig:
     # aggregation, Fig. 2; callers set M = N * b_max): static equal
     # batches, alpha_i = 1/N, no perturbation, no batch scaling
     algo: str = "adaptive"
+    # adaptive scaling frequency (R27): the interval between Alg. 1
+    # runs doubles up to scale_pmax mega-batches; 1 = every mega-batch
+    scale_pmax: int = 1
 
 
 def unpack(p, d, C, h):
@@ -76,6 +79,7 @@ def run(dataset, init, cfg: RunConfig, costs, total_samples, order=None, log_ste
     lr = [float(np.float32(cfg.lr0))] * N
     pos = 0
     records = []
+    period, since, dirs = 1, 0, [0] * N                   # reading R27
     rp = dataset.row_ptr
     while pos < total_samples:
         Mm = min(cfg.M, total_samples - pos)
@@ -102,11 +106,15 @@ def run(dataset, init, cfg: RunConfig, costs, total_samples, order=None, log_ste
             norms, alpha, pert = None, [1.0 / N] * N, False
         b_used, lr_used = list(b), list(lr)
         wbar, wbar_p = omerge.merge(replicas, alpha, wbar, wbar_p, cfg.gamma)
-        if cfg.algo == "adaptive":
+        since += 1
+        if cfg.algo == "adaptive" and since >= period:
             b, lr = osched.alg1(u, b, cfg.beta, cfg.b_min, cfg.b_max, cfg.lr0)
+            period, dirs = osched.scale_period(b_used, b, dirs, period, cfg.scale_pmax)
+            since = 0
         records.append({"log": log, "u": u, "clocks": clocks, "b": b_used, "lr": lr_used,
                         "norms": norms, "alpha": alpha, "perturbed": pert,
                         "b_next": list(b), "lr_next": list(lr), "losses": losses,
+                        "period": period,
                         "wbar": wbar.copy(), "replicas": replicas if log_steps else None})
         pos += Mm
     return records, wbar

@@ -35,6 +35,7 @@ EXPORTS = [
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
     "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
     "as_eval_top1", "as_sched_route_static", "as_sched_alg2_ex", "as_sched_fit_cost",
+    "as_sched_scale_period",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -110,6 +111,7 @@ def load():
         "as_sched_alg1": [I32, P(I32), P(I32), I32, I32, I32, D, P(I32), P(F)],
         "as_sched_alg2": [I32, P(I32), P(I32), P(D), D, D, P(D), P(I32)],
         "as_sched_alg2_ex": [I32, P(I32), P(I32), P(D), D, D, I32, P(D), P(I32)],
+        "as_sched_scale_period": [I32, P(I32), P(I32), P(I32), I32, I32, P(I32)],
         "as_sched_fit_cost": [I64, P(I32), P(I64), P(I64), P(CostModel)],
         "as_sched_permutation": [I64, C.c_uint64, P(I64)],
         "as_live_open": [C.c_char_p, I32, P(VP)],

@@ -125,6 +125,32 @@ int as_sched_alg1(int32_t N, const int32_t *u, const int32_t *b, int32_t beta,
   return AS_OK;
 }
 
+// Adaptive scaling frequency (reading R27).  dir_state[i] holds the
+// sign of the previous run's change of b_i.  This run's signs d_i =
+// sign(b_next_i - b_prev_i); "stability" = every d_i == 0; "oscillatory" =
+// some b_i reversed (d_i * dir_i < 0) and none kept its direction
+// (d_i * dir_i > 0).  In either state the interval doubles (capped at p_max),
+// otherwise it returns to 1 mega-batch; dir_state <- d.
+int as_sched_scale_period(int32_t N, const int32_t *b_prev, const int32_t *b_next,
+                          int32_t *dir_state, int32_t period, int32_t p_max,
+                          int32_t *period_out) {
+  if (N < 1 || !b_prev || !b_next || !dir_state || !period_out || p_max < 1 || period < 1 ||
+      period > p_max)
+    return as_fail(AS_E_INVALID, "as_sched_scale_period: bad arguments");
+  bool moved = false, reversed = false, kept = false;
+  for (int i = 0; i < N; ++i) {
+    const int32_t d = (b_next[i] > b_prev[i]) - (b_next[i] < b_prev[i]);
+    if (d != 0) moved = true;
+    if (d * dir_state[i] < 0) reversed = true;
+    if (d * dir_state[i] > 0) kept = true;
+    dir_state[i] = d;
+  }
+  const bool settle = !moved || (reversed && !kept);
+  const int64_t p2 = 2 * (int64_t)period;
+  *period_out = settle ? (int32_t)(p2 < p_max ? p2 : p_max) : 1;
+  return AS_OK;
+}
+
 // Algorithm 2 "Normalized Model Merging", lines 1-10.
 // R13 exact equality of u; R14 r/s = lexicographic argmax/argmin of (u_i, b_i)
 // with the lowest id on ties, perturbation skipped when (u_r,b_r)==(u_s,b_s);

@@ -25,16 +25,20 @@ def stream_nnz_prefix(row_ptr, n, pos, M, order=None):
 class ReplayState:
     """Host scheduler state shared (identically) by every rank."""
 
-    def __init__(self, world, b_max, b_min, beta, lr0, costs, algo="adaptive"):
+    def __init__(self, world, b_max, b_min, beta, lr0, costs, algo="adaptive", scale_pmax=1):
         """algo: "adaptive" (P:105 dynamic routing + Alg. 1) or a comparison
         method of P:215 ("elastic", "sync": static equal batches, no scaling;
-        the replicas' as_config.algo must match)."""
+        the replicas' as_config.algo must match).  scale_pmax: adaptive
+        scaling frequency (R27) -- Alg. 1 runs every `period`
+        mega-batches, period in [1, scale_pmax] set by as_sched_scale_period;
+        1 = the paper's default (every mega-batch)."""
         self.world, self.b_max, self.b_min, self.beta, self.lr0 = world, b_max, b_min, beta, lr0
         self.algo = algo
         self.costs = [tuple(int(v) for v in (c.c0, c.c_row, c.c_nnz, c.num, c.den)) if hasattr(c, "c0")
                       else tuple(c) for c in costs]
         self.b = [b_max] * world
         self.lr = [float(np.float32(lr0))] * world
+        self.scale_pmax, self.period, self.since, self.dirs = int(scale_pmax), 1, 0, [0] * world
 
     def route(self, row_ptr, n, pos, M, order=None):
         pre = stream_nnz_prefix(row_ptr, n, pos, M, order)
@@ -42,8 +46,11 @@ class ReplayState:
 
     def rescale(self, u):
         b_used = list(self.b)
-        if self.algo == "adaptive":
+        self.since += 1
+        if self.algo == "adaptive" and self.since >= self.period:
             self.b, self.lr = sched.alg1(u, self.b, self.beta, self.b_min, self.b_max, self.lr0)
+            self.period, self.dirs = sched.scale_period(b_used, self.b, self.dirs, self.period, self.scale_pmax)
+            self.since = 0
         return b_used
 
 

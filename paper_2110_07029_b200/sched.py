@@ -42,6 +42,20 @@ def alg1(u, b, beta, b_min, b_max, lr0):
     return bo.tolist(), [float(x) for x in lo]
 
 
+
+def scale_period(b_prev, b_next, dir_state, period, p_max):
+    """as_sched_scale_period (R27): returns (next interval in
+    mega-batches, updated direction state)."""
+    lib = L.load()
+    N = len(b_prev)
+    bp, bn = L.as_np(b_prev, np.int32), L.as_np(b_next, np.int32)
+    ds = np.array(dir_state, np.int32)
+    po = C.c_int32()
+    L.check(lib.as_sched_scale_period(N, L.ptr(bp, C.c_int32), L.ptr(bn, C.c_int32), L.ptr(ds, C.c_int32),
+                                      int(period), int(p_max), C.byref(po)))
+    return po.value, ds.tolist()
+
+
 def alg2(u, b, norms, delta, pert_thr, norm="u"):
     """norm: "u" (Alg. 2 line 5 as printed) or "ub" (the P:175 alternative)."""
     lib = L.load()

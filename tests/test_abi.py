@@ -209,3 +209,54 @@ def test_live_cursor_conserves_samples():
         assert cur.claim(M, 10) == (0, 10)
     finally:
         cur.close()
+
+
+def test_scale_period_golden_cpp():
+    from paper_2110_07029_b200 import sched as psched
+    with open(os.path.join(os.path.dirname(__file__), "golden", "scale_period_cases.json")) as f:
+        cases = json.load(f)["cases"]
+    for case in cases:
+        p, d = psched.scale_period(case["b_prev"], case["b_next"], case["dir"], case["period"], case["p_max"])
+        assert (p, d) == (case["period_out"], case["dir_out"]), case["why"]
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.integers(1, 6), st.data())
+def test_scale_period_bit_exact_vs_oracle(N, data):
+    from paper_2110_07029_b200 import sched as psched
+    bp = [data.draw(st.integers(8, 64)) for _ in range(N)]
+    bn = [x + data.draw(st.integers(-3, 3)) for x in bp]
+    dirs = [data.draw(st.integers(-1, 1)) for _ in range(N)]
+    p_max = data.draw(st.integers(1, 16))
+    period = data.draw(st.integers(1, p_max))
+    assert psched.scale_period(bp, bn, dirs, period, p_max) == osched.scale_period(bp, bn, dirs, period, p_max)
+
+
+def test_scale_period_validation_no_state_change():
+    lib = L.load()
+    b = np.array([8, 8], np.int32)
+    d = np.array([1, -1], np.int32)
+    out = C.c_int32(77)
+    for period, p_max in ((0, 4), (5, 4), (1, 0)):
+        assert lib.as_sched_scale_period(2, L.ptr(b, C.c_int32), L.ptr(b, C.c_int32), L.ptr(d, C.c_int32),
+                                         period, p_max, C.byref(out)) == L.AS_E_INVALID
+    assert d.tolist() == [1, -1] and out.value == 77
+
+
+def test_replay_state_scaling_period_vs_oracle():
+    """driver.ReplayState with scale_pmax (host logic through the C-ABI) follows
+    the oracle's mega-batch loop (oracle/train.py, R27) on a scripted u
+    sequence: converging, oscillating, then stable."""
+    from paper_2110_07029_b200 import driver
+    us = [[6, 2], [5, 3], [3, 5], [5, 3], [3, 5], [4, 4], [4, 4], [4, 4], [6, 2], [4, 4]]
+    st_ = driver.ReplayState(2, 64, 8, 4, 0.1, [(0, 1, 0, 1, 1)] * 2, scale_pmax=4)
+    b, lr, period, since, dirs = [64, 64], None, 1, 0, [0, 0]
+    for u in us:
+        used = st_.rescale(u)
+        assert used == b
+        since += 1
+        if since >= period:
+            nb, lr = osched.alg1(u, b, 4, 8, 64, 0.1)
+            period, dirs = osched.scale_period(b, nb, dirs, period, 4)
+            b, since = nb, 0
+        assert (st_.b, st_.period) == (b, period)

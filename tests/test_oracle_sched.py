@@ -180,3 +180,26 @@ def test_fit_cost_recovers_integer_model():
     t = 2_000_000 + 40_000 * rows + 500 * nnz
     assert osched.fit_cost(rows, nnz, t) == (2_000_000, 40_000, 500, 1, 1)
     assert osched.fit_cost(rows, nnz, t + rng.uniform(-0.4, 0.4, 40)) == (2_000_000, 40_000, 500, 1, 1)
+
+
+def test_scale_period_golden():
+    for case in _load("scale_period_cases.json")["cases"]:
+        p, d = osched.scale_period(case["b_prev"], case["b_next"], case["dir"], case["period"], case["p_max"])
+        assert (p, d) == (case["period_out"], case["dir_out"]), case["why"]
+
+
+def test_scale_period_equal_speeds_doubles_interval():
+    """Equal speeds (P:105 replay with one cost model): every GPU gets the same
+    number of batches, Alg. 1 is a no-op (stable), so with R27 Alg. 1 runs
+    after mega-batches 1, 3, 7 (interval 1, 2, 4) and the interval saturates
+    at p_max; the trajectory of b is the default's (b_max throughout)."""
+    from oracle import train as otrain
+    cfg_x = synthgen.XMLConfig("sp", 300, 40, 60, 6.0, 2.0, 32, 16, 1, 5)
+    ds = synthgen.make_dataset(cfg_x, n=200)
+    p0 = synthgen.make_init_params(cfg_x.d, cfg_x.C, cfg_x.h, 3)
+    costs = [synthgen.CostModel(c0=0, c_row=10, c_nnz=0, num=1, den=1)] * 2
+    rc = otrain.RunConfig(cfg_x.d, cfg_x.C, cfg_x.h, b_max=16, b_min=2, beta=1, M=64, lr0=0.1,
+                          world=2, scale_pmax=4)
+    recs, _ = otrain.run(ds, p0, rc, costs, 64 * 9)
+    assert [r["period"] for r in recs] == [2, 2, 4, 4, 4, 4, 4, 4, 4]
+    assert all(r["b_next"] == [16, 16] for r in recs)
