@@ -185,9 +185,14 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // =====================================================================
 // Combine the split-C partials of output pass 1 (online softmax in log2
 // units): LSE_r, loss_r = LSE_r - zsum_r, dH_r = (O_r/l_r - labW_r)/B and
-// dA_r = dH_r * [A_r > 0]  (R3, R4).  One CTA (h threads) per row.  Partial
+// dA_r = dH_r * [A_r > 0]  (R3, R4).  CTA = 32 rows x COMBINE_CW columns.  Partial
 // layout: pm, pl [split][bpad]; pO [split][h][bpad] (coalesced TC epilogue).
 // =====================================================================
+// columns per combine CTA: 16 = 2 per warp (A/B on B200: 8 and 32 slower)
+#ifndef COMBINE_CW
+#define COMBINE_CW 16
+#endif
+static_assert(COMBINE_CW % 8 == 0, "one or more columns per warp");
 __global__ void __launch_bounds__(256) k_combine_bf16(
     const StepDesc *__restrict__ desc, int h, int bpad, int splits, const float *__restrict__ pm,
     const float *__restrict__ pl, const float *__restrict__ pO, const float *__restrict__ labW,
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
     int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1) {
   griddep_wait();
-  // CTA = 32 rows x 16 columns (8 groups of 2); partial reads coalesced over rows
+  // CTA = 32 rows x COMBINE_CW columns (8 warps); partial reads coalesced over rows
   const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
   const int B = desc->rows;
   if (blockIdx.x * 32 >= B) {         // a CTA of padding rows only
@@ -210,37 +215,48 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   extern __shared__ float sc[];             // [splits][32] per-slot scales of the rows
   // every slot loop is unrolled 12-wide so a thread keeps 12 partial loads in
   // flight (the partials are L2-resident right after pass 1)
+  // M_r and l_r: warp jy reduces slots jy, jy + 8, ...; the 8 warp partials
+  // are combined in warp order (max is exact; the sum order is fixed)
+  __shared__ float red[2][8][33];
   float M = -FLT_MAX;
-#pragma unroll 12
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, pm[(size_t)s * bpad + r]);
+  for (int s = jy; s < splits; s += 8) M = fmaxf(M, pm[(size_t)s * bpad + r]);
+  red[0][jy][rx] = M;
+  __syncthreads();
+  M = red[0][0][rx];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) M = fmaxf(M, red[0][k][rx]);
+  float l = 0.f;
   for (int s = jy; s < splits; s += 8) {
     const float ms = pm[(size_t)s * bpad + r];
-    sc[s * 32 + rx] = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
+    const float e = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
+    sc[s * 32 + rx] = e;
+    l = fmaf(pl[(size_t)s * bpad + r], e, l);
   }
+  red[1][jy][rx] = l;
   __syncthreads();
-  float l = 0.f;
-#pragma unroll 12
-  for (int s = 0; s < splits; ++s) l = fmaf(pl[(size_t)s * bpad + r], sc[s * 32 + rx], l);
+  l = red[1][0][rx];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) l += red[1][k][rx];
   const float invB = 1.0f / (float)B, invl = 1.0f / l;
-  __shared__ float cs[16][33];                // dA of this CTA's rows x columns (db1 partial)
-  for (int j = blockIdx.y * 16 + jy; j < h && j < blockIdx.y * 16 + 16; j += 8) {
+  __shared__ float cs[COMBINE_CW][33];        // dA of this CTA's rows x columns (db1 partial)
+  for (int j = blockIdx.y * COMBINE_CW + jy; j < h && j < blockIdx.y * COMBINE_CW + COMBINE_CW; j += 8) {
     float o = 0.f;
 #pragma unroll 12
     for (int s = 0; s < splits; ++s) o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc[s * 32 + rx], o);
     const float dh = (o * invl - labW[(size_t)r * h + j]) * invB;
     const float da = live && Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
     if (live) dA[(size_t)r * h + j] = da;
-    cs[j - blockIdx.y * 16][rx] = da;
+    cs[j - blockIdx.y * COMBINE_CW][rx] = da;
   }
   // db1 = sum_r dA_r (step a5), fused: per-CTA column sums over its 32 rows in
   // row order, then the last row block to arrive for this column group adds
   // the partials in row-block order and applies b1 -= lr db1 (deterministic)
   __syncthreads();
   const int nrb = (B + 31) / 32;
-  if (threadIdx.x < 16) {
+  if (threadIdx.x < COMBINE_CW) {
     float g = 0.f;
     for (int k = 0; k < 32; ++k) g += cs[threadIdx.x][k];
-    db1p[(size_t)blockIdx.x * h + blockIdx.y * 16 + threadIdx.x] = g;
+    db1p[(size_t)blockIdx.x * h + blockIdx.y * COMBINE_CW + threadIdx.x] = g;
     __threadfence();
   }
   __syncthreads();
@@ -248,12 +264,12 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   if (threadIdx.x == 0) last = atomicAdd(&db1cnt[blockIdx.y], 1) == nrb - 1;
   __syncthreads();
   if (last) {
-    // every partial in flight at once: warp jy sums columns 2 jy, 2 jy + 1 over
+    // every partial in flight at once: warp jy sums columns CW/8 jy ... over
     // the row blocks (lane k takes blocks k, k + 32, ...; fixed xor tree)
     __threadfence();
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int c = blockIdx.y * 16 + 2 * jy + cc;
+    for (int cc = 0; cc < COMBINE_CW / 8; ++cc) {
+      const int c = blockIdx.y * COMBINE_CW + (COMBINE_CW / 8) * jy + cc;
       float g = 0.f;
       for (int k = rx; k < nrb; k += 32) g += __ldcg(db1p + (size_t)k * h + c);
       g = warp_sum(g);
@@ -280,7 +296,7 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
                          float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
                          int *db1cnt, float *b1, float lr, float *dbg_db1) {
-  launch_pdl(k_combine_bf16, dim3(ceil_div(bpad, 32), h / 16), dim3(256), (size_t)splits * 32 * 4, s, desc, h,
+  launch_pdl(k_combine_bf16, dim3(ceil_div(bpad, 32), h / COMBINE_CW), dim3(256), (size_t)splits * 32 * 4, s, desc, h,
              bpad, splits, pm, pl, pO, labW, zsum, Hf, lab_ptr, lse2, lsep, wrow, lossr, dA, db1p, db1cnt, b1, lr,
              dbg_db1);
 }
