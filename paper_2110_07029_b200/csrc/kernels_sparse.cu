@@ -213,6 +213,16 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   const int r = live ? blockIdx.x * 32 + rx : B - 1;   // padding lanes shadow a live row
   if (!live && jy == 0 && blockIdx.y == 0) { lsep[blockIdx.x * 32 + rx] = INFINITY; wrow[blockIdx.x * 32 + rx] = 0.f; }
   extern __shared__ float sc[];             // [splits][32] per-slot scales of the rows
+  // label term and activation of this thread's columns, loaded before the
+  // slot reductions so their latency hides under them
+  constexpr int NCW = COMBINE_CW / 8;
+  const int j0 = blockIdx.y * COMBINE_CW + jy;
+  float lwv[NCW], hv[NCW];
+#pragma unroll
+  for (int c = 0; c < NCW; ++c) {
+    lwv[c] = labW[(size_t)r * h + j0 + 8 * c];
+    hv[c] = Hf[(size_t)r * h + j0 + 8 * c];
+  }
   // every slot loop is unrolled 12-wide so a thread keeps 12 partial loads in
   // flight (the partials are L2-resident right after pass 1)
   // M_r and l_r: warp jy reduces slots jy, jy + 8, ...; the 8 warp partials
@@ -239,12 +249,22 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   for (int k = 1; k < 8; ++k) l += red[1][k][rx];
   const float invB = 1.0f / (float)B, invl = 1.0f / l;
   __shared__ float cs[COMBINE_CW][33];        // dA of this CTA's rows x columns (db1 partial)
-  for (int j = blockIdx.y * COMBINE_CW + jy; j < h && j < blockIdx.y * COMBINE_CW + COMBINE_CW; j += 8) {
-    float o = 0.f;
-#pragma unroll 12
-    for (int s = 0; s < splits; ++s) o = fmaf(pO[((size_t)s * h + j) * bpad + r], sc[s * 32 + rx], o);
-    const float dh = (o * invl - labW[(size_t)r * h + j]) * invB;
-    const float da = live && Hf[(size_t)r * h + j] > 0.f ? dh : 0.f;
+  // the warp's COMBINE_CW / 8 columns j0 + 8c advance together over the slots
+  // (their loads in flight at once); same per-column fmaf order as one by one
+  float o[NCW];
+#pragma unroll
+  for (int c = 0; c < NCW; ++c) o[c] = 0.f;
+#pragma unroll 6
+  for (int s = 0; s < splits; ++s) {
+    const float w = sc[s * 32 + rx];
+#pragma unroll
+    for (int c = 0; c < NCW; ++c) o[c] = fmaf(pO[((size_t)s * h + j0 + 8 * c) * bpad + r], w, o[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < NCW; ++c) {
+    const int j = j0 + 8 * c;
+    const float dh = (o[c] * invl - lwv[c]) * invB;
+    const float da = live && hv[c] > 0.f ? dh : 0.f;
     if (live) dA[(size_t)r * h + j] = da;
     cs[j - blockIdx.y * COMBINE_CW][rx] = da;
   }
