@@ -40,14 +40,16 @@ for name in ALGOS:
     # with the literal ||w||_2 / P metric (R15) perturbation fires at every
     # merge and sum(alpha) = 1 + delta (alpha_r - alpha_s) > 1 inflates the model
     algo = "adaptive" if name.startswith("adaptive") else name
-    pert_thr = 0.0 if name == "adaptive_np" else 0.1
+    # "..._sfK": adaptive scaling frequency (R27) with p_max = K
+    pert_thr = 0.0 if name.startswith("adaptive_np") else 0.1
+    pmax = int(name.split("_sf")[1]) if "_sf" in name else 1
     M = N * b_max if algo == "sync" else 20 * b_max       # sync: one batch per replica per merge
     gamma = 0.9 if algo == "adaptive" else 0.0
     reps = [Replica(cfg.d, cfg.C, cfg.h, b_max, p0, b_min=b_min, beta=b_min // 2, megabatch=M,
                     max_row_nnz=int(np.diff(full.row_ptr).max()), max_row_labels=int(np.diff(full.lab_ptr).max()),
                     lr0=lr0, gamma=gamma, pert_thr=pert_thr, precision="bf16", rank=i, world=N, algo=algo)
             for i in range(N)]
-    st = driver.ReplayState(N, b_max, b_min, b_min // 2, lr0, costs, algo=algo)
+    st = driver.ReplayState(N, b_max, b_min, b_min // 2, lr0, costs, algo=algo, scale_pmax=pmax)
     for r in reps:
         r.upload_dataset(train)
     n = len(train.row_ptr) - 1
@@ -74,7 +76,7 @@ for name in ALGOS:
             continue
         acc = reps[0].evaluate(test)                   # replicas restart from wbar
         print(json.dumps({"algo": name, "lr0": lr0, "samples": seen, "replay_s": sim_ps * 1e-12, "gpu_s": round(gpu_s, 4),
-                          "top1": acc, "u": u, "b": b_used}), flush=True)
+                          "top1": acc, "u": u, "b": b_used, "period": st.period}), flush=True)
     for r in reps:
         r.close()
     torch.cuda.empty_cache()
