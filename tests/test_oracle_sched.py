@@ -203,3 +203,15 @@ def test_scale_period_equal_speeds_doubles_interval():
     recs, _ = otrain.run(ds, p0, rc, costs, 64 * 9)
     assert [r["period"] for r in recs] == [2, 2, 4, 4, 4, 4, 4, 4, 4]
     assert all(r["b_next"] == [16, 16] for r in recs)
+
+
+def test_scale_period_pure_oscillation_saturates():
+    """Two GPUs whose batch sizes swing back and forth every Alg. 1 run (the
+    "oscillatory state" of P:141): the first move resets to 1, every later
+    reversal doubles the interval (R27) until p_max."""
+    b = [[48, 40], [44, 44], [48, 40], [44, 44], [48, 40], [44, 44], [48, 40]]
+    period, dirs, seen = 1, [0, 0], []
+    for prev, nxt in zip(b, b[1:]):
+        period, dirs = osched.scale_period(prev, nxt, dirs, period, 8)
+        seen.append(period)
+    assert seen == [1, 2, 4, 8, 8, 8]
