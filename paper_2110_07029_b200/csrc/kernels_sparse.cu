@@ -188,9 +188,9 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 // dA_r = dH_r * [A_r > 0]  (R3, R4).  CTA = 32 rows x COMBINE_CW columns.  Partial
 // layout: pm, pl [split][bpad]; pO [split][h][bpad] (coalesced TC epilogue).
 // =====================================================================
-// columns per combine CTA: 16 = 2 per warp (A/B on B200: 8 and 32 slower)
+// columns per combine CTA: 8 = one per warp (A/B on B200: 16 and 32 slower)
 #ifndef COMBINE_CW
-#define COMBINE_CW 16
+#define COMBINE_CW 8
 #endif
 static_assert(COMBINE_CW % 8 == 0, "one or more columns per warp");
 __global__ void __launch_bounds__(256) k_combine_bf16(
