@@ -120,6 +120,9 @@ void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_
 // Label terms (R3): zsum_r = (1/k_r) sum_{y in Y_r} z_ry and
 // labW_r = (1/k_r) sum_{y in Y_r} W2T[y]  (fp32 master weights).  Warp per row.
 // =====================================================================
+#ifndef AS_LT_G
+#define AS_LT_G 8
+#endif
 template <int H>
 __global__ void k_label_terms(const StepDesc *__restrict__ desc, const int64_t *__restrict__ lab_ptr,
                               const int32_t *__restrict__ lab, const float *__restrict__ Hf,
@@ -138,12 +141,13 @@ __global__ void k_label_terms(const StepDesc *__restrict__ desc, const int64_t *
     lw[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   float zs = 0.f;
-  // labels 4 at a time: all four W2T rows (and b2 values) in flight at once
-  for (int64_t j0 = s; j0 < e; j0 += 4) {
-    float4 w[4][V];
-    float bb[4];
+  // labels AS_LT_G at a time: all their W2T rows (and b2 values) in flight at
+  // once; padding slots add zeros (same sums for any group size)
+  for (int64_t j0 = s; j0 < e; j0 += AS_LT_G) {
+    float4 w[AS_LT_G][V];
+    float bb[AS_LT_G];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < AS_LT_G; ++u) {
       const bool ok = j0 + u < e;
       const int y = ok ? lab[j0 + u] : 0;
       bb[u] = ok ? b2[y] : 0.f;
@@ -153,7 +157,7 @@ __global__ void k_label_terms(const StepDesc *__restrict__ desc, const int64_t *
                      : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < AS_LT_G; ++u) {
       float d = 0.f;
 #pragma unroll
       for (int q = 0; q < V; ++q) {
