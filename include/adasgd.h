@@ -199,6 +199,19 @@ int as_eval_top1(as_ctx *ctx, int32_t rows, const int64_t *row_ptr,
 int as_merge(as_ctx *ctx, const int32_t *u, const int32_t *b,
              double *alpha_out, int32_t *perturbed_out);
 
+/* Replica norm (step a9, Alg. 2 line 7, "||w_i||_2 / |w|", reading R15):
+ * the regularisation metric of this replica's packed parameters, computed on
+ * the device in fp64 with a fixed reduction order; metric = AS_METRIC_*.
+ * *out (host) receives the value.  Synchronises the stream. */
+int as_replica_norm(as_ctx *ctx, int32_t metric, double *out);
+
+/* Merge with caller-given weights alpha[world] (host, identical on every rank):
+ * steps a11-a13 exactly as in as_merge, with Alg. 2 (a9-a10) replaced by the
+ * given weights -- w' = sum_i alpha_i w_i + gamma (wbar - wbar_p).  Used by
+ * drivers that compute the weights themselves and by the tests that force
+ * alpha_i != 1 at world = 1 (prescale path).  Collective when world > 1. */
+int as_merge_weighted(as_ctx *ctx, const double *alpha);
+
 /* Local-group merge: the n contexts ctxs[0..n-1] live in THIS process (one per
  * device, or several on one device for testing), were created with
  * world == n, rank == index and nccl_unique_id == NULL.  Same semantics as
@@ -233,7 +246,10 @@ enum {
                        csc rows, csc vals (float bits) -- step a3           */
   AS_DBG_LSEG = 9,  /* int32 [1+V+(V+1)+L]: V, label ids, seg ptr, rows      */
   AS_DBG_BATCH = 10,/* int32 [4]: rows, nnz, L, U of the loaded batch        */
-  AS_DBG_LOGITS = 11 /* float [rows*C] logits (AS_FP32 only)                 */
+  AS_DBG_LOGITS = 11,/* float [rows*C] logits (AS_FP32 only)                 */
+  AS_DBG_DHSOFT = 12 /* float [rows*h]   softmax part of dL/dH before the label
+                       term (R3): (1/B) sum_c softmax(z_r)_c W2T[c] -- pass 1's
+                       O / l in AS_BF16; needs AS_FLAG_DEBUG_GRADS            */
 };
 /* Copy a debug view of the last step to host_out (capacity `bytes`);
  * *written receives the byte count.  Synchronises. */

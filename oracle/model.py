@@ -19,6 +19,9 @@ pre-update parameters:
     dW2T  = dz^T H,  db2 = sum_r dz_r,  dH = dz W2T,  dA = dH * [A > 0]  (R4)
     dW1[f] = sum_{r: f in x_r} v_rf dA_r,  db1 = sum_r dA_r
 
+dH splits into its softmax part and its label part (the two terms of dz):
+    dHsoft_r = (1/B) sum_c softmax(z_r)_c W2T[c],   dH_r = dHsoft_r - (1/(k_r B)) sum_{y in Y_r} W2T[y]
+
 Update ("the third pass ... updates the model with the computed gradient
 using the learning rate"):  theta <- theta - lr * dtheta, computed in
 fp64 and stored in fp32 (parameters are fp32 in the packed layout, R2).
@@ -77,6 +80,7 @@ def gradients(batch, params, fwd=None):
     A, H, Z, LSE = fwd["A"], fwd["H"], fwd["Z"], fwd["LSE"]
     B = A.shape[0]
     G = np.exp(Z - LSE[:, None])                    # softmax(z_r)
+    dHsoft = (G @ W2T) / B                          # softmax part of dH
     tr, tc, tw = target_matrix_rows(batch.lab_ptr, batch.lab)
     np.add.at(G, (tr, tc), -tw)                     # - T
     G /= B                                          # dz
@@ -90,7 +94,7 @@ def gradients(batch, params, fwd=None):
     np.add.at(dW1, np.asarray(batch.col, np.int64),
               np.asarray(batch.val, np.float64)[:, None] * dA[rid])
     db1 = dA.sum(axis=0)
-    return {"W1": dW1, "b1": db1, "W2T": dW2T, "b2": db2, "dZ": G, "dH": dH, "dA": dA}
+    return {"W1": dW1, "b1": db1, "W2T": dW2T, "b2": db2, "dZ": G, "dH": dH, "dA": dA, "dHsoft": dHsoft}
 
 
 def sgd_step(batch, params, lr):
@@ -118,6 +122,7 @@ def gradients_chunked(batch, params, chunk=64):
     LSE = np.empty(B)
     label_term = np.zeros(B)
     dH = np.empty_like(H)
+    dHsoft = np.empty_like(H)
     dW2T = np.zeros_like(W2T)
     db2 = np.zeros_like(b2)
     for r0 in range(0, B, chunk):
@@ -128,6 +133,7 @@ def gradients_chunked(batch, params, chunk=64):
         sel = (tr >= r0) & (tr < r1)
         np.add.at(label_term, tr[sel], tw[sel] * Z[tr[sel] - r0, tc[sel]])
         G = np.exp(Z - LSE[r0:r1, None])
+        dHsoft[r0:r1] = (G @ W2T) / B
         np.add.at(G, (tr[sel] - r0, tc[sel]), -tw[sel])
         G /= B
         dW2T += G.T @ H[r0:r1]
@@ -139,7 +145,7 @@ def gradients_chunked(batch, params, chunk=64):
     rid = np.repeat(np.arange(B), np.diff(np.asarray(batch.row_ptr)))
     np.add.at(dW1, np.asarray(batch.col, np.int64), np.asarray(batch.val, np.float64)[:, None] * dA[rid])
     return {"A": A, "H": H, "LSE": LSE, "loss": float(np.mean(LSE - label_term)), "dA": dA,
-            "db1": dA.sum(axis=0), "dW1": dW1, "dW2T": dW2T, "db2": db2}
+            "db1": dA.sum(axis=0), "dW1": dW1, "dW2T": dW2T, "db2": db2, "dHsoft": dHsoft}
 
 
 def bf16_round(x):

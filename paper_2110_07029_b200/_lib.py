@@ -24,7 +24,7 @@ AS_NORM_METRIC_SHIFT = 2
 METRICS = {"l2/P": 0, "l2^2/P": 1, "l2/sqrt(P)": 2, "l2": 3}
 AS_PARAMS_REPLICA, AS_PARAMS_GLOBAL, AS_PARAMS_GLOBAL_PREV = 0, 1, 2
 (AS_DBG_H, AS_DBG_LSE, AS_DBG_LOSS, AS_DBG_DA, AS_DBG_DB1, AS_DBG_DW2T, AS_DBG_DB2, AS_DBG_DW1,
- AS_DBG_FSEG, AS_DBG_LSEG, AS_DBG_BATCH, AS_DBG_LOGITS) = range(12)
+ AS_DBG_FSEG, AS_DBG_LSEG, AS_DBG_BATCH, AS_DBG_LOGITS, AS_DBG_DHSOFT) = range(13)
 
 # every exported symbol of include/adasgd.h (checked by tests/test_abi.py)
 EXPORTS = [
@@ -35,7 +35,7 @@ EXPORTS = [
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
     "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
     "as_eval_top1", "as_sched_route_static", "as_sched_alg2_ex", "as_sched_fit_cost",
-    "as_sched_scale_period",
+    "as_sched_scale_period", "as_replica_norm", "as_merge_weighted",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -123,6 +123,8 @@ def load():
         "as_tc_selftest2": [VP, VP, P(F), P(F)],
         "as_trace_dump": [P(I64), I32],
         "as_profile_read": [VP, P(D), P(I64), P(I64)],
+        "as_replica_norm": [VP, I32, P(D)],
+        "as_merge_weighted": [VP, P(D)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

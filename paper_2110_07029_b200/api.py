@@ -132,6 +132,17 @@ class Replica:
         L.check(self.lib.as_merge(self.ctx, L.ptr(u, C.c_int32), L.ptr(b, C.c_int32), None, None))
         return None, None
 
+    def merge_weighted(self, alpha):
+        """as_merge_weighted: steps a11-a13 with caller-given weights alpha[world]."""
+        a = L.as_np(alpha, np.float64)
+        L.check(self.lib.as_merge_weighted(self.ctx, L.ptr(a, C.c_double)))
+
+    def replica_norm(self, metric="l2/P"):
+        """as_replica_norm: the Alg. 2 line-7 metric of this replica (step a9), fp64."""
+        out = C.c_double()
+        L.check(self.lib.as_replica_norm(self.ctx, L.METRICS[metric], C.byref(out)))
+        return out.value
+
     def set_batch_sizes(self, b, lr):
         b = L.as_np(b, np.int32); lr = L.as_np(lr, np.float32)
         L.check(self.lib.as_set_batch_sizes(self.ctx, L.ptr(b, C.c_int32), L.ptr(lr, C.c_float)))

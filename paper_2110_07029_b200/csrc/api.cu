@@ -79,7 +79,7 @@ struct as_ctx {
   int32_t *top1;              // top-1 evaluation (NEXT f1)
   unsigned long long *hits;
   float *Z, *dH, *dW2, *splitk_tmp;
-  float *dbg_dW2, *dbg_db2, *dbg_dW1, *dbg_db1;
+  float *dbg_dW2, *dbg_db2, *dbg_dW1, *dbg_db1, *dbg_dHs;
   double *norm_part, *norm_dev, *norms_all;
   float *alpha_dev;
   const float **reps_dev;
@@ -229,6 +229,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
     p = P(4 * (size_t)D.C); if (x) x->dbg_db2 = (float *)p;
     p = P(4 * (size_t)D.nnz_cap * D.h); if (x) x->dbg_dW1 = (float *)p;
     p = P(4 * (size_t)D.h); if (x) x->dbg_db1 = (float *)p;
+    p = P(4 * (size_t)D.b_max * D.h); if (x) x->dbg_dHs = (float *)p;
   }
   p = P(8 * kNormBlocks); if (x) x->norm_part = (double *)p;
   p = P(8); if (x) x->norm_dev = (double *)p;
@@ -414,6 +415,12 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
     x->plan = (as::TcPlan *)malloc(as::tc_plan_bytes());
     if (as::tc_plan_init(x->plan, D.h, D.b_max, D.C, x->num_sms, x->Hb, x->w2b, x->w + D.d * D.h + D.h) != 0)
       rc = as_fail(AS_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
+  }
+  if (!rc && cfg->world == 1 && getenv("ADASGD_NCCL_SELF") && atoi(getenv("ADASGD_NCCL_SELF")) > 0) {
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r == ncclSuccess) r = ncclCommInitRank(&x->comm, 1, id, 0);
+    if (r != ncclSuccess) rc = as_fail(AS_E_NCCL, "one-rank ncclCommInitRank: %s", ncclGetErrorString(r));
   }
   if (!rc && cfg->world > 1 && cfg->nccl_unique_id) {
     ncclUniqueId id;
@@ -685,7 +692,8 @@ int as_train_step(as_ctx *x, float *loss_out) {
 #endif
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
                             x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lab_ptr, x->lse2, x->lsep, x->wrow,
-                            x->lossr, x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr);
+                            x->lossr, x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr,
+                            dbg ? x->dbg_dHs : nullptr);
     ph_end(x, AS_PH_COMBINE);
     cudaStreamWaitEvent(s, x->ev_join, 0);   // label transpose ready
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
@@ -714,7 +722,8 @@ int as_train_step(as_ctx *x, float *loss_out) {
                         D.splitk, x->splitk_tmp, &d->rows);
     as::launch_gemm_f32_kdev(s, (int)C, D.h, D.b_max, x->Z, 1, C, x->Hf, D.h, 1, x->dW2, D.h,
                              &d->rows);
-    as::launch_finish_f32(s, D.h, d, D.b_max, x->dH, x->Hf, x->zsum, x->lse2, x->lossr, x->dA);
+    as::launch_finish_f32(s, D.h, d, D.b_max, x->dH, x->Hf, x->zsum, x->lse2, x->lossr, x->dA, x->labW,
+                          dbg ? x->dbg_dHs : nullptr);
     as::launch_colsum_sgd(s, d, D.b_max, (int)C, x->Z, C, b2, lr, dbg ? x->dbg_db2 : nullptr);
     as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
     if (dbg) cudaMemcpyAsync(x->dbg_dW2, x->dW2, 4 * (size_t)C * D.h, cudaMemcpyDeviceToDevice, s);
@@ -758,6 +767,79 @@ int as_set_batch_sizes(as_ctx *x, const int32_t *b, const float *lr) {
   return AS_OK;
 }
 
+// a11-a13 with the weights alpha[world] (identical on every rank): prescale,
+// all-reduce, momentum + reset + shadow, wbar / wbar_p rotation.
+static int merge_apply(as_ctx *x, const double *alpha) {
+  const int N = x->cfg.world;
+  const Dims &D = x->D;
+  cudaStream_t s = x->stream;
+  x->launches += 1;                          // momentum (+1 below if a prescale kernel runs)
+  // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset.
+  // N > 1: the prescale rides inside the allreduce (NCCL PreMulSum: every
+  // rank's input multiplied by its own alpha_i as it is reduced), saving an
+  // 8P-byte pass; plain prescale + sum if the op cannot be created.  N = 1:
+  // alpha = b / sum(b) = 1 exactly (Alg. 2 line 3, no perturbation, R14),
+  // so there is nothing to scale unless a caller-forced alpha differs.
+  const float a_me = (float)alpha[x->cfg.rank];
+  const long long w2_off = D.d * D.h + D.h, w2_len = D.C * D.h;
+  // Partitioned merge (SURVEY 8(f) rank 3, P:197-199 "multi-stream" transfer
+  // overlapping the combine): the all-reduce runs chunk by chunk on the
+  // communication stream and the momentum kernel of chunk c runs on the main
+  // stream as soon as chunk c is reduced, overlapping the reduction of c+1.
+  // ADASGD_MERGE_CHUNKS=k forces k chunks (also at N = 1, without a reduction:
+  // tests the chunk bookkeeping on one GPU); default 8 for N > 1, 1 at N = 1.
+  // The NCCL path runs whenever the ctx has a communicator: N > 1, or N = 1
+  // with ADASGD_NCCL_SELF=1 (a one-rank communicator: exercises the PreMulSum
+  // all-reduce and its chunking on one GPU).
+  const bool use_nccl = x->comm != nullptr;
+  const int K = x->merge_chunks > 0 ? x->merge_chunks : (N > 1 ? 8 : 1);
+  ncclRedOp_t premul = ncclSum;
+  bool have_premul = false;
+  if (use_nccl) {
+    float a_host = a_me;
+    have_premul = ncclRedOpCreatePreMulSum(&premul, &a_host, ncclFloat, ncclScalarHostImmediate, x->comm) ==
+                  ncclSuccess;
+    if (!have_premul) {
+      x->launches += 1;
+      as::launch_scale(s, x->w, D.P, a_me);
+      premul = ncclSum;
+    }
+  } else if (a_me != 1.0f) {
+    x->launches += 1;
+    as::launch_scale(s, x->w, D.P, a_me);
+  }
+  if (K == 1) {
+    if (use_nccl) {
+      const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
+      if (have_premul) ncclRedOpDestroy(premul, x->comm);
+      if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
+    }
+    as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, w2_off, w2_len, x->w2b);
+  } else {
+    cudaEventRecord(x->ev_mg[0], s);          // training, norms and any prescale are done
+    cudaStreamWaitEvent(x->comm_s, x->ev_mg[0], 0);
+    x->launches += K - 1;
+    for (int c = 0; c < K; ++c) {
+      const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
+      if (use_nccl) {
+        const ncclResult_t r = ncclAllReduce(x->w + off, x->w + off, len, ncclFloat, premul, x->comm, x->comm_s);
+        if (r != ncclSuccess) {
+          if (have_premul) ncclRedOpDestroy(premul, x->comm);
+          x->sticky = AS_E_NCCL;
+          return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+        }
+      }
+      cudaEventRecord(x->ev_mg[1 + (c & 1)], x->comm_s);
+      cudaStreamWaitEvent(s, x->ev_mg[1 + (c & 1)], 0);
+      as::launch_momentum(s, x->w + off, x->wbarp + off, x->wbar + off, len, (float)x->cfg.gamma, w2_off - off,
+                          w2_len, x->w2b);
+    }
+    if (have_premul) ncclRedOpDestroy(premul, x->comm);
+  }
+  std::swap(x->wbar, x->wbarp);
+  return cuda_check(x, cudaSuccess, "merge launch");
+}
+
 int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
              int32_t *perturbed_out) {
   AS_GUARD(x);
@@ -797,72 +879,37 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
     // comparison methods: plain average, no norms
     for (int i = 0; i < N; ++i) alpha[i] = 1.0 / N;
   }
-  x->launches += 1;                          // momentum (+1 below if a prescale kernel runs)
-  // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset.
-  // N > 1: the prescale rides inside the allreduce (NCCL PreMulSum: every
-  // rank's input multiplied by its own alpha_i as it is reduced), saving an
-  // 8P-byte pass; plain prescale + sum if the op cannot be created.  N = 1:
-  // alpha = b / sum(b) = 1 exactly (Alg. 2 line 3, no perturbation, R14),
-  // so there is nothing to scale unless a caller-forced alpha differs.
-  const float a_me = (float)alpha[x->cfg.rank];
-  const long long w2_off = D.d * D.h + D.h, w2_len = D.C * D.h;
-  // Partitioned merge (SURVEY 8(f) rank 3, P:197-199 "multi-stream" transfer
-  // overlapping the combine): the all-reduce runs chunk by chunk on the
-  // communication stream and the momentum kernel of chunk c runs on the main
-  // stream as soon as chunk c is reduced, overlapping the reduction of c+1.
-  // ADASGD_MERGE_CHUNKS=k forces k chunks (also at N = 1, without a reduction:
-  // tests the chunk bookkeeping on one GPU); default 8 for N > 1, 1 at N = 1.
-  const int K = x->merge_chunks > 0 ? x->merge_chunks : (N > 1 ? 8 : 1);
-  ncclRedOp_t premul = ncclSum;
-  bool have_premul = false;
-  if (N > 1) {
-    float a_host = a_me;
-    have_premul = ncclRedOpCreatePreMulSum(&premul, &a_host, ncclFloat, ncclScalarHostImmediate, x->comm) ==
-                  ncclSuccess;
-    if (!have_premul) {
-      x->launches += 1;
-      as::launch_scale(s, x->w, D.P, a_me);
-      premul = ncclSum;
-    }
-  } else if (a_me != 1.0f) {
-    x->launches += 1;
-    as::launch_scale(s, x->w, D.P, a_me);
-  }
-  if (K == 1) {
-    if (N > 1) {
-      const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
-      if (have_premul) ncclRedOpDestroy(premul, x->comm);
-      if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
-    }
-    as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, w2_off, w2_len, x->w2b);
-  } else {
-    cudaEventRecord(x->ev_mg[0], s);          // training, norms and any prescale are done
-    cudaStreamWaitEvent(x->comm_s, x->ev_mg[0], 0);
-    x->launches += K - 1;
-    for (int c = 0; c < K; ++c) {
-      const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
-      if (N > 1) {
-        const ncclResult_t r = ncclAllReduce(x->w + off, x->w + off, len, ncclFloat, premul, x->comm, x->comm_s);
-        if (r != ncclSuccess) {
-          if (have_premul) ncclRedOpDestroy(premul, x->comm);
-          x->sticky = AS_E_NCCL;
-          return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
-        }
-      }
-      cudaEventRecord(x->ev_mg[1 + (c & 1)], x->comm_s);
-      cudaStreamWaitEvent(s, x->ev_mg[1 + (c & 1)], 0);
-      as::launch_momentum(s, x->w + off, x->wbarp + off, x->wbar + off, len, (float)x->cfg.gamma, w2_off - off,
-                          w2_len, x->w2b);
-    }
-    if (have_premul) ncclRedOpDestroy(premul, x->comm);
-  }
-  std::swap(x->wbar, x->wbarp);
+  rc = merge_apply(x, alpha.data());
+  if (rc) return rc;
   ph_end(x, AS_PH_MERGE);
   rc = cuda_check(x, cudaSuccess, "merge launch");
   if (rc) return rc;
   if (alpha_out) std::copy(alpha.begin(), alpha.end(), alpha_out);
   if (perturbed_out) *perturbed_out = pert;
   return AS_OK;
+}
+
+int as_merge_weighted(as_ctx *x, const double *alpha) {
+  AS_GUARD(x);
+  if (!alpha) return as_fail(AS_E_INVALID, "alpha is NULL");
+  for (int i = 0; i < x->cfg.world; ++i)
+    if (!(alpha[i] == alpha[i]) || alpha[i] < 0.0 || alpha[i] > 1e6)
+      return as_fail(AS_E_INVALID, "alpha[%d] not a finite weight >= 0", i);
+  if (x->cfg.world > 1 && !x->comm) return as_fail(AS_E_STATE, "as_merge_weighted needs an NCCL ctx");
+  ph_begin(x, AS_PH_MERGE);
+  const int rc = merge_apply(x, alpha);
+  ph_end(x, AS_PH_MERGE);
+  return rc;
+}
+
+int as_replica_norm(as_ctx *x, int32_t metric, double *out) {
+  AS_GUARD(x);
+  if (!out || metric < AS_METRIC_L2_P || metric > AS_METRIC_L2) return as_fail(AS_E_INVALID, "bad arguments");
+  x->launches += 2;
+  as::launch_sumsq(x->stream, x->w, x->D.P, x->norm_part, kNormBlocks, x->norm_dev, metric);
+  int rc = cuda_check(x, cudaMemcpyAsync(out, x->norm_dev, 8, cudaMemcpyDeviceToHost, x->stream), "norm D2H");
+  if (!rc) rc = cuda_check(x, cudaStreamSynchronize(x->stream), "norm");
+  return rc;
 }
 
 int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32_t *b,
@@ -897,6 +944,30 @@ int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32
   std::vector<float> af(n);
   std::vector<const float *> reps(n);
   for (int i = 0; i < n; ++i) { af[i] = (float)alpha[i]; reps[i] = ctxs[i]->w; }
+  // replicas on other devices are read through peer mappings (NVLink)
+  for (int i = 1; i < n; ++i) {
+    const int di = ctxs[i]->cfg.device, d0 = x0->cfg.device;
+    if (di == d0) continue;
+    int ok01 = 0;
+    cudaDeviceCanAccessPeer(&ok01, d0, di);
+    if (!ok01) return as_fail(AS_E_CUDA, "device %d cannot access device %d (peer access)", d0, di);
+    cudaSetDevice(d0);
+    cudaError_t e = cudaDeviceEnablePeerAccess(di, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_check(x0, e, "enable peer access");
+    cudaSetDevice(di);
+    e = cudaDeviceEnablePeerAccess(d0, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_check(ctxs[i], e, "enable peer access");
+    cudaGetLastError();                      // clear a tolerated AlreadyEnabled
+  }
+  // the reduction on x0's stream waits for every replica's training (any algo)
+  for (int i = 1; i < n; ++i) {
+    cudaSetDevice(ctxs[i]->cfg.device);
+    rc = cuda_check(ctxs[i], cudaEventRecord(ctxs[i]->ev_mg[0], ctxs[i]->stream), "merge event");
+    if (rc) return rc;
+    cudaSetDevice(x0->cfg.device);
+    rc = cuda_check(x0, cudaStreamWaitEvent(x0->stream, ctxs[i]->ev_mg[0], 0), "merge wait");
+    if (rc) return rc;
+  }
   cudaSetDevice(x0->cfg.device);
   cudaMemcpyAsync(x0->alpha_dev, af.data(), 4 * n, cudaMemcpyHostToDevice, x0->stream);
   cudaMemcpyAsync(x0->reps_dev, reps.data(), 8 * n, cudaMemcpyHostToDevice, x0->stream);
@@ -980,6 +1051,7 @@ int as_debug_get(as_ctx *x, int32_t which, void *host_out, size_t bytes, size_t 
       parts.push_back({x->lseg_row, 4 * (size_t)dd.nlab});
       break;
     case AS_DBG_BATCH: head = {dd.rows, dd.nnz, dd.nlab, dd.U}; break;
+    case AS_DBG_DHSOFT: if (!dbg) return as_fail(AS_E_STATE, "needs AS_FLAG_DEBUG_GRADS"); parts.push_back({x->dbg_dHs, 4 * (size_t)dd.rows * D.h}); break;
     case AS_DBG_LOGITS:
       if (x->cfg.precision != AS_FP32) return as_fail(AS_E_STATE, "logits exist only in AS_FP32");
       parts.push_back({x->Z, 4 * (size_t)dd.rows * D.C});

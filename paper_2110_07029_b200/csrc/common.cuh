@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <utility>
 
 namespace as {
@@ -58,6 +59,18 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 __device__ __forceinline__ int ceil_div_dev(int a, int b) { return (a + b - 1) / b; }
+
+// cudaFuncSetAttribute is per device: `mask` (one per kernel instantiation)
+// records the devices already configured (idempotent, so a race between two
+// host threads only repeats the call).
+inline bool first_on_device(std::atomic<unsigned long long> &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return false;
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return true;
+}
 
 // Arguments of the batch transposes (step a3, kernels_transpose.cu).  Dense
 // per-key state lives in the arena and is idle (0 / -1) between steps.
@@ -115,7 +128,7 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          int splits, const float *pm, const float *pl, const float *pO,
                          const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
                          float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
-                         int *db1cnt, float *b1, float lr, float *dbg_db1);
+                         int *db1cnt, float *b1, float lr, float *dbg_db1, float *dbg_dHs);
 // fp32 (SIMT) output layer (steps a5/a6 in parity mode)
 void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
                      long long sak, const float *B, long long sbk, long long sbn, float *Cm,
@@ -127,7 +140,7 @@ void launch_softmax_grad(cudaStream_t s, const StepDesc *desc, int b_max, int C,
                          const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2);
 void launch_finish_f32(cudaStream_t s, int h, const StepDesc *desc, int b_max, const float *dH,
                        const float *Hf, const float *zsum, const float *lse2, float *lossr,
-                       float *dA);
+                       float *dA, const float *labW, float *dbg_dHs);
 // column sums with fused SGD (db1 / db2)
 void launch_colsum_sgd(cudaStream_t s, const StepDesc *desc, int n_rows_cap, int ncols,
                        const float *X, long long ldx, float *param, float lr, float *grad_out);

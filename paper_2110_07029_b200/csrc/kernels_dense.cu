@@ -244,18 +244,21 @@ void launch_softmax_grad(cudaStream_t s, const StepDesc *desc, int b_max, int C,
 __global__ void k_finish_f32(const StepDesc *__restrict__ desc, int h, const float *__restrict__ dH,
                              const float *__restrict__ Hf, const float *__restrict__ zsum,
                              const float *__restrict__ lse2, float *__restrict__ lossr,
-                             float *__restrict__ dA) {
+                             float *__restrict__ dA, const float *__restrict__ labW,
+                             float *__restrict__ dbg_dHs) {
   const int r = blockIdx.x, j = threadIdx.x;
   if (r >= desc->rows) return;
   const size_t i = (size_t)r * h + j;
   dA[i] = Hf[i] > 0.f ? dH[i] : 0.f;
+  // softmax part of dH (tests): dH + (1/k_r) sum_y W2T[y] / B removes the label term
+  if (dbg_dHs) dbg_dHs[i] = dH[i] + labW[i] / (float)desc->rows;
   if (j == 0) lossr[r] = lse2[r] * 0.69314718055994531f - zsum[r];
 }
 
 void launch_finish_f32(cudaStream_t s, int h, const StepDesc *desc, int b_max, const float *dH,
                        const float *Hf, const float *zsum, const float *lse2, float *lossr,
-                       float *dA) {
-  k_finish_f32<<<b_max, h, 0, s>>>(desc, h, dH, Hf, zsum, lse2, lossr, dA);
+                       float *dA, const float *labW, float *dbg_dHs) {
+  k_finish_f32<<<b_max, h, 0, s>>>(desc, h, dH, Hf, zsum, lse2, lossr, dA, labW, dbg_dHs);
 }
 
 __global__ void k_sgd_dense(long long n, float *__restrict__ p, const float *__restrict__ g,

@@ -359,11 +359,9 @@ static void seg_bulk_launch(cudaStream_t s, int num_sms, const int *n_dev, const
                             const int32_t *seg_of, const PtrT *seg_ptr, const int32_t *gidx, const float *scale,
                             const float *src, float *part, int *arrive, const SegArgs &a) {
   using Cfg = SegCfg<H, MODE>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_dev{0};
+  if (first_on_device(attr_dev))
     cudaFuncSetAttribute(k_seg_bulk<H, MODE, PtrT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr = true;
-  }
 #ifndef AS_SEG_CPS
 #define AS_SEG_CPS 1                            // CTAs per SM (experiment override)
 #endif

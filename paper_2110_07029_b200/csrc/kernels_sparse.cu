@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     const float *__restrict__ zsum, const float *__restrict__ Hf, const int64_t *__restrict__ lab_ptr,
     float *__restrict__ lse2, float *__restrict__ lsep, float *__restrict__ wrow,
     float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
-    int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1) {
+    int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1,
+    float *__restrict__ dbg_dHs) {
   griddep_wait();
   // CTA = 32 rows x COMBINE_CW columns (8 warps); partial reads coalesced over rows
   const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     const float dh = (o[c] * invl - lwv[c]) * invB;
     const float da = live && hv[c] > 0.f ? dh : 0.f;
     if (live) dA[(size_t)r * h + j] = da;
+    if (dbg_dHs && live) dbg_dHs[(size_t)r * h + j] = o[c] * invl * invB;   // softmax part of dH (tests)
     cs[j - blockIdx.y * COMBINE_CW][rx] = da;
   }
   // db1 = sum_r dA_r (step a5), fused: per-CTA column sums over its 32 rows in
@@ -319,10 +321,10 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          int splits, const float *pm, const float *pl, const float *pO,
                          const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
                          float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
-                         int *db1cnt, float *b1, float lr, float *dbg_db1) {
+                         int *db1cnt, float *b1, float lr, float *dbg_db1, float *dbg_dHs) {
   launch_pdl(k_combine_bf16, dim3(ceil_div(bpad, 32), h / COMBINE_CW), dim3(256), (size_t)splits * 32 * 4, s, desc, h,
              bpad, splits, pm, pl, pO, labW, zsum, Hf, lab_ptr, lse2, lsep, wrow, lossr, dA, db1p, db1cnt, b1, lr,
-             dbg_db1);
+             dbg_db1, dbg_dHs);
 }
 
 // =====================================================================

@@ -253,6 +253,9 @@ __device__ __forceinline__ void ex2_emu2(uint64_t x, float &p0, float &p1) {
 // library): AS_X_NOEXP replaces ex2 by a move, AS_X_NOSOFT skips the softmax
 // TMEM work, AS_X_NOMMA1 / AS_X_NOMMA2 skip the first / second GEMM of a pass,
 // AS_X_NOTMA reuses the first operand stages, AS_X_NOUPD skips pass 2's SGD.
+// Mutants for the parity tests' sensitivity (must FAIL them): AS_X_P1NOO zeroes
+// pass 1's P operand of the O MMA (O = 0), AS_X_P2NOSOFT drops the softmax
+// term from pass 2's G (only the label term remains).
 #ifdef AS_X_NOEXP
 #define XEX2(v) (v)
 #else
@@ -552,6 +555,9 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
           }
           acc[u & 3] = fadd2(acc[u & 3], f2(p0, p1));
           pk[u] = pack_bf16x2(p0, p1);
+#ifdef AS_X_P1NOO
+          pk[u] = 0u;                          // mutant: O = 0 (parity tests must fail)
+#endif
         }
         AS_TMEM_ST16(tS + ch * 16, pk);
         if (PQ == 4 || (ch & 1)) {             // this part of P is in TMEM
@@ -979,6 +985,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             }
             // p / B straight into the db2 sums and the packed bf16 G^T: no
             // 64-value array stays live (register pressure)
+#ifdef AS_X_P2NOSOFT
+            e0 = e1 = 0.f;                     // mutant: no softmax term in pass 2 (parity tests must fail)
+#endif
             dacc[u & 3] = fadd2(dacc[u & 3], f2(e0, e1));
             pk[u] = pack_bf16x2(e0, e1);
           }
@@ -1721,9 +1730,8 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
   if (make_map(&plan->mapH, Hb, plan->bpad, h) != 0) return -1;
   if (make_map(&plan->mapW, W2b, C, h) != 0) return -1;
   if (make_map_f32(&plan->mapWf, W2T, C, h) != 0) return -1;
-  static bool attr_done[2] = {false, false};
-  const int hi = h == 128 ? 0 : 1;
-  if (!attr_done[hi]) {
+  // every ctx sets the attributes on its own device (cheap, idempotent)
+  {
     if (h == 128) {
       cudaFuncSetAttribute(tc::k_out_fwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::FwdCfg<128>::SMEM);
@@ -1739,19 +1747,26 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
       cudaFuncSetAttribute(tc::k_out_top1<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::Top1Cfg<256>::SMEM);
     }
-    attr_done[hi] = true;
   }
   return 0;
+}
+
+// pass-1 / top-1 grid: one CTA per SM, or one per 128-row tile when the
+// batch has more tiles than SMs (b_max > 128 * num_sms; the CTAs then run in
+// several waves with one class split each)
+static int fwd_grid(const TcPlan *p) {
+  const int rt = p->bpad / tc::BM;
+  return rt > p->num_sms ? rt : p->num_sms;
 }
 
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2,
                        float *pm, float *pl, float *pO) {
   if (p->h == 128)
-    launch_pdl(tc::k_out_fwd<128>, dim3(p->num_sms), dim3(tc::FwdCfg<128>::THREADS), tc::FwdCfg<128>::SMEM, s,
+    launch_pdl(tc::k_out_fwd<128>, dim3(fwd_grid(p)), dim3(tc::FwdCfg<128>::THREADS), tc::FwdCfg<128>::SMEM, s,
                p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
                p->max_splits, p->bpad, pm, pl, pO);
   else
-    launch_pdl(tc::k_out_fwd<256>, dim3(p->num_sms), dim3(tc::FwdCfg<256>::THREADS), tc::FwdCfg<256>::SMEM, s,
+    launch_pdl(tc::k_out_fwd<256>, dim3(fwd_grid(p)), dim3(tc::FwdCfg<256>::THREADS), tc::FwdCfg<256>::SMEM, s,
                p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
                p->max_splits, p->bpad, pm, pl, pO);
 }
@@ -1759,16 +1774,16 @@ void launch_out_fwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
 void launch_out_top1_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2, float *pmax,
                         int *pidx) {
   if (p->h == 128)
-    tc::k_out_top1<128><<<p->num_sms, tc::Top1Cfg<128>::THREADS, tc::Top1Cfg<128>::SMEM, s>>>(
+    tc::k_out_top1<128><<<fwd_grid(p), tc::Top1Cfg<128>::THREADS, tc::Top1Cfg<128>::SMEM, s>>>(
         p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pmax, pidx);
   else
-    tc::k_out_top1<256><<<p->num_sms, tc::Top1Cfg<256>::THREADS, tc::Top1Cfg<256>::SMEM, s>>>(
+    tc::k_out_top1<256><<<fwd_grid(p), tc::Top1Cfg<256>::THREADS, tc::Top1Cfg<256>::SMEM, s>>>(
         p->mapH, p->mapW, desc, b2, (int)p->C, p->n_cblocks, p->max_splits, p->bpad, pmax, pidx);
 }
 
 // number of pass-1 partial slots for a batch of B rows (one per CTA split)
 int tc_fwd_splits_host(const TcPlan *p, int B) {
-  return tc::fwd_splits(B, p->n_cblocks, p->num_sms, p->max_splits);
+  return tc::fwd_splits(B, p->n_cblocks, fwd_grid(p), p->max_splits);
 }
 
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lsep,

@@ -8,10 +8,13 @@ Tolerances (north star, reading R22: per tensor
   1e-5       merged weights
 """
 import math
+import os
 import struct
 
 import numpy as np
 import pytest
+
+import _parity_log as plog
 
 import synthgen
 from oracle import csr as ocsr
@@ -33,10 +36,38 @@ def rel_err(a, o):
     return max(e1, e2)
 
 
+def _test_name():
+    return os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
+
+
 def assert_close(name, a, o, tol):
     e = rel_err(a, o)
+    plog.record(_test_name(), name, e, tol, "rel (R22)")
     assert e <= tol, "%s: rel err %.3e > %.1e" % (name, e, tol)
     return e
+
+
+def assert_abs(name, a, o, tol):
+    """max |a - o| <= tol (absolute): used for LSE, whose error in natural-log
+    units is the relative error of the partition function sum_c exp(z_rc)."""
+    a = np.asarray(a, np.float64); o = np.asarray(o, np.float64)
+    e = float(np.max(np.abs(a - o))) if o.size else 0.0
+    plog.record(_test_name(), name, e, tol, "abs")
+    assert e <= tol, "%s: max abs err %.3e > %.1e" % (name, e, tol)
+    return e
+
+
+def check_softmax_terms(name, rep, sub, ref, C, h, tol):
+    """The softmax parts of the gradients on their own, where the label term
+    cannot hide them: pass 1's O / l (dHsoft, AS_DBG_DHSOFT) and the dW2T
+    rows / db2 entries of classes with no label in the batch (pure softmax)."""
+    B = len(sub.row_ptr) - 1
+    assert_close(name + " dHsoft", _f32(rep.debug_get(12, 4 * B * h)).reshape(B, h), ref["dHsoft"], tol)
+    unl = np.setdiff1d(np.arange(C), sub.lab)
+    if len(unl):
+        dW2T = _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h)
+        assert_close(name + " dW2T unlabelled", dW2T[unl], ref["dW2T"][unl], tol)
+        assert_close(name + " db2 unlabelled", _f32(rep.debug_get(6, 4 * C))[unl], ref["db2"][unl], tol)
 
 
 def _cfg(d, C, h, n, b_max, avg_nnz=20.0, avg_labels=3.0, seed=0):
@@ -155,7 +186,9 @@ def test_one_step_parity(gpu_lib, case, precision, tol):
     assert_close("H", H, ref["H"], 1e-5)                       # SpMM is fp32 in both modes
     lse = _f32(rep.debug_get(1, 4 * B)) * LN2
     assert_close("LSE", lse, ref["LSE"], tol)
+    assert_abs("LSE abs", lse, ref["LSE"], tol)
     assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    check_softmax_terms("step", rep, sub, ref, C, h, tol)
     dA = _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h)
     assert_close("dA", dA, ref["dA"], tol)
     db1 = _f32(rep.debug_get(4, 4 * h))
@@ -230,6 +263,8 @@ def test_bf16_online_softmax_rescale_paths(gpu_lib, h):
     ref = om.gradients_chunked(sub, otrain.unpack(p, d, C, h), chunk=64)
     assert abs(loss - ref["loss"]) <= 2e-2 * abs(ref["loss"])
     assert_close("LSE", _f32(rep.debug_get(1, 4 * B)) * LN2, ref["LSE"], 2e-2)
+    assert_abs("LSE abs", _f32(rep.debug_get(1, 4 * B)) * LN2, ref["LSE"], 2e-2)
+    check_softmax_terms("rescale", rep, sub, ref, C, h, 2e-2)
     assert_close("dA", _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h), ref["dA"], 2e-2)
     assert_close("dW2T", _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h), ref["dW2T"], 2e-2)
 
@@ -469,13 +504,24 @@ def test_end_to_end_tiny_comparison_methods(gpu_lib, algo, M):
 
 
 @pytest.mark.slow
-def test_full_size_amazon670k_sampled(gpu_lib):
+@pytest.mark.parametrize("peaked", [False, True])
+def test_full_size_amazon670k_sampled(gpu_lib, peaked):
     """Amazon-670K shape at b = 1024 in the bench's launch configuration
     (bf16, resident dataset, stream batch): the oracle recomputes the whole
-    step in fp64 (chunked over rows) and every output is compared."""
+    step in fp64 (chunked over rows) and every output is compared -- including
+    the softmax terms on their own (pass 1's O / l and the ~668K unlabelled
+    classes of pass 2), which the label term dominates in dA / dW2T / db2.
+    peaked: W2T x 8 and a b2 ramp to 40 (as in the rescale test) so the softmax
+    of every row is concentrated and the online rescale fires across blocks."""
     cfg = synthgen.CONFIGS["amazon670k"]
     ds = synthgen.make_dataset(cfg, n=40_000)
     p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    if peaked:
+        lay = synthgen.param_layout(cfg.d, cfg.C, cfg.h)
+        o, _ = lay["b2"]
+        p[o:o + cfg.C] = np.linspace(0.0, 40.0, cfg.C, dtype=np.float32)
+        o, _ = lay["W2T"]
+        p[o:o + cfg.C * cfg.h] *= np.float32(8.0)
     rep = _replica(cfg, p, ds, "bf16", lr=0.5)
     rep.upload_dataset(ds)
     rep.load_batch_stream(1000, 1024)
@@ -484,7 +530,10 @@ def test_full_size_amazon670k_sampled(gpu_lib):
     ref = om.gradients_chunked(sub, otrain.unpack(p, cfg.d, cfg.C, cfg.h), chunk=128)
     tol = 2e-2
     assert abs(loss - ref["loss"]) <= tol * ref["loss"]
-    assert_close("LSE", _f32(rep.debug_get(1, 4 * 1024)) * LN2, ref["LSE"], tol)
+    lse = _f32(rep.debug_get(1, 4 * 1024)) * LN2
+    assert_close("LSE", lse, ref["LSE"], tol)
+    assert_abs("LSE abs", lse, ref["LSE"], tol)
+    check_softmax_terms("full", rep, sub, ref, cfg.C, 128, tol)
     assert_close("dA", _f32(rep.debug_get(3, 4 * 1024 * 128)).reshape(1024, 128), ref["dA"], tol)
     dW2T = _f32(rep.debug_get(5, 4 * cfg.C * 128)).reshape(cfg.C, 128)
     assert_close("dW2T", dW2T, ref["dW2T"], tol)
@@ -492,6 +541,7 @@ def test_full_size_amazon670k_sampled(gpu_lib):
     keys = np.unique(sub.col)
     dW1 = _f32(rep.debug_get(7, 4 * len(keys) * 128)).reshape(len(keys), 128)
     assert_close("dW1", dW1, ref["dW1"][keys], tol)
+    rep.close()
 
 
 @pytest.mark.slow
@@ -663,4 +713,84 @@ def test_label_heavy_batches(gpu_lib, h, C, avg_labels):
     assert_close("dW2T", _f32(rep.debug_get(5, 4 * C * h)).reshape(C, h), ref["dW2T"], 2e-2)
     assert_close("db2", _f32(rep.debug_get(6, 4 * C)), ref["db2"], 2e-2)
     assert_close("dA", _f32(rep.debug_get(3, 4 * B * h)).reshape(B, h), ref["dA"], 2e-2)
+    rep.close()
+
+
+@pytest.mark.parametrize("metric", ["l2/P", "l2^2/P", "l2/sqrt(P)", "l2"])
+def test_replica_norm_vs_oracle(gpu_lib, metric):
+    """Step a9 (Alg. 2 line 7, R15): the device fp64 norm of a trained replica
+    against oracle.merge.replica_norm of the same parameters, <= 1e-12 relative."""
+    cfg = _cfg(3000, 2000, 128, 300, 128)
+    ds = synthgen.make_dataset(cfg, n=300)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, "bf16", debug=False)
+    sub = ds.rows(np.arange(100))
+    rep.load_batch_csr(100, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    rep.train_step()
+    w = rep.get_params()
+    got = rep.replica_norm(metric)
+    want = omerge.replica_norm(w, metric)
+    e = abs(got - want) / abs(want)
+    plog.record(_test_name(), "norm " + metric, e, 1e-12, "rel")
+    assert e <= 1e-12, (got, want)
+    rep.close()
+
+
+@pytest.mark.parametrize("nccl_self,chunks", [(False, None), (True, None), (True, "7")])
+def test_merge_weighted_forced_alpha(gpu_lib, monkeypatch, nccl_self, chunks):
+    """Steps a11-a13 with a forced weight alpha = 0.7 at world = 1: the prescale
+    kernel (no communicator), or with ADASGD_NCCL_SELF=1 the NCCL PreMulSum
+    all-reduce on a one-rank communicator (the N > 1 code path: PreMulSum op,
+    chunked all-reduce on the communication stream, momentum chasing the
+    chunks).  Two merges (gamma = 0.9 momentum) against oracle.merge.merge,
+    <= 1e-5; replicas restart from wbar; wbar_p rotation."""
+    if nccl_self:
+        monkeypatch.setenv("ADASGD_NCCL_SELF", "1")
+    if chunks:
+        monkeypatch.setenv("ADASGD_MERGE_CHUNKS", chunks)
+    cfg = _cfg(1500, 900, 128, 300, 128)
+    ds = synthgen.make_dataset(cfg, n=300)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, "bf16", debug=False)
+    wbar, wbar_p = p.copy(), p.copy()
+    for m in range(2):
+        sub = ds.rows(np.arange(100) + 50 * m)
+        rep.load_batch_csr(100, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+        rep.train_step()
+        w = rep.get_params()
+        rep.merge_weighted([0.7])
+        wbar, wbar_p = omerge.merge([w], [0.7], wbar, wbar_p, 0.9)
+        assert_close("wbar merge %d" % m, rep.get_params(1), wbar, 1e-5)
+        assert np.array_equal(rep.get_params(2), wbar_p)
+        assert np.array_equal(rep.get_params(0), rep.get_params(1))
+    rep.close()
+
+
+def test_pass1_grid_more_row_tiles_than_sms(gpu_lib):
+    """b = 18 945 rows = 149 row tiles > 148 SMs: pass 1 launches one CTA per
+    row tile (several waves) instead of leaving tiles 148+ unwritten (advisor
+    finding); one bf16 step against the oracle, plus top-1 on the same rows."""
+    B = 148 * 128 + 1
+    cfg = _cfg(2000, 300, 128, B + 10, B, avg_nnz=8.0, seed=4)
+    ds = synthgen.make_dataset(cfg, n=B + 10)
+    p = _params(cfg)
+    rep = _replica(cfg, p, ds, "bf16", lr=0.5)
+    sub = ds.rows(np.arange(B))
+    rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    loss = rep.train_step(want_loss=True)
+    prm = otrain.unpack(p, cfg.d, cfg.C, cfg.h)
+    ref = om.gradients_chunked(sub, prm, chunk=2048)
+    assert abs(loss - ref["loss"]) <= 2e-2 * abs(ref["loss"])
+    lse = _f32(rep.debug_get(1, 4 * B)) * LN2
+    assert_abs("LSE abs", lse, ref["LSE"], 2e-2)
+    assert_close("dA", _f32(rep.debug_get(3, 4 * B * 128)).reshape(B, 128), ref["dA"], 2e-2)
+    assert_close("dW2T", _f32(rep.debug_get(5, 4 * cfg.C * 128)).reshape(cfg.C, 128), ref["dW2T"], 2e-2)
+    rep.close()
+    rep = _replica(cfg, p, ds, "bf16", debug=False)
+    top, hits = rep.eval_top1(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    otop, ohits, zmax, logit = om.top1(sub, prm, operands="bf16")
+    diff = np.nonzero(top != otop)[0]
+    assert len(diff) <= B // 50
+    for r in diff[:50]:
+        assert zmax[r] - logit(r, int(top[r])) <= 1e-4 * (1.0 + abs(zmax[r]))
     rep.close()

@@ -184,3 +184,50 @@ def test_bf16_round_matches_torch_bfloat16():
     x = np.concatenate([x, half])
     want = torch.tensor(x).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(om.bf16_round(x), want)
+
+
+def test_dHsoft_closed_form_uniform_softmax():
+    """H = 0 (W1 = 0, b1 < 0) and b2 = 0 make every logit 0, so softmax(z_r) =
+    1/C exactly and the softmax part of dH is the mean row of W2T over B:
+    dHsoft_r = (1/B) (1/C) sum_c W2T[c] for every row (both oracle routes)."""
+    ds, p = _tiny(seed=5)
+    d, C, h = ds.d, ds.C, 8
+    lay = synthgen.param_layout(d, C, h)
+    o, shp = lay["W1"]; p[o:o + shp[0] * shp[1]] = 0.0
+    o, _ = lay["b1"]; p[o:o + h] = -1.0
+    o, _ = lay["b2"]; p[o:o + C] = 0.0
+    prm = otrain.unpack(p, d, C, h)
+    B = ds.n
+    want = np.tile(np.asarray(prm["W2T"], np.float64).mean(axis=0) / B, (B, 1))
+    g = om.gradients(ds, prm)
+    gc = om.gradients_chunked(ds, prm, chunk=5)
+    assert np.allclose(g["dHsoft"], want, rtol=1e-12, atol=1e-18)
+    assert np.allclose(gc["dHsoft"], want, rtol=1e-12, atol=1e-18)
+
+
+def test_dHsoft_plus_label_part_is_dH_brute_force():
+    """dH = dHsoft - (1/(k_r B)) sum_{y in Y_r} W2T[y] (the two terms of dz), with
+    dHsoft recomputed here by explicit loops over rows and classes (math.exp,
+    max-shifted) on a tiny case; dH from torch autograd w.r.t. H."""
+    ds, p = _tiny(seed=6, n=6, C=7)
+    h = 8
+    prm = otrain.unpack(p, ds.d, ds.C, h)
+    g = om.gradients(ds, prm)
+    W2T = np.asarray(prm["W2T"], np.float64); b2 = np.asarray(prm["b2"], np.float64)
+    X, T = _dense_x(ds)
+    A = X @ np.asarray(prm["W1"], np.float64) + np.asarray(prm["b1"], np.float64)
+    Hn = np.maximum(A, 0.0)
+    B = ds.n
+    brute = np.zeros((B, h))
+    for r in range(B):
+        z = [float(Hn[r] @ W2T[c] + b2[c]) for c in range(ds.C)]
+        m = max(z)
+        e = [math.exp(v - m) for v in z]
+        tot = sum(e)
+        for c in range(ds.C):
+            brute[r] += (e[c] / tot) * W2T[c] / B
+    assert np.allclose(g["dHsoft"], brute, rtol=1e-12, atol=1e-18)
+    Ht = torch.tensor(Hn, requires_grad=True)
+    Z = Ht @ torch.tensor(W2T).T + torch.tensor(b2)
+    torch.nn.functional.cross_entropy(Z, torch.tensor(T)).backward()
+    assert np.allclose(brute - (T @ W2T) / B, Ht.grad.numpy(), rtol=1e-10, atol=1e-15)

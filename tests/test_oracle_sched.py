@@ -116,6 +116,29 @@ def test_splitmix64_reference_vector():
     assert z == 0xE220A8397B1DCDAF
 
 
+def test_splitmix64_reference_stream():
+    # the first five outputs of the published SplitMix64 reference generator from
+    # state 0 (Vigna, splitmix64.c; the same constants as Steele et al. 2014)
+    ref = [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F, 0xF88BB8A8724C81EC,
+           0x1B39896A51A8749B]
+    s, out = 0, []
+    for _ in range(5):
+        s, z = osched.splitmix64(s)
+        out.append(z)
+    assert out == ref
+
+
+def test_permutation_hand_derived_n5():
+    """Reading R10 worked by hand for n = 5, seed 0: Fisher-Yates from the top,
+    i = 4, 3, 2, 1, with j = floor(r (i + 1) / 2^64) and r the reference
+    SplitMix64 outputs above (their leading bytes give r / 2^64):
+      i = 4: r = 0xE220.. (0.883) -> j = floor(4.41) = 4  swap(4, 4): [0 1 2 3 4]
+      i = 3: r = 0x6E78.. (0.431) -> j = floor(1.73) = 1  swap(3, 1): [0 3 2 1 4]
+      i = 2: r = 0x06C4.. (0.026) -> j = floor(0.08) = 0  swap(2, 0): [2 3 0 1 4]
+      i = 1: r = 0xF88B.. (0.971) -> j = floor(1.94) = 1  swap(1, 1): [2 3 0 1 4]"""
+    assert osched.permutation(5, 0) == [2, 3, 0, 1, 4]
+
+
 def test_permutation_is_permutation():
     for n, seed in [(1, 0), (2, 5), (100, 7), (1000, 123)]:
         p = osched.permutation(n, seed)
