@@ -50,7 +50,25 @@ def parse():
     ap.add_argument("--verbose", action="store_true", help="progress on stderr")
     ap.add_argument("--no-spmm-sweep", action="store_true",
                     help="skip the in-loop SpMM / dW1 HBM measurement on the W1-larger-than-L2 shapes")
+    ap.add_argument("--merge", default=os.environ.get("ADASGD_MERGE", "p2p"), choices=["p2p", "nccl"],
+                    help="N > 1 merge transport: fused peer-memory kernel (p2p) or NCCL PreMulSum all-reduce")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks (one
+    per GPU) through torch.distributed.run on 127.0.0.1 and return its exit
+    code; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")              # keep NCCL's communicator log (stderr)
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def peaks():
@@ -113,6 +131,35 @@ def oracle_sample_step(ds, params, cfg, rows, pos):
     t0 = time.perf_counter()
     om.sgd_step(bt, params, 0.1)
     return time.perf_counter() - t0
+
+
+def oracle_baseline(ds, p, cfg, steps=2):
+    """cpu_baseline as SURVEY 8(d) plans it: K = 2 SGD steps at b_max on one
+    replica plus one merge, timed on the host cores with the oracle as it
+    stands (oracle.model.gradients_chunked + the fp64 update, then
+    oracle.merge.replica_norm, oracle.sched.alg2 and oracle.merge.merge);
+    samples/s = K b_max / time."""
+    from oracle import csr as ocsr
+    from oracle import merge as omerge
+    from oracle import model as om
+    from oracle import sched as osched
+    from oracle import train as otrain
+    prm = otrain.unpack(p, cfg.d, cfg.C, cfg.h)
+    wbar = np.asarray(p, np.float32)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        bt = otrain.batch_of(ds, ocsr.stream_ids(k * cfg.b_max, cfg.b_max, ds.n))
+        g = om.gradients_chunked(bt, prm, chunk=128)
+        prm = {key: (np.asarray(prm[key], np.float64) - 0.1 * g[key]).astype(np.float32)
+               for key in ("W1", "b1", "W2T", "b2")}
+    w = np.concatenate([prm[key].ravel() for key in ("W1", "b1", "W2T", "b2")])
+    norm = omerge.replica_norm(w)
+    alpha, _ = osched.alg2([steps], [cfg.b_max], [norm], 0.1, 0.1)
+    omerge.merge([w], alpha, wbar, wbar, 0.9)
+    t = time.perf_counter() - t0
+    return {"value": steps * cfg.b_max / t, "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": "SURVEY 8(d): %d SGD steps at b_max = %d on one replica (oracle.model.gradients_chunked, "
+                      "fp64) + one merge (replica_norm, alg2, merge), %.1f s" % (steps, cfg.b_max, t)}
 
 
 def cpu_threads():
@@ -219,6 +266,8 @@ def main():
     global VERBOSE
     args = parse()
     VERBOSE = args.verbose
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         return run_reference(args)
     import ctypes as C
@@ -234,15 +283,26 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, "--gpus must match WORLD_SIZE"
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # ranks sharing a GPU (more ranks than devices: a functional run only, the
+    # ranks time-slice the device) cannot use NCCL; plumbing then goes over gloo
+    # and the merge over peer memory
+    shared = world > torch.cuda.device_count()
+    if shared:
+        args.merge = "p2p"
+    pg_dev = torch.device("cpu") if shared else dev
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = synthgen.CONFIGS[args.config]
     ds = synthgen.make_dataset(cfg)
     p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
     log("dataset + init generated")
-    nccl_id = driver.broadcast_nccl_id(dist, rank, device=dev) if world > 1 else None
+    nccl_id = driver.broadcast_nccl_id(dist, rank, device=pg_dev) if (world > 1 and args.merge == "nccl") else None
     # high priority: the step's critical path (SpMM, passes 1/2) wins SMs over the
     # library's low-priority side stream (batch transposes)
     stream = torch.cuda.Stream(dev, priority=-1)
@@ -250,7 +310,9 @@ def main():
     rep = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta, megabatch=cfg.megabatch,
                   max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
                   lr0=lr0, precision=args.precision, rank=rank, world=world, nccl_id=nccl_id, device=local,
-                  stream=stream)
+                  stream=stream, merge_backend=args.merge if world > 1 else "nccl")
+    if world > 1 and args.merge == "p2p":
+        driver.open_p2p(rep, dist)
     rep.upload_dataset(ds)
     log("replica ready, dataset resident")
     costs = synthgen.make_cost_models(world, hetero=args.hetero)
@@ -260,19 +322,22 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if shared:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
 
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=pg_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=pg_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -382,8 +447,9 @@ def main():
     calls_out = max(1, ph_calls[3])
     tflops_alg = fl_alg / t_out / 1e12 if t_out > 0 else 0.0
     peak_t = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    peak_burst = pk.get("bf16_tflops", peak_t)
     if args.precision == "fp32":
-        peak_t = 0.0
+        peak_t = peak_burst = 0.0
     # SURVEY 8(d) a4 algorithmic bytes nnz (4h + 8) + 8 (b + 1) + 4 b h over the
     # profiled region's actual batches (the stream's row lengths)
     nnz_prof = int(driver.stream_nnz_prefix(ds.row_ptr, ds.n, pos_prof, args.steps * M)[-1]) / world
@@ -410,6 +476,8 @@ def main():
             "flops_per_launch_alg": 6.0 * cfg.h * cfg.C * cfg.b_max,
             "issued_frac": (fl_iss / t_out / 1e12) / peak_t if (peak_t and t_out) else None,
             "peak_kind": "%s bf16_tflops_sustained (kernel timed inside a long step)" % pk_kind,
+            "peak_burst": peak_burst, "frac_burst": tflops_alg / peak_burst if peak_burst else None,
+            "peak_sustained_clock_mhz": pk.get("clocks_under_load", {}).get("sm_mhz_median"),
             "avg_launch_ms": {"out_fwd": ph_ms[3] / calls_out, "out_bwd": ph_ms[5] / max(1, ph_calls[5])},
             "spmm": {"bound": "hbm", "achieved": spmm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": spmm_gbs / pk["hbm_gbs"], "avg_launch_ms": ph_ms[2] / max(1, ph_calls[2]),
@@ -418,15 +486,7 @@ def main():
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import train as otrain
-        prm = otrain.unpack(p, cfg.d, cfg.C, cfg.h)
-        ts, k = [], 0
-        t_start = time.perf_counter()
-        while k < 3 or (time.perf_counter() - t_start < 10 and k < 8):
-            ts.append(oracle_sample_step(ds, prm, cfg, 64, 64 * k))
-            k += 1
-        cpu = {"value": 64 * len(ts) / sum(ts), "unit": "samples/s", "cores": cpu_threads(), "kind": "oracle",
-               "sample": "%d SGD steps of 64 stream rows (oracle.model.sgd_step, fp64 numpy), no merge" % len(ts)}
+        cpu = oracle_baseline(ds, p, cfg)
     sweep = None
     if world == 1 and not args.no_spmm_sweep:
         log("spmm sweep")
@@ -438,9 +498,11 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
                 "data": "synthetic (synthgen, Table-1-shaped, seed %d); random-init (Glorot) weights" % cfg.seed,
                 "config": {"workload": args.config, "d": cfg.d, "C": cfg.C, "h": cfg.h, "n": cfg.n,
+                           "ranks_share_one_gpu": bool(shared),
                            "b_max": cfg.b_max, "megabatch": M, "step": "one mega-batch (all of SURVEY 8(a))",
                            "routing": "replay, %s cost models" % ("heterogeneous" if args.hetero else "equal"),
-                           "parallelism": "dp%d (one replica per GPU, NCCL merge)" % world,
+                           "parallelism": "dp%d (one replica per GPU, %s merge)" % (
+                               world, ("fused peer-memory" if args.merge == "p2p" else "NCCL") if world > 1 else "local"),
                            "l2": "inputs larger than L2 (W2T fp32 343 MB + bf16 171 MB streamed per step)"},
                 "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": int(h2d_step),
                         "d2h_bytes_per_step": int(world * (4 + 8 * world))},

@@ -100,7 +100,28 @@ typedef struct {
   void *stream;           /* cudaStream_t borrowed from the caller             */
   int32_t device;         /* CUDA device ordinal of this replica               */
   int32_t algo;           /* AS_ALGO_* merge rule (0 = the paper's Adaptive SGD) */
+  int32_t merge_backend;  /* AS_MERGE_* transport of steps a11-a13 when world > 1 */
 } as_config;
+
+/* Largest number of replicas (world) one merge handles. */
+enum { AS_MAX_WORLD = 64 };
+
+/* Merge transports (as_config.merge_backend), world > 1 (P:197-199 all-reduce
+ * model merging; the paper's own is a multi-stream ring over PCIe/NVLink):
+ * AS_MERGE_NCCL  prescale fused into an NCCL PreMulSum all-reduce (weights read
+ *                from device memory), partitioned into chunks on a
+ *                communication stream, momentum chasing the chunks; needs
+ *                nccl_unique_id.
+ * AS_MERGE_P2P   ONE fused kernel over peer memory (CUDA IPC mappings over
+ *                NVLink / NVSwitch): rank r reduces its 1/N slice of the
+ *                packed vector from every replica (sum alpha_i w_i), applies
+ *                the momentum step and pushes w' into every rank's replica,
+ *                global model and bf16 shadow; cross-rank barriers are flags in
+ *                peer memory.  Needs as_p2p_export / as_p2p_open after as_init.
+ * Both compute the merge weights on the device (Alg. 2 from the all-gathered
+ * norms), so as_merge does not synchronise the host unless alpha_out /
+ * perturbed_out is requested. */
+enum { AS_MERGE_NCCL = 0, AS_MERGE_P2P = 1 };
 
 /* Merge rules (as_config.algo).  AS_ALGO_ADAPTIVE: Alg. 2 normalized,
  * perturbed weights.  The comparison methods of P:215-217 use
@@ -211,6 +232,16 @@ int as_replica_norm(as_ctx *ctx, int32_t metric, double *out);
  * drivers that compute the weights themselves and by the tests that force
  * alpha_i != 1 at world = 1 (prescale path).  Collective when world > 1. */
 int as_merge_weighted(as_ctx *ctx, const double *alpha);
+
+/* AS_MERGE_P2P setup (collective, world > 1, after as_init on every rank).
+ * as_p2p_export writes this rank's export record (AS_P2P_EXPORT_BYTES: a CUDA
+ * IPC handle of the workspace allocation and the workspace offset in it) to
+ * out (host).  The caller all-gathers the records of all ranks (rank order) and
+ * passes them to as_p2p_open, which maps every peer's workspace (cudaIpc,
+ * NVLink / NVSwitch peer access).  Ranks may share a device (testing). */
+enum { AS_P2P_EXPORT_BYTES = 128 };
+int as_p2p_export(as_ctx *ctx, void *out);
+int as_p2p_open(as_ctx *ctx, const void *records /* world * AS_P2P_EXPORT_BYTES */);
 
 /* Local-group merge: the n contexts ctxs[0..n-1] live in THIS process (one per
  * device, or several on one device for testing), were created with

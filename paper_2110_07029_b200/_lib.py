@@ -17,6 +17,10 @@ LIB_PATH = os.environ.get("ADASGD_LIB", os.path.join(HERE, "libadasgd.so"))
 AS_OK, AS_E_INVALID, AS_E_CUDA, AS_E_NCCL, AS_E_OOM, AS_E_STATE = 0, -1, -2, -3, -4, -5
 AS_FP32, AS_BF16 = 0, 1
 AS_ALGO_ADAPTIVE, AS_ALGO_ELASTIC, AS_ALGO_SYNC = 0, 1, 2
+AS_MERGE_NCCL, AS_MERGE_P2P = 0, 1
+MERGE_BACKENDS = {"nccl": AS_MERGE_NCCL, "p2p": AS_MERGE_P2P}
+AS_MAX_WORLD = 64
+AS_P2P_EXPORT_BYTES = 128
 ALGOS = {"adaptive": AS_ALGO_ADAPTIVE, "elastic": AS_ALGO_ELASTIC, "sync": AS_ALGO_SYNC}
 AS_FLAG_DEBUG_GRADS, AS_FLAG_NORM_UB = 1, 2
 AS_NORM_UPDATES, AS_NORM_UB = 0, 1
@@ -35,7 +39,7 @@ EXPORTS = [
     "as_sched_alg2", "as_sched_permutation", "as_live_open", "as_live_claim", "as_live_reset",
     "as_live_close", "as_profile", "as_profile_read", "as_tc_bench", "as_trace_dump", "as_tc_selftest2",
     "as_eval_top1", "as_sched_route_static", "as_sched_alg2_ex", "as_sched_fit_cost",
-    "as_sched_scale_period", "as_replica_norm", "as_merge_weighted",
+    "as_sched_scale_period", "as_replica_norm", "as_merge_weighted", "as_p2p_export", "as_p2p_open",
 ]
 AS_PH_NAMES = ["batch", "transpose", "spmm", "out_fwd", "combine", "out_bwd", "dw1", "merge"]
 
@@ -55,6 +59,7 @@ class Config(C.Structure):
         ("precision", C.c_int32), ("flags", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("stream", C.c_void_p), ("device", C.c_int32), ("algo", C.c_int32),
+        ("merge_backend", C.c_int32),
     ]
 
 
@@ -125,6 +130,8 @@ def load():
         "as_profile_read": [VP, P(D), P(I64), P(I64)],
         "as_replica_norm": [VP, I32, P(D)],
         "as_merge_weighted": [VP, P(D)],
+        "as_p2p_export": [VP, VP],
+        "as_p2p_open": [VP, VP],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)

@@ -26,7 +26,8 @@ class Replica:
     def __init__(self, d, C_labels, h, b_max, init_params, *, b_min=None, beta=None, megabatch=None,
                  max_row_nnz=1024, max_row_labels=64, lr0=0.1, gamma=0.9, delta=0.1, pert_thr=0.1,
                  precision="bf16", rank=0, world=1, nccl_id=None, device=0, stream=None,
-                 debug_grads=False, algo="adaptive", merge_norm="u", norm_metric="l2/P"):
+                 debug_grads=False, algo="adaptive", merge_norm="u", norm_metric="l2/P",
+                 merge_backend="nccl"):
         torch = _torch()
         self.lib = L.load()
         b_min = b_max // 8 if b_min is None else b_min
@@ -44,6 +45,7 @@ class Replica:
         cfg.flags = ((L.AS_FLAG_DEBUG_GRADS if debug_grads else 0) | (L.AS_FLAG_NORM_UB if merge_norm == "ub" else 0)
                      | (L.METRICS[norm_metric] << L.AS_NORM_METRIC_SHIFT))
         cfg.rank, cfg.world, cfg.device = rank, world, device
+        cfg.merge_backend = L.MERGE_BACKENDS[merge_backend]
         self._nccl_buf = None
         if nccl_id is not None:
             self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -142,6 +144,19 @@ class Replica:
         out = C.c_double()
         L.check(self.lib.as_replica_norm(self.ctx, L.METRICS[metric], C.byref(out)))
         return out.value
+
+    def p2p_export(self):
+        """as_p2p_export: this rank's peer-mapping record (bytes, AS_P2P_EXPORT_BYTES)."""
+        buf = C.create_string_buffer(L.AS_P2P_EXPORT_BYTES)
+        L.check(self.lib.as_p2p_export(self.ctx, buf))
+        return buf.raw
+
+    def p2p_open(self, records):
+        """as_p2p_open: records = the export records of all ranks, rank order."""
+        blob = b"".join(bytes(r) for r in records)
+        assert len(blob) == L.AS_P2P_EXPORT_BYTES * self.world
+        buf = C.create_string_buffer(blob, len(blob))
+        L.check(self.lib.as_p2p_open(self.ctx, buf))
 
     def set_batch_sizes(self, b, lr):
         b = L.as_np(b, np.int32); lr = L.as_np(lr, np.float32)

@@ -1,6 +1,7 @@
 // C-ABI of the Adaptive SGD hot path (include/adasgd.h): replica context,
 // workspace arena, input validation, step and merge orchestration.
 // P:N = PAPER.md line N; Rk = DESIGN.md reading k.
+#include <cuda.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -81,8 +82,18 @@ struct as_ctx {
   float *Z, *dH, *dW2, *splitk_tmp;
   float *dbg_dW2, *dbg_db2, *dbg_dW1, *dbg_db1, *dbg_dHs;
   double *norm_part, *norm_dev, *norms_all;
-  float *alpha_dev;
+  float *alpha_dev;            // local-group merge weights
   const float **reps_dev;
+  // device-side merge weights (Alg. 2 on the device) and the peer-memory merge
+  uint8_t *arena;              // workspace base (offsets are identical on every rank)
+  double *alpha_d;             // [world] fp64
+  float *alpha_f;              // [world] fp32 (PreMulSum scalar / fused merge)
+  int32_t *pert_dev;
+  unsigned long long *p2p_flags;  // [AS_MAX_WORLD] barrier epochs written by the peers
+  uint8_t *peer_base[AS_MAX_WORLD];
+  void *peer_map[AS_MAX_WORLD];   // cudaIpcOpenMemHandle mappings (closed at destroy)
+  bool p2p_ready;
+  unsigned long long p2p_epoch;
   as::TcPlan *plan;
   // host state
   std::vector<int32_t> b_all;
@@ -133,8 +144,10 @@ int validate_cfg(const as_config *c) {
   if (c->algo < AS_ALGO_ADAPTIVE || c->algo > AS_ALGO_SYNC) return as_fail(AS_E_INVALID, "unknown algo %d", c->algo);
   if (c->precision != AS_FP32 && c->precision != AS_BF16)
     return as_fail(AS_E_INVALID, "precision must be AS_FP32 or AS_BF16");
-  if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
-    return as_fail(AS_E_INVALID, "need 0 <= rank < world");
+  if (c->world < 1 || c->world > AS_MAX_WORLD || c->rank < 0 || c->rank >= c->world)
+    return as_fail(AS_E_INVALID, "need 0 <= rank < world <= %d", (int)AS_MAX_WORLD);
+  if (c->merge_backend != AS_MERGE_NCCL && c->merge_backend != AS_MERGE_P2P)
+    return as_fail(AS_E_INVALID, "unknown merge_backend %d", c->merge_backend);
   if (!(c->lr0 > 0.0)) return as_fail(AS_E_INVALID, "lr0 must be > 0");
   return AS_OK;
 }
@@ -233,8 +246,12 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   }
   p = P(8 * kNormBlocks); if (x) x->norm_part = (double *)p;
   p = P(8); if (x) x->norm_dev = (double *)p;
-  p = P(8 * (size_t)c->world); if (x) x->norms_all = (double *)p;
+  p = P(8 * (size_t)AS_MAX_WORLD); if (x) x->norms_all = (double *)p;
   p = P(4 * (size_t)c->world); if (x) x->alpha_dev = (float *)p;
+  p = P(8 * (size_t)AS_MAX_WORLD); if (x) x->alpha_d = (double *)p;
+  p = P(4 * (size_t)AS_MAX_WORLD); if (x) x->alpha_f = (float *)p;
+  p = P(8); if (x) x->pert_dev = (int32_t *)p;
+  p = P(8 * (size_t)AS_MAX_WORLD); if (x) x->p2p_flags = (unsigned long long *)p;
   p = P(8 * (size_t)c->world); if (x) x->reps_dev = (const float **)p;
   return L.total;
 }
@@ -371,6 +388,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   x->stream = (cudaStream_t)cfg->stream;
   cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   carve(cfg, D, x, (uint8_t *)cfg->workspace);
+  x->arena = (uint8_t *)cfg->workspace;
   x->b_all.assign(cfg->world, cfg->b_max);
   x->lr = (float)cfg->lr0;
   const size_t P4 = 4 * (size_t)D.P;
@@ -392,6 +410,8 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->db1cnt, 0, 4 * (size_t)D.h, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->arrive, 0, 4 * (size_t)D.sort_cap, x->stream), "memset");
   if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->Hb, 0, 2 * (size_t)D.bpad * D.h, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->p2p_flags, 0, 8 * (size_t)AS_MAX_WORLD, x->stream), "memset");
+  if (!rc) rc = cuda_check(x, cudaMemsetAsync(x->norms_all, 0, 8 * (size_t)AS_MAX_WORLD, x->stream), "memset");
   // side stream at the lowest priority: the transposes fill SMs the critical
   // path (SpMM, pass 1 on the caller's stream) leaves idle
   int prio_lo = 0, prio_hi = 0;
@@ -446,6 +466,8 @@ int as_destroy(as_ctx *x) {
     if (x->pin_ev[i]) cudaEventDestroy(x->pin_ev[i]);
   }
   if (x->comm) ncclCommDestroy(x->comm);
+  for (int k = 0; k < AS_MAX_WORLD; ++k)
+    if (x->peer_map[k]) cudaIpcCloseMemHandle(x->peer_map[k]);
   if (x->side) { cudaStreamSynchronize(x->side); cudaStreamDestroy(x->side); }
   if (x->ev_fork) cudaEventDestroy(x->ev_fork);
   if (x->ev_join) cudaEventDestroy(x->ev_join);
@@ -713,7 +735,14 @@ int as_train_step(as_ctx *x, float *loss_out) {
     as::launch_gemm_f32(s, D.b_max, (int)C, D.h, x->Hf, D.h, 1, W2T, 1, D.h, x->Z, C, b2, 1,
                         nullptr, &d->rows);
     as::launch_row_lse(s, d, D.b_max, (int)C, x->Z, x->lse2);
-    as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2);
+    if (dbg) {                                // softmax part of dH on its own (AS_DBG_DHSOFT)
+      as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2, 1);
+      as::launch_gemm_f32(s, D.b_max, D.h, (int)C, x->Z, C, 1, W2T, D.h, 1, x->dbg_dHs, D.h, nullptr,
+                          D.splitk, x->splitk_tmp, &d->rows);
+      as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2, 2);
+    } else {
+      as::launch_softmax_grad(s, d, D.b_max, (int)C, x->lab_ptr, x->lab, x->Z, x->lse2, 3);
+    }
     ph_end(x, AS_PH_OUT_FWD);
     cudaStreamWaitEvent(s, x->ev_join, 0);   // transposes ready
     ph_begin(x, AS_PH_OUT_BWD);
@@ -722,8 +751,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
                         D.splitk, x->splitk_tmp, &d->rows);
     as::launch_gemm_f32_kdev(s, (int)C, D.h, D.b_max, x->Z, 1, C, x->Hf, D.h, 1, x->dW2, D.h,
                              &d->rows);
-    as::launch_finish_f32(s, D.h, d, D.b_max, x->dH, x->Hf, x->zsum, x->lse2, x->lossr, x->dA, x->labW,
-                          dbg ? x->dbg_dHs : nullptr);
+    as::launch_finish_f32(s, D.h, d, D.b_max, x->dH, x->Hf, x->zsum, x->lse2, x->lossr, x->dA, x->labW, nullptr);
     as::launch_colsum_sgd(s, d, D.b_max, (int)C, x->Z, C, b2, lr, dbg ? x->dbg_db2 : nullptr);
     as::launch_colsum_sgd(s, d, D.b_max, D.h, x->dA, D.h, b1, lr, dbg ? x->dbg_db1 : nullptr);
     if (dbg) cudaMemcpyAsync(x->dbg_dW2, x->dW2, 4 * (size_t)C * D.h, cudaMemcpyDeviceToDevice, s);
@@ -767,47 +795,81 @@ int as_set_batch_sizes(as_ctx *x, const int32_t *b, const float *lr) {
   return AS_OK;
 }
 
-// a11-a13 with the weights alpha[world] (identical on every rank): prescale,
-// all-reduce, momentum + reset + shadow, wbar / wbar_p rotation.
-static int merge_apply(as_ctx *x, const double *alpha) {
+// ---------------------------------------------------------------------------
+// Merge (steps a9-a13).  The weights alpha live on the device (alpha_d fp64,
+// alpha_f fp32): Alg. 2 runs in a one-thread kernel on the all-gathered norms
+// (the same code as the host export), so no host synchronisation is needed.
+static as::PeerArgs peer_args(const as_ctx *x) {
+  as::PeerArgs a{};
+  a.N = x->cfg.world;
+  a.rank = x->cfg.rank;
+  a.P = x->D.P;
+  a.w2_off = x->D.d * x->D.h + x->D.h;
+  a.w2_len = x->D.C * x->D.h;
+  a.gamma = (float)x->cfg.gamma;
+  a.off_w = (uint8_t *)x->w - x->arena;
+  a.off_wbarp = (uint8_t *)x->wbarp - x->arena;
+  a.off_w2b = (uint8_t *)x->w2b - x->arena;
+  a.off_flags = (uint8_t *)x->p2p_flags - x->arena;
+  a.off_norms = (uint8_t *)x->norms_all - x->arena;
+  for (int k = 0; k < a.N; ++k) a.base[k] = x->peer_base[k];
+  return a;
+}
+
+// cross-rank barrier over peer memory (AS_MERGE_P2P); my_norm (device,
+// nullable) is published into every rank's norms_all[rank] first
+static void p2p_barrier(as_ctx *x, const double *my_norm) {
+  as::PeerArgs a = peer_args(x);
+  a.epoch = ++x->p2p_epoch;
+  x->launches += 1;
+  as::launch_p2p_barrier(x->stream, a, my_norm);
+}
+
+// a11-a13 with the weights already in alpha_f (device), all replicas' training
+// complete (N > 1: after the first barrier / inside the NCCL stream order):
+// prescale, all-reduce, momentum + reset + shadow, wbar / wbar_p rotation.
+static int merge_apply_dev(as_ctx *x, float alpha_host_me /* NaN: unknown */) {
   const int N = x->cfg.world;
   const Dims &D = x->D;
   cudaStream_t s = x->stream;
-  x->launches += 1;                          // momentum (+1 below if a prescale kernel runs)
-  // a11: prescale; a12: allreduce over NVLink; a13: momentum + reset.
-  // N > 1: the prescale rides inside the allreduce (NCCL PreMulSum: every
-  // rank's input multiplied by its own alpha_i as it is reduced), saving an
-  // 8P-byte pass; plain prescale + sum if the op cannot be created.  N = 1:
-  // alpha = b / sum(b) = 1 exactly (Alg. 2 line 3, no perturbation, R14),
-  // so there is nothing to scale unless a caller-forced alpha differs.
-  const float a_me = (float)alpha[x->cfg.rank];
   const long long w2_off = D.d * D.h + D.h, w2_len = D.C * D.h;
+  if (x->cfg.merge_backend == AS_MERGE_P2P && N > 1) {
+    // ONE fused kernel over peer memory: sum alpha_k w_k of this rank's slice
+    // from every replica, momentum, pushed into every rank
+    x->launches += 1;
+    as::launch_merge_p2p(s, peer_args(x), x->alpha_f, x->wbar, x->wbarp);
+    p2p_barrier(x, nullptr);               // every slice has landed everywhere
+    std::swap(x->wbar, x->wbarp);
+    return cuda_check(x, cudaSuccess, "p2p merge launch");
+  }
+  // NCCL (N > 1, or a one-rank communicator with ADASGD_NCCL_SELF=1) or local
+  // (N = 1).  N > 1: the prescale rides inside the all-reduce (NCCL PreMulSum
+  // with the weight read from device memory), saving an 8P-byte pass; plain
+  // prescale + sum if the op cannot be created.
+  const bool use_nccl = x->comm != nullptr;
   // Partitioned merge ("multi-stream" transfer
   // overlapping the combine): the all-reduce runs chunk by chunk on the
   // communication stream and the momentum kernel of chunk c runs on the main
   // stream as soon as chunk c is reduced, overlapping the reduction of c+1.
   // ADASGD_MERGE_CHUNKS=k forces k chunks (also at N = 1, without a reduction:
   // tests the chunk bookkeeping on one GPU); default 8 for N > 1, 1 at N = 1.
-  // The NCCL path runs whenever the ctx has a communicator: N > 1, or N = 1
-  // with ADASGD_NCCL_SELF=1 (a one-rank communicator: exercises the PreMulSum
-  // all-reduce and its chunking on one GPU).
-  const bool use_nccl = x->comm != nullptr;
   const int K = x->merge_chunks > 0 ? x->merge_chunks : (N > 1 ? 8 : 1);
   ncclRedOp_t premul = ncclSum;
   bool have_premul = false;
   if (use_nccl) {
-    float a_host = a_me;
-    have_premul = ncclRedOpCreatePreMulSum(&premul, &a_host, ncclFloat, ncclScalarHostImmediate, x->comm) ==
-                  ncclSuccess;
+    have_premul = ncclRedOpCreatePreMulSum(&premul, x->alpha_f + x->cfg.rank, ncclFloat, ncclScalarDevice,
+                                           x->comm) == ncclSuccess;
     if (!have_premul) {
       x->launches += 1;
-      as::launch_scale(s, x->w, D.P, a_me);
+      as::launch_scale_dev(s, x->w, D.P, x->alpha_f + x->cfg.rank);
       premul = ncclSum;
     }
-  } else if (a_me != 1.0f) {
+  } else if (!(alpha_host_me == 1.0f)) {     // N = 1 without a communicator
     x->launches += 1;
-    as::launch_scale(s, x->w, D.P, a_me);
+    if (alpha_host_me == alpha_host_me) as::launch_scale(s, x->w, D.P, alpha_host_me);
+    else as::launch_scale_dev(s, x->w, D.P, x->alpha_f + x->cfg.rank);
   }
+  x->launches += K;
   if (K == 1) {
     if (use_nccl) {
       const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
@@ -816,9 +878,8 @@ static int merge_apply(as_ctx *x, const double *alpha) {
     }
     as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, w2_off, w2_len, x->w2b);
   } else {
-    cudaEventRecord(x->ev_mg[0], s);          // training, norms and any prescale are done
+    cudaEventRecord(x->ev_mg[0], s);          // training, weights and any prescale are done
     cudaStreamWaitEvent(x->comm_s, x->ev_mg[0], 0);
-    x->launches += K - 1;
     for (int c = 0; c < K; ++c) {
       const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
       if (use_nccl) {
@@ -840,52 +901,89 @@ static int merge_apply(as_ctx *x, const double *alpha) {
   return cuda_check(x, cudaSuccess, "merge launch");
 }
 
+static bool merge_transport_ready(const as_ctx *x) {
+  if (x->cfg.world == 1) return true;
+  return x->cfg.merge_backend == AS_MERGE_P2P ? x->p2p_ready : x->comm != nullptr;
+}
+
+// caller-given weights (host) -> device, then a11-a13
+static int merge_given(as_ctx *x, const double *alpha) {
+  const int N = x->cfg.world;
+  as::MergeWeightArgs wa{};
+  wa.N = N;
+  wa.mode = 2;
+  for (int i = 0; i < N; ++i) wa.given[i] = alpha[i];
+  if (x->cfg.merge_backend == AS_MERGE_P2P && N > 1) p2p_barrier(x, nullptr);   // training done everywhere
+  const bool need_dev = x->comm != nullptr || N > 1;
+  if (need_dev) {
+    x->launches += 1;
+    as::launch_alg2(x->stream, wa, x->norms_all, x->alpha_d, x->alpha_f, x->pert_dev);
+  }
+  return merge_apply_dev(x, need_dev ? NAN : (float)alpha[x->cfg.rank]);
+}
+
 int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
              int32_t *perturbed_out) {
   AS_GUARD(x);
   if (!u || !b) return as_fail(AS_E_INVALID, "u / b is NULL");
   const int N = x->cfg.world;
-  if (N > 1 && !x->comm)
-    return as_fail(AS_E_STATE, "as_merge needs an NCCL ctx (use as_group_merge in local-group mode)");
+  for (int i = 0; i < N; ++i)
+    if (u[i] < 0 || b[i] < 1) return as_fail(AS_E_INVALID, "need u[i] >= 0 and b[i] >= 1 (i = %d)", i);
+  if (!merge_transport_ready(x))
+    return as_fail(AS_E_STATE, x->cfg.merge_backend == AS_MERGE_P2P
+                                   ? "as_merge: peer mappings not open (as_p2p_export / as_p2p_open)"
+                                   : "as_merge needs an NCCL ctx (use as_group_merge in local-group mode)");
   const Dims &D = x->D;
   cudaStream_t s = x->stream;
   ph_begin(x, AS_PH_MERGE);
-  std::vector<double> norms(N), alpha(N);
-  int32_t pert = 0;
   int rc = AS_OK;
-  if (x->cfg.algo == AS_ALGO_ADAPTIVE && N == 1) {
+  int32_t pert_host = 0;
+  double alpha1 = 1.0;
+  if (N == 1) {
     // Alg. 2 with one replica: line 3 gives alpha = b / b = 1 and r = s, so
-    // the perturbation is skipped whatever the norm (R14): no norm pass, no
-    // host synchronisation
-    alpha[0] = 1.0;
-  } else if (x->cfg.algo == AS_ALGO_ADAPTIVE) {
-    // a9: replica norm
-    x->launches += 2;
-    as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev, (x->cfg.flags >> AS_NORM_METRIC_SHIFT) & 3);
-    if (N > 1) {
+    // the perturbation is skipped whatever the norm (R14); the comparison
+    // methods' 1/N is 1 too: no norm pass, no host synchronisation
+    rc = merge_given(x, &alpha1);
+  } else {
+    as::MergeWeightArgs wa{};
+    wa.N = N;
+    wa.mode = x->cfg.algo == AS_ALGO_ADAPTIVE ? 0 : 1;     // comparison methods: 1/N
+    wa.norm_mode = (x->cfg.flags & AS_FLAG_NORM_UB) ? 1 : 0;
+    wa.delta = x->cfg.delta;
+    wa.pert_thr = x->cfg.pert_thr;
+    for (int i = 0; i < N; ++i) { wa.u[i] = u[i]; wa.b[i] = b[i]; }
+    const bool adaptive = wa.mode == 0;
+    if (adaptive) {                           // a9: replica norm (fp64, fixed order)
+      x->launches += 2;
+      as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev,
+                       (x->cfg.flags >> AS_NORM_METRIC_SHIFT) & 3);
+    }
+    if (x->cfg.merge_backend == AS_MERGE_P2P) {
+      p2p_barrier(x, adaptive ? x->norm_dev : nullptr);   // norms all-gathered; training done everywhere
+    } else if (adaptive) {
       const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
       if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r)); }
-    } else {
-      cudaMemcpyAsync(x->norms_all, x->norm_dev, 8, cudaMemcpyDeviceToDevice, s);
     }
-    rc = cuda_check(x, cudaMemcpyAsync(norms.data(), x->norms_all, 8 * N, cudaMemcpyDeviceToHost, s), "norms D2H");
-    if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "norms");
-    if (rc) return rc;
-    // a10: merge weights (host, identical on all ranks)
-    rc = as_sched_alg2_ex(N, u, b, norms.data(), x->cfg.delta, x->cfg.pert_thr,
-                          (x->cfg.flags & AS_FLAG_NORM_UB) ? AS_NORM_UB : AS_NORM_UPDATES, alpha.data(), &pert);
-    if (rc) return rc;
-  } else {
-    // comparison methods: plain average, no norms
-    for (int i = 0; i < N; ++i) alpha[i] = 1.0 / N;
+    x->launches += 1;                         // a10: Alg. 2 on the device
+    as::launch_alg2(s, wa, x->norms_all, x->alpha_d, x->alpha_f, x->pert_dev);
+    rc = merge_apply_dev(x, NAN);
   }
-  rc = merge_apply(x, alpha.data());
-  if (rc) return rc;
   ph_end(x, AS_PH_MERGE);
+  if (rc) return rc;
   rc = cuda_check(x, cudaSuccess, "merge launch");
   if (rc) return rc;
-  if (alpha_out) std::copy(alpha.begin(), alpha.end(), alpha_out);
-  if (perturbed_out) *perturbed_out = pert;
+  if (N == 1) {
+    if (alpha_out) alpha_out[0] = alpha1;
+    if (perturbed_out) *perturbed_out = 0;
+  } else if (alpha_out || perturbed_out) {
+    std::vector<double> al(N);
+    rc = cuda_check(x, cudaMemcpyAsync(al.data(), x->alpha_d, 8 * N, cudaMemcpyDeviceToHost, s), "alpha D2H");
+    if (!rc) rc = cuda_check(x, cudaMemcpyAsync(&pert_host, x->pert_dev, 4, cudaMemcpyDeviceToHost, s), "pert D2H");
+    if (!rc) rc = cuda_check(x, cudaStreamSynchronize(s), "merge sync");
+    if (rc) return rc;
+    if (alpha_out) std::copy(al.begin(), al.end(), alpha_out);
+    if (perturbed_out) *perturbed_out = pert_host;
+  }
   return AS_OK;
 }
 
@@ -895,11 +993,82 @@ int as_merge_weighted(as_ctx *x, const double *alpha) {
   for (int i = 0; i < x->cfg.world; ++i)
     if (!(alpha[i] == alpha[i]) || alpha[i] < 0.0 || alpha[i] > 1e6)
       return as_fail(AS_E_INVALID, "alpha[%d] not a finite weight >= 0", i);
-  if (x->cfg.world > 1 && !x->comm) return as_fail(AS_E_STATE, "as_merge_weighted needs an NCCL ctx");
+  if (!merge_transport_ready(x)) return as_fail(AS_E_STATE, "as_merge_weighted: merge transport not ready");
   ph_begin(x, AS_PH_MERGE);
-  const int rc = merge_apply(x, alpha);
+  const int rc = merge_given(x, alpha);
   ph_end(x, AS_PH_MERGE);
   return rc;
+}
+
+// ---- AS_MERGE_P2P setup ----------------------------------------------------
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+struct P2PRecord {
+  uint32_t magic;
+  int32_t rank, world, device;
+  uint64_t offset;                // workspace offset inside its allocation
+  uint64_t bytes;                 // workspace bytes
+  cudaIpcMemHandle_t handle;      // 64 bytes
+  uint8_t pad[AS_P2P_EXPORT_BYTES - 32 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(P2PRecord) == AS_P2P_EXPORT_BYTES, "P2P record size");
+constexpr uint32_t kP2PMagic = 0x41535032u;   // "ASP2"
+
+int as_p2p_export(as_ctx *x, void *out) {
+  AS_GUARD(x);
+  if (!out) return as_fail(AS_E_INVALID, "out is NULL");
+  static PFN_getAddressRange range = nullptr;
+  if (!range) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return as_fail(AS_E_CUDA, "cuMemGetAddressRange entry point missing");
+    range = (PFN_getAddressRange)p;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)x->arena) != CUDA_SUCCESS)
+    return as_fail(AS_E_CUDA, "cuMemGetAddressRange failed on the workspace");
+  P2PRecord r{};
+  r.magic = kP2PMagic;
+  r.rank = x->cfg.rank;
+  r.world = x->cfg.world;
+  r.device = x->cfg.device;
+  r.offset = (uint64_t)((CUdeviceptr)x->arena - base);
+  r.bytes = x->cfg.workspace_bytes;
+  const int rc = cuda_check(x, cudaIpcGetMemHandle(&r.handle, (void *)base), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  memcpy(out, &r, sizeof(r));
+  return AS_OK;
+}
+
+int as_p2p_open(as_ctx *x, const void *records) {
+  AS_GUARD(x);
+  if (!records) return as_fail(AS_E_INVALID, "records is NULL");
+  if (x->cfg.merge_backend != AS_MERGE_P2P) return as_fail(AS_E_STATE, "ctx merge_backend is not AS_MERGE_P2P");
+  if (x->p2p_ready) return as_fail(AS_E_STATE, "peer mappings already open");
+  const int N = x->cfg.world;
+  const P2PRecord *rec = (const P2PRecord *)records;
+  for (int k = 0; k < N; ++k)
+    if (rec[k].magic != kP2PMagic || rec[k].rank != k || rec[k].world != N ||
+        rec[k].bytes != x->cfg.workspace_bytes)
+      return as_fail(AS_E_INVALID, "P2P record %d invalid (magic / rank order / world / workspace size)", k);
+  for (int k = 0; k < N; ++k) {
+    if (k == x->cfg.rank) { x->peer_base[k] = x->arena; continue; }
+    void *p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, rec[k].handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < k; ++j)
+        if (j != x->cfg.rank && x->peer_map[j]) { cudaIpcCloseMemHandle(x->peer_map[j]); x->peer_map[j] = nullptr; }
+      cudaGetLastError();
+      return as_fail(AS_E_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", k, cudaGetErrorString(e));
+    }
+    x->peer_map[k] = p;
+    x->peer_base[k] = (uint8_t *)p + rec[k].offset;
+  }
+  x->p2p_ready = true;
+  return AS_OK;
 }
 
 int as_replica_norm(as_ctx *x, int32_t metric, double *out) {

@@ -137,7 +137,8 @@ void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long l
 void launch_row_lse(cudaStream_t s, const StepDesc *desc, int b_max, int C, const float *Z,
                     float *lse2);
 void launch_softmax_grad(cudaStream_t s, const StepDesc *desc, int b_max, int C,
-                         const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2);
+                         const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2,
+                         int part /* 1: softmax / B, 2: label term, 3: both */);
 void launch_finish_f32(cudaStream_t s, int h, const StepDesc *desc, int b_max, const float *dH,
                        const float *Hf, const float *zsum, const float *lse2, float *lossr,
                        float *dA, const float *labW, float *dbg_dHs);
@@ -148,6 +149,27 @@ void launch_sgd_dense(cudaStream_t s, long long n, float *param, const float *gr
                       __nv_bfloat16 *shadow);
 void launch_loss_mean(cudaStream_t s, const StepDesc *desc, const float *lossr, float *loss);
 // merge (steps a9-a13)
+constexpr int kMaxWorld = 64;                   // == AS_MAX_WORLD of adasgd.h
+struct MergeWeightArgs {                        // k_alg2 (by value)
+  int N, mode, norm_mode;                       // mode 0: Alg. 2, 1: uniform 1/N, 2: given
+  double delta, pert_thr;
+  int32_t u[kMaxWorld], b[kMaxWorld];
+  double given[kMaxWorld];
+};
+struct PeerArgs {                               // peer-memory merge (by value)
+  int N, rank;
+  unsigned long long epoch;
+  long long P, w2_off, w2_len;
+  float gamma;
+  long long off_w, off_wbarp, off_w2b, off_flags, off_norms;   // byte offsets in every workspace
+  uint8_t *base[kMaxWorld];                     // workspace of rank k, mapped here
+};
+void launch_scale_dev(cudaStream_t s, float *w, long long P, const float *alpha);
+void launch_alg2(cudaStream_t s, const MergeWeightArgs &a, const double *norms, double *alpha_d, float *alpha_f,
+                 int32_t *pert);
+void launch_p2p_barrier(cudaStream_t s, const PeerArgs &a, const double *my_norm);
+void launch_merge_p2p(cudaStream_t s, const PeerArgs &a, const float *alpha_f, const float *wbar,
+                      const float *wbarp);
 void launch_sumsq(cudaStream_t s, const float *w, long long P, double *partials, int nblocks,
                   double *out_norm, int metric);
 void launch_scale(cudaStream_t s, float *w, long long P, float alpha);

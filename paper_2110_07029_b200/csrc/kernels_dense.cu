@@ -2,6 +2,7 @@
 // merge kernels (steps a9-a13).  P:N = PAPER.md line N; Rk = DESIGN.md.
 #include <cfloat>
 
+#include "alg2.h"
 #include "common.cuh"
 
 namespace as {
@@ -233,11 +234,15 @@ __global__ void k_softmax_labels(const StepDesc *__restrict__ desc, int C,
 }
 
 void launch_softmax_grad(cudaStream_t s, const StepDesc *desc, int b_max, int C,
-                         const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2) {
-  dim3 g(ceil_div(C, 256 * 8) < 64 ? ceil_div(C, 256 * 8) : 64, b_max);
-  if (g.x < 1) g.x = 1;
-  k_softmax<<<g, 256, 0, s>>>(desc, C, Z, lse2);
-  k_softmax_labels<<<ceil_div(b_max, 128), 128, 0, s>>>(desc, C, lab_ptr, lab, Z);
+                         const int64_t *lab_ptr, const int32_t *lab, float *Z, const float *lse2,
+                         int part) {
+  if (part & 1) {                 // Z <- softmax(Z) / B
+    dim3 g(ceil_div(C, 256 * 8) < 64 ? ceil_div(C, 256 * 8) : 64, b_max);
+    if (g.x < 1) g.x = 1;
+    k_softmax<<<g, 256, 0, s>>>(desc, C, Z, lse2);
+  }
+  if (part & 2)                   // Z -= T / B (R3)
+    k_softmax_labels<<<ceil_div(b_max, 128), 128, 0, s>>>(desc, C, lab_ptr, lab, Z);
 }
 
 // dA = dH * [A > 0]; loss_r = LSE_r - zsum_r
@@ -250,8 +255,7 @@ __global__ void k_finish_f32(const StepDesc *__restrict__ desc, int h, const flo
   if (r >= desc->rows) return;
   const size_t i = (size_t)r * h + j;
   dA[i] = Hf[i] > 0.f ? dH[i] : 0.f;
-  // softmax part of dH (tests): dH + (1/k_r) sum_y W2T[y] / B removes the label term
-  if (dbg_dHs) dbg_dHs[i] = dH[i] + labW[i] / (float)desc->rows;
+  (void)labW; (void)dbg_dHs;
   if (j == 0) lossr[r] = lse2[r] * 0.69314718055994531f - zsum[r];
 }
 
@@ -334,6 +338,139 @@ __global__ void k_scale(float *__restrict__ w, long long P, float alpha) {
 
 void launch_scale(cudaStream_t s, float *w, long long P, float alpha) {
   k_scale<<<148 * 8, 256, 0, s>>>(w, P, alpha);
+}
+
+// a11 with the weight in device memory (the device-computed alpha_rank)
+__global__ void k_scale_dev(float *__restrict__ w, long long P, const float *__restrict__ alpha) {
+  const float a = *alpha;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+       i += (long long)gridDim.x * blockDim.x)
+    w[i] *= a;
+}
+
+void launch_scale_dev(cudaStream_t s, float *w, long long P, const float *alpha) {
+  k_scale_dev<<<148 * 8, 256, 0, s>>>(w, P, alpha);
+}
+
+// a10 on the device: Alg. 2 from the all-gathered norms (as::alg2_weights, the
+// same code as the host export), or the comparison methods' uniform 1/N, or
+// caller-given weights.  One thread; writes alpha in fp64 and fp32 and the
+// perturbation flag.  A zero normaliser (rejected on the host before launch)
+// cannot occur here.
+__global__ void k_alg2(MergeWeightArgs a, const double *__restrict__ norms, double *__restrict__ alpha_d,
+                       float *__restrict__ alpha_f, int32_t *__restrict__ pert) {
+  double al[kMaxWorld];
+  int32_t pt = 0;
+  if (a.mode == 0) {
+    if (alg2_weights(a.N, a.u, a.b, norms, a.delta, a.pert_thr, a.norm_mode, al, &pt) != 0)
+      for (int i = 0; i < a.N; ++i) al[i] = 0.0;
+  } else if (a.mode == 1) {
+    for (int i = 0; i < a.N; ++i) al[i] = 1.0 / (double)a.N;
+  } else {
+    for (int i = 0; i < a.N; ++i) al[i] = a.given[i];
+  }
+  for (int i = 0; i < a.N; ++i) {
+    alpha_d[i] = al[i];
+    alpha_f[i] = (float)al[i];
+  }
+  *pert = pt;
+}
+
+void launch_alg2(cudaStream_t s, const MergeWeightArgs &a, const double *norms, double *alpha_d, float *alpha_f,
+                 int32_t *pert) {
+  k_alg2<<<1, 1, 0, s>>>(a, norms, alpha_d, alpha_f, pert);
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory merge (AS_MERGE_P2P).  Every rank's workspace is mapped into
+// every other rank (CUDA IPC over NVLink / NVSwitch); buffers are addressed as
+// base[k] + offset (identical carve on every rank).
+//
+// Barrier: rank r writes `epoch` into flags[r] of every rank (after its
+// optional payload, e.g. its norm into norms[r]) with a system-scope release,
+// then waits until its own flags[k] >= epoch for every k (acquire).
+__global__ void k_p2p_barrier(PeerArgs a, const double *__restrict__ my_norm) {
+  const int k = threadIdx.x;
+  if (k < a.N) {
+    uint8_t *pb = a.base[k];
+    if (my_norm) reinterpret_cast<volatile double *>(pb + a.off_norms)[a.rank] = *my_norm;
+    __threadfence_system();
+    unsigned long long *f = reinterpret_cast<unsigned long long *>(pb + a.off_flags) + a.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.epoch) : "memory");
+  }
+  if (k < a.N) {
+    const unsigned long long *mine = reinterpret_cast<const unsigned long long *>(a.base[a.rank] + a.off_flags) + k;
+    unsigned long long v = 0;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= a.epoch) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+void launch_p2p_barrier(cudaStream_t s, const PeerArgs &a, const double *my_norm) {
+  k_p2p_barrier<<<1, kMaxWorld, 0, s>>>(a, my_norm);
+}
+
+// a11-a13 fused: rank r owns elements [lo, hi) (multiples of 4 floats); for
+// each of them S = sum_k alpha_k w_k (peer loads, replica order),
+// w' = S + gamma (wbar - wbar_p) (this rank's copies; identical on every
+// rank), then w' is pushed into every rank's replica and new global model
+// (the wbar_p buffer, which becomes wbar after the pointer rotation) and, in
+// the W2T range, its bf16 shadow.  Slice r of every replica is read and
+// written only by rank r, so no ordering beyond the two barriers is needed.
+__global__ void __launch_bounds__(256) k_merge_p2p(PeerArgs a, const float *__restrict__ alpha_f,
+                                                   const float *__restrict__ wbar,
+                                                   const float *__restrict__ wbarp) {
+  __shared__ float al[kMaxWorld];
+  if (threadIdx.x < a.N) al[threadIdx.x] = alpha_f[threadIdx.x];
+  __syncthreads();
+  const long long nv = a.P / 4;                         // whole float4 vectors
+  const long long v0 = nv * a.rank / a.N, v1 = nv * (a.rank + 1) / a.N;
+  for (long long v = v0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
+       v += (long long)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < a.N; ++k) {
+      const float4 x = reinterpret_cast<const float4 *>(a.base[k] + a.off_w)[v];
+      const float c = al[k];
+      acc.x = fmaf(c, x.x, acc.x); acc.y = fmaf(c, x.y, acc.y);
+      acc.z = fmaf(c, x.z, acc.z); acc.w = fmaf(c, x.w, acc.w);
+    }
+    const float4 g = reinterpret_cast<const float4 *>(wbar)[v], q = reinterpret_cast<const float4 *>(wbarp)[v];
+    float4 o;
+    o.x = acc.x + a.gamma * (g.x - q.x); o.y = acc.y + a.gamma * (g.y - q.y);
+    o.z = acc.z + a.gamma * (g.z - q.z); o.w = acc.w + a.gamma * (g.w - q.w);
+    const long long i = 4 * v;
+    const bool sh = i >= a.w2_off && i < a.w2_off + a.w2_len;
+    const uint2 ob = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+    for (int k = 0; k < a.N; ++k) {
+      uint8_t *pb = a.base[k];
+      reinterpret_cast<float4 *>(pb + a.off_w)[v] = o;
+      reinterpret_cast<float4 *>(pb + a.off_wbarp)[v] = o;
+      if (sh) reinterpret_cast<uint2 *>(pb + a.off_w2b)[(i - a.w2_off) / 4] = ob;
+    }
+  }
+  // the tail P % 4 (last rank)
+  if (a.rank == a.N - 1 && blockIdx.x == 0 && threadIdx.x < (int)(a.P - 4 * nv)) {
+    const long long i = 4 * nv + threadIdx.x;
+    float acc = 0.f;
+    for (int k = 0; k < a.N; ++k) acc = fmaf(al[k], reinterpret_cast<const float *>(a.base[k] + a.off_w)[i], acc);
+    const float o = acc + a.gamma * (wbar[i] - wbarp[i]);
+    for (int k = 0; k < a.N; ++k) {
+      reinterpret_cast<float *>(a.base[k] + a.off_w)[i] = o;
+      reinterpret_cast<float *>(a.base[k] + a.off_wbarp)[i] = o;
+      if (i >= a.w2_off && i < a.w2_off + a.w2_len)
+        reinterpret_cast<__nv_bfloat16 *>(a.base[k] + a.off_w2b)[i - a.w2_off] = __float2bfloat16_rn(o);
+    }
+  }
+}
+
+void launch_merge_p2p(cudaStream_t s, const PeerArgs &a, const float *alpha_f, const float *wbar,
+                      const float *wbarp) {
+  k_merge_p2p<<<148 * 4, 256, 0, s>>>(a, alpha_f, wbar, wbarp);
 }
 
 // a13: w' = S + gamma (wbar - wbar_p) written over wbar_p (pointer rotation

@@ -15,6 +15,7 @@
 #include <string>
 
 #include "adasgd.h"
+#include "alg2.h"
 #include "common_host.h"
 
 extern "C" {
@@ -169,41 +170,9 @@ int as_sched_alg2_ex(int32_t N, const int32_t *u, const int32_t *b, const double
                      int32_t *perturbed_out) {
   if (N < 1 || !u || !b || !norms || !alpha_out || (norm_mode != AS_NORM_UPDATES && norm_mode != AS_NORM_UB))
     return as_fail(AS_E_INVALID, "as_sched_alg2: bad arguments");
-  bool all_equal = true;
-  for (int i = 1; i < N; ++i)
-    if (u[i] != u[0]) all_equal = false;
-  if (all_equal) {  // line 3: alpha_i = b_i / sum(b)
-    int64_t sb = 0;
-    for (int i = 0; i < N; ++i) sb += b[i];
-    if (sb <= 0) return as_fail(AS_E_INVALID, "as_sched_alg2: sum(b) == 0");
-    for (int i = 0; i < N; ++i) alpha_out[i] = (double)b[i] / (double)sb;
-  } else if (norm_mode == AS_NORM_UPDATES) {  // line 5: alpha_i = u_i / sum(u)
-    int64_t su = 0;
-    for (int i = 0; i < N; ++i) su += u[i];
-    for (int i = 0; i < N; ++i) alpha_out[i] = (double)u[i] / (double)su;
-  } else {  // P:175 variant: alpha_i = u_i b_i / sum(u b)
-    int64_t sub = 0;
-    for (int i = 0; i < N; ++i) sub += (int64_t)u[i] * b[i];
-    if (sub <= 0) return as_fail(AS_E_INVALID, "as_sched_alg2: sum(u b) == 0");
-    for (int i = 0; i < N; ++i) alpha_out[i] = (double)((int64_t)u[i] * b[i]) / (double)sub;
-  }
-  int32_t pert = 0;
-  bool regular = true;  // line 7
-  for (int i = 0; i < N; ++i)
-    if (!(norms[i] < pert_thr)) regular = false;
-  if (regular) {
-    int r = 0, s = 0;
-    for (int i = 1; i < N; ++i) {
-      if (u[i] > u[r] || (u[i] == u[r] && b[i] > b[r])) r = i;
-      if (u[i] < u[s] || (u[i] == u[s] && b[i] < b[s])) s = i;
-    }
-    if (!(u[r] == u[s] && b[r] == b[s])) {  // line 9
-      alpha_out[r] = alpha_out[r] * (1.0 + delta);
-      alpha_out[s] = alpha_out[s] * (1.0 - delta);
-      pert = 1;
-    }
-  }
-  if (perturbed_out) *perturbed_out = pert;
+  if (as::alg2_weights(N, u, b, norms, delta, pert_thr, norm_mode == AS_NORM_UB ? 1 : 0, alpha_out,
+                       perturbed_out) != 0)
+    return as_fail(AS_E_INVALID, "as_sched_alg2: zero normaliser (sum(b) or sum(u b))");
   return AS_OK;
 }
 

@@ -122,3 +122,15 @@ def broadcast_nccl_id(dist, rank, device=None, make_id=None):
         buf.copy_(torch.frombuffer(bytearray(make_id()), dtype=torch.uint8))
     dist.broadcast(buf, src=0)
     return bytes(buf.cpu().numpy().tobytes())
+
+
+def open_p2p(rep, dist):
+    """AS_MERGE_P2P setup: all-gather every rank's export record over the
+    torch.distributed group (plumbing) and map the peers' workspaces."""
+    import torch
+    mine = torch.frombuffer(bytearray(rep.p2p_export()), dtype=torch.uint8)
+    backend = dist.get_backend()
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    parts = [torch.zeros_like(mine, device=dev) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, mine.to(dev))
+    rep.p2p_open([bytes(p.cpu().numpy().tobytes()) for p in parts])
