@@ -150,7 +150,7 @@ def oracle_baseline(ds, p, cfg, steps=2):
     for k in range(steps):
         bt = otrain.batch_of(ds, ocsr.stream_ids(k * cfg.b_max, cfg.b_max, ds.n))
         g = om.gradients_chunked(bt, prm, chunk=128)
-        prm = {key: (np.asarray(prm[key], np.float64) - 0.1 * g[key]).astype(np.float32)
+        prm = {key: (np.asarray(prm[key], np.float64) - 0.1 * g["d" + key]).astype(np.float32)
                for key in ("W1", "b1", "W2T", "b2")}
     w = np.concatenate([prm[key].ravel() for key in ("W1", "b1", "W2T", "b2")])
     norm = omerge.replica_norm(w)

@@ -68,10 +68,15 @@ def batch_of(dataset, ids):
     return bt
 
 
-def run(dataset, init, cfg: RunConfig, costs, total_samples, order=None, log_steps=False):
+def run(dataset, init, cfg: RunConfig, costs, total_samples, order=None, log_steps=False, logs=None):
     """Adaptive SGD over ``total_samples`` stream samples.  Returns a list of
     per-mega-batch records (routing log, u, b, lr, norms, alpha, perturbed,
-    wbar) and the final global model."""
+    wbar) and the final global model.
+
+    logs (optional): the dispatch log [(replica, start, rows)] of every
+    mega-batch as a LIVE run observed it ("dispatched one-by-one based
+    on GPU availability"); the oracle then follows it instead of replaying the
+    cost models, and u_i counts the batches dispatched to replica i."""
     N = cfg.world
     wbar = np.asarray(init, np.float32).copy()
     wbar_p = wbar.copy()                                   # reading R17
@@ -89,7 +94,11 @@ def run(dataset, init, cfg: RunConfig, costs, total_samples, order=None, log_ste
             ids = ocsr.stream_ids(_pos + start, rows, dataset.n, order)
             return int(np.sum(rp[ids + 1] - rp[ids]))
 
-        if cfg.algo == "adaptive":
+        if logs is not None:
+            log = [tuple(x) for x in logs[len(records)]]
+            u, clocks = [sum(1 for x in log if x[0] == i) for i in range(N)], None
+            assert sorted(x for (_, s0, r0) in log for x in range(s0, s0 + r0)) == list(range(Mm))
+        elif cfg.algo == "adaptive":
             log, u, clocks = osched.route_replay(costs, b, Mm, nnz_of)
         else:
             log, u, clocks = osched.route_static(costs, b, Mm, nnz_of)

@@ -870,33 +870,26 @@ static int merge_apply_dev(as_ctx *x, float alpha_host_me /* NaN: unknown */) {
     else as::launch_scale_dev(s, x->w, D.P, x->alpha_f + x->cfg.rank);
   }
   x->launches += K;
-  if (K == 1) {
-    if (use_nccl) {
-      const ncclResult_t r = ncclAllReduce(x->w, x->w, D.P, ncclFloat, premul, x->comm, s);
-      if (have_premul) ncclRedOpDestroy(premul, x->comm);
-      if (r != ncclSuccess) { x->sticky = AS_E_NCCL; return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r)); }
-    }
-    as::launch_momentum(s, x->w, x->wbarp, x->wbar, D.P, (float)x->cfg.gamma, w2_off, w2_len, x->w2b);
-  } else {
-    cudaEventRecord(x->ev_mg[0], s);          // training, weights and any prescale are done
+  if (use_nccl) {                             // training, weights and any prescale are done
+    cudaEventRecord(x->ev_mg[0], s);
     cudaStreamWaitEvent(x->comm_s, x->ev_mg[0], 0);
-    for (int c = 0; c < K; ++c) {
-      const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
-      if (use_nccl) {
-        const ncclResult_t r = ncclAllReduce(x->w + off, x->w + off, len, ncclFloat, premul, x->comm, x->comm_s);
-        if (r != ncclSuccess) {
-          if (have_premul) ncclRedOpDestroy(premul, x->comm);
-          x->sticky = AS_E_NCCL;
-          return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
-        }
+  }
+  for (int c = 0; c < K; ++c) {
+    const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
+    if (use_nccl) {
+      const ncclResult_t r = ncclAllReduce(x->w + off, x->w + off, len, ncclFloat, premul, x->comm, x->comm_s);
+      if (r != ncclSuccess) {
+        if (have_premul) ncclRedOpDestroy(premul, x->comm);
+        x->sticky = AS_E_NCCL;
+        return as_fail(AS_E_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
       }
       cudaEventRecord(x->ev_mg[1 + (c & 1)], x->comm_s);
       cudaStreamWaitEvent(s, x->ev_mg[1 + (c & 1)], 0);
-      as::launch_momentum(s, x->w + off, x->wbarp + off, x->wbar + off, len, (float)x->cfg.gamma, w2_off - off,
-                          w2_len, x->w2b);
     }
-    if (have_premul) ncclRedOpDestroy(premul, x->comm);
+    as::launch_momentum(s, x->w + off, x->wbarp + off, x->wbar + off, len, (float)x->cfg.gamma, w2_off - off,
+                        w2_len, x->w2b);
   }
+  if (have_premul) ncclRedOpDestroy(premul, x->comm);
   std::swap(x->wbar, x->wbarp);
   return cuda_check(x, cudaSuccess, "merge launch");
 }

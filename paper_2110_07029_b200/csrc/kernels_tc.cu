@@ -361,8 +361,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   const int splits = fwd_splits(B, n_cblocks, gridDim.x, max_splits);
   const int rt = blockIdx.x / splits, sp = blockIdx.x % splits;
   if (rt >= RT) return;
-  const int cb0 = (int)((long long)sp * n_cblocks / splits);
-  const int nloc = (int)((long long)(sp + 1) * n_cblocks / splits) - cb0;
+  (void)sp;                                   // the role branches recompute cb0 / nloc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = 10, kMmaWarp = 11;  // highest ids: scheduler priority; 8-9 idle
 
@@ -389,6 +388,13 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 
   if (warp == kProdWarp) {
     AS_REG_DEC();
+    // split range recomputed after setmaxnreg from an opaque copy (the
+    // compiler otherwise spills the prologue's values across the role switch)
+    int ncq_ = n_cblocks;
+    asm volatile("" : "+r"(ncq_));
+    const int splits_ = fwd_splits(B, ncq_, gridDim.x, max_splits);
+    const int cb0 = (int)((long long)(blockIdx.x % splits_) * ncq_ / splits_);
+    const int nloc = (int)((long long)(blockIdx.x % splits_ + 1) * ncq_ / splits_) - cb0;
     if (lane == 0) {  // ---------------- TMA producer
       mbar_expect_tx(h_full, TILE);
       for (int a = 0; a < H / 64; ++a) tma_load_2d(&mapH, h_full, sH + a * ATOM_BYTES, a * 64, rt * BM);
@@ -405,6 +411,13 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     }
   } else if (warp == kMmaWarp) {
     AS_REG_DEC();
+    // split range recomputed after setmaxnreg from an opaque copy (the
+    // compiler otherwise spills the prologue's values across the role switch)
+    int ncq_ = n_cblocks;
+    asm volatile("" : "+r"(ncq_));
+    const int splits_ = fwd_splits(B, ncq_, gridDim.x, max_splits);
+    const int cb0 = (int)((long long)(blockIdx.x % splits_) * ncq_ / splits_);
+    const int nloc = (int)((long long)(blockIdx.x % splits_ + 1) * ncq_ / splits_) - cb0;
     {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
       constexpr uint32_t idS = idesc_bf16(BM, BM, 0, 0);
       constexpr uint32_t idO = idesc_bf16(BM, H, 0, 1);
@@ -455,6 +468,13 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     }
   } else if (warp < 4 * NWG) {  // ---------------- softmax warpgroups (thread = row)
     AS_REG_INC();
+    // split range recomputed after setmaxnreg from an opaque copy (the
+    // compiler otherwise spills the prologue's values across the role switch)
+    int ncq_ = n_cblocks;
+    asm volatile("" : "+r"(ncq_));
+    const int splits_ = fwd_splits(B, ncq_, gridDim.x, max_splits);
+    const int cb0 = (int)((long long)(blockIdx.x % splits_) * ncq_ / splits_);
+    const int nloc = (int)((long long)(blockIdx.x % splits_ + 1) * ncq_ / splits_) - cb0;
     const int g = warp >> 2;
     const int q = warp & 3;
     const int row = q * 32 + lane;            // TMEM lane == tile row == loader index
@@ -723,17 +743,29 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   // p_full[PH b + half]: G^T of one 64-row half of the unit in S^T buffer b is
   // in TMEM; the dW MMA of that half starts without waiting for the other
   constexpr int PH = UNIT / 64;
-  uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + NSB,
+  // RING (h = 128): a unit's S^T is computed in two 64-row halves whose TMEM
+  // columns alternate with the WG's unit parity p: S half 0 at 64 p, half 1 at
+  // 64 (1 - p), G^T (packed bf16) at 64 p + 32 half.  Half 1's columns are free
+  // as soon as the softmax has loaded them (s_free), so the first half of the
+  // WG's NEXT unit is computed while this one is still in the softmax, and the
+  // second half as soon as this unit's dW has read its G^T (MMA order).
+#ifdef AS_X_NORING
+  constexpr bool RING = false;
+#else
+  constexpr bool RING = UNIT == 128;
+#endif
+  constexpr int SF = RING ? 2 * NSB : NSB;        // s_full per buffer (and half)
+  uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + SF,
            *wt_full = p_full + PH * NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
-           *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1;
-  uint32_t *tmem_slot = (uint32_t *)(wf_full + 1);
+           *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1, *s_free = wf_full + 1;
+  uint32_t *tmem_slot = (uint32_t *)(s_free + NSB);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
 
   const int B = desc->rows;
   const int RT = (B + BM - 1) / BM;               // 128-row H tiles
   const int NU = HPT * RT;                        // units per class block
-  const int NB = blockIdx.x < n_cblocks ? (n_cblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int NT = NB * NU;                         // units of this CTA
+  // NB (class blocks of this CTA) and NT = NB * NU (its units) are computed in
+  // each role branch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kProdWarp = 12, kMmaWarp = 13;   // highest ids: scheduler priority
 #ifdef AS_X_SWAPROLES
@@ -744,7 +776,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSH; ++i) { mbar_init(&h_full[i], 1); mbar_init(&h_empty[i], 1); }
-    for (int i = 0; i < NSB; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < SF; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < NSB; ++i) mbar_init(&s_free[i], 4);
     for (int i = 0; i < PH * NSB; ++i) mbar_init(&p_full[i], 4);
     for (int i = 0; i < NWT; ++i) mbar_init(&wt_full[i], 4);
     mbar_init(dw_full, 1);
@@ -768,6 +801,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #define AS_REG_INC2() asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory")
   if (warp == kProdWarp) {
     AS_REG_DEC2();
+    // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
+    // the compiler reusing the prologue's value, which it otherwise spills)
+    int nbq_ = n_cblocks;
+    asm volatile("" : "+r"(nbq_));
+    const int NB = blockIdx.x < nbq_ ? (nbq_ - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int NT = NB * NU;
+    (void)NT;
     if (lane == 0) {  // ---------------- TMA producer (H tiles)
       TRACE_INIT;
       int it = 0;
@@ -788,6 +828,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     }
   } else if (warp == kMmaWarp) {
     AS_REG_DEC2();
+    // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
+    // the compiler reusing the prologue's value, which it otherwise spills)
+    int nbq_ = n_cblocks;
+    asm volatile("" : "+r"(nbq_));
+    const int NB = blockIdx.x < nbq_ ? (nbq_ - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int NT = NB * NU;
+    (void)NT;
     {  // ---------------- MMA issuer (warp-converged; one elected lane issues)
       constexpr uint32_t idS = idesc_bf16(BM, UNIT, 0, 0); // S^T_u = W2T_blk . H_u^T
       constexpr uint32_t idW = idesc_bf16(BM, H, 0, 1);    // dW2T += G^T_u . H_u
@@ -852,6 +899,58 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       };
       Cur cs{0, 0, 0, 0, 0, 0, 0u, 0u, 0u}, cd{0, 0, 0, 0, 0, 0, 0u, 0u, 0u};
       int ns = 0;                             // S units issued
+      if constexpr (RING) {
+        // unit gu belongs to WG gu % 2 (buffer b = gu % NSB), its parity within
+        // the WG is p = (gu / 2) & 1: S half h at columns 64 ((h + p) & 1)
+        constexpr uint32_t idS64 = idesc_bf16(BM, 64, 0, 0);
+        auto issue_S_half = [&](const Cur &c, int half, int par) {
+          if (half == 0) {
+            if (c.v == 0) mbar_wait(&wt_full[c.wb], c.wph);
+            if (c.hh == 0) mbar_wait(&h_full[c.st], c.hph);
+          }
+          fence_after();
+#ifndef AS_X_NOMMA1
+          mma_grp_ts_k_8(tmem + c.b * UNIT + (uint32_t)(((half + par) & 1) * 64), tmem + COL_W + c.wb * WCOLS,
+                         sdesc(aH + c.st * TILE + half * 64 * 128, 16, 1024), idS64, 0u);
+#endif
+          mma_commit_w(&s_full[2 * c.b + half]);
+        };
+        for (; ns < NT && ns < NSB; ++ns) {
+          issue_S_half(cs, 0, 0);
+          issue_S_half(cs, 1, 0);
+          advance(cs);
+        }
+        for (int gu = 0; gu < NT; ++gu) {
+          const uint32_t gcol = cd.b * UNIT + (uint32_t)(((gu >> 1) & 1) * 64);   // G^T of unit gu
+          const int pn = ((gu + NSB) >> 1) & 1;                                    // parity of unit gu + 2
+          const bool nxt = ns < NT;
+          mbar_wait(&p_full[PH * cd.b], cd.bph);
+          if (cd.v == 0 && cd.kb >= 1) { mbar_wait(dw_empty, dwe_ph); dwe_ph ^= 1u; }
+          fence_after();
+#ifndef AS_X_NOMMA2
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + gcol, sdesc(aH + cd.st * TILE, ATOM_BYTES, 1024), idW,
+                          cd.v > 0 ? 1u : 0u);
+#endif
+          if (nxt) {                          // S half 0 of the WG's next unit: into the columns
+            mbar_wait(&s_free[cd.b], cd.bph); // this unit's half 1 has left (loaded by the softmax)
+            issue_S_half(cs, 0, pn);
+          }
+          mbar_wait(&p_full[PH * cd.b + 1], cd.bph);
+          fence_after();
+#ifndef AS_X_NOMMA2
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + gcol + 32, sdesc(aH + cd.st * TILE + 64 * 128, ATOM_BYTES, 1024),
+                          idW, 1u);
+#endif
+          if (cd.hh == HPT - 1) mma_commit_w(&h_empty[cd.st]);
+          if (cd.v == NU - 1) mma_commit_w(dw_full);
+          if (nxt) {                          // half 1: after this unit's dW (in-order MMA)
+            issue_S_half(cs, 1, pn);
+            advance(cs);
+            ++ns;
+          }
+          advance(cd);
+        }
+      } else {
       for (; ns < NT && ns < NSB; ++ns) { issue_S(cs); advance(cs); }
       for (int gu = 0; gu < NT; ++gu) {
         do_dw(cd);
@@ -864,9 +963,17 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         }
         advance(cd);
       }
+      }
     }
   } else if (warp >= kSoftLo && warp < kSoftLo + 8) {  // ---------------- softmax warpgroups (units gu % 2 == g)
     AS_REG_INC2();
+    // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
+    // the compiler reusing the prologue's value, which it otherwise spills)
+    int nbq_ = n_cblocks;
+    asm volatile("" : "+r"(nbq_));
+    const int NB = blockIdx.x < nbq_ ? (nbq_ - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int NT = NB * NU;
+    (void)NT;
     const int g = (warp - kSoftLo) >> 2;
     const int q = warp & 3;
     const int i = q * 32 + lane;              // class inside the block (TMEM lane)
@@ -940,10 +1047,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         cp_async_commit();
       }
       TRACE(1, tix == 0, 6, v);
-      mbar_wait(&s_full[b], sph);
+      if constexpr (!RING) mbar_wait(&s_full[b], sph);
       TRACE(1, tix == 0, 7, v);
       fence_after();
       cp_async_wait<1>();                     // this unit's bitmap (all but the newest group)
+      const uint32_t par = RING ? (uint32_t)(jj & 1) : 0u;   // column parity of this unit (RING)
       uint32_t mk[4];
       if constexpr (UNIT == 128) {
         const uint4 q4 = sMk[(jj & 1) * 256 + tix];
@@ -956,12 +1064,22 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #pragma unroll 1
       for (int half = 0; half < UNIT / 64; ++half) {   // 64 rows of the unit at a time
         uint32_t r0[32], r1[32];
-        AS_TMEM_LD32(tl + b * UNIT + half * 64, r0);
-        AS_TMEM_LD32(tl + b * UNIT + half * 64 + 32, r1);
+        const uint32_t scol = RING ? (uint32_t)(((half + (int)par) & 1) * 64) : (uint32_t)(half * 64);
+        if constexpr (RING) {
+          mbar_wait(&s_full[2 * b + half], sph);
+          fence_after();
+        }
+        AS_TMEM_LD32(tl + b * UNIT + scol, r0);
+        AS_TMEM_LD32(tl + b * UNIT + scol + 32, r1);
         // lse' = LSE_r * log2e + log2 B of these 64 rows (smem broadcast)
         const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v % HPT) * UNIT + half * 64);
         AS_TMEM_WAIT_LD(r0);
         AS_TMEM_WAIT_LD(r1);
+        if (RING && half == 1) {              // half 1's S columns are free for the next unit
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[b]);
+        }
         uint32_t pk[32];                      // 64 bf16 of G^T, packed in pairs
         uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
         const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
@@ -1026,7 +1144,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         }
         // G^T over S^T columns already consumed (cols [32 half, 32 half + 32)),
         // then this half's dW MMA may start
-        AS_TMEM_ST32(tl + b * UNIT + half * 32, pk);
+        AS_TMEM_ST32(tl + b * UNIT + (RING ? par * 64u : 0u) + half * 32, pk);
         tmem_wait_st();
         fence_before();
         __syncwarp();
@@ -1034,10 +1152,17 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       }
       TRACE(1, tix == 0, 8, v);
 #else
+      if constexpr (RING) {
+        mbar_wait(&s_full[2 * b], sph);
+        mbar_wait(&s_full[2 * b + 1], sph);
+      }
       fence_before();
       __syncwarp();
-      if (lane == 0)
+      if (lane == 0) {
         for (int hf = 0; hf < PH; ++hf) mbar_arrive(&p_full[PH * b + hf]);
+        if (RING) mbar_arrive(&s_free[b]);
+      }
+      (void)par;
 #endif
       TRACE(1, tix == 0, 9, v);
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
@@ -1060,6 +1185,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
     }
   } else if (warp >= kUpdLo && warp < kUpdLo + 4) {  // ---------------- update warps
+    // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
+    // the compiler reusing the prologue's value, which it otherwise spills)
+    int nbq_ = n_cblocks;
+    asm volatile("" : "+r"(nbq_));
+    const int NB = blockIdx.x < nbq_ ? (nbq_ - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int NT = NB * NU;
+    (void)NT;
     const int q = warp & 3;
     const int i = q * 32 + lane;              // thread = class (TMEM lane)
     const int ut = threadIdx.x - kUpdLo * 32;  // 0..127
@@ -1135,48 +1267,75 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         // 32-column boxes, conflict-free), bf16 shadow into its staging boxes
         mbar_wait(wf_full, kb & 1);
         const uint32_t sw = (uint32_t)(i & 7);
-        const uint32_t aWf = smem_u32(sT) + i * 128;
+        uint8_t *rowWf = reinterpret_cast<uint8_t *>(sT) + i * 128;
         const int cls_i = cb * BM + i;
+        // chunk c + 1's TMEM load is in flight while chunk c is updated; the
+        // accumulator is released as soon as the last chunk is in registers
+        // (the MMA warp waits for it before block kb + 1's first dW)
+        uint32_t ra[32], rb[32];
+        AS_TMEM_LD32(tl + COL_DW, ra);
+        auto sgd_chunk = [&](int ch, uint32_t (&r)[32]) {
+#ifndef AS_X_NOUPD
+#pragma unroll
+          for (int g0 = 0; g0 < 8; g0 += 4) {   // 4 swizzled 16-B rows at a time (register budget)
+            float4 w[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              w[g] = *reinterpret_cast<const float4 *>(rowWf + ch * 16384 + (((uint32_t)(g0 + g) ^ sw) << 4));
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              w[g].x = fmaf(-lr, __uint_as_float(r[4 * (g0 + g)]), w[g].x);
+              w[g].y = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 1]), w[g].y);
+              w[g].z = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 2]), w[g].z);
+              w[g].w = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 3]), w[g].w);
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              *reinterpret_cast<float4 *>(rowWf + ch * 16384 + (((uint32_t)(g0 + g) ^ sw) << 4)) = w[g];
+            if (cls_i < C) {                  // bf16 shadow: 8 columns per 16-byte store
+#pragma unroll
+              for (int g = 0; g < 4; g += 2)
+                *reinterpret_cast<uint4 *>(W2b + (size_t)cls_i * H + ch * 32 + 4 * (g0 + g)) =
+                    make_uint4(pack_bf16x2(w[g].x, w[g].y), pack_bf16x2(w[g].z, w[g].w),
+                               pack_bf16x2(w[g + 1].x, w[g + 1].y), pack_bf16x2(w[g + 1].z, w[g + 1].w));
+            }
+          }
+#endif
+          if (dbg_dW2T && cls_i < C) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls_i * H + ch * 32 + k] = __uint_as_float(r[k]);
+          }
+        };
+        static_assert(NCH == 4, "h = 128: four 32-column chunks");
+#ifdef AS_X_UPD_PIPE
+        AS_TMEM_WAIT_LD(ra);
+        AS_TMEM_LD32(tl + COL_DW + 32, rb);
+        sgd_chunk(0, ra);
+        AS_TMEM_WAIT_LD(rb);
+        AS_TMEM_LD32(tl + COL_DW + 64, ra);
+        sgd_chunk(1, rb);
+        AS_TMEM_WAIT_LD(ra);
+        AS_TMEM_LD32(tl + COL_DW + 96, rb);
+        sgd_chunk(2, ra);
+        AS_TMEM_WAIT_LD(rb);
+        fence_before();                       // accumulator free for block kb + 1
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dw_empty);
+        sgd_chunk(3, rb);
+#else
+        (void)rb;
 #pragma unroll 1
         for (int ch = 0; ch < NCH; ++ch) {
-          uint32_t r[32];
-          AS_TMEM_LD32(tl + COL_DW + ch * 32, r);
-          AS_TMEM_WAIT_LD(r);
-          if (ch == NCH - 1) {                  // accumulator free for block kb+1
+          if (ch) AS_TMEM_LD32(tl + COL_DW + ch * 32, ra);
+          AS_TMEM_WAIT_LD(ra);
+          if (ch == NCH - 1) {                  // accumulator free for block kb + 1
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dw_empty);
           }
-#ifndef AS_X_NOUPD
-#pragma unroll
-          for (int g = 0; g < 8; g += 2) {
-            float4 w0, w1;
-            const uint32_t a0 = aWf + ch * 16384 + (((uint32_t)g ^ sw) << 4);
-            const uint32_t a1 = aWf + ch * 16384 + (((uint32_t)(g + 1) ^ sw) << 4);
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(w0.x), "=f"(w0.y), "=f"(w0.z), "=f"(w0.w) : "r"(a0));
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(w1.x), "=f"(w1.y), "=f"(w1.z), "=f"(w1.w) : "r"(a1));
-            w0.x -= lr * __uint_as_float(r[4 * g]);     w0.y -= lr * __uint_as_float(r[4 * g + 1]);
-            w0.z -= lr * __uint_as_float(r[4 * g + 2]); w0.w -= lr * __uint_as_float(r[4 * g + 3]);
-            w1.x -= lr * __uint_as_float(r[4 * g + 4]); w1.y -= lr * __uint_as_float(r[4 * g + 5]);
-            w1.z -= lr * __uint_as_float(r[4 * g + 6]); w1.w -= lr * __uint_as_float(r[4 * g + 7]);
-            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a0), "f"(w0.x), "f"(w0.y),
-                         "f"(w0.z), "f"(w0.w) : "memory");
-            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a1), "f"(w1.x), "f"(w1.y),
-                         "f"(w1.z), "f"(w1.w) : "memory");
-            if (cls_i < C)                    // bf16 shadow: 8 columns, one 16-byte store
-              *reinterpret_cast<uint4 *>(W2b + (size_t)cls_i * H + ch * 32 + 4 * g) =
-                  make_uint4(pack_bf16x2(w0.x, w0.y), pack_bf16x2(w0.z, w0.w), pack_bf16x2(w1.x, w1.y),
-                             pack_bf16x2(w1.z, w1.w));
-          }
-#endif
-          if (dbg_dW2T) {
-            const int cls = cb * BM + i;
-            if (cls < C)
-              for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls * H + ch * 32 + k] = __uint_as_float(r[k]);
-          }
+          sgd_chunk(ch, ra);
         }
+#endif
         // (2) block kb + NWT's W2T already in TMEM (put_wt above)
         // (3) TMA store of the updated block, then the next block's fp32 W2T
         //     into the same buffer once the store has read it

@@ -134,3 +134,89 @@ def open_p2p(rep, dist):
     parts = [torch.zeros_like(mine, device=dev) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, mine.to(dev))
     rep.p2p_open([bytes(p.cpu().numpy().tobytes()) for p in parts])
+
+
+# ---------------------------------------------------------------------------
+# Live event-timed routing ("batches are dispatched one-by-one based on
+# GPU availability. Whenever a GPU finishes an epoch, it is assigned the next
+# batch"; P:193-195 the scheduler counts u_i at dispatch).  One process per
+# replica: a rank claims its next min(b_i, M - claimed) samples from the shared
+# cursor (as_live_claim) as soon as its previous batch has COMPLETED on its
+# device; the first dispatch of a mega-batch goes in id order (R8).  Every
+# batch's device time is recorded, giving the trace (replica, rows, nnz, ps)
+# from which the replay cost models are fitted (R9, as_sched_fit_cost).
+# ---------------------------------------------------------------------------
+def run_live(rank, world, dist, cursor, row_ptr, n, state, M, total, train_fn, merge_fn=None, order=None):
+    """train_fn(gpos, rows) -> picoseconds the batch took (it returns after the
+    batch completed).  merge_fn(u, b_used) runs the merge (steps a9-a13).
+    Returns per-mega-batch records: log [(replica, start, rows)] in dispatch
+    (cursor) order, u, b, and trace [(replica, start, rows, nnz, ps)]."""
+    pos, recs = 0, []
+    while pos < total:
+        Mm = int(min(M, total - pos))
+        pre = stream_nnz_prefix(row_ptr, n, pos, Mm, order)
+        if rank == 0:
+            cursor.reset()
+        dist.barrier()
+        b_me = int(state.b[rank])
+        mine = []
+        claim = None
+        for k in range(world):                 # first dispatch in id order (R8)
+            if k == rank:
+                claim = cursor.claim(Mm, b_me)
+            dist.barrier()
+        start, rows = claim
+        while rows > 0:
+            ps = int(train_fn(pos + start, rows))
+            mine.append((rank, int(start), int(rows), int(pre[start + rows] - pre[start]), ps))
+            start, rows = cursor.claim(Mm, b_me)
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        trace = sorted([t for part in every for t in part], key=lambda t: t[1])
+        log = [(t[0], t[1], t[2]) for t in trace]
+        u = [sum(1 for t in trace if t[0] == i) for i in range(world)]
+        assert sum(t[2] for t in trace) == Mm          # samples conserved (R8)
+        b_used = list(state.b)
+        if merge_fn is not None:
+            merge_fn(u, b_used)
+        state.rescale(u)
+        recs.append({"log": log, "u": u, "b": b_used, "trace": trace, "samples": Mm, "pos": pos})
+        pos += Mm
+    return recs
+
+
+def fit_live_costs(recs, world):
+    """Replay cost model of every replica fitted to the live trace (R9)."""
+    out = []
+    for i in range(world):
+        tr = [t for r in recs for t in r["trace"] if t[0] == i]
+        out.append(sched.fit_cost([t[2] for t in tr], [t[3] for t in tr], [t[4] for t in tr]))
+    return out
+
+
+def replay_live(recs, costs, row_ptr, n, order=None):
+    """Replay every recorded mega-batch with the given cost models and the
+    batch sizes that were in force: the logs the replay scheduler produces."""
+    out = []
+    for r in recs:
+        pre = stream_nnz_prefix(row_ptr, n, r["pos"], r["samples"], order)
+        log, u, _ = sched.route_replay(costs, r["b"], r["samples"], pre)
+        out.append(log)
+    return out
+
+
+def gpu_train_fn(rep, stream=None):
+    """train_fn for run_live on a replica: load the stream batch, run the SGD
+    step and time it with CUDA events on the replica stream (returns ps)."""
+    import torch
+    s = stream or rep.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def fn(gpos, rows):
+        e0.record(s)
+        rep.load_batch_stream(gpos, rows)
+        rep.train_step(False)
+        e1.record(s)
+        e1.synchronize()
+        return int(round(e0.elapsed_time(e1) * 1e9))
+    return fn

@@ -107,3 +107,80 @@ def test_two_processes_nccl_merge(gpu_lib):
     if torch.cuda.device_count() < 2:
         pytest.skip("AS_MERGE_NCCL across processes needs 2 GPUs (one rank per device)")
     _run("nccl", "adaptive")
+
+
+def _live_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_07029_b200 import driver, sched
+    from paper_2110_07029_b200.api import Replica
+    torch.cuda.set_device(0)
+    cfg = synthgen.CONFIGS["tiny"]
+    ds = synthgen.make_dataset(cfg)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    name = "/adasgd_glive_%d" % port
+    if rank == 0:
+        cur = sched.LiveCursor(name, create=True)
+    dist.barrier()
+    if rank != 0:
+        cur = sched.LiveCursor(name, create=False)
+    rep = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=cfg.b_min, beta=cfg.beta, megabatch=1024,
+                  max_row_nnz=int(np.diff(ds.row_ptr).max()), max_row_labels=int(np.diff(ds.lab_ptr).max()),
+                  lr0=0.5, precision="fp32", rank=rank, world=world, device=0, merge_backend="p2p")
+    driver.open_p2p(rep, dist)
+    rep.upload_dataset(ds)
+    st = driver.ReplayState(world, cfg.b_max, cfg.b_min, cfg.beta, 0.5, synthgen.make_cost_models(world))
+    alphas = []
+
+    def merge_fn(u, b):
+        a, _ = rep.merge(u, b, want_alpha=True)
+        alphas.append(list(a))
+    recs = driver.run_live(rank, world, dist, cur, ds.row_ptr, ds.n, st, 1024, ds.n, driver.gpu_train_fn(rep),
+                           merge_fn=merge_fn)
+    np.save(os.path.join(outdir, "wbar%d.npy" % rank), rep.get_params(1))
+    if rank == 0:
+        import pickle
+        with open(os.path.join(outdir, "recs.pkl"), "wb") as f:
+            pickle.dump({"recs": recs, "alphas": alphas}, f)
+    dist.barrier()
+    cur.close()
+    rep.close()
+    dist.destroy_process_group()
+
+
+def test_two_processes_live_routing_p2p_one_gpu(gpu_lib):
+    """Live event-timed routing on the device: two replica
+    processes claim batches from the shared cursor when their previous batch
+    has completed (CUDA events), u_i counted at dispatch, merged over peer
+    memory.  The oracle follows the observed dispatch logs: alpha bit-exact,
+    global model within 1e-4 (fp32); the trace gives per-replica cost fits."""
+    import pickle
+    import torch.multiprocessing as mp
+    from paper_2110_07029_b200 import driver
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_live_worker, args=(world, _free_port(), d), nprocs=world, join=True,
+                           start_method="spawn")
+        wbar = [np.load(os.path.join(d, "wbar%d.npy" % r)) for r in range(world)]
+        with open(os.path.join(d, "recs.pkl"), "rb") as f:
+            got = pickle.load(f)
+    recs = got["recs"]
+    cfg = synthgen.CONFIGS["tiny"]
+    ds = synthgen.make_dataset(cfg)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    ocfg = otrain.RunConfig(d=cfg.d, C=cfg.C, h=cfg.h, b_max=cfg.b_max, b_min=cfg.b_min, beta=cfg.beta,
+                            M=1024, lr0=0.5, world=world)
+    orecs, owbar = otrain.run(ds, p, ocfg, None, ds.n, logs=[r["log"] for r in recs])
+    assert len(orecs) == len(recs) == 4
+    for g, o, a in zip(recs, orecs, got["alphas"]):
+        assert g["u"] == o["u"] and g["b"] == o["b"]
+        assert a == o["alpha"]
+    assert np.array_equal(wbar[0], wbar[1])
+    e = max(np.linalg.norm(wbar[0].astype(np.float64) - owbar) / np.linalg.norm(owbar),
+            np.max(np.abs(wbar[0] - owbar)) / np.max(np.abs(owbar)))
+    assert e <= 1e-4, e
+    fitted = driver.fit_live_costs(recs, world)
+    assert all(f[0] + f[1] * cfg.b_max + f[2] > 0 for f in fitted)

@@ -139,3 +139,77 @@ def test_two_ranks_merge_protocol_matches_oracle():
         assert a0 == oa and p0 == op
         ow, _ = omerge.merge(reps, oa, wbar, wbar_p, 0.9)
         np.testing.assert_allclose(m0, ow, rtol=0, atol=1e-7)
+
+
+# true per-replica speeds of the simulated "devices" (R9 integer model, ps):
+# replica 0: 2 ms + 2 ms per row; replica 1 the same x 7/4 (a 75% slower GPU)
+LIVE_COSTS = [(2_000_000_000, 2_000_000_000, 0, 1, 1), (2_000_000_000, 2_000_000_000, 0, 7, 4)]
+
+
+def _live_worker(rank, world, port, q):
+    """Live event-timed routing over the shared cursor: each
+    rank claims its next batch when its previous one has completed; the batch
+    'runs' by sleeping its true cost; per-batch durations are recorded."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import time
+        from paper_2110_07029_b200 import driver, sched
+        ds = synthgen.tiny_dataset(n=200, d=50, C=30, seed=12)
+        name = "/adasgd_live_%d" % port
+        if rank == 0:
+            cur = sched.LiveCursor(name, create=True)
+        dist.barrier()
+        if rank != 0:
+            cur = sched.LiveCursor(name, create=False)
+        st = driver.ReplayState(world, 8, 2, 2, 0.1, LIVE_COSTS)
+        c0, cr, cz, num, den = LIVE_COSTS[rank]
+        row_ptr = ds.row_ptr
+
+        def train_fn(gpos, rows):
+            ids = (np.arange(rows) + gpos) % ds.n
+            nnz = int(np.sum(row_ptr[ids + 1] - row_ptr[ids]))
+            t0 = time.perf_counter_ns()
+            time.sleep(((c0 + cr * rows + cz * nnz) * num // den) * 1e-12)
+            return (time.perf_counter_ns() - t0) * 1000        # ns -> ps
+        recs = driver.run_live(rank, world, dist, cur, row_ptr, ds.n, st, 60, 120, train_fn)
+        dist.barrier()
+        cur.close()
+        if rank == 0:
+            q.put(recs)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_live_routing_trace_fit_replays_bit_exactly():
+    """Live dispatch on completion with a shared cursor across two processes,
+    the per-batch trace fitted to replay cost models (as_sched_fit_cost), and
+    the replay scheduler (as_sched_route_replay) on the fitted models
+    reproducing the live dispatch log of every mega-batch exactly (the
+    simulated speeds keep every dispatch decision >= 2 ms from a tie)."""
+    from paper_2110_07029_b200 import driver
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_live_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    recs = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ds = synthgen.tiny_dataset(n=200, d=50, C=30, seed=12)
+    assert len(recs) == 2
+    for r in recs:
+        cover = sorted(x for (_, s, rows) in r["log"] for x in range(s, s + rows))
+        assert cover == list(range(60))                     # every sample of the mega-batch once
+        assert r["u"][1] < r["u"][0]                        # the slower replica takes fewer batches
+    fitted = driver.fit_live_costs(recs, 2)
+    for i, f in enumerate(fitted):                          # fitted speeds close to the true ones
+        c0, cr, _, num, den = LIVE_COSTS[i]
+        true8 = (c0 + 8 * cr) * num // den
+        fit8 = f[0] + 8 * f[1]
+        assert abs(fit8 - true8) <= 0.1 * true8, (i, f)
+    replayed = driver.replay_live(recs, fitted, ds.row_ptr, ds.n)
+    for r, log in zip(recs, replayed):
+        assert [tuple(x) for x in log] == [tuple(x) for x in r["log"]]
