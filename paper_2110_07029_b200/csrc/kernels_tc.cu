@@ -794,11 +794,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   // registers: 128 per thread at launch; warpgroup 3 (producer, MMA, 2 idle
-  // warps) drops to 40 and the two softmax warpgroups rise to 168 (a whole
-  // 64-column S^T unit plus its lse' values in registers); the update
-  // warpgroup keeps 128.
+  // warps) drops to 40.  h = 128: the softmax warpgroups keep 128 (their code
+  // fits) and the update warpgroup rises to 208 so that it can drain the whole
+  // dW2T accumulator (128 fp32 per lane) in one go; h = 256: the softmax
+  // warpgroups rise to 168 and the update warpgroup keeps 128.
 #define AS_REG_DEC2() asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory")
-#define AS_REG_INC2() asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory")
+#define AS_REG_INC2() do { if constexpr (H != 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory"); } while (0)
+#define AS_REG_UPD() asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory")
   if (warp == kProdWarp) {
     AS_REG_DEC2();
     // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
@@ -1185,6 +1187,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if (sb >= NSB) { sb -= NSB; sph ^= 1u; }
     }
   } else if (warp >= kUpdLo && warp < kUpdLo + 4) {  // ---------------- update warps
+#ifdef AS_X_EARLYREL
+    if constexpr (TMAUPD) AS_REG_UPD();
+#endif
     // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
     // the compiler reusing the prologue's value, which it otherwise spills)
     int nbq_ = n_cblocks;
@@ -1265,19 +1270,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         // fused SGD of the block from the TMEM accumulator (lane i = class i)
         // and the TMA-loaded fp32 block: W2T -= lr dW2T in place (swizzled
         // 32-column boxes, conflict-free), bf16 shadow into its staging boxes
-        mbar_wait(wf_full, kb & 1);
         const uint32_t sw = (uint32_t)(i & 7);
         uint8_t *rowWf = reinterpret_cast<uint8_t *>(sT) + i * 128;
         const int cls_i = cb * BM + i;
-        // chunk c + 1's TMEM load is in flight while chunk c is updated; the
-        // accumulator is released as soon as the last chunk is in registers
-        // (the MMA warp waits for it before block kb + 1's first dW)
-        uint32_t ra[32], rb[32];
-        AS_TMEM_LD32(tl + COL_DW, ra);
-        auto sgd_chunk = [&](int ch, uint32_t (&r)[32]) {
+        auto sgd_chunk = [&](int ch, const uint32_t (&r)[32]) {
 #ifndef AS_X_NOUPD
 #pragma unroll
-          for (int g0 = 0; g0 < 8; g0 += 4) {   // 4 swizzled 16-B rows at a time (register budget)
+          for (int g0 = 0; g0 < 8; g0 += 4) {   // 4 swizzled 16-B rows at a time
             float4 w[4];
 #pragma unroll
             for (int g = 0; g < 4; ++g)
@@ -1292,13 +1291,15 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #pragma unroll
             for (int g = 0; g < 4; ++g)
               *reinterpret_cast<float4 *>(rowWf + ch * 16384 + (((uint32_t)(g0 + g) ^ sw) << 4)) = w[g];
-            if (cls_i < C) {                  // bf16 shadow: 8 columns per 16-byte store
+#ifdef AS_X_ROWSHADOW
+            if (cls_i < C) {                  // bf16 shadow: 8 columns per 16-byte store (row per thread)
 #pragma unroll
               for (int g = 0; g < 4; g += 2)
                 *reinterpret_cast<uint4 *>(W2b + (size_t)cls_i * H + ch * 32 + 4 * (g0 + g)) =
                     make_uint4(pack_bf16x2(w[g].x, w[g].y), pack_bf16x2(w[g].z, w[g].w),
                                pack_bf16x2(w[g + 1].x, w[g + 1].y), pack_bf16x2(w[g + 1].z, w[g + 1].w));
             }
+#endif
           }
 #endif
           if (dbg_dW2T && cls_i < C) {
@@ -1307,28 +1308,34 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           }
         };
         static_assert(NCH == 4, "h = 128: four 32-column chunks");
-#ifdef AS_X_UPD_PIPE
-        AS_TMEM_WAIT_LD(ra);
-        AS_TMEM_LD32(tl + COL_DW + 32, rb);
-        sgd_chunk(0, ra);
-        AS_TMEM_WAIT_LD(rb);
-        AS_TMEM_LD32(tl + COL_DW + 64, ra);
-        sgd_chunk(1, rb);
-        AS_TMEM_WAIT_LD(ra);
-        AS_TMEM_LD32(tl + COL_DW + 96, rb);
-        sgd_chunk(2, ra);
-        AS_TMEM_WAIT_LD(rb);
+#ifdef AS_X_EARLYREL
+        // the whole accumulator (lane i = class i, 128 fp32) into registers at
+        // once, then it is released: block kb + 1's first dW MMA waits only for
+        // these loads, not for the SGD below (this warpgroup runs with 208
+        // registers, AS_REG_UPD; measured no faster than releasing after the
+        // last chunk's load, which is the default)
+        uint32_t racc[128];
+        AS_TMEM_LD64(tl + COL_DW, racc);
+        AS_TMEM_LD64(tl + COL_DW + 64, (racc + 64));
+        AS_TMEM_WAIT_LD64(racc);
+        AS_TMEM_WAIT_LD64((racc + 64));
         fence_before();                       // accumulator free for block kb + 1
         __syncwarp();
         if (lane == 0) mbar_arrive(dw_empty);
-        sgd_chunk(3, rb);
+        TRACE(3, ut == 0, 15, kb);
+        mbar_wait(wf_full, kb & 1);           // this block's fp32 W2T (TMA, issued a block ahead)
+        sgd_chunk(0, *reinterpret_cast<const uint32_t(*)[32]>(racc));
+        sgd_chunk(1, *reinterpret_cast<const uint32_t(*)[32]>(racc + 32));
+        sgd_chunk(2, *reinterpret_cast<const uint32_t(*)[32]>(racc + 64));
+        sgd_chunk(3, *reinterpret_cast<const uint32_t(*)[32]>(racc + 96));
 #else
-        (void)rb;
+        mbar_wait(wf_full, kb & 1);
 #pragma unroll 1
-        for (int ch = 0; ch < NCH; ++ch) {
-          if (ch) AS_TMEM_LD32(tl + COL_DW + ch * 32, ra);
+        for (int ch = 0; ch < NCH; ++ch) {    // chunk by chunk; released after the last load
+          uint32_t ra[32];
+          AS_TMEM_LD32(tl + COL_DW + ch * 32, ra);
           AS_TMEM_WAIT_LD(ra);
-          if (ch == NCH - 1) {                  // accumulator free for block kb + 1
+          if (ch == NCH - 1) {
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dw_empty);
@@ -1341,10 +1348,33 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         //     into the same buffer once the store has read it
         fence_proxy_async();
         named_bar(3, 128);
-        if (ut == 0) {
 #ifndef AS_X_NOUPD
+        if (ut == 0) {
           for (int c = 0; c < 4; ++c) tma_store_2d(&mapWf, (uint8_t *)sT + c * 16384, c * 32, cb * BM);
           bulk_commit();
+        }
+#ifndef AS_X_ROWSHADOW
+        // bf16 shadow of the updated block, coalesced: 16 threads per class row,
+        // 16 bytes (8 columns) each, read from the swizzled fp32 boxes
+#pragma unroll 4
+        for (int k = 0; k < 16; ++k) {
+          const int idx = k * 128 + ut;
+          const int row = idx >> 4, c8 = idx & 15;
+          const int cls = cb * BM + row;
+          const uint8_t *rb = reinterpret_cast<const uint8_t *>(sT) + (c8 >> 2) * 16384 + row * 128;
+          const uint32_t g0 = (uint32_t)((c8 & 3) * 2), rs = (uint32_t)(row & 7);
+          const float4 a = *reinterpret_cast<const float4 *>(rb + ((g0 ^ rs) << 4));
+          const float4 b = *reinterpret_cast<const float4 *>(rb + (((g0 + 1) ^ rs) << 4));
+          if (cls < C)
+            *reinterpret_cast<uint4 *>(W2b + (size_t)cls * H + 8 * c8) =
+                make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                           pack_bf16x2(b.z, b.w));
+        }
+        named_bar(3, 128);                    // every thread's reads of the block are done
+#endif
+#endif
+        if (ut == 0) {
+#ifndef AS_X_NOUPD
           bulk_wait_read0();
 #endif
           if (kb + 1 < NB) {

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+export ADASGD_NO_BUILD=1
+P=paper_2110_07029_b200
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "one_step_parity or full_size_amazon670k_sampled or label_heavy or rescale or deterministic" > gpurun_out/t_gpu_r02f.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/t_gpu_r02f.log
+for rep in 1 2; do for v in libadasgd_x_oldupd libadasgd libadasgd_x_noupd libadasgd_x_nosoft libadasgd_x_emu0; do
+  ADASGD_LIB=$PWD/$P/$v.so timeout -s KILL 120 python scripts/x_probe.py amazon670k 2>&1 | tail -1
+done; done | tee gpurun_out/x_probe_upd2.log
+ADASGD_LIB=$PWD/$P/libadasgd_trace.so timeout -s KILL 120 python scripts/trace_stats.py > gpurun_out/trace_upd2.txt 2>&1; tail -22 gpurun_out/trace_upd2.txt
