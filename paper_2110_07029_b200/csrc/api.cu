@@ -72,6 +72,7 @@ struct as_ctx {
   float *lw;
   float *Hf;
   __nv_bfloat16 *Hb;
+  __nv_bfloat16 *Hx;          // pass 2's B_ext rows (FOLD): [bpad][16]
   float *dA, *lse2, *lsep, *zsum, *labW, *lossr, *loss;
   float *pm, *pl, *pO;
   float *db1p;                // db1 partials of the fused combine
@@ -215,6 +216,7 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(16 * D.C); if (x) x->cls_lab = (int4 *)p;
   p = P(4 * (size_t)D.bpad * D.h); if (x) x->Hf = (float *)p;
   p = P(2 * (size_t)D.bpad * D.h); if (x) x->Hb = (__nv_bfloat16 *)p;
+  p = P(2 * 16 * (size_t)D.bpad); if (x) x->Hx = (__nv_bfloat16 *)p;
   p = P(4 * (size_t)D.b_max * D.h); if (x) x->dA = (float *)p;
   p = P(4 * (size_t)D.bpad); if (x) x->lse2 = (float *)p;
   p = P(4 * (size_t)D.bpad); if (x) x->lsep = (float *)p;
@@ -433,7 +435,7 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   }
   if (!rc && cfg->precision == AS_BF16) {
     x->plan = (as::TcPlan *)malloc(as::tc_plan_bytes());
-    if (as::tc_plan_init(x->plan, D.h, D.b_max, D.C, x->num_sms, x->Hb, x->w2b, x->w + D.d * D.h + D.h) != 0)
+    if (as::tc_plan_init(x->plan, D.h, D.b_max, D.C, x->num_sms, x->Hb, x->w2b, x->w + D.d * D.h + D.h, x->Hx) != 0)
       rc = as_fail(AS_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point missing?)");
   }
   if (!rc && cfg->world == 1 && getenv("ADASGD_NCCL_SELF") && atoi(getenv("ADASGD_NCCL_SELF")) > 0) {
@@ -715,7 +717,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
                             x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lab_ptr, x->lse2, x->lsep, x->wrow,
                             x->lossr, x->dA, x->db1p, x->db1cnt, b1, lr, dbg ? x->dbg_db1 : nullptr,
-                            dbg ? x->dbg_dHs : nullptr);
+                            dbg ? x->dbg_dHs : nullptr, as::tc_fold(D.h) ? x->Hx : nullptr);
     ph_end(x, AS_PH_COMBINE);
     cudaStreamWaitEvent(s, x->ev_join, 0);   // label transpose ready
     // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2

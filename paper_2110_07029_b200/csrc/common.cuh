@@ -128,7 +128,8 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          int splits, const float *pm, const float *pl, const float *pO,
                          const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
                          float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
-                         int *db1cnt, float *b1, float lr, float *dbg_db1, float *dbg_dHs);
+                         int *db1cnt, float *b1, float lr, float *dbg_db1, float *dbg_dHs,
+                         __nv_bfloat16 *Hx /* FOLD B_ext rows [bpad][16], nullable */);
 // fp32 (SIMT) output layer (steps a5/a6 in parity mode)
 void launch_gemm_f32(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
                      long long sak, const float *B, long long sbk, long long sbn, float *Cm,
@@ -187,7 +188,8 @@ void launch_f32_to_bf16(cudaStream_t s, const float *src, __nv_bfloat16 *dst, lo
 struct TcPlan;
 size_t tc_plan_bytes();
 int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const void *Hb,
-                 const void *W2b, const void *W2T);
+                 const void *W2b, const void *W2T, const void *Hx);
+bool tc_fold(int h);   // pass 2 takes b2 and -(LSE + ln B) in its S^T MMA (B_ext rows from the combine)
 int tc_splits(int h, int b_max, long long C, int num_sms);
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
                        const float *b2, float *pm, float *pl, float *pO);

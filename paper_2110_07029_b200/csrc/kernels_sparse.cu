@@ -204,19 +204,35 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     float *__restrict__ lse2, float *__restrict__ lsep, float *__restrict__ wrow,
     float *__restrict__ lossr, float *__restrict__ dA, float *__restrict__ db1p,
     int *__restrict__ db1cnt, float *__restrict__ b1, float lr, float *__restrict__ dbg_db1,
-    float *__restrict__ dbg_dHs) {
+    float *__restrict__ dbg_dHs, __nv_bfloat16 *__restrict__ Hx) {
   griddep_wait();
+  // pass 2's B_ext row (the FOLD K-step): [1, 1, 1, -(LSE_r + ln B) in three
+  // bf16 parts, 0 ...]; padding rows -1e30 (p = 0)
+  auto put_hx = [&](int row, float negL) {
+    if (!Hx) return;
+    const float hi = __bfloat162float(__float2bfloat16_rn(negL));
+    const float r1 = negL - hi;
+    const float mid = __bfloat162float(__float2bfloat16_rn(r1));
+    const float lo = r1 - mid;
+    uint4 *o = reinterpret_cast<uint4 *>(Hx + (size_t)row * 16);
+    o[0] = make_uint4(pack_bf16x2(1.f, 1.f), pack_bf16x2(1.f, hi), pack_bf16x2(mid, lo), 0u);
+    o[1] = make_uint4(0u, 0u, 0u, 0u);
+  };
   // CTA = 32 rows x COMBINE_CW columns (8 warps); partial reads coalesced over rows
   const int rx = threadIdx.x & 31, jy = threadIdx.x >> 5;
   const int B = desc->rows;
   if (blockIdx.x * 32 >= B) {         // a CTA of padding rows only
     const int r = blockIdx.x * 32 + rx;
-    if (jy == 0 && r < bpad && blockIdx.y == 0) { lsep[r] = INFINITY; wrow[r] = 0.f; }
+    if (jy == 0 && r < bpad && blockIdx.y == 0) { lsep[r] = INFINITY; wrow[r] = 0.f; put_hx(r, -1e30f); }
     return;
   }
   const bool live = blockIdx.x * 32 + rx < B;
   const int r = live ? blockIdx.x * 32 + rx : B - 1;   // padding lanes shadow a live row
-  if (!live && jy == 0 && blockIdx.y == 0) { lsep[blockIdx.x * 32 + rx] = INFINITY; wrow[blockIdx.x * 32 + rx] = 0.f; }
+  if (!live && jy == 0 && blockIdx.y == 0) {
+    lsep[blockIdx.x * 32 + rx] = INFINITY;
+    wrow[blockIdx.x * 32 + rx] = 0.f;
+    put_hx(blockIdx.x * 32 + rx, -1e30f);
+  }
   extern __shared__ float sc[];             // [splits][32] per-slot scales of the rows
   // label term and activation of this thread's columns, loaded before the
   // slot reductions so their latency hides under them
@@ -310,6 +326,7 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
     const float L2 = M + log2f(l);
     lse2[r] = L2;
     lsep[r] = L2 + log2f((float)B);   // pass 2: p / B = 2^(s log2e - lsep)
+    put_hx(r, -(lsep[r] * 0.69314718055994531f));   // FOLD: -(LSE + ln B), natural units
     // pass 2's label weight of the row, 1 / (k_r B) (R3), same fp32 operations
     // as the label transpose's per-entry weights
     wrow[r] = (1.0f / (float)B) / (float)(lab_ptr[r + 1] - lab_ptr[r]);
@@ -321,10 +338,11 @@ void launch_combine_bf16(cudaStream_t s, int h, const StepDesc *desc, int b_max,
                          int splits, const float *pm, const float *pl, const float *pO,
                          const float *labW, const float *zsum, const float *Hf, const int64_t *lab_ptr,
                          float *lse2, float *lsep, float *wrow, float *lossr, float *dA, float *db1p,
-                         int *db1cnt, float *b1, float lr, float *dbg_db1, float *dbg_dHs) {
+                         int *db1cnt, float *b1, float lr, float *dbg_db1, float *dbg_dHs,
+                         __nv_bfloat16 *Hx) {
   launch_pdl(k_combine_bf16, dim3(ceil_div(bpad, 32), h / COMBINE_CW), dim3(256), (size_t)splits * 32 * 4, s, desc, h,
              bpad, splits, pm, pl, pO, labW, zsum, Hf, lab_ptr, lse2, lsep, wrow, lossr, dA, db1p, db1cnt, b1, lr,
-             dbg_db1, dbg_dHs);
+             dbg_db1, dbg_dHs, Hx);
 }
 
 // =====================================================================

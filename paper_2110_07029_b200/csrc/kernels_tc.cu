@@ -218,6 +218,11 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
   uint64_t d;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -274,6 +279,17 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// K-major tile of 16 bf16 per row with 32-byte swizzle (SWIZZLE_32B = 6): one
+// K-step; 8-row groups 256 B apart (SBO).  Written by TMA (SWIZZLE_32B box) or
+// by threads with the same pattern: 16-B chunk c of row r at
+// r * 32 + ((c ^ ((r >> 2) & 1)) << 4).
+__device__ __forceinline__ uint64_t sdesc32(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(256 >> 4) << 32) | (1ull << 46) |
+         (6ull << 61);
+}
+__device__ __forceinline__ uint32_t swz32(int r, int c) {
+  return (uint32_t)(r * 32 + ((c ^ ((r >> 2) & 1)) << 4));
 }
 // K-major operand tile [K/64 atoms][128 rows][64 elems]: MMA k-step kk (16 elems)
 __device__ __forceinline__ uint64_t desc_k(uint32_t base, int kk) {
@@ -667,7 +683,20 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 
 template <int H>
 struct BwdCfg {
-  static constexpr int NSH = H == 128 ? 4 : 2;    // H tile stages (128 rows each)
+  // FOLD (h = 128): b2_c and -(LSE_r + ln B) enter the S^T MMA as one more
+  // K-step of 16 (a per-class tile A_ext = [b2 in three bf16 parts, 1, 1, 1, 0..]
+  // and a per-row tile B_ext = [1, 1, 1, -(LSE + ln B) in three parts, 0..],
+  // both SWIZZLE_32B in shared memory), so S^T = z - LSE - ln B exactly (fp32
+  // accumulation of exact bf16 products) and the softmax is p / B = 2^(S log2e):
+  // no per-element bias / lse' arithmetic and no lse' loads.
+#if defined(AS_X_NORING) || defined(AS_X_NOFOLD) || defined(AS_X_U64)
+  static constexpr bool FOLD = false;
+#else
+  static constexpr bool FOLD = H == 128;
+#endif
+  static constexpr int NSH = H == 128 ? (FOLD ? 3 : 4) : 2;    // H tile stages (128 rows each)
+  static constexpr int HXB = FOLD ? BM * 32 : 0;  // B_ext tile of an H stage (128 rows x 16 bf16)
+  static constexpr int AXB = FOLD ? BM * 32 : 0;  // A_ext tile of a class block (two buffers)
 #ifdef AS_X_U64
   static constexpr int UNIT = 64;                 // experiment: 64-row units, 4 S^T buffers
   static constexpr int HPT = 128 / UNIT;
@@ -688,7 +717,8 @@ struct BwdCfg {
   static constexpr bool TMAUPD = H == 128;
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
   static constexpr int TSTAGE = TMAUPD ? BM * H * 4 : BM * SROW * 4;
-  static constexpr int SMEM = NSH * TILE + TSTAGE + 2 * NSH * BM * 4 /*lse' and label-weight rings*/ +
+  static constexpr int SMEM = NSH * TILE + NSH * HXB + 2 * AXB + TSTAGE +
+                              (FOLD ? 1 : 2) * NSH * BM * 4 /*(lse' and) label-weight rings*/ +
                               2 * BM * 4 /*db2*/ + 2 * 256 * (16 + 16 + 4) /*softmax prefetch slots*/ +
                               512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
@@ -717,7 +747,8 @@ struct BwdCfg {
 template <int H>
 __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
-              const __grid_constant__ CUtensorMap mapWf, const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
+              const __grid_constant__ CUtensorMap mapWf, const __grid_constant__ CUtensorMap mapHx,
+              const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
               int n_cblocks, const int4 *__restrict__ cls_lab,
               const uint32_t *__restrict__ lbits, int lbw, const float *__restrict__ wrow,
               float *__restrict__ W2T, float *__restrict__ b2,
@@ -728,13 +759,16 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
   constexpr int UNIT = Cfg::UNIT, HPT = Cfg::HPT;
   constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
-  constexpr bool TMAUPD = Cfg::TMAUPD;
+  constexpr bool TMAUPD = Cfg::TMAUPD, FOLD = Cfg::FOLD;
+  constexpr int HXB = Cfg::HXB, AXB = Cfg::AXB;
   constexpr uint32_t COL_W = NSB * UNIT, COL_DW = NSB * UNIT + NWT * WCOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sHt = smem_raw;
-  float *sT = (float *)(sHt + NSH * TILE);      // h = 128: W2T fp32 block; else dW2T staging
-  float *sL = (float *)((uint8_t *)sT + Cfg::TSTAGE);    // lse' of the rows of each H stage
-  float *sWr = sL + NSH * BM;                   // label weight 1/(k_r B) of those rows (R3)
+  uint8_t *sHx = sHt + NSH * TILE;              // FOLD: B_ext of each H stage
+  uint8_t *sAx = sHx + NSH * HXB;               // FOLD: A_ext of the class blocks in TMEM
+  float *sT = (float *)(sAx + 2 * AXB);         // h = 128: W2T fp32 block; else dW2T staging
+  float *sL = (float *)((uint8_t *)sT + Cfg::TSTAGE);    // lse' of the rows of each H stage (!FOLD)
+  float *sWr = sL + (FOLD ? 0 : NSH * BM);      // label weight 1/(k_r B) of those rows (R3)
   float *sDB = sWr + NSH * BM;                  // [2][128] db2 partials of the two WGs
   uint4 *sMk = (uint4 *)(sDB + 2 * BM);          // [2][256] label-row bitmaps (softmax prefetch)
   int4 *sCl = (int4 *)(sMk + 2 * 256);           // [2][256] cls_lab of the next block
@@ -821,10 +855,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #ifdef AS_X_NOTMA
           if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
 #endif
-          mbar_expect_tx(&h_full[st], TILE + 2 * BM * 4);
+          mbar_expect_tx(&h_full[st], TILE + HXB + (FOLD ? 1 : 2) * BM * 4);
           for (int a = 0; a < H / 64; ++a)
             tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
-          bulk_load_1d(sL + st * BM, lsep + t * BM, BM * 4, &h_full[st]);
+          if constexpr (FOLD) tma_load_2d(&mapHx, &h_full[st], sHx + st * HXB, 0, t * BM);
+          else bulk_load_1d(sL + st * BM, lsep + t * BM, BM * 4, &h_full[st]);
           bulk_load_1d(sWr + st * BM, wrow + t * BM, BM * 4, &h_full[st]);
         }
     }
@@ -912,8 +947,12 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           }
           fence_after();
 #ifndef AS_X_NOMMA1
-          mma_grp_ts_k_8(tmem + c.b * UNIT + (uint32_t)(((half + par) & 1) * 64), tmem + COL_W + c.wb * WCOLS,
+          const uint32_t dcol = c.b * UNIT + (uint32_t)(((half + par) & 1) * 64);
+          mma_grp_ts_k_8(tmem + dcol, tmem + COL_W + c.wb * WCOLS,
                          sdesc(aH + c.st * TILE + half * 64 * 128, 16, 1024), idS64, 0u);
+          if constexpr (FOLD)                 // + b2_c - (LSE_r + ln B): one K-step from A_ext / B_ext
+            mma_ss_w(tmem + dcol, sdesc32(smem_u32(sAx) + c.wb * AXB),
+                     sdesc32(smem_u32(sHx) + c.st * HXB + half * 64 * 32), idS64, 1u);
 #endif
           mma_commit_w(&s_full[2 * c.b + half]);
         };
@@ -1074,7 +1113,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         AS_TMEM_LD32(tl + b * UNIT + scol, r0);
         AS_TMEM_LD32(tl + b * UNIT + scol + 32, r1);
         // lse' = LSE_r * log2e + log2 B of these 64 rows (smem broadcast)
-        const float4 *lq = reinterpret_cast<const float4 *>(sL + lst * BM + (v % HPT) * UNIT + half * 64);
+        const float4 *lq = reinterpret_cast<const float4 *>(sL + (FOLD ? 0 : lst * BM + (v % HPT) * UNIT + half * 64));
         AS_TMEM_WAIT_LD(r0);
         AS_TMEM_WAIT_LD(r1);
         if (RING && half == 1) {              // half 1's S columns are free for the next unit
@@ -1087,13 +1126,18 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         const uint64_t l2e2 = f2(LOG2E, LOG2E), b2c2 = f2(b2c, b2c);
 #pragma unroll
         for (int k4 = 0; k4 < 16; ++k4) {
-          const float4 l4 = lq[k4];
+          const float4 l4 = FOLD ? make_float4(0.f, 0.f, 0.f, 0.f) : lq[k4];
 #pragma unroll
           for (int m = 0; m < 2; ++m) {       // packed: x = s log2e + b2 - lse'
             const int k = 4 * k4 + 2 * m, u = 2 * k4 + m;
             const uint32_t xa = k < 32 ? r0[k] : r1[k - 32], xb = k < 32 ? r0[k + 1] : r1[k - 31];
-            uint64_t x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
-            x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
+            uint64_t x;
+            if constexpr (FOLD) {             // S^T already holds z - LSE - ln B: p / B = 2^(S log2e)
+              x = fmul2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2);
+            } else {
+              x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
+              x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
+            }
             float e0, e1;
             if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
               ex2_emu2(x, e0, e1);
@@ -1204,6 +1248,26 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     constexpr int NCH = H / 32;               // 32-column chunks of dW2T
     const int sub = lane >> 3, hq = (lane & 7) * 4;
     TRACE_INIT;
+    // FOLD: row i of the class block's A_ext tile = [b2 in three bf16 parts (-1e30
+    // past C: p = 0), 1, 1, 1, 0 ...] (SWIZZLE_32B), visible to the MMA (async proxy)
+    auto put_ax = [&](int kb_, float b2v) {
+      if constexpr (FOLD) {
+        const int wb = kb_ % NWT;
+        const float hi = __bfloat162float(__float2bfloat16_rn(b2v));
+        const float r1 = b2v - hi;
+        const float mid = __bfloat162float(__float2bfloat16_rn(r1));
+        const float lo = r1 - mid;
+        uint8_t *row = sAx + wb * AXB;
+        *reinterpret_cast<uint4 *>(row + swz32(i, 0)) =
+            make_uint4(pack_bf16x2(hi, mid), pack_bf16x2(lo, 1.f), pack_bf16x2(1.f, 1.f), 0u);
+        *reinterpret_cast<uint4 *>(row + swz32(i, 1)) = make_uint4(0u, 0u, 0u, 0u);
+        fence_proxy_async();
+      }
+    };
+    auto b2_of = [&](int kb_) {
+      const int cls = (blockIdx.x + kb_ * gridDim.x) * BM + i;
+      return cls < C ? b2[cls] : -1e30f;
+    };
     // W2T block (bf16 shadow, row of class i) -> TMEM A-operand columns of buffer wb
     auto load_wt = [&](int kb_) {
       const int wb = kb_ % NWT;
@@ -1221,6 +1285,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 64 * half, r);
         AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 64 * half + 32, (r + 32));
       }
+      put_ax(kb_, b2_of(kb_));
       tmem_wait_st();
       fence_before();
       __syncwarp();
@@ -1235,7 +1300,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     // h = 128: the bf16 W2T rows of block kb + NWT are fetched into registers
     // BEFORE waiting for block kb's accumulator (the HBM latency hides in that
     // wait) and written into the TMEM buffer block kb's S MMAs have released
+    float b2pre = 0.f;                        // FOLD: b2 of the prefetched block's class i
     auto fetch_wt = [&](int kb_, uint32_t (&r)[64]) {
+      if constexpr (FOLD) b2pre = b2_of(kb_);
       const int cls = (blockIdx.x + kb_ * gridDim.x) * BM + i;
       const uint4 *src = reinterpret_cast<const uint4 *>(W2b + (size_t)(cls < C ? cls : 0) * H);
 #pragma unroll
@@ -1249,6 +1316,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       const int wb = kb_ % NWT;
       AS_TMEM_ST32(tl + COL_W + wb * WCOLS, r);
       AS_TMEM_ST32(tl + COL_W + wb * WCOLS + 32, (r + 32));
+      put_ax(kb_, b2pre);
       tmem_wait_st();
       fence_before();
       __syncwarp();
@@ -1878,7 +1946,7 @@ static int make_map(CUtensorMap *m, const void *base, long long rows, int cols) 
 }
 
 struct TcPlan {
-  CUtensorMap mapH, mapW, mapWf;
+  CUtensorMap mapH, mapW, mapWf, mapHx;
   const void *Hb;
   int h, b_max, bpad, n_cblocks, num_sms, max_splits;
   long long C;
@@ -1906,8 +1974,24 @@ static int make_map_f32(CUtensorMap *m, const void *base, long long rows, int co
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// bf16 row-major [rows][16] (the FOLD B_ext rows) with a {16, 128} box and 32-byte swizzle
+static int make_map_x(CUtensorMap *m, const void *base, long long rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[2] = {16, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {32};
+  cuuint32_t box[2] = {16, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+bool tc_fold(int h) { return h == 128 ? tc::BwdCfg<128>::FOLD : tc::BwdCfg<256>::FOLD; }
+
 int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const void *Hb,
-                 const void *W2b, const void *W2T) {
+                 const void *W2b, const void *W2T, const void *Hx) {
   plan->h = h;
   plan->Hb = Hb;
   plan->b_max = b_max;
@@ -1919,6 +2003,7 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
   if (make_map(&plan->mapH, Hb, plan->bpad, h) != 0) return -1;
   if (make_map(&plan->mapW, W2b, C, h) != 0) return -1;
   if (make_map_f32(&plan->mapWf, W2T, C, h) != 0) return -1;
+  if (make_map_x(&plan->mapHx, Hx, plan->bpad) != 0) return -1;
   // every ctx sets the attributes on its own device (cheap, idempotent)
   {
     if (h == 128) {
@@ -1982,11 +2067,11 @@ void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
   if (p->h == 128)
     // plain launch: pass 2 follows the wait on the transposes' join event
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
+        p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
   else
     tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
+        p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2);
 }
 
