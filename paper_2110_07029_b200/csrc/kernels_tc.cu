@@ -689,12 +689,24 @@ struct BwdCfg {
   // both SWIZZLE_32B in shared memory), so S^T = z - LSE - ln B exactly (fp32
   // accumulation of exact bf16 products) and the softmax is p / B = 2^(S log2e):
   // no per-element bias / lse' arithmetic and no lse' loads.
-#if defined(AS_X_NORING) || defined(AS_X_NOFOLD) || defined(AS_X_U64)
-  static constexpr bool FOLD = false;
-#else
+  // Measured (x_probe A/B on B200): numerically exact (GPU parity green) but
+  // slower, because its shared memory leaves room for only 3 H stages
+  // (out_bwd 0.362 -> 0.409 ms; 3 stages alone cost 0.036 ms) -- an experiment
+  // switch (AS_X_FOLD), off in the product build.
+#if defined(AS_X_FOLD) && !defined(AS_X_NORING) && !defined(AS_X_U64)
   static constexpr bool FOLD = H == 128;
+#else
+  static constexpr bool FOLD = false;
 #endif
+#ifdef AS_X_NSH
+  static constexpr int NSH = H == 128 ? AS_X_NSH : 2;   // experiment: H tile stages (>= 3 with the ring)
+#else
+#ifdef AS_X_HALFUPD
+  static constexpr int NSH = H == 128 ? (FOLD ? 4 : 5) : 2;    // H tile stages (128 rows each)
+#else
   static constexpr int NSH = H == 128 ? (FOLD ? 3 : 4) : 2;    // H tile stages (128 rows each)
+#endif
+#endif
   static constexpr int HXB = FOLD ? BM * 32 : 0;  // B_ext tile of an H stage (128 rows x 16 bf16)
   static constexpr int AXB = FOLD ? BM * 32 : 0;  // A_ext tile of a class block (two buffers)
 #ifdef AS_X_U64
@@ -715,8 +727,17 @@ struct BwdCfg {
   // TMA-stored; the bf16 shadow is written from registers.
   // h = 256: chunked register path through a small staging tile.
   static constexpr bool TMAUPD = H == 128;
+  // HALF: the fp32 W2T block is staged 64 columns at a time (32 KB instead of
+  // 64 KB of shared memory), leaving room for a deeper H ring.  Measured
+  // slower (out_bwd 0.367 -> 0.40 ms with 5 H stages): experiment switch
+  // AS_X_HALFUPD, off in the product build.
+#ifdef AS_X_HALFUPD
+  static constexpr bool HALF = TMAUPD;
+#else
+  static constexpr bool HALF = false;
+#endif
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
-  static constexpr int TSTAGE = TMAUPD ? BM * H * 4 : BM * SROW * 4;
+  static constexpr int TSTAGE = TMAUPD ? BM * (HALF ? H / 2 : H) * 4 : BM * SROW * 4;
   static constexpr int SMEM = NSH * TILE + NSH * HXB + 2 * AXB + TSTAGE +
                               (FOLD ? 1 : 2) * NSH * BM * 4 /*(lse' and) label-weight rings*/ +
                               2 * BM * 4 /*db2*/ + 2 * 256 * (16 + 16 + 4) /*softmax prefetch slots*/ +
@@ -759,7 +780,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
   constexpr int UNIT = Cfg::UNIT, HPT = Cfg::HPT;
   constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
-  constexpr bool TMAUPD = Cfg::TMAUPD, FOLD = Cfg::FOLD;
+  constexpr bool TMAUPD = Cfg::TMAUPD, FOLD = Cfg::FOLD, HALF = Cfg::HALF;
   constexpr int HXB = Cfg::HXB, AXB = Cfg::AXB;
   constexpr uint32_t COL_W = NSB * UNIT, COL_DW = NSB * UNIT + NWT * WCOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -950,7 +971,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           const uint32_t dcol = c.b * UNIT + (uint32_t)(((half + par) & 1) * 64);
           mma_grp_ts_k_8(tmem + dcol, tmem + COL_W + c.wb * WCOLS,
                          sdesc(aH + c.st * TILE + half * 64 * 128, 16, 1024), idS64, 0u);
+#ifdef AS_X_NOEXTMMA
+          if constexpr (false)
+#else
           if constexpr (FOLD)                 // + b2_c - (LSE_r + ln B): one K-step from A_ext / B_ext
+#endif
             mma_ss_w(tmem + dcol, sdesc32(smem_u32(sAx) + c.wb * AXB),
                      sdesc32(smem_u32(sHx) + c.st * HXB + half * 64 * 32), idS64, 1u);
 #endif
@@ -1291,10 +1316,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&wt_full[wb]);
     };
-    if constexpr (TMAUPD) {                   // fp32 W2T of the first block
+    if constexpr (TMAUPD) {                   // fp32 W2T of the first block (its first half)
       if (ut == 0 && NB > 0) {
-        mbar_expect_tx(wf_full, BM * H * 4);
-        for (int c = 0; c < 4; ++c) tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, c * 32, blockIdx.x * BM);
+        constexpr int NBOX = HALF ? 2 : 4;
+        mbar_expect_tx(wf_full, BM * 32 * 4 * NBOX);
+        for (int c = 0; c < NBOX; ++c) tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, c * 32, blockIdx.x * BM);
       }
     }
     // h = 128: the bf16 W2T rows of block kb + NWT are fetched into registers
@@ -1333,7 +1359,101 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
-      if constexpr (TMAUPD) {
+      if constexpr (HALF) {
+        if (kb + NWT < NB) put_wt(kb + NWT, wpre);
+        // fused SGD of the block, 64 columns at a time: the TMEM accumulator
+        // (lane i = class i) and the TMA-staged fp32 half block (two swizzled
+        // 32-column boxes): W2T -= lr dW2T in place, TMA store, coalesced bf16
+        // shadow; the other half is TMA-loaded meanwhile.  The accumulator is
+        // released once the second half's columns are in registers.
+        // opaque copies: the compiler would otherwise hoist every swizzled
+        // address of the two passes out of the block loop and spill the
+        // prefetched W2T rows to make room
+        uint32_t sw = (uint32_t)(i & 7);
+        asm volatile("" : "+r"(sw));
+        uint8_t *rowWf = reinterpret_cast<uint8_t *>(sT) + i * 128;
+        asm volatile("" : "+l"(rowWf));
+        const int cls_i = cb * BM + i;
+        auto sgd_box = [&](int bx, int ch, const uint32_t (&r)[32]) {
+#ifndef AS_X_NOUPD
+#pragma unroll
+          for (int g0 = 0; g0 < 8; g0 += 4) {
+            float4 w[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              w[g] = *reinterpret_cast<const float4 *>(rowWf + bx * 16384 + (((uint32_t)(g0 + g) ^ sw) << 4));
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              w[g].x = fmaf(-lr, __uint_as_float(r[4 * (g0 + g)]), w[g].x);
+              w[g].y = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 1]), w[g].y);
+              w[g].z = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 2]), w[g].z);
+              w[g].w = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 3]), w[g].w);
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              *reinterpret_cast<float4 *>(rowWf + bx * 16384 + (((uint32_t)(g0 + g) ^ sw) << 4)) = w[g];
+          }
+#endif
+          if (dbg_dW2T && cls_i < C) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls_i * H + ch * 32 + k] = __uint_as_float(r[k]);
+          }
+        };
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t ra[32], rb[32];
+          AS_TMEM_LD32(tl + COL_DW + hh * 64, ra);
+          AS_TMEM_LD32(tl + COL_DW + hh * 64 + 32, rb);
+          AS_TMEM_WAIT_LD(ra);
+          AS_TMEM_WAIT_LD(rb);
+          if (hh == 1) {                      // accumulator free for block kb + 1
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dw_empty);
+          }
+          mbar_wait(wf_full, (2 * kb + hh) & 1);
+          sgd_box(0, 2 * hh, ra);
+          sgd_box(1, 2 * hh + 1, rb);
+          fence_proxy_async();
+          named_bar(3, 128);
+#ifndef AS_X_NOUPD
+          if (ut == 0) {
+            for (int c = 0; c < 2; ++c) tma_store_2d(&mapWf, (uint8_t *)sT + c * 16384, 64 * hh + c * 32, cb * BM);
+            bulk_commit();
+          }
+          // bf16 shadow of these 64 columns, coalesced (8 threads per class row)
+          int utv = ut;
+          asm volatile("" : "+r"(utv));
+#pragma unroll 4
+          for (int k = 0; k < 8; ++k) {
+            const int idx = k * 128 + utv;
+            const int row = idx >> 3, c8 = idx & 7;
+            const int cls = cb * BM + row;
+            const uint8_t *rbp = reinterpret_cast<const uint8_t *>(sT) + (c8 >> 2) * 16384 + row * 128;
+            const uint32_t g0 = (uint32_t)((c8 & 3) * 2), rs = (uint32_t)(row & 7);
+            const float4 a = *reinterpret_cast<const float4 *>(rbp + ((g0 ^ rs) << 4));
+            const float4 b = *reinterpret_cast<const float4 *>(rbp + (((g0 + 1) ^ rs) << 4));
+            if (cls < C)
+              *reinterpret_cast<uint4 *>(W2b + (size_t)cls * H + 64 * hh + 8 * c8) =
+                  make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                             pack_bf16x2(b.z, b.w));
+          }
+          named_bar(3, 128);                  // every thread's reads of the staging are done
+#endif
+          if (ut == 0) {
+#ifndef AS_X_NOUPD
+            bulk_wait_read0();
+#endif
+            const bool more = hh == 0 || kb + 1 < NB;
+            if (more) {                       // the other half of this block, or the next block's first
+              const int nrow = (hh == 0 ? cb : cb + (int)gridDim.x) * BM, ncol = hh == 0 ? 64 : 0;
+              mbar_expect_tx(wf_full, BM * 64 * 4);
+              for (int c = 0; c < 2; ++c)
+                tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, ncol + c * 32, nrow);
+            }
+          }
+        }
+      } else if constexpr (TMAUPD) {
         if (kb + NWT < NB) put_wt(kb + NWT, wpre);
         // fused SGD of the block from the TMEM accumulator (lane i = class i)
         // and the TMA-loaded fp32 block: W2T -= lr dW2T in place (swizzled
