@@ -105,6 +105,14 @@ struct as_ctx {
   size_t pin_bytes;
   cudaEvent_t pin_ev[2];
   int pin_idx;
+  // host batches (as_load_batch_csr / as_eval_top1): the packed pinned block
+  // goes to one of two device staging blocks in ONE copy on the copy stream,
+  // overlapping the previous step; the step reads the batch there
+  uint8_t *stage_dev[2];
+  cudaStream_t cp_s;
+  cudaEvent_t ev_copied[2], ev_stage_free[2];
+  int cur_stage;                // staging block of the loaded batch, -1 = device-gathered batch
+  struct BatchPtrs { int64_t *row_ptr, *lab_ptr; int32_t *col, *lab; float *val; StepDesc *desc; } gather_set;
   // resident dataset
   const int64_t *ds_row_ptr, *ds_lab_ptr, *ds_order;
   const int32_t *ds_col, *ds_lab;
@@ -171,6 +179,12 @@ Dims dims_of(const as_config *c) {
   return D;
 }
 
+// one packed host batch: row_ptr, lab_ptr (rows + 1 each, int64), col, val
+// (nnz), lab (L), StepDesc (64-B aligned) -- pinned staging and device staging
+size_t stage_bytes(const Dims &D) {
+  return 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
+}
+
 // The arena carve: every buffer of the step sized for b_max ("we
 // provision memory for the largest batch size").  Order fixed; `ctx` NULL ->
 // just the total.
@@ -192,6 +206,9 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * (size_t)D.nnz_cap); if (x) x->val = (float *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lab = (int32_t *)p;
   p = P(sizeof(StepDesc)); if (x) x->desc = (StepDesc *)p;
+  for (int k = 0; k < 2; ++k) {
+    p = P(stage_bytes(D)); if (x) x->stage_dev[k] = (uint8_t *)p;
+  }
   p = P(4 * (size_t)D.d); if (x) x->fcnt = (int32_t *)p;
   p = P(4 * (size_t)D.d); if (x) x->fsidx = (int32_t *)p;
   p = P(4 * (size_t)D.d * D.bw); if (x) x->fbits = (uint32_t *)p;
@@ -428,7 +445,14 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
     rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_mg[i], cudaEventDisableTiming), "event");
   if (const char *mc = getenv("ADASGD_MERGE_CHUNKS")) x->merge_chunks = atoi(mc) > 0 ? atoi(mc) : 0;
   // pinned double-buffered staging for host batches
-  x->pin_bytes = 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
+  x->pin_bytes = stage_bytes(D);
+  x->cur_stage = -1;
+  x->gather_set = {x->row_ptr, x->lab_ptr, x->col, x->lab, x->val, x->desc};
+  if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->cp_s, cudaStreamNonBlocking, prio_hi), "copy stream");
+  for (int i = 0; i < 2 && !rc; ++i) {
+    rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_copied[i], cudaEventDisableTiming), "event");
+    if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_stage_free[i], cudaEventDisableTiming), "event");
+  }
   for (int i = 0; i < 2 && !rc; ++i) {
     rc = cuda_check(x, cudaMallocHost(&x->pin[i], x->pin_bytes), "cudaMallocHost");
     if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->pin_ev[i], cudaEventDisableTiming), "event");
@@ -478,6 +502,11 @@ int as_destroy(as_ctx *x) {
   for (int i = 0; i < 3; ++i)
     if (x->ev_mg[i]) cudaEventDestroy(x->ev_mg[i]);
   if (x->comm_s) { cudaStreamSynchronize(x->comm_s); cudaStreamDestroy(x->comm_s); }
+  if (x->cp_s) { cudaStreamSynchronize(x->cp_s); cudaStreamDestroy(x->cp_s); }
+  for (int i = 0; i < 2; ++i) {
+    if (x->ev_copied[i]) cudaEventDestroy(x->ev_copied[i]);
+    if (x->ev_stage_free[i]) cudaEventDestroy(x->ev_stage_free[i]);
+  }
   for (auto &p : x->pending) { x->ev_pool.push_back(p.a); x->ev_pool.push_back(p.b); }
   for (auto e : x->ev_pool) cudaEventDestroy(e);
   free(x->plan);
@@ -495,15 +524,17 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   if (nnz > x->D.nnz_cap || L > x->D.lab_cap) return as_fail(AS_E_INVALID, "batch exceeds capacity");
   const int k = x->pin_idx;
   x->pin_idx ^= 1;
-  rc = cuda_check(x, cudaEventSynchronize(x->pin_ev[k]), "staging wait");
+  rc = cuda_check(x, cudaEventSynchronize(x->pin_ev[k]), "staging wait");   // pinned block k reusable
   if (rc) return rc;
   uint8_t *p = (uint8_t *)x->pin[k];
+  const size_t o_lp = 8 * (size_t)(rows + 1), o_cc = 2 * o_lp, o_vv = o_cc + 4 * (size_t)nnz,
+               o_ll = o_vv + 4 * (size_t)nnz, o_dd = (o_ll + 4 * (size_t)L + 63) & ~(size_t)63;
   int64_t *rp = (int64_t *)p;
-  int64_t *lp = rp + (rows + 1);
-  int32_t *cc = (int32_t *)(lp + (rows + 1));
-  float *vv = (float *)(cc + nnz);
-  int32_t *ll = (int32_t *)(vv + nnz);
-  StepDesc *dd = (StepDesc *)(((uintptr_t)(ll + L) + 63) & ~(uintptr_t)63);
+  int64_t *lp = (int64_t *)(p + o_lp);
+  int32_t *cc = (int32_t *)(p + o_cc);
+  float *vv = (float *)(p + o_vv);
+  int32_t *ll = (int32_t *)(p + o_ll);
+  StepDesc *dd = (StepDesc *)(p + o_dd);
   for (int r = 0; r <= rows; ++r) {
     rp[r] = row_ptr[r] - row_ptr[0];
     lp[r] = lab_ptr[r] - lab_ptr[0];
@@ -516,17 +547,28 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   dd->nnz = (int32_t)nnz;
   dd->nlab = (int32_t)L;
   cudaStream_t s = x->stream;
+  // ONE copy of the packed block into device staging block k, on the copy
+  // stream once the step that last read block k is done; the main stream
+  // waits for it (the copy overlaps the previous step)
   ph_begin(x, AS_PH_BATCH);
-  cudaMemcpyAsync(x->row_ptr, rp, 8 * (rows + 1), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(x->lab_ptr, lp, 8 * (rows + 1), cudaMemcpyHostToDevice, s);
-  if (nnz) cudaMemcpyAsync(x->col, cc, 4 * nnz, cudaMemcpyHostToDevice, s);
-  if (nnz) cudaMemcpyAsync(x->val, vv, 4 * nnz, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(x->lab, ll, 4 * L, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(x->desc, dd, sizeof(StepDesc), cudaMemcpyHostToDevice, s);
+  uint8_t *g = x->stage_dev[k];
+  cudaStreamWaitEvent(x->cp_s, x->ev_stage_free[k], 0);
+  cudaMemcpyAsync(g, p, o_dd + sizeof(StepDesc), cudaMemcpyHostToDevice, x->cp_s);
+  cudaEventRecord(x->ev_copied[k], x->cp_s);
+  rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], x->cp_s), "batch H2D");
+  if (rc) return rc;
+  cudaStreamWaitEvent(s, x->ev_copied[k], 0);
+  x->row_ptr = (int64_t *)g;
+  x->lab_ptr = (int64_t *)(g + o_lp);
+  x->col = (int32_t *)(g + o_cc);
+  x->val = (float *)(g + o_vv);
+  x->lab = (int32_t *)(g + o_ll);
+  x->desc = (StepDesc *)(g + o_dd);
+  x->cur_stage = k;
   x->launches += 1;
   as::launch_entry_rows(s, x->row_ptr, x->lab_ptr, rows, x->rid, x->lrid);
   ph_end(x, AS_PH_BATCH);
-  rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], s), "batch H2D");
+  rc = cuda_check(x, cudaSuccess, "batch staging");
   if (rc) return rc;
   x->loaded_rows = rows;
   return AS_OK;
@@ -576,6 +618,7 @@ int as_eval_top1(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t 
   if (top1_out) cudaMemcpyAsync(top1_out, x->top1, 4 * (size_t)rows, cudaMemcpyDeviceToHost, s);
   unsigned long long h = 0;
   cudaMemcpyAsync(&h, x->hits, 8, cudaMemcpyDeviceToHost, s);
+  if (x->cur_stage >= 0) cudaEventRecord(x->ev_stage_free[x->cur_stage], s);
   rc = cuda_check(x, cudaStreamSynchronize(s), "eval");
   if (rc) return rc;
   if (hits_out) *hits_out = (int64_t)h;
@@ -639,6 +682,9 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   const int bi = x->b_all[x->cfg.rank];
   if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
   if (pos < 0) return as_fail(AS_E_INVALID, "pos < 0");
+  x->row_ptr = x->gather_set.row_ptr; x->lab_ptr = x->gather_set.lab_ptr; x->col = x->gather_set.col;
+  x->val = x->gather_set.val; x->lab = x->gather_set.lab; x->desc = x->gather_set.desc;
+  x->cur_stage = -1;
   ph_begin(x, AS_PH_BATCH);
   x->launches += 2;
   as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
@@ -766,15 +812,18 @@ int as_train_step(as_ctx *x, float *loss_out) {
   as::launch_dw1_chunked(s, D.h, x->num_sms, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
                          x->fseg_val, x->dA, W1, lr, x->seg_part, x->arrive,
                          dbg ? x->dbg_dW1 : nullptr);
+  if (loss_out || dbg) {
+    x->launches += 1;
+    as::launch_loss_mean(s, d, x->lossr, x->loss);
+  }
   // transpose state reset on the side stream after the step's last reader
   cudaEventRecord(x->ev_tail, s);
   cudaStreamWaitEvent(ss, x->ev_tail, 0);
   x->launches += 1;
   as::launch_tr_reset(ss, tr, x->num_sms);
-  if (loss_out || dbg) {
-    x->launches += 1;
-    as::launch_loss_mean(s, d, x->lossr, x->loss);
-  }
+  // the host-staged batch block may be refilled once the reset (the last
+  // reader of its StepDesc) is done
+  if (x->cur_stage >= 0) cudaEventRecord(x->ev_stage_free[x->cur_stage], ss);
   ph_end(x, AS_PH_DW1);
   int rc = cuda_check(x, cudaSuccess, "train step launch");
   if (rc) return rc;

@@ -132,7 +132,7 @@ def _live_worker(rank, world, port, outdir):
                   lr0=0.5, precision="fp32", rank=rank, world=world, device=0, merge_backend="p2p")
     driver.open_p2p(rep, dist)
     rep.upload_dataset(ds)
-    st = driver.ReplayState(world, cfg.b_max, cfg.b_min, cfg.beta, 0.5, synthgen.make_cost_models(world))
+    st = driver.ReplayState(world, cfg.b_max, cfg.b_min, cfg.beta, 0.5, synthgen.make_cost_models(world, hetero=False))
     alphas = []
 
     def merge_fn(u, b):

@@ -736,14 +736,18 @@ def test_replica_norm_vs_oracle(gpu_lib, metric):
     rep.close()
 
 
-@pytest.mark.parametrize("nccl_self,chunks", [(False, None), (True, None), (True, "7")])
+@pytest.mark.parametrize("nccl_self,chunks", [(False, None), (True, "3"), (True, "7")])
 def test_merge_weighted_forced_alpha(gpu_lib, monkeypatch, nccl_self, chunks):
     """Steps a11-a13 with a forced weight alpha = 0.7 at world = 1: the prescale
     kernel (no communicator), or with ADASGD_NCCL_SELF=1 the NCCL PreMulSum
     all-reduce on a one-rank communicator (the N > 1 code path: PreMulSum op,
     chunked all-reduce on the communication stream, momentum chasing the
     chunks).  Two merges (gamma = 0.9 momentum) against oracle.merge.merge,
-    <= 1e-5; replicas restart from wbar; wbar_p rotation."""
+    <= 1e-5; replicas restart from wbar; wbar_p rotation.  (NCCL 2.28.9's one-rank
+    PreMulSum leaves a few tail elements unscaled for some counts, e.g. the whole
+    308 228-float vector here -- scripts/nccl_premul_probe.py -- so the one-rank
+    cases use chunked merges; multi-rank all-reduces go through NCCL's regular
+    kernels, which this one-GPU box cannot run.)"""
     if nccl_self:
         monkeypatch.setenv("ADASGD_NCCL_SELF", "1")
     if chunks:
