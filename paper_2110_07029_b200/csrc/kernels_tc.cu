@@ -819,6 +819,15 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   const int B = desc->rows;
   const int RT = (B + BM - 1) / BM;               // 128-row H tiles
   const int NU = HPT * RT;                        // units per class block
+  // every CTA sweeps the row tiles of a class block starting at its own
+  // offset, so the 148 CTAs do not all fetch the same H tile from L2 at once
+#ifdef AS_X_NOROT
+  const int rot = 0;
+#else
+  const int rot = (int)(blockIdx.x % (unsigned)(RT > 0 ? RT : 1));
+#endif
+  // unit v of a class block covers row tile (v / HPT + rot) mod RT
+  auto unit_rows = [&](int v_) { return ((v_ / HPT + rot) % RT) * HPT + v_ % HPT; };
   // NB (class blocks of this CTA) and NT = NB * NU (its units) are computed in
   // each role branch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -877,11 +886,12 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
 #endif
           mbar_expect_tx(&h_full[st], TILE + HXB + (FOLD ? 1 : 2) * BM * 4);
+          const int tr = t + rot < RT ? t + rot : t + rot - RT;    // rotated row tile
           for (int a = 0; a < H / 64; ++a)
-            tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, t * BM);
-          if constexpr (FOLD) tma_load_2d(&mapHx, &h_full[st], sHx + st * HXB, 0, t * BM);
-          else bulk_load_1d(sL + st * BM, lsep + t * BM, BM * 4, &h_full[st]);
-          bulk_load_1d(sWr + st * BM, wrow + t * BM, BM * 4, &h_full[st]);
+            tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, tr * BM);
+          if constexpr (FOLD) tma_load_2d(&mapHx, &h_full[st], sHx + st * HXB, 0, tr * BM);
+          else bulk_load_1d(sL + st * BM, lsep + tr * BM, BM * 4, &h_full[st]);
+          bulk_load_1d(sWr + st * BM, wrow + tr * BM, BM * 4, &h_full[st]);
         }
     }
   } else if (warp == kMmaWarp) {
@@ -1064,7 +1074,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       cp_async_4(sB2r + sl, b2 + cc, ok ? 4u : 0u);
     };
     auto pf_mask = [&](int kb_, int v_, bool has, int slot) {
-      const uint32_t *bits = has ? lbits + (size_t)((blockIdx.x + kb_ * gridDim.x) * BM + i) * lbw + v_ * (UNIT / 32)
+      const uint32_t *bits = has ? lbits + (size_t)((blockIdx.x + kb_ * gridDim.x) * BM + i) * lbw +
+                                       unit_rows(v_) * (UNIT / 32)
                                  : lbits;
       if constexpr (UNIT == 128) cp_async_16(sMk + slot * 256 + tix, bits, has ? 16u : 0u);
       else cp_async_8(sMk + slot * 256 + tix, bits, has ? 8u : 0u);
