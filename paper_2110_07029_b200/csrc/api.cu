@@ -111,8 +111,8 @@ struct as_ctx {
   uint8_t *stage_dev[2];
   cudaStream_t cp_s;
   cudaEvent_t ev_copied[2], ev_stage_free[2];
-  int cur_stage;                // staging block of the loaded batch, -1 = device-gathered batch
-  struct BatchPtrs { int64_t *row_ptr, *lab_ptr; int32_t *col, *lab; float *val; StepDesc *desc; } gather_set;
+  int cur_stage;                // staging block of the loaded batch
+  int stage_next;               // block the next load writes
   // resident dataset
   const int64_t *ds_row_ptr, *ds_lab_ptr, *ds_order;
   const int32_t *ds_col, *ds_lab;
@@ -179,10 +179,26 @@ Dims dims_of(const as_config *c) {
   return D;
 }
 
-// one packed host batch: row_ptr, lab_ptr (rows + 1 each, int64), col, val
-// (nnz), lab (L), StepDesc (64-B aligned) -- pinned staging and device staging
-size_t stage_bytes(const Dims &D) {
-  return 16 * (size_t)(D.b_max + 1) + 8 * (size_t)D.nnz_cap + 4 * (size_t)D.lab_cap + 256;
+// A batch staging block (two per ctx; a step reads its batch from one while the
+// next batch is written into the other).  Capacity layout: row_ptr, lab_ptr
+// (b_max + 1 each, int64), col, val (nnz_cap), lab (lab_cap), StepDesc (64-B
+// aligned), then the per-batch work arrays ids (b_max), rid (nnz_cap), lrid
+// (lab_cap).  A host batch is packed with its actual sizes into the same
+// leading region (so one copy moves it) and never extends past `desc + 64`.
+struct StageLayout { size_t lp, col, val, lab, desc, ids, rid, lrid, total; };
+StageLayout stage_layout(const Dims &D) {
+  StageLayout L;
+  const size_t b1 = (size_t)D.b_max + 1;
+  L.lp = 8 * b1;
+  L.col = 16 * b1;
+  L.val = L.col + 4 * (size_t)D.nnz_cap;
+  L.lab = L.val + 4 * (size_t)D.nnz_cap;
+  L.desc = (L.lab + 4 * (size_t)D.lab_cap + 63) & ~(size_t)63;
+  L.ids = L.desc + 64;
+  L.rid = L.ids + 8 * (size_t)D.b_max;
+  L.lrid = L.rid + 4 * (size_t)D.nnz_cap;
+  L.total = L.lrid + 4 * (size_t)D.lab_cap;
+  return L;
 }
 
 // The arena carve: every buffer of the step sized for b_max ("we
@@ -199,15 +215,8 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(4 * D.P); if (x) x->wbar = (float *)p;
   p = P(4 * D.P); if (x) x->wbarp = (float *)p;
   p = P(2 * D.C * D.h); if (x) x->w2b = (__nv_bfloat16 *)p;
-  p = P(8 * (D.b_max + 1)); if (x) x->row_ptr = (int64_t *)p;
-  p = P(8 * (D.b_max + 1)); if (x) x->lab_ptr = (int64_t *)p;
-  p = P(8 * D.b_max); if (x) x->ids = (int64_t *)p;
-  p = P(4 * (size_t)D.nnz_cap); if (x) x->col = (int32_t *)p;
-  p = P(4 * (size_t)D.nnz_cap); if (x) x->val = (float *)p;
-  p = P(4 * (size_t)D.lab_cap); if (x) x->lab = (int32_t *)p;
-  p = P(sizeof(StepDesc)); if (x) x->desc = (StepDesc *)p;
   for (int k = 0; k < 2; ++k) {
-    p = P(stage_bytes(D)); if (x) x->stage_dev[k] = (uint8_t *)p;
+    p = P(stage_layout(D).total); if (x) x->stage_dev[k] = (uint8_t *)p;
   }
   p = P(4 * (size_t)D.d); if (x) x->fcnt = (int32_t *)p;
   p = P(4 * (size_t)D.d); if (x) x->fsidx = (int32_t *)p;
@@ -217,13 +226,11 @@ size_t carve(const as_config *c, const Dims &D, as_ctx *x, uint8_t *base) {
   p = P(8 * (size_t)D.tr_tiles); if (x) x->tile_state = (unsigned long long *)p;
   p = P(16); if (x) x->ticket = (int *)p;
   p = P(4 * S); if (x) x->arrive = (int *)p;
-  p = P(4 * (size_t)D.lab_cap); if (x) x->lrid = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.nnz_cap + 1)); if (x) x->fseg_ptr = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_row = (int32_t *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_val = (float *)p;
   p = P(4 * (size_t)D.nnz_cap); if (x) x->fseg_of = (int32_t *)p;
-  p = P(4 * (size_t)D.nnz_cap); if (x) x->rid = (int32_t *)p;
   p = P(4 * 2 * (size_t)D.h * (std::max<size_t>((size_t)D.sort_cap * D.h / 2048, 1024) + 2)); if (x) x->seg_part = (float *)p;
   p = P(4 * (size_t)D.lab_cap); if (x) x->lseg_id = (int32_t *)p;
   p = P(4 * ((size_t)D.lab_cap + 1)); if (x) x->lseg_ptr = (int32_t *)p;
@@ -349,6 +356,25 @@ int validate_csr(const as_ctx *x, int64_t rows, const int64_t *row_ptr, const in
   return AS_OK;
 }
 
+// point the ctx's batch arrays at staging block k: capacity layout (device
+// gather) or, with `packed` = {lp, col, val, lab, desc} offsets, a host batch
+void use_stage(as_ctx *x, int k, const size_t *packed) {
+  const StageLayout L = stage_layout(x->D);
+  uint8_t *g = x->stage_dev[k];
+  const size_t lp = packed ? packed[0] : L.lp, col = packed ? packed[1] : L.col, val = packed ? packed[2] : L.val,
+               lab = packed ? packed[3] : L.lab, desc = packed ? packed[4] : L.desc;
+  x->row_ptr = (int64_t *)g;
+  x->lab_ptr = (int64_t *)(g + lp);
+  x->col = (int32_t *)(g + col);
+  x->val = (float *)(g + val);
+  x->lab = (int32_t *)(g + lab);
+  x->desc = (StepDesc *)(g + desc);
+  x->ids = (int64_t *)(g + L.ids);
+  x->rid = (int32_t *)(g + L.rid);
+  x->lrid = (int32_t *)(g + L.lrid);
+  x->cur_stage = k;
+}
+
 as::TrArgs tr_args(as_ctx *x) {
   const Dims &D = x->D;
   as::TrArgs a{};
@@ -445,9 +471,9 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
     rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_mg[i], cudaEventDisableTiming), "event");
   if (const char *mc = getenv("ADASGD_MERGE_CHUNKS")) x->merge_chunks = atoi(mc) > 0 ? atoi(mc) : 0;
   // pinned double-buffered staging for host batches
-  x->pin_bytes = stage_bytes(D);
-  x->cur_stage = -1;
-  x->gather_set = {x->row_ptr, x->lab_ptr, x->col, x->lab, x->val, x->desc};
+  x->pin_bytes = stage_layout(D).desc + 64;
+  use_stage(x, 0, nullptr);
+  x->stage_next = 0;
   if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->cp_s, cudaStreamNonBlocking, prio_hi), "copy stream");
   for (int i = 0; i < 2 && !rc; ++i) {
     rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_copied[i], cudaEventDisableTiming), "event");
@@ -522,8 +548,8 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   int rc = validate_csr(x, rows, row_ptr, col, val, lab_ptr, lab, &nnz, &L);
   if (rc) return rc;
   if (nnz > x->D.nnz_cap || L > x->D.lab_cap) return as_fail(AS_E_INVALID, "batch exceeds capacity");
-  const int k = x->pin_idx;
-  x->pin_idx ^= 1;
+  const int k = x->stage_next;
+  x->stage_next ^= 1;
   rc = cuda_check(x, cudaEventSynchronize(x->pin_ev[k]), "staging wait");   // pinned block k reusable
   if (rc) return rc;
   uint8_t *p = (uint8_t *)x->pin[k];
@@ -551,22 +577,16 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   // stream once the step that last read block k is done; the main stream
   // waits for it (the copy overlaps the previous step)
   ph_begin(x, AS_PH_BATCH);
-  uint8_t *g = x->stage_dev[k];
   cudaStreamWaitEvent(x->cp_s, x->ev_stage_free[k], 0);
-  cudaMemcpyAsync(g, p, o_dd + sizeof(StepDesc), cudaMemcpyHostToDevice, x->cp_s);
-  cudaEventRecord(x->ev_copied[k], x->cp_s);
+  cudaMemcpyAsync(x->stage_dev[k], p, o_dd + sizeof(StepDesc), cudaMemcpyHostToDevice, x->cp_s);
   rc = cuda_check(x, cudaEventRecord(x->pin_ev[k], x->cp_s), "batch H2D");
   if (rc) return rc;
+  const size_t packed[5] = {o_lp, o_cc, o_vv, o_ll, o_dd};
+  use_stage(x, k, packed);
+  x->launches += 1;                     // entry -> row maps, also off the main stream
+  as::launch_entry_rows(x->cp_s, x->row_ptr, x->lab_ptr, rows, x->rid, x->lrid);
+  cudaEventRecord(x->ev_copied[k], x->cp_s);
   cudaStreamWaitEvent(s, x->ev_copied[k], 0);
-  x->row_ptr = (int64_t *)g;
-  x->lab_ptr = (int64_t *)(g + o_lp);
-  x->col = (int32_t *)(g + o_cc);
-  x->val = (float *)(g + o_vv);
-  x->lab = (int32_t *)(g + o_ll);
-  x->desc = (StepDesc *)(g + o_dd);
-  x->cur_stage = k;
-  x->launches += 1;
-  as::launch_entry_rows(s, x->row_ptr, x->lab_ptr, rows, x->rid, x->lrid);
   ph_end(x, AS_PH_BATCH);
   rc = cuda_check(x, cudaSuccess, "batch staging");
   if (rc) return rc;
@@ -618,7 +638,7 @@ int as_eval_top1(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t 
   if (top1_out) cudaMemcpyAsync(top1_out, x->top1, 4 * (size_t)rows, cudaMemcpyDeviceToHost, s);
   unsigned long long h = 0;
   cudaMemcpyAsync(&h, x->hits, 8, cudaMemcpyDeviceToHost, s);
-  if (x->cur_stage >= 0) cudaEventRecord(x->ev_stage_free[x->cur_stage], s);
+  cudaEventRecord(x->ev_stage_free[x->cur_stage], s);
   rc = cuda_check(x, cudaStreamSynchronize(s), "eval");
   if (rc) return rc;
   if (hits_out) *hits_out = (int64_t)h;
@@ -682,14 +702,19 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   const int bi = x->b_all[x->cfg.rank];
   if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
   if (pos < 0) return as_fail(AS_E_INVALID, "pos < 0");
-  x->row_ptr = x->gather_set.row_ptr; x->lab_ptr = x->gather_set.lab_ptr; x->col = x->gather_set.col;
-  x->val = x->gather_set.val; x->lab = x->gather_set.lab; x->desc = x->gather_set.desc;
-  x->cur_stage = -1;
+  // gathered on the copy stream into the staging block the step before last
+  // has released, overlapping the previous step; the step waits for it
+  const int k = x->stage_next;
+  x->stage_next ^= 1;
+  use_stage(x, k, nullptr);
   ph_begin(x, AS_PH_BATCH);
+  cudaStreamWaitEvent(x->cp_s, x->ev_stage_free[k], 0);
   x->launches += 2;
-  as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
+  as::launch_gather_batch(x->cp_s, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
                           x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
                           x->lab, x->ids, x->rid, x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+  cudaEventRecord(x->ev_copied[k], x->cp_s);
+  cudaStreamWaitEvent(x->stream, x->ev_copied[k], 0);
   ph_end(x, AS_PH_BATCH);
   const int rc = cuda_check(x, cudaSuccess, "gather batch");
   if (rc) return rc;
@@ -823,7 +848,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
   as::launch_tr_reset(ss, tr, x->num_sms);
   // the host-staged batch block may be refilled once the reset (the last
   // reader of its StepDesc) is done
-  if (x->cur_stage >= 0) cudaEventRecord(x->ev_stage_free[x->cur_stage], ss);
+  cudaEventRecord(x->ev_stage_free[x->cur_stage], ss);
   ph_end(x, AS_PH_DW1);
   int rc = cuda_check(x, cudaSuccess, "train step launch");
   if (rc) return rc;
