@@ -702,19 +702,18 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   const int bi = x->b_all[x->cfg.rank];
   if (rows < 1 || rows > bi) return as_fail(AS_E_INVALID, "rows=%d not in [1, b_i=%d]", rows, bi);
   if (pos < 0) return as_fail(AS_E_INVALID, "pos < 0");
-  // gathered on the copy stream into the staging block the step before last
-  // has released, overlapping the previous step; the step waits for it
+  // gathered on the main stream into the staging block the step before last
+  // has released (a gather on the copy stream, overlapping the previous step,
+  // measured slower: its kernels contend with the dW1 / SpMM of the step)
   const int k = x->stage_next;
   x->stage_next ^= 1;
   use_stage(x, k, nullptr);
+  cudaStreamWaitEvent(x->stream, x->ev_stage_free[k], 0);
   ph_begin(x, AS_PH_BATCH);
-  cudaStreamWaitEvent(x->cp_s, x->ev_stage_free[k], 0);
   x->launches += 2;
-  as::launch_gather_batch(x->cp_s, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
+  as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
                           x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
                           x->lab, x->ids, x->rid, x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
-  cudaEventRecord(x->ev_copied[k], x->cp_s);
-  cudaStreamWaitEvent(x->stream, x->ev_copied[k], 0);
   ph_end(x, AS_PH_BATCH);
   const int rc = cuda_check(x, cudaSuccess, "gather batch");
   if (rc) return rc;
