@@ -736,6 +736,16 @@ struct BwdCfg {
 #else
   static constexpr bool HALF = false;
 #endif
+  // PING: the 64 KB staging holds two 64-column half blocks that ping-pong:
+  // half h of block kb is updated and TMA-stored from buffer h while the other
+  // buffer's store drains / next load lands, and the load of half h of block
+  // kb + 1 is issued as soon as buffer h's store has been read -- a full block
+  // ahead of its use (one 64 KB buffer serialised store -> load -> update)
+#if defined(AS_X_FULLBUF) || defined(AS_X_HALFUPD)
+  static constexpr bool PING = false;
+#else
+  static constexpr bool PING = TMAUPD;
+#endif
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
   static constexpr int TSTAGE = TMAUPD ? BM * (HALF ? H / 2 : H) * 4 : BM * SROW * 4;
   static constexpr int SMEM = NSH * TILE + NSH * HXB + 2 * AXB + TSTAGE +
@@ -780,7 +790,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
   constexpr int UNIT = Cfg::UNIT, HPT = Cfg::HPT;
   constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
-  constexpr bool TMAUPD = Cfg::TMAUPD, FOLD = Cfg::FOLD, HALF = Cfg::HALF;
+  constexpr bool TMAUPD = Cfg::TMAUPD, FOLD = Cfg::FOLD, HALF = Cfg::HALF, PING = Cfg::PING;
   constexpr int HXB = Cfg::HXB, AXB = Cfg::AXB;
   constexpr uint32_t COL_W = NSB * UNIT, COL_DW = NSB * UNIT + NWT * WCOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -812,8 +822,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   constexpr int SF = RING ? 2 * NSB : NSB;        // s_full per buffer (and half)
   uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + SF,
            *wt_full = p_full + PH * NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
-           *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1, *s_free = wf_full + 1;
-  uint32_t *tmem_slot = (uint32_t *)(s_free + NSB);
+           *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1, *s_free = wf_full + 1,
+           *wf2 = s_free + NSB;                 // PING: the two half-block staging buffers
+  uint32_t *tmem_slot = (uint32_t *)(wf2 + 2);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
 
   const int B = desc->rows;
@@ -849,6 +860,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     mbar_init(db_full, 8);
     mbar_init(db_empty, 4);
     mbar_init(wf_full, 1);
+    mbar_init(&wf2[0], 1);
+    mbar_init(&wf2[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
@@ -1269,6 +1282,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   } else if (warp >= kUpdLo && warp < kUpdLo + 4) {  // ---------------- update warps
 #ifdef AS_X_EARLYREL
     if constexpr (TMAUPD) AS_REG_UPD();
+#else
+    // the half-block update loop holds a prefetched W2T block (64 registers)
+    // next to its working set: 160 registers (the pool has the 88 x 128 that
+    // warpgroup 3 released; the softmax warpgroups keep 128)
+    if constexpr (PING || HALF) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
 #endif
     // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
     // the compiler reusing the prologue's value, which it otherwise spills)
@@ -1327,7 +1345,14 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&wt_full[wb]);
     };
-    if constexpr (TMAUPD) {                   // fp32 W2T of the first block (its first half)
+    if constexpr (PING) {                     // fp32 W2T of the first block: both halves
+      if (ut == 0 && NB > 0)
+        for (int hh = 0; hh < 2; ++hh) {
+          mbar_expect_tx(&wf2[hh], BM * 64 * 4);
+          for (int c = 0; c < 2; ++c)
+            tma_load_2d(&mapWf, &wf2[hh], (uint8_t *)sT + hh * 32768 + c * 16384, 64 * hh + c * 32, blockIdx.x * BM);
+        }
+    } else if constexpr (TMAUPD) {            // fp32 W2T of the first block (its first half)
       if (ut == 0 && NB > 0) {
         constexpr int NBOX = HALF ? 2 : 4;
         mbar_expect_tx(wf_full, BM * 32 * 4 * NBOX);
@@ -1370,20 +1395,15 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
-      if constexpr (HALF) {
+      if constexpr (HALF || PING) {
         if (kb + NWT < NB) put_wt(kb + NWT, wpre);
         // fused SGD of the block, 64 columns at a time: the TMEM accumulator
         // (lane i = class i) and the TMA-staged fp32 half block (two swizzled
         // 32-column boxes): W2T -= lr dW2T in place, TMA store, coalesced bf16
         // shadow; the other half is TMA-loaded meanwhile.  The accumulator is
         // released once the second half's columns are in registers.
-        // opaque copies: the compiler would otherwise hoist every swizzled
-        // address of the two passes out of the block loop and spill the
-        // prefetched W2T rows to make room
-        uint32_t sw = (uint32_t)(i & 7);
-        asm volatile("" : "+r"(sw));
+        const uint32_t sw = (uint32_t)(i & 7);
         uint8_t *rowWf = reinterpret_cast<uint8_t *>(sT) + i * 128;
-        asm volatile("" : "+l"(rowWf));
         const int cls_i = cb * BM + i;
         auto sgd_box = [&](int bx, int ch, const uint32_t (&r)[32]) {
 #ifndef AS_X_NOUPD
@@ -1412,6 +1432,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         };
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
+          const int bo = PING ? hh * 2 : 0;   // staging box index of this half (PING: buffer hh)
           uint32_t ra[32], rb[32];
           AS_TMEM_LD32(tl + COL_DW + hh * 64, ra);
           AS_TMEM_LD32(tl + COL_DW + hh * 64 + 32, rb);
@@ -1422,25 +1443,25 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(dw_empty);
           }
-          mbar_wait(wf_full, (2 * kb + hh) & 1);
-          sgd_box(0, 2 * hh, ra);
-          sgd_box(1, 2 * hh + 1, rb);
+          if constexpr (PING) mbar_wait(&wf2[hh], kb & 1);
+          else mbar_wait(wf_full, (2 * kb + hh) & 1);
+          sgd_box(bo, 2 * hh, ra);
+          sgd_box(bo + 1, 2 * hh + 1, rb);
           fence_proxy_async();
           named_bar(3, 128);
 #ifndef AS_X_NOUPD
           if (ut == 0) {
-            for (int c = 0; c < 2; ++c) tma_store_2d(&mapWf, (uint8_t *)sT + c * 16384, 64 * hh + c * 32, cb * BM);
+            for (int c = 0; c < 2; ++c)
+              tma_store_2d(&mapWf, (uint8_t *)sT + (bo + c) * 16384, 64 * hh + c * 32, cb * BM);
             bulk_commit();
           }
           // bf16 shadow of these 64 columns, coalesced (8 threads per class row)
-          int utv = ut;
-          asm volatile("" : "+r"(utv));
 #pragma unroll 4
           for (int k = 0; k < 8; ++k) {
-            const int idx = k * 128 + utv;
+            const int idx = k * 128 + ut;
             const int row = idx >> 3, c8 = idx & 7;
             const int cls = cb * BM + row;
-            const uint8_t *rbp = reinterpret_cast<const uint8_t *>(sT) + (c8 >> 2) * 16384 + row * 128;
+            const uint8_t *rbp = reinterpret_cast<const uint8_t *>(sT) + (bo + (c8 >> 2)) * 16384 + row * 128;
             const uint32_t g0 = (uint32_t)((c8 & 3) * 2), rs = (uint32_t)(row & 7);
             const float4 a = *reinterpret_cast<const float4 *>(rbp + ((g0 ^ rs) << 4));
             const float4 b = *reinterpret_cast<const float4 *>(rbp + (((g0 + 1) ^ rs) << 4));
@@ -1455,12 +1476,21 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #ifndef AS_X_NOUPD
             bulk_wait_read0();
 #endif
-            const bool more = hh == 0 || kb + 1 < NB;
-            if (more) {                       // the other half of this block, or the next block's first
-              const int nrow = (hh == 0 ? cb : cb + (int)gridDim.x) * BM, ncol = hh == 0 ? 64 : 0;
-              mbar_expect_tx(wf_full, BM * 64 * 4);
-              for (int c = 0; c < 2; ++c)
-                tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, ncol + c * 32, nrow);
+            if constexpr (PING) {
+              if (kb + 1 < NB) {              // this half of the next block, into the same buffer
+                mbar_expect_tx(&wf2[hh], BM * 64 * 4);
+                for (int c = 0; c < 2; ++c)
+                  tma_load_2d(&mapWf, &wf2[hh], (uint8_t *)sT + (bo + c) * 16384, 64 * hh + c * 32,
+                              (cb + (int)gridDim.x) * BM);
+              }
+            } else {
+              const bool more = hh == 0 || kb + 1 < NB;
+              if (more) {                     // the other half of this block, or the next block's first
+                const int nrow = (hh == 0 ? cb : cb + (int)gridDim.x) * BM, ncol = hh == 0 ? 64 : 0;
+                mbar_expect_tx(wf_full, BM * 64 * 4);
+                for (int c = 0; c < 2; ++c)
+                  tma_load_2d(&mapWf, wf_full, (uint8_t *)sT + c * 16384, ncol + c * 32, nrow);
+              }
             }
           }
         }
