@@ -743,7 +743,8 @@ struct BwdCfg {
   // ahead of its use (one 64 KB buffer serialised store -> load -> update)
   // Measured slower than one 64 KB buffer (out_bwd 0.364 -> 0.373 ms): the
   // update loop's serial latency grows with the extra store / barrier rounds.
-  // Experiment switch AS_X_PING.
+  // Experiment switch AS_X_PING.  (Fetching the next block's bf16 rows during
+  // the SGD with a 160-register update warpgroup was slower too: 0.374 ms.)
 #if defined(AS_X_PING) && !defined(AS_X_HALFUPD)
   static constexpr bool PING = TMAUPD;
 #else
@@ -1289,7 +1290,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     // the half-block update loop holds a prefetched W2T block (64 registers)
     // next to its working set: 160 registers (the pool has the 88 x 128 that
     // warpgroup 3 released; the softmax warpgroups keep 128)
-    if constexpr (TMAUPD) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
+    if constexpr (PING || HALF) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
 #endif
     // NB / NT recomputed after setmaxnreg (an opaque copy of n_cblocks stops
     // the compiler reusing the prologue's value, which it otherwise spills)
@@ -1388,22 +1389,18 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if (lane == 0) mbar_arrive(&wt_full[wb]);
     };
     for (int kb = 0; kb < NB && kb < NWT; ++kb) load_wt(kb);
-    // h = 128: the bf16 rows of block kb + NWT are loaded into wpre during block
-    // kb - 1's SGD (right after that block's put), so their HBM latency never
-    // sits on the update loop, which paces pass 2 when the softmax is fast
-    uint32_t wpre[TMAUPD ? 64 : 1];
-    if constexpr (TMAUPD) {
-      if (NWT < NB) fetch_wt(NWT, wpre);
-    }
     for (int kb = 0; kb < NB; ++kb) {
       const int cb = blockIdx.x + kb * gridDim.x;
+      uint32_t wpre[TMAUPD ? 64 : 1];
+      if constexpr (TMAUPD) {
+        if (kb + NWT < NB) fetch_wt(kb + NWT, wpre);
+      }
       TRACE(3, ut == 0, 11, kb);
       mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
       if constexpr (HALF || PING) {
         if (kb + NWT < NB) put_wt(kb + NWT, wpre);
-        if (kb + NWT + 1 < NB) fetch_wt(kb + NWT + 1, wpre);
         // fused SGD of the block, 64 columns at a time: the TMEM accumulator
         // (lane i = class i) and the TMA-staged fp32 half block (two swizzled
         // 32-column boxes): W2T -= lr dW2T in place, TMA store, coalesced bf16
@@ -1503,7 +1500,6 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         }
       } else if constexpr (TMAUPD) {
         if (kb + NWT < NB) put_wt(kb + NWT, wpre);
-        if (kb + NWT + 1 < NB) fetch_wt(kb + NWT + 1, wpre);   // consumed by the next block's put
         // fused SGD of the block from the TMEM accumulator (lane i = class i)
         // and the TMA-loaded fp32 block: W2T -= lr dW2T in place (swizzled
         // 32-column boxes, conflict-free), bf16 shadow into its staging boxes
