@@ -732,6 +732,8 @@ int as_train_step(as_ctx *x, float *loss_out) {
   const float lr = x->lr;
   const bool dbg = (x->cfg.flags & AS_FLAG_DEBUG_GRADS) != 0;
   float *W1 = x->w, *b1 = x->w + D.d * D.h, *W2T = b1 + D.h, *b2 = W2T + D.C * D.h;
+  static const bool no_fuse = getenv("ADASGD_NO_DW1_FUSE") && atoi(getenv("ADASGD_NO_DW1_FUSE")) > 0;
+  const bool dw1_fused = x->cfg.precision == AS_BF16 && as::tc_fuses_dw1(D.h) && !no_fuse;
 
   // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2) on
   // the side stream, concurrent with a4/a5; joined before a6 and a7
@@ -790,12 +792,19 @@ int as_train_step(as_ctx *x, float *loss_out) {
                             dbg ? x->dbg_dHs : nullptr, as::tc_fold(D.h) ? x->Hx : nullptr);
     ph_end(x, AS_PH_COMBINE);
     cudaStreamWaitEvent(s, x->ev_join, 0);   // label transpose ready
-    // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2
+    // a6: pass 2 (tcgen05): dW2T, db2 and the fused SGD update of W2T, b2;
+    // at h = 128 its two idle warps per CTA also run a7 (dW1 + SGD of W1,
+    // which touches none of pass 2's data)
     ph_begin(x, AS_PH_OUT_BWD);
     x->launches += 1;
+    as::Dw1Args dw{};
+    if (dw1_fused) {
+      dw.desc = d; dw.seg_ptr = x->fseg_ptr; dw.seg_row = x->fseg_row; dw.seg_key = x->fseg_id;
+      dw.seg_val = x->fseg_val; dw.dA = x->dA; dw.W1 = W1; dw.lr = lr; dw.dbg = dbg ? x->dbg_dW1 : nullptr;
+    }
     as::launch_out_bwd_tc(s, x->plan, d, x->lsep, x->cls_lab, x->lbits, D.bw, x->wrow,
                           W2T, b2, x->w2b, lr, dbg ? x->dbg_dW2 : nullptr,
-                          dbg ? x->dbg_db2 : nullptr);
+                          dbg ? x->dbg_db2 : nullptr, dw);
     ph_end(x, AS_PH_OUT_BWD);
   } else {
     // fp32 parity mode: logits materialised
@@ -830,12 +839,15 @@ int as_train_step(as_ctx *x, float *loss_out) {
     as::launch_sgd_dense(s, C * D.h, W2T, x->dW2, lr, x->w2b);
     ph_end(x, AS_PH_OUT_BWD);
   }
-  // a7: first-layer gradient (deterministic segmented reduction) + SGD
+  // a7: first-layer gradient (deterministic segmented reduction) + SGD,
+  // unless pass 2 ran it
   ph_begin(x, AS_PH_DW1);
-  x->launches += 1;
-  as::launch_dw1_chunked(s, D.h, x->num_sms, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
-                         x->fseg_val, x->dA, W1, lr, x->seg_part, x->arrive,
-                         dbg ? x->dbg_dW1 : nullptr);
+  if (!dw1_fused) {
+    x->launches += 1;
+    as::launch_dw1_chunked(s, D.h, x->num_sms, d, D.nnz_cap, x->fseg_id, x->fseg_of, x->fseg_ptr, x->fseg_row,
+                           x->fseg_val, x->dA, W1, lr, x->seg_part, x->arrive,
+                           dbg ? x->dbg_dW1 : nullptr);
+  }
   if (loss_out || dbg) {
     x->launches += 1;
     as::launch_loss_mean(s, d, x->lossr, x->loss);

@@ -209,9 +209,20 @@ int tc_selftest(const void *A, const void *B, float *S, float *O, float *T, cuda
 void launch_gemm_f32_kdev(cudaStream_t s, int M, int N, int K, const float *A, long long sam,
                           long long sak, const float *B, long long sbk, long long sbn, float *Cm,
                           long long ldc, const int *K_dev);
+// step a7 fused into pass 2's idle warps (h = 128): feature segments of the
+// batch transpose, dA, W1 (W1 == nullptr: not fused)
+struct Dw1Args {
+  const StepDesc *desc;
+  const int32_t *seg_ptr, *seg_row, *seg_key;
+  const float *seg_val, *dA;
+  float *W1;
+  float lr;
+  float *dbg;
+};
+bool tc_fuses_dw1(int h);
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
                        const float *lsep, const int4 *cls_lab, const uint32_t *lbits, int lbw,
                        const float *wrow, float *W2T, float *b2, __nv_bfloat16 *W2b, float lr,
-                       float *dbg_dW2T, float *dbg_db2);
+                       float *dbg_dW2T, float *dbg_db2, const Dw1Args &dw);
 
 }  // namespace as

@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               const uint32_t *__restrict__ lbits, int lbw, const float *__restrict__ wrow,
               float *__restrict__ W2T, float *__restrict__ b2,
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
-              float *__restrict__ dbg_db2) {
+              float *__restrict__ dbg_db2, Dw1Args dw) {
   griddep_wait();
   using Cfg = BwdCfg<H>;
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
@@ -879,7 +879,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   // fits) and the update warpgroup rises to 208 so that it can drain the whole
   // dW2T accumulator (128 fp32 per lane) in one go; h = 256: the softmax
   // warpgroups rise to 168 and the update warpgroup keeps 128.
-#define AS_REG_DEC2() asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory")
+#define AS_REG_DEC2() do { if constexpr (H != 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory"); } while (0)
 #define AS_REG_INC2() do { if constexpr (H != 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory"); } while (0)
 #define AS_REG_UPD() asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory")
   if (warp == kProdWarp) {
@@ -1667,6 +1667,63 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       TRACE(3, ut == 0, 14, kb);
     }
     if (TMAUPD && ut == 0) bulk_wait0();      // stores complete before the grid ends
+  } else if (H == 128 && dw.W1) {           // warps 14-15: step a7 (dW1 + SGD) alongside
+    // First-layer gradient with fused SGD on the feature-sorted entries (a3's
+    // transpose): warp gw of the grid's 2 * gridDim.x takes segments gw, gw +
+    // GW, ...; dW1[f] = sum over the segment's entries, in entry order, of
+    // v * dA[row] (lane = 4 consecutive of the h columns), W1[f] -= lr dW1[f].
+    // Independent of pass 2's data (W2T, b2) and hidden inside its runtime;
+    // deterministic (one warp per segment, fixed order).
+    constexpr int V = H / 128;
+    const int gw = blockIdx.x * 2 + (warp - 14), GW = gridDim.x * 2;
+    const int U = dw.desc->U;
+    for (int sg = gw; sg < U; sg += GW) {
+      const int p0 = dw.seg_ptr[sg], p1 = dw.seg_ptr[sg + 1];
+      const int f = dw.seg_key[sg];
+      float4 *w1 = reinterpret_cast<float4 *>(dw.W1 + (size_t)f * H);
+      float4 wv[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) wv[q] = w1[lane + 32 * q];      // in flight during the sums
+      float4 acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      int e = p0;
+      for (; e + 4 <= p1; e += 4) {             // four entries' rows in flight
+        int r[4];
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { r[u] = dw.seg_row[e + u]; v[u] = dw.seg_val[e + u]; }
+        float4 d[4][V];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < V; ++q) d[u][q] = reinterpret_cast<const float4 *>(dw.dA + (size_t)r[u] * H)[lane + 32 * q];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            acc[q].x = fmaf(v[u], d[u][q].x, acc[q].x); acc[q].y = fmaf(v[u], d[u][q].y, acc[q].y);
+            acc[q].z = fmaf(v[u], d[u][q].z, acc[q].z); acc[q].w = fmaf(v[u], d[u][q].w, acc[q].w);
+          }
+      }
+      for (; e < p1; ++e) {
+        const int r = dw.seg_row[e];
+        const float v = dw.seg_val[e];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const float4 d = reinterpret_cast<const float4 *>(dw.dA + (size_t)r * H)[lane + 32 * q];
+          acc[q].x = fmaf(v, d.x, acc[q].x); acc[q].y = fmaf(v, d.y, acc[q].y);
+          acc[q].z = fmaf(v, d.z, acc[q].z); acc[q].w = fmaf(v, d.w, acc[q].w);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        float4 w = wv[q];
+        w.x -= dw.lr * acc[q].x; w.y -= dw.lr * acc[q].y; w.z -= dw.lr * acc[q].z; w.w -= dw.lr * acc[q].w;
+        w1[lane + 32 * q] = w;
+        if (dw.dbg) reinterpret_cast<float4 *>(dw.dbg + (size_t)sg * H)[lane + 32 * q] = acc[q];
+      }
+    }
   } else {                                    // warps 14-15: idle
     AS_REG_DEC2();
   }
@@ -2225,19 +2282,22 @@ int tc_fwd_splits_host(const TcPlan *p, int B) {
   return tc::fwd_splits(B, p->n_cblocks, fwd_grid(p), p->max_splits);
 }
 
+bool tc_fuses_dw1(int h) { return h == 128; }
+
 void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *lsep,
                        const int4 *cls_lab, const uint32_t *lbits, int lbw, const float *wrow, float *W2T,
-                       float *b2, __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2) {
+                       float *b2, __nv_bfloat16 *W2b, float lr, float *dbg_dW2T, float *dbg_db2,
+                       const Dw1Args &dw) {
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
     // plain launch: pass 2 follows the wait on the transposes' join event
     tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
         p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
-        b2, W2b, lr, dbg_dW2T, dbg_db2);
+        b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
   else
     tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
         p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
-        b2, W2b, lr, dbg_dW2T, dbg_db2);
+        b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
 }
 
 int tc_trace_dump(long long *out, int max_events) {

@@ -209,13 +209,16 @@ def test_one_step_parity(gpu_lib, case, precision, tol):
     assert np.all(dnew["W1"][untouched] == 0)                  # untouched rows bit-identical
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("h,B,avg_nnz,d", [(128, 64, 400.0, 3000), (256, 96, 250.0, 2000), (128, 1, 600.0, 5000),
                                             (128, 700, 3.0, 900)])
-def test_sparse_long_segments(gpu_lib, h, B, avg_nnz, d):
+def test_sparse_long_segments(gpu_lib, h, B, avg_nnz, d, precision):
     """SpMM rows and dW1 feature segments far longer than one CTA's entry range
     (every segment crosses warp and CTA ranges: the ordered shared-memory and
-    last-arriver combines), plus many very short rows; fp32, twice for
-    bit-identical results (deterministic sum order)."""
+    last-arriver combines), plus many very short rows; twice for
+    bit-identical results (deterministic sum order).  bf16 at h = 128 runs a7
+    inside pass 2's idle warps (one warp per feature segment)."""
+    tol = 1e-4 if precision == "fp32" else 2e-2
     cfg = _cfg(d, 300, h, 4 * B + 8, max(B, 8), avg_nnz=avg_nnz, seed=5)
     ds = synthgen.make_dataset(cfg, n=cfg.n)
     p = _params(cfg)
@@ -224,16 +227,16 @@ def test_sparse_long_segments(gpu_lib, h, B, avg_nnz, d):
     keys = np.unique(sub.col)
     outs = []
     for _ in range(2):
-        rep = _replica(cfg, p, ds, "fp32", lr=0.5)
+        rep = _replica(cfg, p, ds, precision, lr=0.5)
         rep.load_batch_csr(B, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
         rep.train_step(want_loss=True)
         H = _f32(rep.debug_get(0, 4 * B * h)).reshape(B, h)
         assert_close("H", H, ref["H"], 1e-5)
         dW1 = _f32(rep.debug_get(7, 4 * len(keys) * h)).reshape(len(keys), h)
-        assert_close("dW1", dW1, ref["dW1"][keys], 1e-4)
+        assert_close("dW1", dW1, ref["dW1"][keys], tol)
         new = rep.get_params()
         dnew = otrain.unpack(new.astype(np.float64) - p.astype(np.float64), d, cfg.C, h)
-        assert_close("W1 update", dnew["W1"][keys], -0.5 * ref["dW1"][keys], 1e-3)
+        assert_close("W1 update", dnew["W1"][keys], -0.5 * ref["dW1"][keys], max(tol, 1e-3))
         untouched = np.setdiff1d(np.arange(d), keys)
         assert np.all(dnew["W1"][untouched] == 0)
         outs.append((H.copy(), new.copy()))
