@@ -100,6 +100,8 @@ struct as_ctx {
   std::vector<int32_t> b_all;
   float lr;
   int loaded_rows;
+  long long loaded_nnz;         // host-side nnz of the loaded batch (estimate for a device gather)
+  double ds_mean_nnz;           // resident dataset: mean nnz per sample
   bool has_batch;
   void *pin[2];
   size_t pin_bytes;
@@ -591,6 +593,7 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   rc = cuda_check(x, cudaSuccess, "batch staging");
   if (rc) return rc;
   x->loaded_rows = rows;
+  x->loaded_nnz = nnz;
   return AS_OK;
 }
 
@@ -693,6 +696,7 @@ int as_dataset_upload(as_ctx *x, void *dev_buf, size_t dev_bytes, int64_t n,
   x->ds_row_ptr = drp; x->ds_col = dcol; x->ds_val = dval; x->ds_lab_ptr = dlp; x->ds_lab = dlab;
   x->ds_order = order ? dord : nullptr;
   x->ds_n = n;
+  x->ds_mean_nnz = (double)nnz / (double)n;
   return AS_OK;
 }
 
@@ -718,6 +722,7 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   const int rc = cuda_check(x, cudaSuccess, "gather batch");
   if (rc) return rc;
   x->loaded_rows = rows;
+  x->loaded_nnz = (long long)(x->ds_mean_nnz * rows + 0.5);
   x->has_batch = true;
   return AS_OK;
 }
@@ -732,8 +737,15 @@ int as_train_step(as_ctx *x, float *loss_out) {
   const float lr = x->lr;
   const bool dbg = (x->cfg.flags & AS_FLAG_DEBUG_GRADS) != 0;
   float *W1 = x->w, *b1 = x->w + D.d * D.h, *W2T = b1 + D.h, *b2 = W2T + D.C * D.h;
+  // a7 inside pass 2's idle warps (one warp per feature segment) pays when its
+  // work hides in pass 2's runtime: measured on B200, Amazon-670K (78K entries,
+  // C = 670K, W1 in L2): step -1.7%; WikiLSHTC-325K (43K entries, C = 325K, W1
+  // 828 MB: HBM-latency-bound gathers): +0.5%; Delicious-200K (309K entries,
+  // C = 205K): +72%.  Rule: entries <= 0.15 C (0.075 C when W1 exceeds L2).
   static const bool no_fuse = getenv("ADASGD_NO_DW1_FUSE") && atoi(getenv("ADASGD_NO_DW1_FUSE")) > 0;
-  const bool dw1_fused = x->cfg.precision == AS_BF16 && as::tc_fuses_dw1(D.h) && !no_fuse;
+  const bool w1_in_l2 = 4.0 * (double)D.d * D.h <= 100e6;
+  const bool dw1_fused = x->cfg.precision == AS_BF16 && as::tc_fuses_dw1(D.h) && !no_fuse &&
+                         (double)x->loaded_nnz <= (w1_in_l2 ? 0.15 : 0.075) * (double)D.C;
 
   // a3: batch transposes (feature-sorted CSC for dW1, label-sorted for dW2) on
   // the side stream, concurrent with a4/a5; joined before a6 and a7
