@@ -744,6 +744,14 @@ int as_train_step(as_ctx *x, float *loss_out) {
   // C = 205K): +72%.  Rule: entries <= 0.15 C (0.075 C when W1 exceeds L2).
   static const bool no_fuse = getenv("ADASGD_NO_DW1_FUSE") && atoi(getenv("ADASGD_NO_DW1_FUSE")) > 0;
   const bool w1_in_l2 = 4.0 * (double)D.d * D.h <= 100e6;
+  // the label terms in pass 1's idle warps unless ADASGD_LT_SEPARATE=1 (or the
+  // AS_X_LABSIDE experiment build)
+  static const bool lt_sep_env = getenv("ADASGD_LT_SEPARATE") && atoi(getenv("ADASGD_LT_SEPARATE")) > 0;
+#ifdef AS_X_LABSIDE
+  const bool lt_sep = true;
+#else
+  const bool lt_sep = lt_sep_env;
+#endif
   const bool dw1_fused = x->cfg.precision == AS_BF16 && as::tc_fuses_dw1(D.h) && !no_fuse &&
                          (double)x->loaded_nnz <= (w1_in_l2 ? 0.15 : 0.075) * (double)D.C;
 
@@ -785,7 +793,9 @@ int as_train_step(as_ctx *x, float *loss_out) {
     // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
     ph_begin(x, AS_PH_OUT_FWD);
     x->launches += 1;
-    as::launch_out_fwd_tc(s, x->plan, d, b2, x->pm, x->pl, x->pO);
+    as::LtArgs lt{};
+    if (!lt_sep) lt = {x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW};
+    as::launch_out_fwd_tc(s, x->plan, d, b2, x->pm, x->pl, x->pO, lt);
     ph_end(x, AS_PH_OUT_FWD);
     if (AS_X_FORK == 2) fork_transposes();
     ph_begin(x, AS_PH_COMBINE);
@@ -795,8 +805,11 @@ int as_train_step(as_ctx *x, float *loss_out) {
     x->launches += 1;
     cudaStreamWaitEvent(s, x->ev_lab, 0);
 #else
-    x->launches += 2;
-    as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
+    x->launches += 1;
+    if (lt_sep) {                             // (else pass 1's idle warps computed them)
+      x->launches += 1;
+      as::launch_label_terms(s, D.h, d, D.b_max, x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW);
+    }
 #endif
     as::launch_combine_bf16(s, D.h, d, D.b_max, D.bpad, as::tc_fwd_splits_host(x->plan, rows), x->pm,
                             x->pl, x->pO, x->labW, x->zsum, x->Hf, x->lab_ptr, x->lse2, x->lsep, x->wrow,

@@ -191,8 +191,16 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
                  const void *W2b, const void *W2T, const void *Hx);
 bool tc_fold(int h);   // pass 2 takes b2 and -(LSE + ln B) in its S^T MMA (B_ext rows from the combine)
 int tc_splits(int h, int b_max, long long C, int num_sms);
+// label terms of the loss and dH (a5, R3) computed by pass 1's two idle warps
+// per CTA (zsum == nullptr: not computed there)
+struct LtArgs {
+  const int64_t *lab_ptr;
+  const int32_t *lab;
+  const float *Hf, *W2T, *b2;
+  float *zsum, *labW;
+};
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc,
-                       const float *b2, float *pm, float *pl, float *pO);
+                       const float *b2, float *pm, float *pl, float *pO, const LtArgs &lt);
 int tc_fwd_splits_host(const TcPlan *plan, int B);
 // top-1 evaluation (NEXT f1): per-split (max, argmax) partials, then the ordered combine
 void launch_out_top1_tc(cudaStream_t s, const TcPlan *plan, const StepDesc *desc, const float *b2,

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     k_out_fwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
               const StepDesc *__restrict__ desc, const __nv_bfloat16 *__restrict__ Hb,
               const float *__restrict__ b2, int C, int n_cblocks, int max_splits, int bpad,
-              float *__restrict__ pm, float *__restrict__ pl, float *__restrict__ pO) {
+              float *__restrict__ pm, float *__restrict__ pl, float *__restrict__ pO, LtArgs lt) {
   griddep_wait();
   using Cfg = FwdCfg<H>;
   constexpr int NST = Cfg::NST, TILE = Cfg::TILE;
@@ -672,8 +672,46 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     }
   } else if (NWG == 1 && warp < 8) {          // h = 256: the second WG is idle
     AS_REG_INC();
-  } else {                                    // warps 8-9: idle
+  } else {                                    // warps 8-9: the label terms (a5, R3) alongside
     AS_REG_DEC();
+    // zsum_r = (1/k_r) sum_{y in Y_r} z_ry and labW_r = (1/k_r) sum_y W2T[y]
+    // (fp32 master weights, pre-update) for rows r = gw, gw + GW, ... (warp per
+    // row, labels in order, lane = 4 consecutive of the h columns); they need
+    // only H and W2T, so they hide in pass 1 and the combine reads them after
+    if (lt.zsum) {
+      constexpr int V = H / 128;
+      const int gw = (int)blockIdx.x * 2 + (warp - 8), GW = RT * splits * 2;
+      for (int r = gw; r < B; r += GW) {
+        const int64_t s0 = lt.lab_ptr[r], s1 = lt.lab_ptr[r + 1];
+        const float inv_k = 1.0f / (float)(s1 - s0);
+        float4 hr[V], lw[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          hr[q] = reinterpret_cast<const float4 *>(lt.Hf + (size_t)r * H)[lane + 32 * q];
+          lw[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float zs = 0.f;
+        for (int64_t j = s0; j < s1; ++j) {
+          const int y = lt.lab[j];
+          const float bb = lt.b2[y];
+          float d = 0.f;
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            const float4 w = reinterpret_cast<const float4 *>(lt.W2T + (size_t)y * H)[lane + 32 * q];
+            d = fmaf(hr[q].x, w.x, fmaf(hr[q].y, w.y, fmaf(hr[q].z, w.z, fmaf(hr[q].w, w.w, d))));
+            lw[q].x += w.x; lw[q].y += w.y; lw[q].z += w.z; lw[q].w += w.w;
+          }
+          zs += warp_sum(d) + bb;
+        }
+        if (lane == 0) lt.zsum[r] = zs * inv_k;
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          float4 o = lw[q];
+          o.x *= inv_k; o.y *= inv_k; o.z *= inv_k; o.w *= inv_k;
+          reinterpret_cast<float4 *>(lt.labW + (size_t)r * H)[lane + 32 * q] = o;
+        }
+      }
+    }
   }
   fence_before();
   __syncthreads();
@@ -2256,15 +2294,15 @@ static int fwd_grid(const TcPlan *p) {
 }
 
 void launch_out_fwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2,
-                       float *pm, float *pl, float *pO) {
+                       float *pm, float *pl, float *pO, const LtArgs &lt) {
   if (p->h == 128)
     launch_pdl(tc::k_out_fwd<128>, dim3(fwd_grid(p)), dim3(tc::FwdCfg<128>::THREADS), tc::FwdCfg<128>::SMEM, s,
                p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
-               p->max_splits, p->bpad, pm, pl, pO);
+               p->max_splits, p->bpad, pm, pl, pO, lt);
   else
     launch_pdl(tc::k_out_fwd<256>, dim3(fwd_grid(p)), dim3(tc::FwdCfg<256>::THREADS), tc::FwdCfg<256>::SMEM, s,
                p->mapH, p->mapW, desc, (const __nv_bfloat16 *)p->Hb, b2, (int)p->C, p->n_cblocks,
-               p->max_splits, p->bpad, pm, pl, pO);
+               p->max_splits, p->bpad, pm, pl, pO, lt);
 }
 
 void launch_out_top1_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, const float *b2, float *pmax,
