@@ -101,7 +101,8 @@ struct as_ctx {
   float lr;
   int loaded_rows;
   long long loaded_nnz;         // host-side nnz of the loaded batch (estimate for a device gather)
-  double ds_mean_nnz;           // resident dataset: mean nnz per sample
+  long long loaded_lab;         // the same for its labels
+  double ds_mean_nnz, ds_mean_lab;   // resident dataset: mean nnz / labels per sample
   bool has_batch;
   void *pin[2];
   size_t pin_bytes;
@@ -594,6 +595,7 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   if (rc) return rc;
   x->loaded_rows = rows;
   x->loaded_nnz = nnz;
+  x->loaded_lab = L;
   return AS_OK;
 }
 
@@ -697,6 +699,7 @@ int as_dataset_upload(as_ctx *x, void *dev_buf, size_t dev_bytes, int64_t n,
   x->ds_order = order ? dord : nullptr;
   x->ds_n = n;
   x->ds_mean_nnz = (double)nnz / (double)n;
+  x->ds_mean_lab = (double)L / (double)n;
   return AS_OK;
 }
 
@@ -723,6 +726,7 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   if (rc) return rc;
   x->loaded_rows = rows;
   x->loaded_nnz = (long long)(x->ds_mean_nnz * rows + 0.5);
+  x->loaded_lab = (long long)(x->ds_mean_lab * rows + 0.5);
   x->has_batch = true;
   return AS_OK;
 }
@@ -747,10 +751,13 @@ int as_train_step(as_ctx *x, float *loss_out) {
   // the label terms in pass 1's idle warps unless ADASGD_LT_SEPARATE=1 (or the
   // AS_X_LABSIDE experiment build)
   static const bool lt_sep_env = getenv("ADASGD_LT_SEPARATE") && atoi(getenv("ADASGD_LT_SEPARATE")) > 0;
+  // measured on B200: Amazon-670K (5 labels / row, C = 670K) step -0.25%,
+  // Delicious-200K (75 labels / row, C = 205K) +2.6% when fused: fuse when the
+  // batch has at most 0.05 C labels
 #ifdef AS_X_LABSIDE
   const bool lt_sep = true;
 #else
-  const bool lt_sep = lt_sep_env;
+  const bool lt_sep = lt_sep_env || (double)x->loaded_lab > 0.05 * (double)D.C;
 #endif
   const bool dw1_fused = x->cfg.precision == AS_BF16 && as::tc_fuses_dw1(D.h) && !no_fuse &&
                          (double)x->loaded_nnz <= (w1_in_l2 ? 0.15 : 0.075) * (double)D.C;
