@@ -118,6 +118,7 @@ struct as_ctx {
   int stage_next;               // block the next load writes
   // resident dataset
   const int64_t *ds_row_ptr, *ds_lab_ptr, *ds_order;
+  std::vector<int64_t> ds_rp_host, ds_lp_host;   // the dataset's pointers (slice offsets)
   const int32_t *ds_col, *ds_lab;
   const float *ds_val;
   int64_t ds_n;
@@ -699,6 +700,8 @@ int as_dataset_upload(as_ctx *x, void *dev_buf, size_t dev_bytes, int64_t n,
   x->ds_order = order ? dord : nullptr;
   x->ds_n = n;
   x->ds_mean_nnz = (double)nnz / (double)n;
+  x->ds_rp_host.assign(row_ptr, row_ptr + n + 1);
+  x->ds_lp_host.assign(lab_ptr, lab_ptr + n + 1);
   x->ds_mean_lab = (double)L / (double)n;
   return AS_OK;
 }
@@ -717,10 +720,22 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
   use_stage(x, k, nullptr);
   cudaStreamWaitEvent(x->stream, x->ev_stage_free[k], 0);
   ph_begin(x, AS_PH_BATCH);
-  x->launches += 2;
-  as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
-                          x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
-                          x->lab, x->ids, x->rid, x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+  const int64_t p0 = pos % x->ds_n;
+  static const bool no_slice = getenv("ADASGD_NO_SLICE") && atoi(getenv("ADASGD_NO_SLICE")) > 0;
+  if (!x->ds_order && p0 + rows <= x->ds_n && !no_slice) {
+    // contiguous slice of the resident dataset: features and labels in place
+    x->col = const_cast<int32_t *>(x->ds_col) + x->ds_rp_host[p0];
+    x->val = const_cast<float *>(x->ds_val) + x->ds_rp_host[p0];
+    x->lab = const_cast<int32_t *>(x->ds_lab) + x->ds_lp_host[p0];
+    x->launches += 1;
+    as::launch_slice_batch(x->stream, x->ds_row_ptr, x->ds_lab_ptr, p0, rows, x->row_ptr, x->lab_ptr, x->rid,
+                           x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+  } else {
+    x->launches += 2;
+    as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
+                            x->ds_order, x->ds_n, pos, rows, x->row_ptr, x->col, x->val, x->lab_ptr,
+                            x->lab, x->ids, x->rid, x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+  }
   ph_end(x, AS_PH_BATCH);
   const int rc = cuda_check(x, cudaSuccess, "gather batch");
   if (rc) return rc;

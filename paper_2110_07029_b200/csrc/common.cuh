@@ -105,6 +105,9 @@ void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_
                          int64_t *row_ptr, int32_t *col, float *val, int64_t *lab_ptr,
                          int32_t *lab, int64_t *ids, int32_t *rid, int32_t *lrid, StepDesc *desc,
                          int nnz_cap, int lab_cap);
+void launch_slice_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int64_t *ds_lab_ptr, int64_t p0,
+                        int rows, int64_t *row_ptr, int64_t *lab_ptr, int32_t *rid, int32_t *lrid,
+                        StepDesc *desc, int nnz_cap, int lab_cap);
 void launch_entry_rows(cudaStream_t s, const int64_t *row_ptr, const int64_t *lab_ptr, int rows,
                        int32_t *rid, int32_t *lrid);
 void launch_transposes(cudaStream_t s, const TrArgs &a);

@@ -104,6 +104,48 @@ __global__ void k_gather_copy(const int64_t *__restrict__ rp, const int32_t *__r
   }
 }
 
+// The batch is a CONTIGUOUS slice [p0, p0 + rows) of the resident dataset
+// (stream order = dataset order, no wrap): its col / val / lab are used in
+// place, and one kernel writes the rebased pointers, the entry -> row maps and
+// the descriptor (warp per row).
+__global__ void k_slice_batch(const int64_t *__restrict__ rp, const int64_t *__restrict__ lp, int64_t p0, int rows,
+                              int64_t *__restrict__ row_ptr, int64_t *__restrict__ lab_ptr,
+                              int32_t *__restrict__ rid, int32_t *__restrict__ lrid, StepDesc *__restrict__ desc,
+                              int nnz_cap, int lab_cap) {
+  griddep_wait();
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int64_t b0 = rp[p0], l0 = lp[p0];
+  if (r < rows) {
+    const int64_t s = rp[p0 + r] - b0, e = rp[p0 + r + 1] - b0;
+    const int64_t ls = lp[p0 + r] - l0, le = lp[p0 + r + 1] - l0;
+    if (lane == 0) {
+      row_ptr[r + 1] = e;
+      lab_ptr[r + 1] = le;
+    }
+    for (int64_t j = s + lane; j < e; j += 32) rid[j] = r;
+    for (int64_t j = ls + lane; j < le; j += 32) lrid[j] = r;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    row_ptr[0] = 0;
+    lab_ptr[0] = 0;
+    const long long nnz = rp[p0 + rows] - b0, nl = lp[p0 + rows] - l0;
+    desc->rows = rows;
+    desc->nnz = (int)nnz;
+    desc->nlab = (int)nl;
+    desc->U = 0;
+    desc->V = 0;
+    desc->n_long = 0;
+    desc->err = (nnz > nnz_cap || nl > lab_cap) ? 1 : 0;
+  }
+}
+
+void launch_slice_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int64_t *ds_lab_ptr, int64_t p0,
+                        int rows, int64_t *row_ptr, int64_t *lab_ptr, int32_t *rid, int32_t *lrid,
+                        StepDesc *desc, int nnz_cap, int lab_cap) {
+  launch_pdl(k_slice_batch, dim3(ceil_div((long long)rows * 32, 256)), dim3(256), 0, s, ds_row_ptr, ds_lab_ptr, p0,
+             rows, row_ptr, lab_ptr, rid, lrid, desc, nnz_cap, lab_cap);
+}
+
 void launch_gather_batch(cudaStream_t s, const int64_t *ds_row_ptr, const int32_t *ds_col,
                          const float *ds_val, const int64_t *ds_lab_ptr, const int32_t *ds_lab,
                          const int64_t *order, int64_t n, int64_t pos, int rows,
