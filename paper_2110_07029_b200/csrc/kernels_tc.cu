@@ -76,6 +76,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+// the same with a suspend-time hint (ns): for waits off the critical path
+// (producers, the update loop), so the waiting warp sleeps in the barrier
+// instead of re-polling (issue slots and power under the power cap)
+__device__ __forceinline__ void mbar_wait_idle(uint64_t *b, uint32_t parity) {
+#ifdef AS_X_NOSUSPEND
+  mbar_wait(b, parity);
+#else
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity), "r"(2000u)
+        : "memory");
+  } while (!ok);
+#endif
+}
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst,
                                             int c0, int c1) {
   asm volatile(
@@ -416,7 +435,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       for (int a = 0; a < H / 64; ++a) tma_load_2d(&mapH, h_full, sH + a * ATOM_BYTES, a * 64, rt * BM);
       for (int j = 0; j < nloc; ++j) {
         const int st = j % NST;
-        if (j >= NST) mbar_wait(&w_empty[st], ((j / NST) - 1) & 1);
+        if (j >= NST) mbar_wait_idle(&w_empty[st], ((j / NST) - 1) & 1);
 #ifdef AS_X_NOTMA
         if (j >= NST) { mbar_arrive(&w_full[st]); continue; }
 #endif
@@ -935,7 +954,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       for (int kb = 0; kb < NB; ++kb)
         for (int t = 0; t < RT; ++t, ++it) {
           const int st = it % NSH;
-          if (it >= NSH) mbar_wait(&h_empty[st], ((it / NSH) - 1) & 1);
+          if (it >= NSH) mbar_wait_idle(&h_empty[st], ((it / NSH) - 1) & 1);
           TRACE(2, true, 10, t);
 #ifdef AS_X_NOTMA
           if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
@@ -1434,7 +1453,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         if (kb + NWT < NB) fetch_wt(kb + NWT, wpre);
       }
       TRACE(3, ut == 0, 11, kb);
-      mbar_wait(dw_full, kb & 1);             // also: every S of block kb completed
+      mbar_wait_idle(dw_full, kb & 1);        // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
       if constexpr (HALF || PING) {
@@ -1693,7 +1712,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       }
       // db2 (thread ut = class ut of the block; label term already in G), SGD on b2
       TRACE(3, ut == 0, 13, kb);
-      mbar_wait(db_full, kb & 1);
+      mbar_wait_idle(db_full, kb & 1);
       const float dsum = sDB[ut] + sDB[BM + ut];
       named_bar(3, 128);
       if (lane == 0) mbar_arrive(db_empty);
@@ -2102,7 +2121,7 @@ __global__ void __launch_bounds__(Top1Cfg<H>::THREADS, 1)
       for (int a = 0; a < H / 64; ++a) tma_load_2d(&mapH, h_full, sH + a * ATOM_BYTES, a * 64, rt * BM);
       for (int j = 0; j < nloc; ++j) {
         const int st = j % NST;
-        if (j >= NST) mbar_wait(&w_empty[st], ((j / NST) - 1) & 1);
+        if (j >= NST) mbar_wait_idle(&w_empty[st], ((j / NST) - 1) & 1);
         mbar_expect_tx(&w_full[st], TILE);
         for (int a = 0; a < H / 64; ++a)
           tma_load_2d(&mapW, &w_full[st], sW + st * TILE + a * ATOM_BYTES, a * 64, (cb0 + j) * BM);
