@@ -728,8 +728,17 @@ int as_load_batch_stream(as_ctx *x, int64_t pos, int32_t rows) {
     x->val = const_cast<float *>(x->ds_val) + x->ds_rp_host[p0];
     x->lab = const_cast<int32_t *>(x->ds_lab) + x->ds_lp_host[p0];
     x->launches += 1;
-    as::launch_slice_batch(x->stream, x->ds_row_ptr, x->ds_lab_ptr, p0, rows, x->row_ptr, x->lab_ptr, x->rid,
-                           x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+    static const bool slice_main = getenv("ADASGD_SLICE_MAIN") && atoi(getenv("ADASGD_SLICE_MAIN")) > 0;
+    if (slice_main) {
+      as::launch_slice_batch(x->stream, x->ds_row_ptr, x->ds_lab_ptr, p0, rows, x->row_ptr, x->lab_ptr, x->rid,
+                             x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+    } else {                                  // on the copy stream, overlapping the previous step
+      cudaStreamWaitEvent(x->cp_s, x->ev_stage_free[k], 0);
+      as::launch_slice_batch(x->cp_s, x->ds_row_ptr, x->ds_lab_ptr, p0, rows, x->row_ptr, x->lab_ptr, x->rid,
+                             x->lrid, x->desc, x->D.nnz_cap, x->D.lab_cap);
+      cudaEventRecord(x->ev_copied[k], x->cp_s);
+      cudaStreamWaitEvent(x->stream, x->ev_copied[k], 0);
+    }
   } else {
     x->launches += 2;
     as::launch_gather_batch(x->stream, x->ds_row_ptr, x->ds_col, x->ds_val, x->ds_lab_ptr, x->ds_lab,
