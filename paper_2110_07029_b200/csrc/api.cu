@@ -1018,7 +1018,9 @@ static int merge_apply_dev(as_ctx *x, float alpha_host_me /* NaN: unknown */) {
     cudaStreamWaitEvent(x->comm_s, x->ev_mg[0], 0);
   }
   for (int c = 0; c < K; ++c) {
-    const long long off = D.P * c / K, len = D.P * (c + 1) / K - off;
+    // chunk borders on multiples of 4 floats (the vectorised momentum kernel)
+    const long long off = (D.P * c / K) & ~3ll, end = c + 1 == K ? D.P : (D.P * (c + 1) / K) & ~3ll,
+                    len = end - off;
     if (use_nccl) {
       const ncclResult_t r = ncclAllReduce(x->w + off, x->w + off, len, ncclFloat, premul, x->comm, x->comm_s);
       if (r != ncclSuccess) {

@@ -488,10 +488,43 @@ __global__ void k_momentum(float *__restrict__ w, float *__restrict__ wp,
   }
 }
 
+// the same on float4 vectors (all pointers 16-B aligned, w2_off % 4 == 0, so a
+// vector lies wholly inside or outside the W2T range); scalar tail P % 4
+__global__ void __launch_bounds__(256) k_momentum4(float *__restrict__ w, float *__restrict__ wp,
+                                                   const float *__restrict__ wbar, long long P, float gamma,
+                                                   long long w2_off, long long w2_len,
+                                                   __nv_bfloat16 *__restrict__ shadow) {
+  const long long nv4 = P / 4;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv4;
+       v += (long long)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4 *>(w)[v], g = reinterpret_cast<const float4 *>(wbar)[v],
+                 q = reinterpret_cast<const float4 *>(wp)[v];
+    float4 o;
+    o.x = a.x + gamma * (g.x - q.x); o.y = a.y + gamma * (g.y - q.y);
+    o.z = a.z + gamma * (g.z - q.z); o.w = a.w + gamma * (g.w - q.w);
+    reinterpret_cast<float4 *>(wp)[v] = o;
+    reinterpret_cast<float4 *>(w)[v] = o;
+    const long long i = 4 * v;
+    if (shadow && i >= w2_off && i < w2_off + w2_len)
+      reinterpret_cast<uint2 *>(shadow)[(i - w2_off) / 4] = make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (int)(P - 4 * nv4)) {
+    const long long i = 4 * nv4 + threadIdx.x;
+    const float nv = w[i] + gamma * (wbar[i] - wp[i]);
+    wp[i] = nv;
+    w[i] = nv;
+    if (shadow && i >= w2_off && i < w2_off + w2_len) shadow[i - w2_off] = __float2bfloat16_rn(nv);
+  }
+}
+
 void launch_momentum(cudaStream_t s, float *w, float *wbar_p_to_new, const float *wbar,
                      long long P, float gamma, long long w2_off, long long w2_len,
                      __nv_bfloat16 *shadow) {
-  k_momentum<<<148 * 8, 256, 0, s>>>(w, wbar_p_to_new, wbar, P, gamma, w2_off, w2_len, shadow);
+  const bool aligned = (((uintptr_t)w | (uintptr_t)wbar_p_to_new | (uintptr_t)wbar) & 15) == 0 && (w2_off & 3) == 0;
+  if (aligned)
+    k_momentum4<<<148 * 4, 256, 0, s>>>(w, wbar_p_to_new, wbar, P, gamma, w2_off, w2_len, shadow);
+  else
+    k_momentum<<<148 * 8, 256, 0, s>>>(w, wbar_p_to_new, wbar, P, gamma, w2_off, w2_len, shadow);
 }
 
 // local-group merge: S = sum_i alpha_i w_i read directly from every replica
