@@ -68,9 +68,8 @@ def _worker(rank, world, port, backend, algo, outdir):
     dist.destroy_process_group()
 
 
-def _run(backend, algo):
+def _run(backend, algo, world=2):
     import torch.multiprocessing as mp
-    world = 2
     with tempfile.TemporaryDirectory() as d:
         mp.start_processes(_worker, args=(world, _free_port(), backend, algo, d), nprocs=world, join=True,
                            start_method="spawn")
@@ -97,9 +96,11 @@ def _run(backend, algo):
         assert len({tuple(a) for a in oalpha}) > 1 and opert.any()    # heterogeneity and perturbation exercised
 
 
-@pytest.mark.parametrize("algo", ["adaptive", "elastic"])
-def test_two_processes_p2p_merge_one_gpu(gpu_lib, algo):
-    _run("p2p", algo)
+@pytest.mark.parametrize("algo,world", [("adaptive", 2), ("elastic", 2), ("adaptive", 3)])
+def test_two_processes_p2p_merge_one_gpu(gpu_lib, algo, world):
+    """world = 3: the slices rP/N of the packed vector (P = 1 409 128 floats is
+    not a multiple of 3 * 4) and three-way barriers."""
+    _run("p2p", algo, world)
 
 
 def test_two_processes_nccl_merge(gpu_lib):
