@@ -265,13 +265,13 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   const int B = desc->rows;
   if (blockIdx.x * 32 >= B) {         // a CTA of padding rows only
     const int r = blockIdx.x * 32 + rx;
-    if (jy == 0 && r < bpad && blockIdx.y == 0) { lsep[r] = INFINITY; wrow[r] = 0.f; put_hx(r, -1e30f); }
+    if (jy == 0 && r < bpad && blockIdx.y == 0) { lsep[r] = -INFINITY; wrow[r] = 0.f; put_hx(r, -1e30f); }
     return;
   }
   const bool live = blockIdx.x * 32 + rx < B;
   const int r = live ? blockIdx.x * 32 + rx : B - 1;   // padding lanes shadow a live row
   if (!live && jy == 0 && blockIdx.y == 0) {
-    lsep[blockIdx.x * 32 + rx] = INFINITY;
+    lsep[blockIdx.x * 32 + rx] = -INFINITY;
     wrow[blockIdx.x * 32 + rx] = 0.f;
     put_hx(blockIdx.x * 32 + rx, -1e30f);
   }
@@ -367,8 +367,8 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   if (jy == 0 && live && blockIdx.y == 0) {
     const float L2 = M + log2f(l);
     lse2[r] = L2;
-    lsep[r] = L2 + log2f((float)B);   // pass 2: p / B = 2^(s log2e - lsep)
-    put_hx(r, -(lsep[r] * 0.69314718055994531f));   // FOLD: -(LSE + ln B), natural units
+    lsep[r] = -(L2 + log2f((float)B));   // pass 2: p / B = 2^(s log2e + lsep), lsep = -lse'
+    put_hx(r, lsep[r] * 0.69314718055994531f);      // FOLD: -(LSE + ln B), natural units
     // pass 2's label weight of the row, 1 / (k_r B) (R3), same fp32 operations
     // as the label transpose's per-entry weights
     wrow[r] = (1.0f / (float)B) / (float)(lab_ptr[r + 1] - lab_ptr[r]);

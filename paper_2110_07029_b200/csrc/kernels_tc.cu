@@ -802,10 +802,57 @@ struct BwdCfg {
   // update loop's serial latency grows with the extra store / barrier rounds.
   // Experiment switch AS_X_PING.  (Fetching the next block's bf16 rows during
   // the SGD with a 160-register update warpgroup was slower too: 0.374 ms.)
+#ifdef AS_X_EARLYREL
+  static constexpr bool EARLYREL_ = true;
+#else
+  static constexpr bool EARLYREL_ = false;
+#endif
 #if defined(AS_X_PING) && !defined(AS_X_HALFUPD)
   static constexpr bool PING = TMAUPD;
 #else
   static constexpr bool PING = false;
+#endif
+  // ECF (h = 128): the class bias leaves the exponent.  p_rc / B =
+  // E_c 2^(s_rc log2e - lse'_r) with E_c = exp(b2_c), so the softmax computes
+  // G'_rc = G_rc / E_c (one FFMA2 per pair: s log2e + (-lse')), the label term
+  // enters G' as w_r / E_c, db2 = E_c sum_r G'_rc, and the update scales its
+  // learning rate per class: W2T_c -= (lr E_c) (G'^T H)_c -- the same G up to
+  // the bf16 rounding of G' instead of G (relative, equal size).  Needs
+  // |b2| < 80 (E_c, 1 / E_c and p / E_c inside the fp32 range).
+  // Experiment switch AS_X_ECF (off in the product build).
+#ifdef AS_X_ECF
+  static constexpr bool ECF = TMAUPD && !FOLD && !HALF && !PING;
+#else
+  static constexpr bool ECF = false;             // measured neutral-to-slower (out_bwd +1%): off
+#endif
+  // REGS3 (h = 128): warpgroup 3 (producer, MMA, dW1 warps) drops to 64
+  // registers and the two softmax warpgroups rise to 160 (AS_X_NOREGS3: all 128).
+  // Measured with LATEMK: out_bwd 0.375 -> 0.368 ms (two x_probe A/B pairs).
+#ifdef AS_X_NOREGS3
+  static constexpr bool REGS3 = false;
+#else
+  static constexpr bool REGS3 = H == 128 && !HALF && !PING && !EARLYREL_;
+#endif
+  // LATEMK: a unit's label-row bitmap is read after its first half's
+  // exponentials (AS_X_NOLATEMK: before the half loop)
+#ifdef AS_X_NOLATEMK
+  static constexpr bool LATEMK = false;
+#else
+  static constexpr bool LATEMK = true;
+#endif
+  // S0POLL (ring): the MMA warp issues the first S^T half of a WG's next unit
+  // as soon as that WG has loaded the S^T columns it reuses (s_free), whatever
+  // the other WG's progress -- it polls (try_wait with a short suspend) instead
+  // of blocking on the other WG's G^T; the dW MMAs stay in unit order
+  // (deterministic).  p_full is then indexed by unit mod 4 so that a WG can
+  // signal the unit two ahead before the MMA warp has observed this one.
+  // Measured slower (out_bwd 0.367 -> 0.400 ms, x_probe A/B): the polling
+  // warp takes issue slots from the softmax warps of its sub-partition, and
+  // the tensor pipe gains nothing.  Experiment switch AS_X_S0POLL.
+#ifdef AS_X_S0POLL
+  static constexpr bool S0POLL = UNIT == 128;
+#else
+  static constexpr bool S0POLL = false;
 #endif
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
   static constexpr int TSTAGE = TMAUPD ? BM * (HALF ? H / 2 : H) * 4 : BM * SROW * 4;
@@ -881,8 +928,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   constexpr bool RING = UNIT == 128;
 #endif
   constexpr int SF = RING ? 2 * NSB : NSB;        // s_full per buffer (and half)
+  constexpr bool S0POLL = RING && Cfg::S0POLL;
+  constexpr int NPF = S0POLL ? 8 : PH * NSB;      // p_full: [unit mod 4][half] under S0POLL
   uint64_t *h_full = bars, *h_empty = h_full + NSH, *s_full = h_empty + NSH, *p_full = s_full + SF,
-           *wt_full = p_full + PH * NSB, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
+           *wt_full = p_full + NPF, *dw_full = wt_full + NWT, *dw_empty = dw_full + 1,
            *db_full = dw_empty + 1, *db_empty = db_full + 1, *wf_full = db_empty + 1, *s_free = wf_full + 1,
            *wf2 = s_free + NSB;                 // PING: the two half-block staging buffers
   uint32_t *tmem_slot = (uint32_t *)(wf2 + 2);
@@ -914,7 +963,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     for (int i = 0; i < NSH; ++i) { mbar_init(&h_full[i], 1); mbar_init(&h_empty[i], 1); }
     for (int i = 0; i < SF; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < NSB; ++i) mbar_init(&s_free[i], 4);
-    for (int i = 0; i < PH * NSB; ++i) mbar_init(&p_full[i], 4);
+    for (int i = 0; i < NPF; ++i) mbar_init(&p_full[i], 4);
     for (int i = 0; i < NWT; ++i) mbar_init(&wt_full[i], 4);
     mbar_init(dw_full, 1);
     mbar_init(dw_empty, 4);
@@ -936,8 +985,16 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
   // fits) and the update warpgroup rises to 208 so that it can drain the whole
   // dW2T accumulator (128 fp32 per lane) in one go; h = 256: the softmax
   // warpgroups rise to 168 and the update warpgroup keeps 128.
-#define AS_REG_DEC2() do { if constexpr (H != 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory"); } while (0)
-#define AS_REG_INC2() do { if constexpr (H != 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory"); } while (0)
+#define AS_REG_DEC2()                                                                       \
+  do {                                                                                      \
+    if constexpr (H != 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory"); \
+    else if constexpr (Cfg::REGS3) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;" ::: "memory"); \
+  } while (0)
+#define AS_REG_INC2()                                                                        \
+  do {                                                                                       \
+    if constexpr (H != 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory"); \
+    else if constexpr (Cfg::REGS3) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory"); \
+  } while (0)
 #define AS_REG_UPD() asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory")
   if (warp == kProdWarp) {
     AS_REG_DEC2();
@@ -1041,7 +1098,86 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       };
       Cur cs{0, 0, 0, 0, 0, 0, 0u, 0u, 0u}, cd{0, 0, 0, 0, 0, 0, 0u, 0u, 0u};
       int ns = 0;                             // S units issued
-      if constexpr (RING) {
+      if constexpr (S0POLL) {
+        constexpr uint32_t idS64 = idesc_bf16(BM, 64, 0, 0);
+        // non-blocking phase test; the suspend variant sleeps up to ~64 ns
+        auto ready = [&](uint64_t *bar, uint32_t ph) {
+          uint32_t ok;
+          asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                       "selp.u32 %0, 1, 0, p;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(bar)), "r"(ph) : "memory");
+          return ok != 0u;
+        };
+        auto ready_sleep = [&](uint64_t *bar, uint32_t ph) {
+          uint32_t ok;
+          asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                       "selp.u32 %0, 1, 0, p;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(bar)), "r"(ph), "r"(64u) : "memory");
+          return ok != 0u;
+        };
+        // S half `half` of the unit at cursor c (parity c.bph): columns 64 ((half + par) & 1)
+        auto issue_half = [&](const Cur &c, int half) {
+#ifndef AS_X_NOMMA1
+          const uint32_t dcol = c.b * UNIT + (uint32_t)(((half + (int)c.bph) & 1) * 64);
+          mma_grp_ts_k_8(tmem + dcol, tmem + COL_W + c.wb * WCOLS,
+                         sdesc(aH + c.st * TILE + half * 64 * 128, 16, 1024), idS64, 0u);
+#endif
+          mma_commit_w(&s_full[2 * c.b + half]);
+        };
+        Cur c0{0, 0, 0, 0, 0, 0, 0u, 0u, 0u}, c1{0, 0, 0, 0, 0, 0, 0u, 0u, 0u};
+        int n0 = 0, n1 = 0, ndw = 0;          // units with S half 0 / S half 1 / both dW halves issued
+        // S half 0 of unit n0: its S^T columns were loaded by the softmax (s_free of
+        // unit n0 - 2), its H tile and W2T block have landed
+        auto try_s0 = [&]() {
+          while (n0 < NT) {
+            if (n0 >= NSB && !ready(&s_free[c0.b], c0.bph ^ 1u)) break;
+            if (c0.v == 0 && !ready(&wt_full[c0.wb], c0.wph)) break;
+            if (c0.hh == 0 && !ready(&h_full[c0.st], c0.hph)) break;
+            fence_after();
+            issue_half(c0, 0);
+            advance(c0);
+            ++n0;
+          }
+        };
+        // S half 1 of unit n1: into the G^T columns of unit n1 - 2, so after that
+        // unit's dW (in-order MMA execution), and after its own half 0
+        auto try_s1 = [&]() {
+          while (n1 < n0 && n1 <= ndw + 1) {
+            fence_after();
+            issue_half(c1, 1);
+            advance(c1);
+            ++n1;
+          }
+        };
+        for (int gu = 0; gu < NT; ++gu) {
+          const uint32_t gcol = cd.b * UNIT + (uint32_t)(((gu >> 1) & 1) * 64);   // G^T of unit gu
+          const int pf = (gu & 3) * 2;
+          const uint32_t pph = (uint32_t)((gu >> 2) & 1);
+          while (!ready_sleep(&p_full[pf], pph)) { try_s0(); try_s1(); }
+          if (cd.v == 0 && cd.kb >= 1) {
+            while (!ready_sleep(dw_empty, dwe_ph)) { try_s0(); try_s1(); }
+            dwe_ph ^= 1u;
+          }
+          fence_after();
+#ifndef AS_X_NOMMA2
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + gcol, sdesc(aH + cd.st * TILE, ATOM_BYTES, 1024), idW,
+                          cd.v > 0 ? 1u : 0u);
+#endif
+          try_s0(); try_s1();
+          while (!ready_sleep(&p_full[pf + 1], pph)) { try_s0(); try_s1(); }
+          fence_after();
+#ifndef AS_X_NOMMA2
+          mma_grp_ts_mn_4(tmem + COL_DW, tmem + gcol + 32, sdesc(aH + cd.st * TILE + 64 * 128, ATOM_BYTES, 1024),
+                          idW, 1u);
+#endif
+          if (cd.hh == HPT - 1) mma_commit_w(&h_empty[cd.st]);
+          if (cd.v == NU - 1) mma_commit_w(dw_full);
+          ++ndw;
+          advance(cd);
+          try_s0(); try_s1();
+        }
+        (void)ns;
+      } else if constexpr (RING) {
         // unit gu belongs to WG gu % 2 (buffer b = gu % NSB), its parity within
         // the WG is p = (gu / 2) & 1: S half h at columns 64 ((h + p) & 1)
         constexpr uint32_t idS64 = idesc_bf16(BM, 64, 0, 0);
@@ -1164,6 +1300,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     int kb_cur = -1;
     bool has_lab = false;                     // class i has labels in this batch
     float b2c = 0.f, db2 = 0.f;
+    float Ec = 0.f, iEc = 0.f;                // ECF: exp(b2_c) and its inverse (0 past C)
     int kb = 0, v = g, lst = g / HPT, sb = g; // unit cursor: block, unit, lse' stage, S buffer
     while (NU > 0 && v >= NU) { v -= NU; ++kb; }   // NU = 1: WG 1 starts in block 1
     pf_cls(kb);
@@ -1178,6 +1315,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         kb_cur = kb;
         const bool ok = cls_ok(kb);
         b2c = ok ? sB2r[(kb & 1) * 256 + tix] * LOG2E : -INFINITY;
+        if constexpr (Cfg::ECF) {
+          Ec = ok ? ex2(b2c) : 0.f;
+          iEc = ok ? ex2(-b2c) : 0.f;
+        }
         has_lab = cls_has(kb);
         db2 = 0.f;
         pf_cls(kb + kstep);                   // slot (kb + kstep) & 1: read above already
@@ -1201,16 +1342,22 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if constexpr (!RING) mbar_wait(&s_full[b], sph);
       TRACE(1, tix == 0, 7, v);
       fence_after();
-      cp_async_wait<1>();                     // this unit's bitmap (all but the newest group)
       const uint32_t par = RING ? (uint32_t)(jj & 1) : 0u;   // column parity of this unit (RING)
       uint32_t mk[4];
-      if constexpr (UNIT == 128) {
-        const uint4 q4 = sMk[(jj & 1) * 256 + tix];
-        mk[0] = q4.x; mk[1] = q4.y; mk[2] = q4.z; mk[3] = q4.w;
-      } else {
-        const uint2 q2 = *reinterpret_cast<const uint2 *>(sMk + (jj & 1) * 256 + tix);
-        mk[0] = q2.x; mk[1] = q2.y; mk[2] = 0u; mk[3] = 0u;
-      }
+      // this unit's bitmap (all cp.async groups but the newest): read where the
+      // label term needs it, after the first half's exponentials (LATEMK), so the
+      // cp.async completion wait is off the unit's critical path
+      auto read_mk = [&]() {
+        cp_async_wait<1>();
+        if constexpr (UNIT == 128) {
+          const uint4 q4 = sMk[(jj & 1) * 256 + tix];
+          mk[0] = q4.x; mk[1] = q4.y; mk[2] = q4.z; mk[3] = q4.w;
+        } else {
+          const uint2 q2 = *reinterpret_cast<const uint2 *>(sMk + (jj & 1) * 256 + tix);
+          mk[0] = q2.x; mk[1] = q2.y; mk[2] = 0u; mk[3] = 0u;
+        }
+      };
+      if constexpr (!Cfg::LATEMK) read_mk();
 #ifndef AS_X_NOSOFT
 #pragma unroll 1
       for (int half = 0; half < UNIT / 64; ++half) {   // 64 rows of the unit at a time
@@ -1222,7 +1369,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         }
         AS_TMEM_LD32(tl + b * UNIT + scol, r0);
         AS_TMEM_LD32(tl + b * UNIT + scol + 32, r1);
-        // lse' = LSE_r * log2e + log2 B of these 64 rows (smem broadcast)
+        // -lse' = -(LSE_r log2e + log2 B) of these 64 rows (smem broadcast)
         const float4 *lq = reinterpret_cast<const float4 *>(sL + (FOLD ? 0 : lst * BM + (v % HPT) * UNIT + half * 64));
         AS_TMEM_WAIT_LD(r0);
         AS_TMEM_WAIT_LD(r1);
@@ -1244,9 +1391,12 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             uint64_t x;
             if constexpr (FOLD) {             // S^T already holds z - LSE - ln B: p / B = 2^(S log2e)
               x = fmul2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2);
+            } else if constexpr (Cfg::ECF) {  // G' = G / E_c: s log2e - lse'
+              x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2,
+                        m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
             } else {
               x = ffma2(f2(__uint_as_float(xa), __uint_as_float(xb)), l2e2, b2c2);
-              x = fsub2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
+              x = fadd2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
             }
             float e0, e1;
             if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
@@ -1276,6 +1426,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         // db2 -= the same weights; row weights from the stage's label-weight
         // ring; only warps with a label of one of their classes in these rows
         {
+          if constexpr (Cfg::LATEMK) {
+            if (half == 0) read_mk();
+          }
           // static register indices (half is a runtime loop counter)
           uint32_t m0 = mk[0], m1 = mk[1];
           if (half) { m0 = mk[2]; m1 = mk[3]; }
@@ -1289,7 +1442,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               const uint32_t mw = u < 16 ? m0 : m1;
               const uint32_t bits = (mw >> ((2 * u) & 31)) & 3u;
               if (bits) {
-                const float2 w2 = reinterpret_cast<const float2 *>(wq)[u];
+                float2 w2 = reinterpret_cast<const float2 *>(wq)[u];
+                if constexpr (Cfg::ECF) { w2.x *= iEc; w2.y *= iEc; }
                 float lo = __uint_as_float(pk[u] << 16), hi = __uint_as_float(pk[u] & 0xffff0000u);
                 if (bits & 1u) { lo -= w2.x; db2 -= w2.x; }
                 if (bits & 2u) { hi -= w2.y; db2 -= w2.y; }
@@ -1304,7 +1458,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         tmem_wait_st();
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[PH * b + half]);
+        if (lane == 0) mbar_arrive(&p_full[S0POLL ? (gu & 3) * 2 + half : PH * b + half]);
       }
       TRACE(1, tix == 0, 8, v);
 #else
@@ -1315,7 +1469,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       fence_before();
       __syncwarp();
       if (lane == 0) {
-        for (int hf = 0; hf < PH; ++hf) mbar_arrive(&p_full[PH * b + hf]);
+        for (int hf = 0; hf < PH; ++hf) mbar_arrive(&p_full[S0POLL ? (gu & 3) * 2 + hf : PH * b + hf]);
         if (RING) mbar_arrive(&s_free[b]);
       }
       (void)par;
@@ -1324,7 +1478,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if (v >= NU - 2) {                      // this WG's last unit of the block: db2 partial
         if (kb >= 1) mbar_wait(db_empty, (kb - 1) & 1);
         TRACE(1, tix == 0, 16, v);
-        sDB[g * BM + i] = db2;
+        sDB[g * BM + i] = Cfg::ECF ? db2 * Ec : db2;
         if (NU == 1) sDB[(1 - g) * BM + i] = 0.f;   // one unit per block: the other WG has none
         __syncwarp();
         if (lane == 0) {
@@ -1452,6 +1606,13 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       if constexpr (TMAUPD) {
         if (kb + NWT < NB) fetch_wt(kb + NWT, wpre);
       }
+      // ECF: this class's bias before its update below (the value the softmax
+      // warps took E_c from); loaded before the accumulator wait
+      float b2u = 0.f;
+      if constexpr (Cfg::ECF) {
+        const int cu = cb * BM + i;
+        b2u = cu < C ? b2[cu] : 0.f;
+      }
       TRACE(3, ut == 0, 11, kb);
       mbar_wait_idle(dw_full, kb & 1);        // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
@@ -1563,6 +1724,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         const uint32_t sw = (uint32_t)(i & 7);
         uint8_t *rowWf = reinterpret_cast<uint8_t *>(sT) + i * 128;
         const int cls_i = cb * BM + i;
+        // W2T_c -= lr dW2T_c, with dW2T_c = E_c (G'^T H)_c under ECF
+        const float Eu = Cfg::ECF ? ex2(b2u * LOG2E) : 1.f;
+        const float nlr = -lr * Eu;
         auto sgd_chunk = [&](int ch, const uint32_t (&r)[32]) {
 #ifndef AS_X_NOUPD
 #pragma unroll
@@ -1573,10 +1737,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               w[g] = *reinterpret_cast<const float4 *>(rowWf + ch * 16384 + (((uint32_t)(g0 + g) ^ sw) << 4));
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
-              w[g].x = fmaf(-lr, __uint_as_float(r[4 * (g0 + g)]), w[g].x);
-              w[g].y = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 1]), w[g].y);
-              w[g].z = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 2]), w[g].z);
-              w[g].w = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 3]), w[g].w);
+              w[g].x = fmaf(nlr, __uint_as_float(r[4 * (g0 + g)]), w[g].x);
+              w[g].y = fmaf(nlr, __uint_as_float(r[4 * (g0 + g) + 1]), w[g].y);
+              w[g].z = fmaf(nlr, __uint_as_float(r[4 * (g0 + g) + 2]), w[g].z);
+              w[g].w = fmaf(nlr, __uint_as_float(r[4 * (g0 + g) + 3]), w[g].w);
             }
 #pragma unroll
             for (int g = 0; g < 4; ++g)
@@ -1594,7 +1758,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #endif
           if (dbg_dW2T && cls_i < C) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls_i * H + ch * 32 + k] = __uint_as_float(r[k]);
+            for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls_i * H + ch * 32 + k] = __uint_as_float(r[k]) * Eu;
           }
         };
         static_assert(NCH == 4, "h = 128: four 32-column chunks");
@@ -1725,6 +1889,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     }
     if (TMAUPD && ut == 0) bulk_wait0();      // stores complete before the grid ends
   } else if (H == 128 && dw.W1) {           // warps 14-15: step a7 (dW1 + SGD) alongside
+    AS_REG_DEC2();
     // First-layer gradient with fused SGD on the feature-sorted entries (a3's
     // transpose): warp gw of the grid's 2 * gridDim.x takes segments gw, gw +
     // GW, ...; dW1[f] = sum over the segment's entries, in entry order, of
