@@ -335,7 +335,19 @@ struct FwdCfg {
   static constexpr int NST = H == 128 ? 4 : 2;    // W stages
   static constexpr int TILE = BM * H * 2;         // bytes of a 128 x H bf16 tile
   static constexpr int THREADS = 12 * 32;        // 3 warpgroups (setmaxnreg granularity)
-  static constexpr int SMEM = TILE /*H*/ + NST * TILE + 2 * 2 * BM * 4 /*b2*/ + 64 /*b2 max*/ + 256;
+  // P1WB2: every softmax warp keeps its own copy of the block's b2 (loaded as
+  // float4 by its lanes) and reduces the block max itself, so the warps of a
+  // warpgroup never meet at a named barrier (default: one copy per WG, named
+  // barrier per block)
+  // Measured neutral (out_fwd 0.2694 vs 0.2676 ms, two x_probe A/B pairs):
+  // experiment switch AS_X_P1WB2, off in the product build.
+#ifdef AS_X_P1WB2
+  static constexpr bool P1WB2 = H == 128;
+#else
+  static constexpr bool P1WB2 = false;
+#endif
+  static constexpr int NB2 = P1WB2 ? 8 * 2 : 2 * 2;  // b2 copies [warp or WG][2]
+  static constexpr int SMEM = TILE /*H*/ + NST * TILE + NB2 * BM * 4 /*b2*/ + 64 /*b2 max*/ + 256;
   static_assert(SMEM <= 232448, "pass-1 shared memory exceeds 227 KB");
   static_assert(H == 128 || H == 256, "h");
 };
@@ -377,7 +389,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   uint8_t *sH = smem_raw;
   uint8_t *sW = smem_raw + TILE;
   float *sB2 = (float *)(sW + NST * TILE);          // [2 WG][2][128]
-  float *sBmax = sB2 + 4 * BM;                       // [2 WG][2][4 warps] block max of b2
+  float *sBmax = sB2 + FwdCfg<H>::NB2 * BM;         // [2 WG][2][4 warps] block max of b2
   uint64_t *bars = (uint64_t *)(sBmax + 16);
   // p_full[2 b + half]: P of classes [64 half, 64 half + 64) of the block in S
   // buffer b is in TMEM; the O MMA of that half starts without the other
@@ -521,25 +533,56 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     // select / multiply right after the load would stall on its latency)
     float b2raw = 0.f;
     bool b2ok = false;
-    if (g < nloc) { const int c = (cb0 + g) * BM + row; b2ok = c < C; b2raw = b2[b2ok ? c : 0]; }
+    float4 b2q = make_float4(0.f, 0.f, 0.f, 0.f);   // P1WB2: classes 4 lane .. 4 lane + 3 of the next block
+    auto ld_b2q = [&](int jb) {
+      const int c = (cb0 + jb) * BM + 4 * lane;
+      if (c + 3 < C) {
+        b2q = *reinterpret_cast<const float4 *>(b2 + c);
+      } else {                                // tail of the class range: clamped scalar loads
+        b2q.x = b2[c < C ? c : C - 1];
+        b2q.y = b2[c + 1 < C ? c + 1 : C - 1];
+        b2q.z = b2[c + 2 < C ? c + 2 : C - 1];
+        b2q.w = b2[c + 3 < C ? c + 3 : C - 1];
+      }
+    };
+    if (g < nloc) {
+      if constexpr (FwdCfg<H>::P1WB2) ld_b2q(g);
+      else { const int c = (cb0 + g) * BM + row; b2ok = c < C; b2raw = b2[b2ok ? c : 0]; }
+    }
     int jj = 0;                               // blocks processed by this WG
     for (int j = g; j < nloc; j += NWG, ++jj) {
       const int b = j & 1;
-      float *myB2 = sB2 + (g * 2 + (jj & 1)) * BM;
-      const float b2n = b2ok ? b2raw * LOG2E : -INFINITY;
-      myB2[row] = b2n;
-      float wm = b2n;                         // max of b2 (log2 units) over the block
+      float *myB2;
+      float bmax;
+      if constexpr (FwdCfg<H>::P1WB2) {
+        myB2 = sB2 + (warp * 2 + (jj & 1)) * BM;
+        const int c = (cb0 + j) * BM + 4 * lane;
+        const float4 bn = make_float4(c < C ? b2q.x * LOG2E : -INFINITY, c + 1 < C ? b2q.y * LOG2E : -INFINITY,
+                                      c + 2 < C ? b2q.z * LOG2E : -INFINITY, c + 3 < C ? b2q.w * LOG2E : -INFINITY);
+        *reinterpret_cast<float4 *>(myB2 + 4 * lane) = bn;
+        float wm = fmaxf(fmaxf(bn.x, bn.y), fmaxf(bn.z, bn.w));   // max of b2 (log2 units) over the block
 #pragma unroll
-      for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-      if (lane == 0) sBmax[(g * 2 + (jj & 1)) * 4 + q] = wm;
-      if (j + NWG < nloc) {
-        const int c = (cb0 + j + NWG) * BM + row;
-        b2ok = c < C;
-        b2raw = b2[b2ok ? c : 0];
+        for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        bmax = wm;
+        if (j + NWG < nloc) ld_b2q(j + NWG);
+        __syncwarp();
+      } else {
+        myB2 = sB2 + (g * 2 + (jj & 1)) * BM;
+        const float b2n = b2ok ? b2raw * LOG2E : -INFINITY;
+        myB2[row] = b2n;
+        float wm = b2n;                         // max of b2 (log2 units) over the block
+#pragma unroll
+        for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        if (lane == 0) sBmax[(g * 2 + (jj & 1)) * 4 + q] = wm;
+        if (j + NWG < nloc) {
+          const int c = (cb0 + j + NWG) * BM + row;
+          b2ok = c < C;
+          b2raw = b2[b2ok ? c : 0];
+        }
+        named_bar(1 + g, 128);
+        const float *bmx = sBmax + (g * 2 + (jj & 1)) * 4;
+        bmax = fmaxf(fmaxf(bmx[0], bmx[1]), fmaxf(bmx[2], bmx[3]));
       }
-      named_bar(1 + g, 128);
-      const float *bmx = sBmax + (g * 2 + (jj & 1)) * 4;
-      const float bmax = fmaxf(fmaxf(bmx[0], bmx[1]), fmaxf(bmx[2], bmx[3]));
       // s_full(j) also implies that the O MMA of this WG's previous block (issued
       // before S_j) completed: O is stable and the P region of buffer b is free.
       mbar_wait(&s_full[b], (j >> 1) & 1);
@@ -1613,6 +1656,21 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         const int cu = cb * BM + i;
         b2u = cu < C ? b2[cu] : 0.f;
       }
+      // h = 256: this thread's W2T values of the block's first 32-column chunk
+      // (8 classes x 4 columns) are loaded before the accumulator wait, and
+      // every chunk's RMW runs on values loaded during the previous chunk
+      float4 wq[TMAUPD ? 1 : 8];
+      auto ld_chunk = [&](int ch_, float4 (&w)[TMAUPD ? 1 : 8]) {
+        if constexpr (!TMAUPD) {
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int cls = cb * BM + q * 32 + 4 * m + sub;
+            w[m] = cls < C ? *reinterpret_cast<const float4 *>(W2T + (size_t)cls * H + ch_ * 32 + hq)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      };
+      ld_chunk(0, wq);
       TRACE(3, ut == 0, 11, kb);
       mbar_wait_idle(dw_full, kb & 1);        // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
@@ -1856,6 +1914,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
                 make_float4(__uint_as_float(r[k]), __uint_as_float(r[k + 1]),
                             __uint_as_float(r[k + 2]), __uint_as_float(r[k + 3]));
           named_bar(3, 128);
+          float4 wn[TMAUPD ? 1 : 8];
+          if (ch + 1 < NCH) ld_chunk(ch + 1, wn);
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
             const int cl = q * 32 + 4 * m + sub;
@@ -1863,7 +1923,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             if (cls < C) {
               const float4 gv = *reinterpret_cast<const float4 *>(sT + cl * SROW + hq);
               const size_t idx = (size_t)cls * H + ch * 32 + hq;
-              float4 nw = *reinterpret_cast<const float4 *>(W2T + idx);
+              float4 nw = wq[TMAUPD ? 0 : m];
               nw.x -= lr * gv.x; nw.y -= lr * gv.y; nw.z -= lr * gv.z; nw.w -= lr * gv.w;
               *reinterpret_cast<float4 *>(W2T + idx) = nw;
               *reinterpret_cast<uint2 *>(W2b + idx) = make_uint2(pack_bf16x2(nw.x, nw.y),
@@ -1871,6 +1931,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               if (dbg_dW2T) *reinterpret_cast<float4 *>(dbg_dW2T + idx) = gv;
             }
           }
+#pragma unroll
+          for (int m = 0; m < (TMAUPD ? 1 : 8); ++m) wq[m] = wn[m];
         }
         if (kb + NWT < NB) load_wt(kb + NWT);
       }
