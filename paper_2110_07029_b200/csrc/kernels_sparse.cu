@@ -239,6 +239,10 @@ void launch_label_terms(cudaStream_t s, int h, const StepDesc *desc, int b_max,
 #define COMBINE_CW 8
 #endif
 static_assert(COMBINE_CW % 8 == 0, "one or more columns per warp");
+// slot count up to which the combine holds all of a thread's partials in registers
+#ifndef COMBINE_MAXS
+#define COMBINE_MAXS 24
+#endif
 __global__ void __launch_bounds__(256) k_combine_bf16(
     const StepDesc *__restrict__ desc, int h, int bpad, int splits, const float *__restrict__ pm,
     const float *__restrict__ pl, const float *__restrict__ pO, const float *__restrict__ labW,
@@ -290,20 +294,58 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   // flight (the partials are L2-resident right after pass 1)
   // M_r and l_r: warp jy reduces slots jy, jy + 8, ...; the 8 warp partials
   // are combined in warp order (max is exact; the sum order is fixed)
+  // splits <= COMBINE_MAXS (every b >= 128 * SMs / COMBINE_MAXS): every
+  // partial this thread reads -- its slots' m and l, and the column's O of
+  // every slot -- is loaded up front (one memory round trip instead of one per
+  // phase); the same operations in the same order as the loop form below
+  constexpr int MAXS = COMBINE_MAXS, MS8 = (MAXS + 7) / 8;
+  const bool pre = splits <= MAXS;
+  float pmv[MS8], plv[MS8], ov[MAXS][NCW];
+  if (pre) {
+#pragma unroll
+    for (int k = 0; k < MS8; ++k) {
+      const int s = jy + 8 * k;
+      if (s < splits) { pmv[k] = pm[(size_t)s * bpad + r]; plv[k] = pl[(size_t)s * bpad + r]; }
+    }
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s)
+      if (s < splits) {
+#pragma unroll
+        for (int c = 0; c < NCW; ++c) ov[s][c] = pO[((size_t)s * h + j0 + 8 * c) * bpad + r];
+      }
+  }
   __shared__ float red[2][8][33];
   float M = -FLT_MAX;
-  for (int s = jy; s < splits; s += 8) M = fmaxf(M, pm[(size_t)s * bpad + r]);
+  if (pre) {
+#pragma unroll
+    for (int k = 0; k < MS8; ++k)
+      if (jy + 8 * k < splits) M = fmaxf(M, pmv[k]);
+  } else {
+    for (int s = jy; s < splits; s += 8) M = fmaxf(M, pm[(size_t)s * bpad + r]);
+  }
   red[0][jy][rx] = M;
   __syncthreads();
   M = red[0][0][rx];
 #pragma unroll
   for (int k = 1; k < 8; ++k) M = fmaxf(M, red[0][k][rx]);
   float l = 0.f;
-  for (int s = jy; s < splits; s += 8) {
-    const float ms = pm[(size_t)s * bpad + r];
-    const float e = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
-    sc[s * 32 + rx] = e;
-    l = fmaf(pl[(size_t)s * bpad + r], e, l);
+  if (pre) {
+#pragma unroll
+    for (int k = 0; k < MS8; ++k) {
+      const int s = jy + 8 * k;
+      if (s < splits) {
+        const float e = pmv[k] == -FLT_MAX ? 0.f : exp2f(pmv[k] - M);
+        sc[s * 32 + rx] = e;
+        l = fmaf(plv[k], e, l);
+      }
+    }
+  } else {
+    for (int s = jy; s < splits; s += 8) {
+      const float ms = pm[(size_t)s * bpad + r];
+      const float e = ms == -FLT_MAX ? 0.f : exp2f(ms - M);
+      sc[s * 32 + rx] = e;
+      l = fmaf(pl[(size_t)s * bpad + r], e, l);
+    }
   }
   red[1][jy][rx] = l;
   __syncthreads();
@@ -317,11 +359,21 @@ __global__ void __launch_bounds__(256) k_combine_bf16(
   float o[NCW];
 #pragma unroll
   for (int c = 0; c < NCW; ++c) o[c] = 0.f;
-#pragma unroll 6
-  for (int s = 0; s < splits; ++s) {
-    const float w = sc[s * 32 + rx];
+  if (pre) {
 #pragma unroll
-    for (int c = 0; c < NCW; ++c) o[c] = fmaf(pO[((size_t)s * h + j0 + 8 * c) * bpad + r], w, o[c]);
+    for (int s = 0; s < MAXS; ++s)
+      if (s < splits) {
+        const float w = sc[s * 32 + rx];
+#pragma unroll
+        for (int c = 0; c < NCW; ++c) o[c] = fmaf(ov[s][c], w, o[c]);
+      }
+  } else {
+#pragma unroll 6
+    for (int s = 0; s < splits; ++s) {
+      const float w = sc[s * 32 + rx];
+#pragma unroll
+      for (int c = 0; c < NCW; ++c) o[c] = fmaf(pO[((size_t)s * h + j0 + 8 * c) * bpad + r], w, o[c]);
+    }
   }
 #pragma unroll
   for (int c = 0; c < NCW; ++c) {
