@@ -59,7 +59,13 @@ enum {
   /* bits 2-3: the regularisation metric of Alg. 2 line 7 tested against
      pert_thr (reading R15; "||w_i||_2/|w|", "L2-norm divided by
      model dimensionality", in tension with P:276): flags |= metric << 2    */
-  AS_NORM_METRIC_SHIFT = 2
+  AS_NORM_METRIC_SHIFT = 2,
+  AS_FLAG_R14_LITERAL = 16 /* as_merge (AS_ALGO_ADAPTIVE): Alg. 2 line 8 read
+                              literally (reading R14 "literal"): r = argmax_i u_i,
+                              s = argmin_i u_i, lowest id on ties, applied even
+                              when r = s (then alpha_r *= (1 + delta)(1 - delta));
+                              default: lexicographic (u_i, b_i), skipped when
+                              every (u_i, b_i) is equal                        */
 };
 enum {
   AS_METRIC_L2_P = 0,       /* ||w||_2 / P   (literal, default)                 */
@@ -68,8 +74,9 @@ enum {
   AS_METRIC_L2 = 3          /* ||w||_2                                          */
 };
 
-/* Alg. 2 line-5 normalisation (as_sched_alg2_ex). */
-enum { AS_NORM_UPDATES = 0, AS_NORM_UB = 1 };
+/* Alg. 2 line-5 normalisation (as_sched_alg2_ex), optionally OR-ed with
+ * AS_NORM_R14_LITERAL (line 8 as printed, see AS_FLAG_R14_LITERAL). */
+enum { AS_NORM_UPDATES = 0, AS_NORM_UB = 1, AS_NORM_R14_LITERAL = 2 };
 
 typedef struct as_ctx as_ctx; /* opaque */
 
@@ -390,7 +397,10 @@ int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b,
 
 /* as_sched_alg2 with the line-5 normalisation selectable: AS_NORM_UPDATES
  * (Alg. 2 as printed) or AS_NORM_UB ("normalize based on the product
- * between the number of updates and the batch size").  Same outputs. */
+ * between the number of updates and the batch size"), either OR-ed with
+ * AS_NORM_R14_LITERAL (P:163 line 8 "r <- argmax_i {u_i}, s <- argmin_i {u_i}"
+ * as printed: ties to the lowest id, no skip).  Same outputs; AS_E_INVALID
+ * for any other norm_mode. */
 int as_sched_alg2_ex(int32_t N, const int32_t *u, const int32_t *b, const double *norms,
                      double delta, double pert_thr, int32_t norm_mode, double *alpha_out,
                      int32_t *perturbed_out);

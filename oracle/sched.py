@@ -149,10 +149,12 @@ def _f32(x):
 # R13 (exact equality), R14 (lexicographic argmax/argmin of (u_i, b_i), skip
 # when identical), R15 (strict <), R16 (no renormalisation).
 # --------------------------------------------------------------------------
-def alg2(u, b, norms, delta, pert_thr, norm="u"):
+def alg2(u, b, norms, delta, pert_thr, norm="u", ties="lex"):
     """norm="ub": line 5 normalises by u_i b_i instead ("an alternative
     for later stages is to normalize based on the product between the number
-    of updates and the batch size")."""
+    of updates and the batch size").  ties="literal": line 8 exactly as printed
+    ("r <- argmax_i {u_i}, s <- argmin_i {u_i}"): the first index of the
+    largest / smallest u, and lines 8-9 applied even when r = s."""
     N = len(u)
     if all(x == u[0] for x in u):                 # line 2
         sb = float(sum(b))
@@ -164,7 +166,13 @@ def alg2(u, b, norms, delta, pert_thr, norm="u"):
         sub = float(sum(ui * bi for ui, bi in zip(u, b)))
         alpha = [float(ui * bi) / sub for ui, bi in zip(u, b)]
     perturbed = 0
-    if all(nrm < pert_thr for nrm in norms):      # line 7
+    if ties == "literal" and all(nrm < pert_thr for nrm in norms):   # line 7
+        r = u.index(max(u))                       # line 8 as printed
+        s = u.index(min(u))
+        alpha[r] = alpha[r] * (1.0 + delta)       # line 9 (r = s: both on alpha_r)
+        alpha[s] = alpha[s] * (1.0 - delta)
+        perturbed = 1
+    elif all(nrm < pert_thr for nrm in norms):    # line 7
         keys = [(u[i], b[i]) for i in range(N)]
         r = max(range(N), key=lambda i: (keys[i], -i))    # argmax, lowest id on ties
         s = min(range(N), key=lambda i: (keys[i], i))     # argmin, lowest id on ties

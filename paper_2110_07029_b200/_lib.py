@@ -23,7 +23,8 @@ AS_MAX_WORLD = 64
 AS_P2P_EXPORT_BYTES = 128
 ALGOS = {"adaptive": AS_ALGO_ADAPTIVE, "elastic": AS_ALGO_ELASTIC, "sync": AS_ALGO_SYNC}
 AS_FLAG_DEBUG_GRADS, AS_FLAG_NORM_UB = 1, 2
-AS_NORM_UPDATES, AS_NORM_UB = 0, 1
+AS_NORM_UPDATES, AS_NORM_UB, AS_NORM_R14_LITERAL = 0, 1, 2
+AS_FLAG_R14_LITERAL = 16
 AS_NORM_METRIC_SHIFT = 2
 METRICS = {"l2/P": 0, "l2^2/P": 1, "l2/sqrt(P)": 2, "l2": 3}
 AS_PARAMS_REPLICA, AS_PARAMS_GLOBAL, AS_PARAMS_GLOBAL_PREV = 0, 1, 2

@@ -27,7 +27,7 @@ class Replica:
                  max_row_nnz=1024, max_row_labels=64, lr0=0.1, gamma=0.9, delta=0.1, pert_thr=0.1,
                  precision="bf16", rank=0, world=1, nccl_id=None, device=0, stream=None,
                  debug_grads=False, algo="adaptive", merge_norm="u", norm_metric="l2/P",
-                 merge_backend="nccl"):
+                 merge_backend="nccl", merge_ties="lex"):
         torch = _torch()
         self.lib = L.load()
         b_min = b_max // 8 if b_min is None else b_min
@@ -43,7 +43,8 @@ class Replica:
         cfg.lr0, cfg.gamma, cfg.delta, cfg.pert_thr = lr0, gamma, delta, pert_thr
         cfg.precision = L.AS_BF16 if precision == "bf16" else L.AS_FP32
         cfg.flags = ((L.AS_FLAG_DEBUG_GRADS if debug_grads else 0) | (L.AS_FLAG_NORM_UB if merge_norm == "ub" else 0)
-                     | (L.METRICS[norm_metric] << L.AS_NORM_METRIC_SHIFT))
+                     | (L.METRICS[norm_metric] << L.AS_NORM_METRIC_SHIFT)
+                     | (L.AS_FLAG_R14_LITERAL if merge_ties == "literal" else 0))
         cfg.rank, cfg.world, cfg.device = rank, world, device
         cfg.merge_backend = L.MERGE_BACKENDS[merge_backend]
         self._nccl_buf = None

@@ -14,8 +14,11 @@
 
 namespace as {
 
-// norm_mode 0: line 5 alpha_i = u_i / sum(u); 1: alpha_i = u_i b_i / sum(u b)
-// (P:175).  Returns 0, or -1 when the normaliser is zero.
+// norm_mode bit 0 clear: line 5 alpha_i = u_i / sum(u); set: alpha_i = u_i b_i /
+// sum(u b).  Bit 1 (R14 "literal"): line 8 as printed, r / s = the
+// lowest-id argmax / argmin of u alone, applied even when r = s; clear:
+// lexicographic (u_i, b_i), skipped when all pairs are equal.  Returns 0, or
+// -1 when the normaliser is zero.
 AS_HD inline int alg2_weights(int N, const int32_t *u, const int32_t *b, const double *norms, double delta,
                               double pert_thr, int norm_mode, double *alpha, int32_t *perturbed) {
   bool all_equal = true;                         // line 2 (R13: exact integer equality)
@@ -26,7 +29,7 @@ AS_HD inline int alg2_weights(int N, const int32_t *u, const int32_t *b, const d
     for (int i = 0; i < N; ++i) sb += b[i];
     if (sb <= 0) return -1;
     for (int i = 0; i < N; ++i) alpha[i] = (double)b[i] / (double)sb;
-  } else if (norm_mode == 0) {                   // line 5: alpha_i = u_i / sum(u)
+  } else if ((norm_mode & 1) == 0) {            // line 5: alpha_i = u_i / sum(u)
     int64_t su = 0;
     for (int i = 0; i < N; ++i) su += u[i];
     for (int i = 0; i < N; ++i) alpha[i] = (double)u[i] / (double)su;
@@ -40,7 +43,16 @@ AS_HD inline int alg2_weights(int N, const int32_t *u, const int32_t *b, const d
   bool regular = true;                           // line 7 (R15: strict <)
   for (int i = 0; i < N; ++i)
     if (!(norms[i] < pert_thr)) regular = false;
-  if (regular) {
+  if (regular && (norm_mode & 2)) {             // line 8 as printed (R14 literal)
+    int r = 0, s = 0;
+    for (int i = 1; i < N; ++i) {
+      if (u[i] > u[r]) r = i;
+      if (u[i] < u[s]) s = i;
+    }
+    alpha[r] = alpha[r] * (1.0 + delta);         // line 9 (r = s: both factors on alpha_r)
+    alpha[s] = alpha[s] * (1.0 - delta);
+    pert = 1;
+  } else if (regular) {
     int r = 0, s = 0;                            // line 8 (R14: lexicographic, lowest id)
     for (int i = 1; i < N; ++i) {
       if (u[i] > u[r] || (u[i] == u[r] && b[i] > b[r])) r = i;

@@ -1077,7 +1077,10 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   int rc = AS_OK;
   int32_t pert_host = 0;
   double alpha1 = 1.0;
-  if (N == 1) {
+  // R14 literal with one replica: r = s = 0 and line 9 applies when the
+  // replica is regular, alpha = (1 + delta)(1 - delta): the norm is needed
+  const bool lit1 = N == 1 && x->cfg.algo == AS_ALGO_ADAPTIVE && (x->cfg.flags & AS_FLAG_R14_LITERAL);
+  if (N == 1 && !lit1) {
     // Alg. 2 with one replica: line 3 gives alpha = b / b = 1 and r = s, so
     // the perturbation is skipped whatever the norm (R14); the comparison
     // methods' 1/N is 1 too: no norm pass, no host synchronisation
@@ -1086,7 +1089,7 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
     as::MergeWeightArgs wa{};
     wa.N = N;
     wa.mode = x->cfg.algo == AS_ALGO_ADAPTIVE ? 0 : 1;     // comparison methods: 1/N
-    wa.norm_mode = (x->cfg.flags & AS_FLAG_NORM_UB) ? 1 : 0;
+    wa.norm_mode = ((x->cfg.flags & AS_FLAG_NORM_UB) ? 1 : 0) | ((x->cfg.flags & AS_FLAG_R14_LITERAL) ? 2 : 0);
     wa.delta = x->cfg.delta;
     wa.pert_thr = x->cfg.pert_thr;
     for (int i = 0; i < N; ++i) { wa.u[i] = u[i]; wa.b[i] = b[i]; }
@@ -1096,7 +1099,10 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
       as::launch_sumsq(s, x->w, D.P, x->norm_part, kNormBlocks, x->norm_dev,
                        (x->cfg.flags >> AS_NORM_METRIC_SHIFT) & 3);
     }
-    if (x->cfg.merge_backend == AS_MERGE_P2P) {
+    if (N == 1) {                             // (lit1) the one norm is the table
+      rc = cuda_check(x, cudaMemcpyAsync(x->norms_all, x->norm_dev, 8, cudaMemcpyDeviceToDevice, s), "norm copy");
+      if (rc) return rc;
+    } else if (x->cfg.merge_backend == AS_MERGE_P2P) {
       p2p_barrier(x, adaptive ? x->norm_dev : nullptr);   // norms all-gathered; training done everywhere
     } else if (adaptive) {
       const ncclResult_t r = ncclAllGather(x->norm_dev, x->norms_all, 1, ncclDouble, x->comm, s);
@@ -1110,7 +1116,7 @@ int as_merge(as_ctx *x, const int32_t *u, const int32_t *b, double *alpha_out,
   if (rc) return rc;
   rc = cuda_check(x, cudaSuccess, "merge launch");
   if (rc) return rc;
-  if (N == 1) {
+  if (N == 1 && !lit1) {
     if (alpha_out) alpha_out[0] = alpha1;
     if (perturbed_out) *perturbed_out = 0;
   } else if (alpha_out || perturbed_out) {
@@ -1243,7 +1249,9 @@ int as_group_merge(as_ctx *const *ctxs, int32_t n, const int32_t *u, const int32
       if (rc) return rc;
     }
     rc = as_sched_alg2_ex(n, u, b, norms.data(), x0->cfg.delta, x0->cfg.pert_thr,
-                          (x0->cfg.flags & AS_FLAG_NORM_UB) ? AS_NORM_UB : AS_NORM_UPDATES, alpha.data(), &pert);
+                          ((x0->cfg.flags & AS_FLAG_NORM_UB) ? AS_NORM_UB : AS_NORM_UPDATES) |
+                              ((x0->cfg.flags & AS_FLAG_R14_LITERAL) ? AS_NORM_R14_LITERAL : 0),
+                          alpha.data(), &pert);
     if (rc) return rc;
   } else {
     for (int i = 0; i < n; ++i) alpha[i] = 1.0 / n;

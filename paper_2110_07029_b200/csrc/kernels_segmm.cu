@@ -82,15 +82,18 @@ __device__ __forceinline__ void sb_copy(void *dst, const void *src, uint32_t byt
 // warps per CTA, ring stages per warp, entries per group: measured on B200 at
 // the Amazon-670K shape (scripts/x_probe.sh sweep); h = 256 keeps the
 // 227 KB shared-memory budget.  -D overrides for experiment builds.
+// h = 256 (AmazonCat-13K, scripts/gpu_r02zb.sh sweeps): dW1 6 -> 16 warps
+// with 3-entry groups 0.039 -> 0.030 ms, SpMM 8 -> 16 warps with 4-entry
+// groups 0.0224 -> 0.0210 ms per SGD step (more warps, each with less in flight)
 #ifndef AS_SEG1_NW
-#define AS_SEG1_NW (H == 128 ? 16 : 6)
+#define AS_SEG1_NW 16
 #define AS_SEG1_NST 2
-#define AS_SEG1_GE (H == 128 ? 6 : 8)
+#define AS_SEG1_GE (H == 128 ? 6 : 3)
 #endif
 #ifndef AS_SEG0_NW
-#define AS_SEG0_NW (H == 128 ? 16 : 8)
+#define AS_SEG0_NW 16
 #define AS_SEG0_NST 3
-#define AS_SEG0_GE 8
+#define AS_SEG0_GE (H == 128 ? 8 : 4)
 #endif
 template <int H, int MODE>
 struct SegCfg {

@@ -168,9 +168,9 @@ int as_sched_alg2(int32_t N, const int32_t *u, const int32_t *b, const double *n
 int as_sched_alg2_ex(int32_t N, const int32_t *u, const int32_t *b, const double *norms,
                      double delta, double pert_thr, int32_t norm_mode, double *alpha_out,
                      int32_t *perturbed_out) {
-  if (N < 1 || !u || !b || !norms || !alpha_out || (norm_mode != AS_NORM_UPDATES && norm_mode != AS_NORM_UB))
+  if (N < 1 || !u || !b || !norms || !alpha_out || norm_mode < 0 || norm_mode > (AS_NORM_UB | AS_NORM_R14_LITERAL))
     return as_fail(AS_E_INVALID, "as_sched_alg2: bad arguments");
-  if (as::alg2_weights(N, u, b, norms, delta, pert_thr, norm_mode == AS_NORM_UB ? 1 : 0, alpha_out,
+  if (as::alg2_weights(N, u, b, norms, delta, pert_thr, norm_mode, alpha_out,
                        perturbed_out) != 0)
     return as_fail(AS_E_INVALID, "as_sched_alg2: zero normaliser (sum(b) or sum(u b))");
   return AS_OK;

@@ -56,15 +56,19 @@ def scale_period(b_prev, b_next, dir_state, period, p_max):
     return po.value, ds.tolist()
 
 
-def alg2(u, b, norms, delta, pert_thr, norm="u"):
-    """norm: "u" (Alg. 2 line 5 as printed) or "ub" (the P:175 alternative)."""
+def alg2(u, b, norms, delta, pert_thr, norm="u", ties="lex"):
+    """norm: "u" (Alg. 2 line 5 as printed) or "ub" (the P:175 alternative);
+    ties: "lex" (reading R14: lexicographic (u, b), skip when all equal) or
+    "literal" (line 8 as printed: argmax / argmin of u, lowest id, no skip)."""
     lib = L.load()
     N = len(u)
     uu, bb, nn = L.as_np(u, np.int32), L.as_np(b, np.int32), L.as_np(norms, np.float64)
     a = np.zeros(N, np.float64)
     p = C.c_int32()
     L.check(lib.as_sched_alg2_ex(N, L.ptr(uu, C.c_int32), L.ptr(bb, C.c_int32), L.ptr(nn, C.c_double),
-                                 float(delta), float(pert_thr), L.AS_NORM_UB if norm == "ub" else L.AS_NORM_UPDATES,
+                                 float(delta), float(pert_thr),
+                                 (L.AS_NORM_UB if norm == "ub" else L.AS_NORM_UPDATES)
+                                 | (L.AS_NORM_R14_LITERAL if ties == "literal" else 0),
                                  L.ptr(a, C.c_double), C.byref(p)))
     return a.tolist(), p.value
 

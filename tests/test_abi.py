@@ -105,6 +105,20 @@ def test_alg2_ub_bit_exact_vs_oracle(N, data):
     assert a == oa and p == op
 
 
+@settings(max_examples=60, deadline=None)
+@given(st.integers(1, 8), st.sampled_from(["u", "ub"]), st.data())
+def test_alg2_r14_literal_bit_exact_vs_oracle(N, norm, data):
+    """AS_NORM_R14_LITERAL (line 8 as printed) in the C++ export against the oracle."""
+    u = [data.draw(st.integers(0, 6)) for _ in range(N)]
+    if sum(u) == 0:
+        u[0] = 1
+    b = [data.draw(st.integers(1, 1024)) for _ in range(N)]
+    norms = [data.draw(st.floats(0.0, 0.2)) for _ in range(N)]
+    a, p = psched.alg2(u, b, norms, 0.1, 0.1, norm=norm, ties="literal")
+    oa, op = osched.alg2(u, b, norms, 0.1, 0.1, norm=norm, ties="literal")
+    assert a == oa and p == op
+
+
 def test_fit_cost_cpp_vs_oracle():
     rng = np.random.default_rng(11)
     for trial in range(20):

@@ -387,6 +387,60 @@ def test_group_merge_ub_normalisation(gpu_lib):
     assert_close("wbar", reps[0].get_params(1), wbar, 1e-5)
 
 
+@pytest.mark.parametrize("u", [[2, 2, 1], [3, 3, 3]])
+def test_group_merge_r14_literal(gpu_lib, u):
+    """AS_FLAG_R14_LITERAL (Alg. 2 line 8 as printed): alpha bit-exact with
+    oracle.sched.alg2(ties="literal") -- ties on u go to the lowest id, and with
+    equal u the perturbation lands on replica 0 twice -- merged model within 1e-5."""
+    from paper_2110_07029_b200.api import Replica, group_merge
+    cfg = _cfg(1000, 500, 128, 200, 64)
+    ds = synthgen.make_dataset(cfg, n=200)
+    p = _params(cfg)
+    b = [48, 64, 32]
+    reps = [Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=8, max_row_nnz=int(np.diff(ds.row_ptr).max()),
+                    max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=0.5, precision="fp32", rank=i, world=3,
+                    pert_thr=1e6, merge_ties="literal") for i in range(3)]
+    for i, r in enumerate(reps):
+        r.set_batch_sizes(b, [0.375, 0.5, 0.25])
+        sub = ds.rows(np.arange(b[i] // 2) + 40 * i)
+        r.load_batch_csr(b[i] // 2, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+        r.train_step()
+    ws = [r.get_params() for r in reps]
+    alpha, pert = group_merge(reps, u, b)
+    oa, op = osched.alg2(u, b, [omerge.replica_norm(w) for w in ws], 0.1, 1e6, ties="literal")
+    lex, _ = osched.alg2(u, b, [omerge.replica_norm(w) for w in ws], 0.1, 1e6)
+    assert oa != lex                          # the case separates the two readings
+    assert list(alpha) == oa and pert == op == 1
+    wbar, _ = omerge.merge(ws, oa, p, p, 0.9)
+    assert_close("wbar", reps[0].get_params(1), wbar, 1e-5)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_merge_one_replica_r14_literal(gpu_lib, precision):
+    """One replica under AS_FLAG_R14_LITERAL: r = s = 0, so a regular replica
+    gets alpha = (1 + delta)(1 - delta) = 0.99 through as_merge (norm pass and
+    Alg. 2 on the device); irregular keeps 1.  Merged model vs oracle within 1e-5."""
+    from paper_2110_07029_b200.api import Replica
+    cfg = _cfg(1000, 500, 128, 200, 64)
+    ds = synthgen.make_dataset(cfg, n=200)
+    p = _params(cfg)
+    for thr, want in ((1e6, 0.99), (0.0, 1.0)):
+        r = Replica(cfg.d, cfg.C, cfg.h, cfg.b_max, p, b_min=8, max_row_nnz=int(np.diff(ds.row_ptr).max()),
+                    max_row_labels=int(np.diff(ds.lab_ptr).max()), lr0=0.5, precision=precision,
+                    pert_thr=thr, merge_ties="literal")
+        sub = ds.rows(np.arange(32))
+        r.load_batch_csr(32, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+        r.train_step()
+        w = r.get_params()
+        alpha, pert = r.merge([1], [64])
+        oa, op = osched.alg2([1], [64], [omerge.replica_norm(w)], 0.1, thr, ties="literal")
+        assert list(alpha) == oa and pert == op
+        assert abs(oa[0] - want) < 1e-15
+        wbar, _ = omerge.merge([w], oa, p, p, 0.9)
+        assert_close("wbar", r.get_params(1), wbar, 1e-5)
+        r.close()
+
+
 @pytest.mark.parametrize("metric,thr", [("l2", 1.0), ("l2", 1e6), ("l2/sqrt(P)", 0.05), ("l2^2/P", 1e-3)])
 def test_group_merge_norm_metrics(gpu_lib, metric, thr):
     """R15's metric switch: the perturbation decision of Alg. 2 line 7 with each

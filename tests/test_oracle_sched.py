@@ -194,6 +194,32 @@ def test_alg2_ub_normalisation_hand_worked():
         osched.alg2([4, 4], [64, 48], [1.0, 1.0], 0.1, 0.1, norm="u")
 
 
+def test_alg2_r14_literal_hand_worked():
+    """Line 8 as printed (reading R14 "literal"): r / s are the FIRST
+    indices of max u / min u, and lines 8-9 apply even when r = s.
+    u = (3, 3, 1), b = (100, 200, 50): line 5 alpha = (3/7, 3/7, 1/7); literal
+    r = 0, s = 2 -> (33/70, 3/7, 9/70), where the lexicographic reading picks
+    r = 1 (larger b) -> (3/7, 33/70, 9/70).  Equal u = (4, 4), b = (64, 48):
+    line 3 alpha = (4/7, 3/7); literal r = s = 0 -> (0.99 * 4/7, 3/7) =
+    (99/175, 3/7); lexicographic r = 0, s = 1 -> (22/35, 27/70).  One replica:
+    literal (0.99,), lexicographic (1.0,) unperturbed."""
+    F = lambda a: [Fraction(x).limit_denominator(10**6) for x in a]
+    a, p = osched.alg2([3, 3, 1], [100, 200, 50], [0.0] * 3, 0.1, 0.1, ties="literal")
+    assert p == 1 and F(a) == [Fraction(33, 70), Fraction(3, 7), Fraction(9, 70)]
+    a, p = osched.alg2([3, 3, 1], [100, 200, 50], [0.0] * 3, 0.1, 0.1)
+    assert p == 1 and F(a) == [Fraction(3, 7), Fraction(33, 70), Fraction(9, 70)]
+    a, p = osched.alg2([4, 4], [64, 48], [0.0] * 2, 0.1, 0.1, ties="literal")
+    assert p == 1 and F(a) == [Fraction(99, 175), Fraction(3, 7)]
+    a, p = osched.alg2([4, 4], [64, 48], [0.0] * 2, 0.1, 0.1)
+    assert p == 1 and F(a) == [Fraction(22, 35), Fraction(27, 70)]
+    a, p = osched.alg2([2], [64], [0.0], 0.1, 0.1, ties="literal")
+    assert p == 1 and F(a) == [Fraction(99, 100)]
+    assert osched.alg2([2], [64], [0.0], 0.1, 0.1) == ([1.0], 0)
+    # not regular: no perturbation in either reading
+    assert osched.alg2([3, 3, 1], [100, 200, 50], [1.0] * 3, 0.1, 0.1, ties="literal") == \
+        osched.alg2([3, 3, 1], [100, 200, 50], [1.0] * 3, 0.1, 0.1)
+
+
 def test_fit_cost_recovers_integer_model():
     """R9 replay model from a live trace: noiseless times generated by a known
     integer model are recovered exactly; with +-0.4 ps of noise too."""
