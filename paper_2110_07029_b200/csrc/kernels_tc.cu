@@ -855,6 +855,13 @@ struct BwdCfg {
 #else
   static constexpr bool PING = false;
 #endif
+  // LASTSMEM (h = 256): the last class block's fp32 update staged through the
+  // then idle H stages by TMA (AS_X_NOLASTSMEM: chunked register path)
+#ifdef AS_X_NOLASTSMEM
+  static constexpr bool LASTSMEM = false;
+#else
+  static constexpr bool LASTSMEM = !TMAUPD && NSH * TILE >= BM * H * 4;
+#endif
   // ECF (h = 128): the class bias leaves the exponent.  p_rc / B =
   // E_c 2^(s_rc log2e - lse'_r) with E_c = exp(b2_c), so the softmax computes
   // G'_rc = G_rc / E_c (one FFMA2 per pair: s log2e + (-lse')), the label term
@@ -1670,7 +1677,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           }
         }
       };
-      ld_chunk(0, wq);
+      // h = 256, last block: the H stages are free once its accumulator is
+      // complete, so the whole fp32 block is TMA-loaded into them (LASTSMEM)
+      const bool last_smem = !TMAUPD && Cfg::LASTSMEM && kb == NB - 1;
+      if (!last_smem) ld_chunk(0, wq);
       TRACE(3, ut == 0, 11, kb);
       mbar_wait_idle(dw_full, kb & 1);        // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
@@ -1896,6 +1906,74 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           }
         }
       } else {
+        if (last_smem) {
+          // fp32 block [128 classes][H] as H / 32 swizzled boxes of 32 columns in the
+          // H stages (free: every MMA of the CTA has completed), updated in place
+          // from the accumulator (lane i = class i), TMA-stored, bf16 shadow written
+          // coalesced from the boxes
+          uint8_t *stg = sHt;
+          if (ut == 0) {
+            mbar_expect_tx(wf_full, BM * H * 4);
+            for (int c = 0; c < NCH; ++c) tma_load_2d(&mapWf, wf_full, stg + c * 16384, c * 32, cb * BM);
+          }
+          const uint32_t sw = (uint32_t)(i & 7);
+          const int cls_i = cb * BM + i;
+          mbar_wait(wf_full, 0u);             // used once per CTA at h = 256
+#pragma unroll 1
+          for (int ch = 0; ch < NCH; ++ch) {
+            uint32_t r[32];
+            AS_TMEM_LD32(tl + COL_DW + ch * 32, r);
+            AS_TMEM_WAIT_LD(r);
+            if (ch == NCH - 1) {
+              fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(dw_empty);
+            }
+            uint8_t *rowWf = stg + ch * 16384 + i * 128;
+#pragma unroll
+            for (int g0 = 0; g0 < 8; g0 += 4) {
+              float4 w[4];
+#pragma unroll
+              for (int g = 0; g < 4; ++g) w[g] = *reinterpret_cast<const float4 *>(rowWf + (((uint32_t)(g0 + g) ^ sw) << 4));
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                w[g].x = fmaf(-lr, __uint_as_float(r[4 * (g0 + g)]), w[g].x);
+                w[g].y = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 1]), w[g].y);
+                w[g].z = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 2]), w[g].z);
+                w[g].w = fmaf(-lr, __uint_as_float(r[4 * (g0 + g) + 3]), w[g].w);
+              }
+#pragma unroll
+              for (int g = 0; g < 4; ++g) *reinterpret_cast<float4 *>(rowWf + (((uint32_t)(g0 + g) ^ sw) << 4)) = w[g];
+            }
+            if (dbg_dW2T && cls_i < C) {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls_i * H + ch * 32 + k] = __uint_as_float(r[k]);
+            }
+          }
+          fence_proxy_async();
+          named_bar(3, 128);
+          if (ut == 0) {
+            for (int c = 0; c < NCH; ++c) tma_store_2d(&mapWf, stg + c * 16384, c * 32, cb * BM);
+            bulk_commit();
+          }
+          // bf16 shadow: H / 8 segments of 8 columns per class row, coalesced
+          constexpr int SEGS = H / 8;
+#pragma unroll 4
+          for (int k = 0; k < SEGS; ++k) {
+            const int idx = k * 128 + ut;
+            const int row = idx / SEGS, c8 = idx % SEGS;
+            const int cls = cb * BM + row;
+            const uint8_t *rb = stg + (c8 >> 2) * 16384 + row * 128;
+            const uint32_t g0 = (uint32_t)((c8 & 3) * 2), rs = (uint32_t)(row & 7);
+            const float4 a = *reinterpret_cast<const float4 *>(rb + ((g0 ^ rs) << 4));
+            const float4 b = *reinterpret_cast<const float4 *>(rb + (((g0 + 1) ^ rs) << 4));
+            if (cls < C)
+              *reinterpret_cast<uint4 *>(W2b + (size_t)cls * H + 8 * c8) =
+                  make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                             pack_bf16x2(b.z, b.w));
+          }
+          if (ut == 0) bulk_wait0();          // the stores have left the H stages
+        } else {
         // chunked staging (h = 256): the accumulator is released after the last chunk
 #pragma unroll 1
         for (int ch = 0; ch < NCH; ++ch) {
@@ -1933,6 +2011,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           }
 #pragma unroll
           for (int m = 0; m < (TMAUPD ? 1 : 8); ++m) wq[m] = wn[m];
+        }
         }
         if (kb + NWT < NB) load_wt(kb + NWT);
       }
