@@ -781,7 +781,9 @@ int as_train_step(as_ctx *x, float *loss_out) {
 #ifdef AS_X_LABSIDE
   const bool lt_sep = true;
 #else
-  const bool lt_sep = lt_sep_env || (double)x->loaded_lab > 0.05 * (double)D.C;
+  // h = 256: pass 1 runs one softmax warpgroup, so six warps per CTA (the idle
+  // second warpgroup too) carry the label terms: fused up to labels <= C
+  const bool lt_sep = lt_sep_env || (double)x->loaded_lab > (D.h == 256 ? 1.0 : 0.05) * (double)D.C;
 #endif
   const bool dw1_fused = x->cfg.precision == AS_BF16 && as::tc_fuses_dw1(D.h) && !no_fuse &&
                          (double)x->loaded_nnz <= (w1_in_l2 ? 0.15 : 0.075) * (double)D.C;

@@ -732,17 +732,20 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
       pm[slot * bpad + grow] = M;
       pl[slot * bpad + grow] = l * s0 + l1 * s1;
     }
-  } else if (NWG == 1 && warp < 8) {          // h = 256: the second WG is idle
-    AS_REG_INC();
-  } else {                                    // warps 8-9: the label terms (a5, R3) alongside
-    AS_REG_DEC();
+  } else {
+    // warps 8-9 (h = 256 also the idle second warpgroup, warps 4-7): the label
+    // terms (a5, R3) alongside
+    if (NWG == 1 && warp < 8) AS_REG_INC();
+    else AS_REG_DEC();
+    constexpr int NLW = NWG == 1 ? 6 : 2;     // label warps per CTA
+    const int lwi = warp >= 8 ? warp - 8 : warp - 4 + 2;
     // zsum_r = (1/k_r) sum_{y in Y_r} z_ry and labW_r = (1/k_r) sum_y W2T[y]
     // (fp32 master weights, pre-update) for rows r = gw, gw + GW, ... (warp per
     // row, labels in order, lane = 4 consecutive of the h columns); they need
     // only H and W2T, so they hide in pass 1 and the combine reads them after
     if (lt.zsum) {
       constexpr int V = H / 128;
-      const int gw = (int)blockIdx.x * 2 + (warp - 8), GW = RT * splits * 2;
+      const int gw = (int)blockIdx.x * NLW + lwi, GW = RT * splits * NLW;
       for (int r = gw; r < B; r += GW) {
         const int64_t s0 = lt.lab_ptr[r], s1 = lt.lab_ptr[r + 1];
         const float inv_k = 1.0f / (float)(s1 - s0);
@@ -781,8 +784,18 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
   if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
-template <int H>
+template <int H, bool ONEB = false>
 struct BwdCfg {
+  // W2S (h = 256, one class block per CTA: C <= 128 SMs, AmazonCat-13K): the bf16
+  // W2T block is TMA-loaded into shared memory once and the S^T MMA reads it
+  // from there (SS), which frees its 128 TMEM columns for two more S^T buffers
+  // (4 x 64 rows: S runs up to two units ahead of each softmax warpgroup); the
+  // block's fp32 update goes through the idle H stages (LASTSMEM)
+#ifdef AS_X_NOW2S
+  static constexpr bool W2S = false;
+#else
+  static constexpr bool W2S = ONEB && H == 256;
+#endif
   // FOLD (h = 128): b2_c and -(LSE_r + ln B) enter the S^T MMA as one more
   // K-step of 16 (a per-class tile A_ext = [b2 in three bf16 parts, 1, 1, 1, 0..]
   // and a per-row tile B_ext = [1, 1, 1, -(LSE + ln B) in three parts, 0..],
@@ -816,10 +829,12 @@ struct BwdCfg {
 #else
   static constexpr int UNIT = H == 128 ? 128 : 64; // batch rows per unit = S^T columns per buffer
   static constexpr int HPT = 128 / UNIT;          // units per 128-row H tile
-  static constexpr int NSB = 2;                   // S^T unit buffers
+  static constexpr int NSB = W2S ? 4 : 2;         // S^T unit buffers
 #endif
   static constexpr int NWT = H == 128 ? 2 : 1;    // W2T blocks resident in TMEM (A operand)
   static constexpr int WCOLS = H / 2;             // TMEM columns of one W2T block (bf16 pairs)
+  static constexpr int WTM = W2S ? 0 : NWT * WCOLS;  // TMEM columns of the W2T blocks
+  static constexpr int W2SMEM = W2S ? BM * H * 2 : 0; // shared-memory W2T block (W2S)
   static constexpr int TILE = BM * H * 2;
   static constexpr int THREADS = 16 * 32;        // 4 warpgroups (setmaxnreg granularity)
   // h = 128: the fp32 W2T block (4 swizzled 32-column boxes) is TMA-loaded one
@@ -905,13 +920,13 @@ struct BwdCfg {
   static constexpr bool S0POLL = false;
 #endif
   static constexpr int SROW = 36;                 // chunked staging row (floats, 16-B aligned)
-  static constexpr int TSTAGE = TMAUPD ? BM * (HALF ? H / 2 : H) * 4 : BM * SROW * 4;
-  static constexpr int SMEM = NSH * TILE + NSH * HXB + 2 * AXB + TSTAGE +
+  static constexpr int TSTAGE = TMAUPD ? BM * (HALF ? H / 2 : H) * 4 : (W2S ? 0 : BM * SROW * 4);
+  static constexpr int SMEM = NSH * TILE + W2SMEM + NSH * HXB + 2 * AXB + TSTAGE +
                               (FOLD ? 1 : 2) * NSH * BM * 4 /*(lse' and) label-weight rings*/ +
                               2 * BM * 4 /*db2*/ + 2 * 256 * (16 + 16 + 4) /*softmax prefetch slots*/ +
                               512 /*barriers*/;
   static_assert(SMEM <= 232448, "pass-2 shared memory exceeds 227 KB");
-  static_assert(NSB * UNIT + NWT * WCOLS + H <= 512, "pass-2 TMEM budget");
+  static_assert(NSB * UNIT + WTM + H <= 512, "pass-2 TMEM budget");
 };
 
 // =====================================================================
@@ -933,8 +948,8 @@ struct BwdCfg {
 //                                             fixed unit order: deterministic)
 // TMEM: S^T units at 64*b; W2T blocks at 64*NSB (+WCOLS each); dW2T last.
 // =====================================================================
-template <int H>
-__global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
+template <int H, bool ONEB>
+__global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
     k_out_bwd(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapW,
               const __grid_constant__ CUtensorMap mapWf, const __grid_constant__ CUtensorMap mapHx,
               const StepDesc *__restrict__ desc, const float *__restrict__ lsep, int C,
@@ -944,16 +959,18 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
               __nv_bfloat16 *__restrict__ W2b, float lr, float *__restrict__ dbg_dW2T,
               float *__restrict__ dbg_db2, Dw1Args dw) {
   griddep_wait();
-  using Cfg = BwdCfg<H>;
+  using Cfg = BwdCfg<H, ONEB>;
   constexpr int NSH = Cfg::NSH, NSB = Cfg::NSB, NWT = Cfg::NWT, WCOLS = Cfg::WCOLS;
+  constexpr bool W2S = Cfg::W2S;
   constexpr int UNIT = Cfg::UNIT, HPT = Cfg::HPT;
   constexpr int TILE = Cfg::TILE, SROW = Cfg::SROW;
   constexpr bool TMAUPD = Cfg::TMAUPD, FOLD = Cfg::FOLD, HALF = Cfg::HALF, PING = Cfg::PING;
   constexpr int HXB = Cfg::HXB, AXB = Cfg::AXB;
-  constexpr uint32_t COL_W = NSB * UNIT, COL_DW = NSB * UNIT + NWT * WCOLS;
+  constexpr uint32_t COL_W = NSB * UNIT, COL_DW = NSB * UNIT + Cfg::WTM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sHt = smem_raw;
-  uint8_t *sHx = sHt + NSH * TILE;              // FOLD: B_ext of each H stage
+  uint8_t *sW2 = sHt + NSH * TILE;              // W2S: the bf16 W2T block (K-major, SW128 atoms)
+  uint8_t *sHx = sW2 + Cfg::W2SMEM;             // FOLD: B_ext of each H stage
   uint8_t *sAx = sHx + NSH * HXB;               // FOLD: A_ext of the class blocks in TMEM
   float *sT = (float *)(sAx + 2 * AXB);         // h = 128: W2T fp32 block; else dW2T staging
   float *sL = (float *)((uint8_t *)sT + Cfg::TSTAGE);    // lse' of the rows of each H stage (!FOLD)
@@ -986,6 +1003,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
            *wf2 = s_free + NSB;                 // PING: the two half-block staging buffers
   uint32_t *tmem_slot = (uint32_t *)(wf2 + 2);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // SW128 needs 1024-B alignment
+  if (W2S && (int)gridDim.x < n_cblocks) __trap();    // W2S: one class block per CTA
 
   const int B = desc->rows;
   const int RT = (B + BM - 1) / BM;               // 128-row H tiles
@@ -1014,7 +1032,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     for (int i = 0; i < SF; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < NSB; ++i) mbar_init(&s_free[i], 4);
     for (int i = 0; i < NPF; ++i) mbar_init(&p_full[i], 4);
-    for (int i = 0; i < NWT; ++i) mbar_init(&wt_full[i], 4);
+    for (int i = 0; i < NWT; ++i) mbar_init(&wt_full[i], W2S ? 1 : 4);
     mbar_init(dw_full, 1);
     mbar_init(dw_empty, 4);
     mbar_init(db_full, 8);
@@ -1057,6 +1075,11 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
     (void)NT;
     if (lane == 0) {  // ---------------- TMA producer (H tiles)
       TRACE_INIT;
+      if (W2S && NB > 0) {                    // the CTA's single W2T block (bf16), once
+        mbar_expect_tx(&wt_full[0], BM * H * 2);
+        for (int a = 0; a < H / 64; ++a)
+          tma_load_2d(&mapW, &wt_full[0], sW2 + a * ATOM_BYTES, a * 64, (int)blockIdx.x * BM);
+      }
       int it = 0;
       for (int kb = 0; kb < NB; ++kb)
         for (int t = 0; t < RT; ++t, ++it) {
@@ -1074,6 +1097,17 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           else bulk_load_1d(sL + st * BM, lsep + tr * BM, BM * 4, &h_full[st]);
           bulk_load_1d(sWr + st * BM, wrow + tr * BM, BM * 4, &h_full[st]);
         }
+      if constexpr (W2S) {
+        // the block's fp32 W2T (the update's staging) in two 64 KB halves, each
+        // into an H stage as soon as its last tile's dW MMAs have read it
+        for (int k = 0; k < 2 && NB > 0; ++k, ++it) {
+          const int st = it % NSH;
+          if (it >= NSH) mbar_wait_idle(&h_empty[st], ((it / NSH) - 1) & 1);
+          mbar_expect_tx(&wf2[k], BM * 128 * 4);
+          for (int c = 0; c < 4; ++c)
+            tma_load_2d(&mapWf, &wf2[k], sHt + st * TILE + c * 16384, (4 * k + c) * 32, (int)blockIdx.x * BM);
+        }
+      }
     }
   } else if (warp == kMmaWarp) {
     AS_REG_DEC2();
@@ -1112,7 +1146,9 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         // this warp: tcgen05.mma executes in issue order
         const uint64_t dB = sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), 16, 1024);
 #ifndef AS_X_NOMMA1
-        if constexpr (H == 128)
+        if constexpr (W2S)
+          mma_grp_ss_kk_16(tmem + c.b * UNIT, sdesc(smem_u32(sW2), 16, 1024), dB, idS, 0u);
+        else if constexpr (H == 128)
           mma_grp_ts_k_8(tmem + c.b * UNIT, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
         else
           mma_grp_ts_k_16(tmem + c.b * UNIT, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
@@ -1292,7 +1328,10 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
         do_dw(cd);
         // S runs NSB units ahead; with a single TMEM W2T buffer the look-ahead
         // may not cross into the next block before this block's last dW
-        while (ns < NT && ns <= gu + NSB && (NWT > 1 || cs.kb == cd.kb || cd.v == NU - 1)) {
+        // ... and only into H tiles whose stage the producer can fill: tile T
+        // goes into stage T % NSH once every dW of tile T - NSH is issued
+        while (ns < NT && ns <= gu + NSB && ns / HPT < (gu + 1) / HPT + NSH &&
+               (NWT > 1 || cs.kb == cd.kb || cd.v == NU - 1)) {
           issue_S(cs);
           advance(cs);
           ++ns;
@@ -1649,7 +1688,8 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&wt_full[wb]);
     };
-    for (int kb = 0; kb < NB && kb < NWT; ++kb) load_wt(kb);
+    if constexpr (!W2S)
+      for (int kb = 0; kb < NB && kb < NWT; ++kb) load_wt(kb);
     for (int kb = 0; kb < NB; ++kb) {
       const int cb = blockIdx.x + kb * gridDim.x;
       uint32_t wpre[TMAUPD ? 64 : 1];
@@ -1679,7 +1719,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
       };
       // h = 256, last block: the H stages are free once its accumulator is
       // complete, so the whole fp32 block is TMA-loaded into them (LASTSMEM)
-      const bool last_smem = !TMAUPD && Cfg::LASTSMEM && kb == NB - 1;
+      const bool last_smem = W2S || (!TMAUPD && Cfg::LASTSMEM && kb == NB - 1);   // W2S: NB = 1
       if (!last_smem) ld_chunk(0, wq);
       TRACE(3, ut == 0, 11, kb);
       mbar_wait_idle(dw_full, kb & 1);        // also: every S of block kb completed
@@ -1911,25 +1951,28 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           // H stages (free: every MMA of the CTA has completed), updated in place
           // from the accumulator (lane i = class i), TMA-stored, bf16 shadow written
           // coalesced from the boxes
-          uint8_t *stg = sHt;
-          if (ut == 0) {
+          // box c (32 columns): W2S -- half c / 4 in the stage the producer
+          // filled after the H tiles; else both stages, loaded here
+          auto box = [&](int c) -> uint8_t * {
+            if constexpr (W2S) return sHt + ((NB * RT + (c >> 2)) % NSH) * TILE + (c & 3) * 16384;
+            else return sHt + c * 16384;
+          };
+          if (!W2S && ut == 0) {
             mbar_expect_tx(wf_full, BM * H * 4);
-            for (int c = 0; c < NCH; ++c) tma_load_2d(&mapWf, wf_full, stg + c * 16384, c * 32, cb * BM);
+            for (int c = 0; c < NCH; ++c) tma_load_2d(&mapWf, wf_full, box(c), c * 32, cb * BM);
           }
           const uint32_t sw = (uint32_t)(i & 7);
           const int cls_i = cb * BM + i;
-          mbar_wait(wf_full, 0u);             // used once per CTA at h = 256
-#pragma unroll 1
-          for (int ch = 0; ch < NCH; ++ch) {
-            uint32_t r[32];
-            AS_TMEM_LD32(tl + COL_DW + ch * 32, r);
-            AS_TMEM_WAIT_LD(r);
+          if (!W2S) mbar_wait(wf_full, 0u);   // used once per CTA at h = 256
+          // chunk c + 1's accumulator columns load while chunk c is applied
+          auto apply = [&](int ch, const uint32_t (&r)[32]) {
             if (ch == NCH - 1) {
               fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(dw_empty);
             }
-            uint8_t *rowWf = stg + ch * 16384 + i * 128;
+            if (W2S && (ch & 3) == 0) mbar_wait(&wf2[ch >> 2], 0u);
+            uint8_t *rowWf = box(ch) + i * 128;
 #pragma unroll
             for (int g0 = 0; g0 < 8; g0 += 4) {
               float4 w[4];
@@ -1949,11 +1992,23 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
 #pragma unroll
               for (int k = 0; k < 32; ++k) dbg_dW2T[(size_t)cls_i * H + ch * 32 + k] = __uint_as_float(r[k]);
             }
+          };
+          uint32_t ra[32], rb[32];
+          AS_TMEM_LD32(tl + COL_DW, ra);
+          AS_TMEM_WAIT_LD(ra);
+#pragma unroll 1
+          for (int ch = 0; ch < NCH; ch += 2) {   // NCH even
+            AS_TMEM_LD32(tl + COL_DW + (ch + 1) * 32, rb);
+            apply(ch, ra);
+            AS_TMEM_WAIT_LD(rb);
+            if (ch + 2 < NCH) AS_TMEM_LD32(tl + COL_DW + (ch + 2) * 32, ra);
+            apply(ch + 1, rb);
+            if (ch + 2 < NCH) AS_TMEM_WAIT_LD(ra);
           }
           fence_proxy_async();
           named_bar(3, 128);
           if (ut == 0) {
-            for (int c = 0; c < NCH; ++c) tma_store_2d(&mapWf, stg + c * 16384, c * 32, cb * BM);
+            for (int c = 0; c < NCH; ++c) tma_store_2d(&mapWf, box(c), c * 32, cb * BM);
             bulk_commit();
           }
           // bf16 shadow: H / 8 segments of 8 columns per class row, coalesced
@@ -1963,7 +2018,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
             const int idx = k * 128 + ut;
             const int row = idx / SEGS, c8 = idx % SEGS;
             const int cls = cb * BM + row;
-            const uint8_t *rb = stg + (c8 >> 2) * 16384 + row * 128;
+            const uint8_t *rb = box(c8 >> 2) + row * 128;
             const uint32_t g0 = (uint32_t)((c8 & 3) * 2), rs = (uint32_t)(row & 7);
             const float4 a = *reinterpret_cast<const float4 *>(rb + ((g0 ^ rs) << 4));
             const float4 b = *reinterpret_cast<const float4 *>(rb + (((g0 + 1) ^ rs) << 4));
@@ -2013,7 +2068,7 @@ __global__ void __launch_bounds__(BwdCfg<H>::THREADS, 1)
           for (int m = 0; m < (TMAUPD ? 1 : 8); ++m) wq[m] = wn[m];
         }
         }
-        if (kb + NWT < NB) load_wt(kb + NWT);
+        if (!W2S && kb + NWT < NB) load_wt(kb + NWT);
       }
       // db2 (thread ut = class ut of the block; label term already in G), SGD on b2
       TRACE(3, ut == 0, 13, kb);
@@ -2594,15 +2649,17 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
     if (h == 128) {
       cudaFuncSetAttribute(tc::k_out_fwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::FwdCfg<128>::SMEM);
-      cudaFuncSetAttribute(tc::k_out_bwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(tc::k_out_bwd<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::BwdCfg<128>::SMEM);
       cudaFuncSetAttribute(tc::k_out_top1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::Top1Cfg<128>::SMEM);
     } else {
       cudaFuncSetAttribute(tc::k_out_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::FwdCfg<256>::SMEM);
-      cudaFuncSetAttribute(tc::k_out_bwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(tc::k_out_bwd<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::BwdCfg<256>::SMEM);
+      cudaFuncSetAttribute(tc::k_out_bwd<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc::BwdCfg<256, true>::SMEM);
       cudaFuncSetAttribute(tc::k_out_top1<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tc::Top1Cfg<256>::SMEM);
     }
@@ -2654,11 +2711,15 @@ void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
   const int grid = p->num_sms < p->n_cblocks ? p->num_sms : p->n_cblocks;
   if (p->h == 128)
     // plain launch: pass 2 follows the wait on the transposes' join event
-    tc::k_out_bwd<128><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
+    tc::k_out_bwd<128, false><<<grid, tc::BwdCfg<128>::THREADS, tc::BwdCfg<128>::SMEM, s>>>(
+        p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
+        b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
+  else if (p->n_cblocks <= grid)             // one class block per CTA (AmazonCat-13K)
+    tc::k_out_bwd<256, true><<<grid, tc::BwdCfg<256, true>::THREADS, tc::BwdCfg<256, true>::SMEM, s>>>(
         p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
   else
-    tc::k_out_bwd<256><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
+    tc::k_out_bwd<256, false><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
         p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
 }
