@@ -465,7 +465,11 @@ int as_init(const as_config *cfg, const float *init_params, as_ctx **out) {
   // path (SpMM, pass 1 on the caller's stream) leaves idle
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+#ifdef AS_X_SIDEHI
+  if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->side, cudaStreamNonBlocking, prio_hi), "side stream");
+#else
   if (!rc) rc = cuda_check(x, cudaStreamCreateWithPriority(&x->side, cudaStreamNonBlocking, prio_lo), "side stream");
+#endif
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_join, cudaEventDisableTiming), "event");
   if (!rc) rc = cuda_check(x, cudaEventCreateWithFlags(&x->ev_tail, cudaEventDisableTiming), "event");
@@ -811,17 +815,23 @@ int as_train_step(as_ctx *x, float *loss_out) {
   // fork point of the transposes (experiment switch): 1 = after the SpMM, so
   // the latency-bound SpMM runs alone and the transposes fill the SMs pass 1
   // has not claimed yet and the combine kernels
-#ifndef AS_X_FORK
-#define AS_X_FORK 1
+  // Runtime default: 1, except when the output layer is small (every class
+  // block fits one CTA: C <= 128 SMs, AmazonCat-13K) -- there the transposes
+  // would gate pass 2, so they fork before the SpMM (measured: AmazonCat-13K
+  // step 0.1247 -> 0.1193 ms; Amazon-670K +0.7% with the early fork)
+#ifdef AS_X_FORK
+  const int fork_at = AS_X_FORK;
+#else
+  const int fork_at = D.C <= 128LL * x->num_sms ? 0 : 1;
 #endif
-  if (AS_X_FORK == 0) fork_transposes();
+  if (fork_at == 0) fork_transposes();
   // a4: SpMM forward
   ph_begin(x, AS_PH_SPMM);
   x->launches += 1;
   as::launch_spmm_chunked(s, D.h, x->num_sms, d, D.bpad, D.nnz_cap, x->row_ptr, x->col, x->val, x->rid, W1, b1,
                           x->Hf, x->Hb, x->seg_part, x->arrive);
   ph_end(x, AS_PH_SPMM);
-  if (AS_X_FORK == 1) fork_transposes();
+  if (fork_at == 1) fork_transposes();
   if (x->cfg.precision == AS_BF16) {
     // a5: pass 1 (tcgen05) + combine -> LSE, loss, dA
     ph_begin(x, AS_PH_OUT_FWD);
@@ -830,7 +840,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
     if (!lt_sep) lt = {x->lab_ptr, x->lab, x->Hf, W2T, b2, x->zsum, x->labW};
     as::launch_out_fwd_tc(s, x->plan, d, b2, x->pm, x->pl, x->pO, lt);
     ph_end(x, AS_PH_OUT_FWD);
-    if (AS_X_FORK == 2) fork_transposes();
+    if (fork_at == 2) fork_transposes();
     ph_begin(x, AS_PH_COMBINE);
     // label terms of the loss and of dH (R3), then the split combine -> LSE,
     // loss, dA, and db1 with b1's SGD fused (ordered last-arriver column sums)
@@ -866,7 +876,7 @@ int as_train_step(as_ctx *x, float *loss_out) {
     ph_end(x, AS_PH_OUT_BWD);
   } else {
     // fp32 parity mode: logits materialised
-    if (AS_X_FORK == 2) fork_transposes();
+    if (fork_at == 2) fork_transposes();
     const long long C = D.C;
     ph_begin(x, AS_PH_OUT_FWD);
     x->launches += 1 + 1 + 1 + 2;

@@ -1987,6 +1987,18 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
               }
 #pragma unroll
               for (int g = 0; g < 4; ++g) *reinterpret_cast<float4 *>(rowWf + (((uint32_t)(g0 + g) ^ sw) << 4)) = w[g];
+              if constexpr (W2S) {
+                // bf16 shadow of these 16 columns into the (now idle) W2T tile, its
+                // K-major SW128 layout: atom ch / 2, 16-byte chunk (ch & 1) 4 + g0 / 2 + jj
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                  const uint32_t j = (uint32_t)((ch & 1) * 4 + g0 / 2 + jj);
+                  *reinterpret_cast<uint4 *>(sW2 + (ch >> 1) * ATOM_BYTES + i * 128 + ((j ^ sw) << 4)) =
+                      make_uint4(pack_bf16x2(w[2 * jj].x, w[2 * jj].y), pack_bf16x2(w[2 * jj].z, w[2 * jj].w),
+                                 pack_bf16x2(w[2 * jj + 1].x, w[2 * jj + 1].y),
+                                 pack_bf16x2(w[2 * jj + 1].z, w[2 * jj + 1].w));
+                }
+              }
             }
             if (dbg_dW2T && cls_i < C) {
 #pragma unroll
@@ -2009,12 +2021,14 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
           named_bar(3, 128);
           if (ut == 0) {
             for (int c = 0; c < NCH; ++c) tma_store_2d(&mapWf, box(c), c * 32, cb * BM);
+            if constexpr (W2S)                // the bf16 shadow too, from the W2T tile
+              for (int a = 0; a < H / 64; ++a) tma_store_2d(&mapW, sW2 + a * ATOM_BYTES, a * 64, cb * BM);
             bulk_commit();
           }
           // bf16 shadow: H / 8 segments of 8 columns per class row, coalesced
           constexpr int SEGS = H / 8;
 #pragma unroll 4
-          for (int k = 0; k < SEGS; ++k) {
+          for (int k = 0; k < (W2S ? 0 : SEGS); ++k) {
             const int idx = k * 128 + ut;
             const int row = idx / SEGS, c8 = idx % SEGS;
             const int cls = cb * BM + row;
@@ -2027,7 +2041,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
                   make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
                              pack_bf16x2(b.z, b.w));
           }
-          if (ut == 0) bulk_wait0();          // the stores have left the H stages
+          if (!W2S && ut == 0) bulk_wait0();  // the stores have left the H stages (W2S: at the end)
         } else {
         // chunked staging (h = 256): the accumulator is released after the last chunk
 #pragma unroll 1
@@ -2083,7 +2097,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
       }
       TRACE(3, ut == 0, 14, kb);
     }
-    if (TMAUPD && ut == 0) bulk_wait0();      // stores complete before the grid ends
+    if ((TMAUPD || W2S) && ut == 0) bulk_wait0();   // stores complete before the grid ends
   } else if (H == 128 && dw.W1) {           // warps 14-15: step a7 (dW1 + SGD) alongside
     AS_REG_DEC2();
     // First-layer gradient with fused SGD on the feature-sorted entries (a3's
