@@ -347,6 +347,21 @@ struct FwdCfg {
   static constexpr bool P1WB2 = false;
 #endif
   static constexpr int NB2 = P1WB2 ? 8 * 2 : 2 * 2;  // b2 copies [warp or WG][2]
+  // P1RING (h = 128): S_j is computed in two 64-class halves whose TMEM columns
+  // alternate with the WG's block parity p: half 0 at 64 p, half 1 at 64 (1 - p)
+  // of the WG's 128 columns, P_j (bf16) packed at 64 p + 32 half.  Half 0 of
+  // the WG's next block goes into the columns of this block's half 1 as soon
+  // as the softmax has loaded them, so the softmax of the next block starts
+  // while this block's O MMAs and the next half 1 are still on the tensor pipe.
+  // Online softmax per 64-class half.  Measured slower (out_fwd 0.273 ->
+  // 0.299 ms, parity green): with the S^T waits gone both softmax warps of a
+  // sub-partition run at once and each runs slower, as with pass 2's ring.
+  // Experiment switch AS_X_P1RING.
+#if defined(AS_X_P1RING) && !defined(AS_X_NOSOFT)
+  static constexpr bool P1RING = H == 128 && !P1WB2;
+#else
+  static constexpr bool P1RING = false;
+#endif
   static constexpr int SMEM = TILE /*H*/ + NST * TILE + NB2 * BM * 4 /*b2*/ + 64 /*b2 max*/ + 256;
   static_assert(SMEM <= 232448, "pass-1 shared memory exceeds 227 KB");
   static_assert(H == 128 || H == 256, "h");
@@ -400,7 +415,10 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 #endif
   uint64_t *h_full = bars, *w_full = bars + 1, *w_empty = w_full + NST, *s_full = w_empty + NST,
            *p_full = s_full + 2, *o_fin = p_full + 2 * PQ, *o_done = o_fin + 1;
-  uint32_t *tmem_slot = (uint32_t *)(o_done + 1);
+  constexpr bool P1RING = Cfg::P1RING;
+  // P1RING: s_full per (buffer, half) [4], s_free per buffer [2], o_half per WG [2]
+  uint64_t *s_full2 = o_done + 1, *s_free = s_full2 + 4, *o_half = s_free + 2;
+  uint32_t *tmem_slot = (uint32_t *)(o_half + 2);
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
 
   const int B = desc->rows;
@@ -419,6 +437,8 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
     for (int i = 0; i < 2 * PQ; ++i) mbar_init(&p_full[i], 4);
     mbar_init(o_fin, 1);
     mbar_init(o_done, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&s_full2[i], 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_free[i], 4); mbar_init(&o_half[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
@@ -486,6 +506,47 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
 #endif
         mma_commit_w(&s_full[b]);
       };
+      if constexpr (P1RING) {
+        constexpr uint32_t idS64 = idesc_bf16(BM, 64, 0, 0);
+        // S_j half h (classes [64 h, 64 h + 64) of W tile j) into 64 ((h + p_j) & 1)
+        auto issue_S_half = [&](int j, int h) {
+          const int st = j % NST, b = j & 1;
+          const uint32_t p = (uint32_t)((j >> 1) & 1);
+          if (h == 0) mbar_wait(&w_full[st], (j / NST) & 1);
+          fence_after();
+#ifndef AS_X_NOMMA1
+          mma_grp_ss_kk_8(tmem + b * BM + (((uint32_t)h + p) & 1u) * 64u, dH,
+                          sdesc(aW + st * TILE + h * 64 * 128, 16, 1024), idS64, 0u);
+#endif
+          mma_commit_w(&s_full2[2 * b + h]);
+        };
+        for (int j = 0; j < nloc && j < 2; ++j) { issue_S_half(j, 0); issue_S_half(j, 1); }
+        for (int j = 0; j < nloc; ++j) {
+          const int st = j % NST, b = j & 1;
+          const uint32_t ph = (uint32_t)((j >> 1) & 1);
+          const uint32_t pcol = b * BM + ph * 64u;      // P_j (bf16): 64 p + 32 half
+          mbar_wait(&p_full[PQ * b], ph);
+          fence_after();
+#ifndef AS_X_NOMMA2
+          mma_grp_ts_mn_4(tmem + 2 * BM + b * BM, tmem + pcol, sdesc(aW + st * TILE, ATOM_BYTES, 1024), idO,
+                          j >= NWG ? 1u : 0u);
+#endif
+          mma_commit_w(&o_half[b]);           // O of this WG up to half 0 (a rescale at half 1 waits)
+          if (j + 2 < nloc) {                 // next half 0 into the columns half 1 has left
+            mbar_wait(&s_free[b], ph);
+            issue_S_half(j + 2, 0);
+          }
+          mbar_wait(&p_full[PQ * b + 1], ph);
+          fence_after();
+#ifndef AS_X_NOMMA2
+          mma_grp_ts_mn_4(tmem + 2 * BM + b * BM, tmem + pcol + 32, sdesc(aW + st * TILE + 64 * 128, ATOM_BYTES, 1024),
+                          idO, 1u);
+#endif
+          mma_commit_w(&w_empty[st]);
+          if (j + 2 < nloc) issue_S_half(j + 2, 1);   // into P_j's columns: after its O (in order)
+        }
+        mma_commit_w(o_fin);
+      } else {
       if (nloc > 0) issue_S(0);
       if (nloc > 1) issue_S(1);
       for (int j = 0; j < nloc; ++j) {
@@ -512,6 +573,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
         if (j + 2 < nloc) issue_S(j + 2);
       }
       mma_commit_w(o_fin);
+      }
     }
   } else if (warp < 4 * NWG) {  // ---------------- softmax warpgroups (thread = row)
     AS_REG_INC();
@@ -583,6 +645,96 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
         const float *bmx = sBmax + (g * 2 + (jj & 1)) * 4;
         bmax = fmaxf(fmaxf(bmx[0], bmx[1]), fmaxf(bmx[2], bmx[3]));
       }
+#ifndef AS_X_NOSOFT
+      if constexpr (P1RING) {
+        // two 64-class halves, each with its own lazy-rescale check (online
+        // softmax per half); the b2 maxima of the halves from the warps' partials
+        const uint32_t par = (uint32_t)((j >> 1) & 1);
+        const float *bmx = sBmax + (g * 2 + (jj & 1)) * 4;
+        const float bmh0 = fmaxf(bmx[0], bmx[1]), bmh1 = fmaxf(bmx[2], bmx[3]);
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        const uint64_t l2e2 = f2(LOG2E, LOG2E);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&s_full2[2 * b + h], par);
+          fence_after();
+          uint32_t r[64];
+          const uint32_t tS = tlq + b * BM + (((uint32_t)h + par) & 1u) * 64u;
+          AS_TMEM_LD32(tS, r);
+          AS_TMEM_LD32(tS + 32, (r + 32));
+          AS_TMEM_WAIT_LD(r);
+          AS_TMEM_WAIT_LD((r + 32));
+          if (h == 1) {                       // half 1's columns free for the next block's half 0
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[b]);
+          }
+          float mt[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mt[k] = __uint_as_float(r[k]);
+#pragma unroll
+          for (int k = 8; k < 64; ++k) mt[k & 7] = fmaxf(mt[k & 7], __uint_as_float(r[k]));
+          const float mx = fmaf(fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
+                                      fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7]))),
+                                LOG2E, h ? bmh1 : bmh0);
+          float m_new = m_used;
+          if (mx > m_used + 8.f) m_new = mx;  // lazy rescale: p <= 2^8 otherwise
+          const bool need = m_new != m_used;
+          const float sc = need ? ((m_used == -FLT_MAX) ? 0.f : ex2(m_used - m_new)) : 1.f;
+          l *= sc;
+          m_used = m_new;
+          if ((jj > 0 || h == 1) && __any_sync(0xffffffffu, need)) {
+            // O must be quiescent: half 0 -- S_j half 1 was issued after this WG's
+            // last O MMA (of block j - 2); half 1 -- O_j's half-0 MMA (o_half)
+            if (h == 0) mbar_wait(&s_full2[2 * b + 1], par);
+            else mbar_wait(&o_half[b], (uint32_t)(jj & 1));
+            fence_after();
+#pragma unroll 1
+            for (int ch = 0; ch < H / 32; ++ch) {
+              uint32_t ro[32];
+              AS_TMEM_LD32(tO + ch * 32, ro);
+              AS_TMEM_WAIT_LD(ro);
+#pragma unroll
+              for (int k = 0; k < 32; ++k) ro[k] = __float_as_uint(__uint_as_float(ro[k]) * sc);
+              AS_TMEM_ST32(tO + ch * 32, ro);
+            }
+          }
+          const uint64_t negm2 = f2(-m_new, -m_new);
+          const float *bh = myB2 + 64 * h;
+          uint32_t pk[32];
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int k = 2 * u;
+            const float2 bv = *reinterpret_cast<const float2 *>(bh + k);
+            uint64_t x = ffma2(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), l2e2, f2(bv.x, bv.y));
+            x = fadd2(x, negm2);
+            float p0, p1;
+            if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
+              ex2_emu2(x, p0, p1);
+            } else {
+              float x0, x1;
+              f2split(x, x0, x1);
+              p0 = XEX2(x0); p1 = XEX2(x1);
+            }
+            acc[u & 3] = fadd2(acc[u & 3], f2(p0, p1));
+            pk[u] = pack_bf16x2(p0, p1);
+#ifdef AS_X_P1NOO
+            pk[u] = 0u;                        // mutant: O = 0 (parity tests must fail)
+#endif
+          }
+          AS_TMEM_ST32(tlq + b * BM + par * 64u + 32u * (uint32_t)h, pk);
+          tmem_wait_st();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[PQ * b + h]);
+        }
+        acc[0] = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        float s0, s1;
+        f2split(acc[0], s0, s1);
+        l += s0 + s1;
+        continue;
+      }
+#endif
       // s_full(j) also implies that the O MMA of this WG's previous block (issued
       // before S_j) completed: O is stable and the P region of buffer b is free.
       mbar_wait(&s_full[b], (j >> 1) & 1);
