@@ -94,6 +94,16 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def ready(self, timeout=5.0):
+        """Block until nvidia-smi has written its first sample (its NVML start-up
+        must not overlap the timed region)."""
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < timeout:
+            if os.path.getsize(self.f.name) > 0:
+                return True
+            time.sleep(0.05)
+        return False
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -383,6 +393,7 @@ def main():
     # ---------------- timed region (device events on the replica stream); the
     # library's per-phase events are OFF here (they cost ~8% of the step)
     clocks = Clocks(local)
+    clocks.ready()
     log("clock sampler started")
     time.sleep(0.3)
     torch.cuda.synchronize()

@@ -13,7 +13,7 @@ OUT = os.path.join(HERE, "libadasgd.so")
 OUT_TRACE = os.path.join(HERE, "libadasgd_trace.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-I", os.path.join(ROOT, "include"),
          "-I", CSRC, "--expt-relaxed-constexpr"]
 SOURCES = ["api.cu", "kernels_sparse.cu", "kernels_segmm.cu", "kernels_dense.cu", "kernels_tc.cu", "kernels_transpose.cu",
            "sched.cpp"]
@@ -58,7 +58,7 @@ def build(force=False, verbose=False, jobs=5, trace=False, variant=None, defines
             sys.stderr.write("nvcc failed on %s\n" % src)
     if failed:
         raise RuntimeError("build failed")
-    link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs + ["-lnccl", "-lrt"]
+    link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs + ["-lnccl", "-lrt", "-lgomp"]
     subprocess.check_call(link)
     return out
 

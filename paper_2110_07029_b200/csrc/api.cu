@@ -11,6 +11,9 @@
 #include "adasgd.h"
 #include "common.cuh"
 #include "common_host.h"
+#ifndef AS_STAGE_THREADS
+#define AS_STAGE_THREADS 8                      // host threads of the batch validation + packing
+#endif
 
 thread_local char g_as_err[512] = "";
 
@@ -552,13 +555,13 @@ int as_destroy(as_ctx *x) {
 // device batch buffers; shared by as_load_batch_csr and as_eval_top1
 static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const int32_t *col, const float *val,
                        const int64_t *lab_ptr, const int32_t *lab) {
-  int64_t nnz = 0, L = 0;
-  int rc = validate_csr(x, rows, row_ptr, col, val, lab_ptr, lab, &nnz, &L);
-  if (rc) return rc;
+  if (!row_ptr || !lab_ptr) return as_fail(AS_E_INVALID, "row_ptr / lab_ptr is NULL");
+  const int64_t nnz = row_ptr[rows] - row_ptr[0], L = lab_ptr[rows] - lab_ptr[0];
+  if (nnz < 0 || L < 0) return as_fail(AS_E_INVALID, "pointers not monotone");
+  if ((nnz > 0 && (!col || !val)) || !lab) return as_fail(AS_E_INVALID, "col/val/lab is NULL");
   if (nnz > x->D.nnz_cap || L > x->D.lab_cap) return as_fail(AS_E_INVALID, "batch exceeds capacity");
   const int k = x->stage_next;
-  x->stage_next ^= 1;
-  rc = cuda_check(x, cudaEventSynchronize(x->pin_ev[k]), "staging wait");   // pinned block k reusable
+  int rc = cuda_check(x, cudaEventSynchronize(x->pin_ev[k]), "staging wait");   // pinned block k reusable
   if (rc) return rc;
   uint8_t *p = (uint8_t *)x->pin[k];
   const size_t o_lp = 8 * (size_t)(rows + 1), o_cc = 2 * o_lp, o_vv = o_cc + 4 * (size_t)nnz,
@@ -569,13 +572,43 @@ static int stage_batch(as_ctx *x, int32_t rows, const int64_t *row_ptr, const in
   float *vv = (float *)(p + o_vv);
   int32_t *ll = (int32_t *)(p + o_ll);
   StepDesc *dd = (StepDesc *)(p + o_dd);
-  for (int r = 0; r <= rows; ++r) {
-    rp[r] = row_ptr[r] - row_ptr[0];
-    lp[r] = lab_ptr[r] - lab_ptr[0];
+  // validation (the rules of validate_csr) fused with the packing, rows split
+  // over host threads for large batches; a thread copies its rows' segments
+  // only once all of them are valid.  On any error the batch is re-validated
+  // serially for validate_csr's message and nothing is enqueued: no state change.
+  const int T = (nnz + L > 32768) ? AS_STAGE_THREADS : 1;
+  int bad[AS_STAGE_THREADS] = {0};
+  const int64_t c0 = row_ptr[0], l0 = lab_ptr[0];
+  const int64_t d = x->D.d, C = x->D.C, mrn = x->cfg.max_row_nnz, mrl = x->cfg.max_row_labels;
+#pragma omp parallel for num_threads(T) schedule(static)
+  for (int t = 0; t < T; ++t) {
+    const int64_t r0 = (int64_t)rows * t / T, r1 = (int64_t)rows * (t + 1) / T;
+    bool ok = true;
+    for (int64_t r = r0; r < r1 && ok; ++r) {
+      const int64_t s0 = row_ptr[r], e0 = row_ptr[r + 1], ls = lab_ptr[r], le = lab_ptr[r + 1];
+      if (e0 < s0 || e0 - s0 > mrn || le <= ls || le - ls > mrl) { ok = false; break; }
+      for (int64_t j = s0; j < e0; ++j)
+        if (col[j] < 0 || col[j] >= d || (j > s0 && col[j] <= col[j - 1])) { ok = false; break; }
+      for (int64_t j = ls; j < le && ok; ++j)
+        if (lab[j] < 0 || lab[j] >= C || (j > ls && lab[j] <= lab[j - 1])) ok = false;
+    }
+    if (!ok) { bad[t] = 1; continue; }
+    for (int64_t r = r0; r < r1; ++r) { rp[r] = row_ptr[r] - c0; lp[r] = lab_ptr[r] - l0; }
+    if (t == T - 1) { rp[rows] = nnz; lp[rows] = L; }
+    const int64_t a = row_ptr[r0], e = row_ptr[r1], la = lab_ptr[r0], lb = lab_ptr[r1];
+    if (e > a) {
+      memcpy(cc + (a - c0), col + a, 4 * (size_t)(e - a));
+      memcpy(vv + (a - c0), val + a, 4 * (size_t)(e - a));
+    }
+    if (lb > la) memcpy(ll + (la - l0), lab + la, 4 * (size_t)(lb - la));
   }
-  memcpy(cc, col + row_ptr[0], 4 * nnz);
-  memcpy(vv, val + row_ptr[0], 4 * nnz);
-  memcpy(ll, lab + lab_ptr[0], 4 * L);
+  for (int t = 0; t < T; ++t)
+    if (bad[t]) {
+      int64_t n2 = 0, L2 = 0;
+      rc = validate_csr(x, rows, row_ptr, col, val, lab_ptr, lab, &n2, &L2);
+      return rc ? rc : as_fail(AS_E_INVALID, "invalid batch");
+    }
+  x->stage_next ^= 1;
   memset(dd, 0, sizeof(StepDesc));
   dd->rows = rows;
   dd->nnz = (int32_t)nnz;

@@ -294,6 +294,43 @@ def test_invalid_batch_is_rejected_without_state_change(gpu_lib):
     assert np.isfinite(rep.train_step(want_loss=True))
 
 
+def test_large_host_batch_threaded_staging(gpu_lib):
+    """Host batches with more than 32K entries are validated and packed by host
+    threads (row ranges): a valid batch trains bit-identically to the same rows
+    built on the device; an error in the first, a middle or the last row range
+    (unsorted features, bad label id, empty label list) is rejected with no
+    state change, and the next valid batch trains normally."""
+    from paper_2110_07029_b200._lib import ASError
+    cfg = _cfg(20000, 3000, 128, 1100, 1024, avg_nnz=60.0, avg_labels=4.0, seed=5)
+    ds = synthgen.make_dataset(cfg, n=1100)
+    p = _params(cfg)
+    sub = ds.rows(np.arange(1024))
+    assert sub.row_ptr[-1] > 32768
+    r1 = _replica(cfg, p, ds, "bf16", debug=False)
+    r2 = _replica(cfg, p, ds, "bf16", debug=False)
+    r1.upload_dataset(ds)
+    for row in (0, 500, 1023):
+        a, e = int(sub.row_ptr[row]), int(sub.row_ptr[row + 1])
+        bad_col = sub.col.copy(); bad_col[a], bad_col[a + 1] = bad_col[a + 1], bad_col[a]
+        bad_lab = sub.lab.copy(); bad_lab[int(sub.lab_ptr[row])] = cfg.C
+        bad_lp = sub.lab_ptr.copy(); bad_lp[row + 1:] -= bad_lp[row + 1] - bad_lp[row]
+        bad_lp = np.ascontiguousarray(bad_lp)
+        assert e - a >= 2
+        for args in [(1024, sub.row_ptr, bad_col, sub.val, sub.lab_ptr, sub.lab),
+                     (1024, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, bad_lab),
+                     (1024, sub.row_ptr, sub.col, sub.val, bad_lp, sub.lab)]:
+            with pytest.raises(ASError) as ex:
+                r2.load_batch_csr(*args)
+            assert ex.value.code == -1
+    assert np.array_equal(r2.get_params(), p)
+    r1.load_batch_stream(0, 1024)
+    l1 = r1.train_step(True)
+    r2.load_batch_csr(1024, sub.row_ptr, sub.col, sub.val, sub.lab_ptr, sub.lab)
+    l2 = r2.train_step(True)
+    assert l1 == l2
+    assert np.array_equal(r1.get_params(), r2.get_params())
+
+
 @pytest.mark.parametrize("shuffled,pos", [(True, 250), (False, 250), (False, 130)])
 def test_resident_stream_batch_equals_host_batch(gpu_lib, shuffled, pos):
     """The device-built batch (a gather for a shuffled or wrapping stream, the
