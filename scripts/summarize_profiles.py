@@ -64,7 +64,8 @@ def traffic(path):
         d, u = dict(zip(hdr, r)), dict(zip(hdr, units))
         b = sum(float(d[k].replace(",", "")) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         name = re.sub(r"^void ", "", d["Kernel Name"].split("(")[0]).split("::")[-1].replace("(int)", "")
-        name = re.sub(r", (false|true|\(bool\)[01])>", ">", name)   # k_out_bwd<h, ONEB> -> k_out_bwd<h>
+        if name.startswith("k_out_bwd<"):
+            name = re.sub(r", [^,>]*>$", ">", name)              # k_out_bwd<h, ONEB> -> k_out_bwd<h>
         out[name] = {"dram_bytes": b, "time_us": float(d["gpu__time_duration.sum"].replace(",", "")),
                      "report": path.split("/")[-1]}
     return json.dumps(out, indent=1)

@@ -643,6 +643,50 @@ def test_full_size_amazon670k_sampled(gpu_lib, peaked):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("peaked", [False, True])
+def test_full_size_amazoncat13k(gpu_lib, peaked):
+    """AmazonCat-13K shape (h = 256, C = 13 330) at b = 1024 in the bench's
+    launch configuration: one class block per CTA (pass 2 with the W2T block in
+    shared memory and four S^T buffers, the last-block update through the H
+    stages, bf16 shadow by TMA), the label terms in pass 1's idle warpgroup,
+    the transposes forked before the SpMM, 16-warp sparse kernels.  Every
+    output against the fp64 oracle, softmax terms on their own; peaked as in
+    the Amazon-670K test."""
+    cfg = synthgen.CONFIGS["amazoncat13k"]
+    ds = synthgen.make_dataset(cfg, n=8_000)
+    p = synthgen.make_init_params(cfg.d, cfg.C, cfg.h, cfg.seed)
+    if peaked:
+        lay = synthgen.param_layout(cfg.d, cfg.C, cfg.h)
+        o, _ = lay["b2"]
+        p[o:o + cfg.C] = np.linspace(0.0, 40.0, cfg.C, dtype=np.float32)
+        o, _ = lay["W2T"]
+        p[o:o + cfg.C * cfg.h] *= np.float32(8.0)
+    h = cfg.h
+    rep = _replica(cfg, p, ds, "bf16", lr=0.5)
+    rep.upload_dataset(ds)
+    rep.load_batch_stream(1000, 1024)
+    loss = rep.train_step(True)
+    sub = ds.rows(ocsr.stream_ids(1000, 1024, ds.n))
+    ref = om.gradients_chunked(sub, otrain.unpack(p, cfg.d, cfg.C, h), chunk=128)
+    tol = 2e-2
+    assert abs(loss - ref["loss"]) <= tol * ref["loss"]
+    lse = _f32(rep.debug_get(1, 4 * 1024)) * LN2
+    assert_close("LSE", lse, ref["LSE"], tol)
+    assert_abs("LSE abs", lse, ref["LSE"], tol)
+    check_softmax_terms("full", rep, sub, ref, cfg.C, h, tol)
+    assert_close("dA", _f32(rep.debug_get(3, 4 * 1024 * h)).reshape(1024, h), ref["dA"], tol)
+    assert_close("dW2T", _f32(rep.debug_get(5, 4 * cfg.C * h)).reshape(cfg.C, h), ref["dW2T"], tol)
+    assert_close("db2", _f32(rep.debug_get(6, 4 * cfg.C)), ref["db2"], tol)
+    keys = np.unique(sub.col)
+    dW1 = _f32(rep.debug_get(7, 4 * len(keys) * h)).reshape(len(keys), h)
+    assert_close("dW1", dW1, ref["dW1"][keys], tol)
+    new = otrain.unpack(rep.get_params(), cfg.d, cfg.C, h)
+    old = otrain.unpack(p, cfg.d, cfg.C, h)
+    assert_close("W2T update", new["W2T"] - old["W2T"], -0.5 * ref["dW2T"], tol)
+    rep.close()
+
+
+@pytest.mark.slow
 def test_full_size_amazon670k_top1_sampled(gpu_lib):
     """Top-1 evaluation at the Amazon-670K shape (670 091 classes, 5236 class
     blocks over the pass-1 splits) on 1024 rows after one training step: 24
