@@ -270,8 +270,22 @@ __device__ __forceinline__ void ex2_emu2(uint64_t x, float &p0, float &p1) {
   p0 = __uint_as_float((__float_as_uint(t0) << 23) + __float_as_uint(q0));
   p1 = __uint_as_float((__float_as_uint(t1) << 23) + __float_as_uint(q1));
 }
+// Exponentials moved from the MUFU to the FMA pipe (ex2_emu2): pairs with index
+// % K == K - 1, per pass (0: none).  Measured (x_probe A/B, per SGD step):
+// pass 1 K = 3 / 4 / 6 / none: 0.274 / 0.270 / 0.270 / 0.287 ms; pass 2
+// 0.375 / 0.366 / 0.362 / 0.360 ms -- pass 1 (online max, fewer other FMA-pipe
+// instructions) wants some offload, pass 2 (db2 sums, label term) none.
+// tools/ubench_softmax.cu: the bare mix runs faster all-MUFU at every warp
+// count (MUFU.EX2 ~32 lanes/clk/SM with independent chains).
+#ifndef AS_EMU_P1
+#define AS_EMU_P1 6
+#endif
+#ifndef AS_EMU_P2
+#define AS_EMU_P2 0
+#endif
+#define AS_EMU_AT(K, u) ((K) > 0 && (u) % ((K) > 0 ? (K) : 1) == (K) - 1)
 #ifndef AS_EMU_MOD
-#define AS_EMU_MOD 3    // pairs with index % AS_EMU_MOD == AS_EMU_MOD - 1 use ex2_emu2 (1 exp in 3)
+#define AS_EMU_MOD 3    // (legacy single knob, unused by the passes)
 #endif
 // Experiment switches (scripts/x_probe.sh builds; never set in the product
 // library): AS_X_NOEXP replaces ex2 by a move, AS_X_NOSOFT skips the softmax
@@ -709,7 +723,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
             uint64_t x = ffma2(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), l2e2, f2(bv.x, bv.y));
             x = fadd2(x, negm2);
             float p0, p1;
-            if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
+            if (AS_EMU_AT(AS_EMU_P1, u)) {
               ex2_emu2(x, p0, p1);
             } else {
               float x0, x1;
@@ -796,7 +810,7 @@ __global__ void __launch_bounds__(FwdCfg<H>::THREADS, 1)
           uint64_t x = ffma2(f2(__uint_as_float(r[k]), __uint_as_float(r[k + 1])), l2e2, f2(bv.x, bv.y));
           x = fadd2(x, negm2);
           float p0, p1;
-          if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
+          if (AS_EMU_AT(AS_EMU_P1, u)) {
             ex2_emu2(x, p0, p1);
           } else {
             float x0, x1;
@@ -1640,7 +1654,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
               x = fadd2(x, m == 0 ? f2(l4.x, l4.y) : f2(l4.z, l4.w));
             }
             float e0, e1;
-            if (u % AS_EMU_MOD == AS_EMU_MOD - 1) {
+            if (AS_EMU_AT(AS_EMU_P2, u)) {
               ex2_emu2(x, e0, e1);
             } else {
               float x0, x1;
