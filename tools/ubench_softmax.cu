@@ -159,17 +159,83 @@ __global__ void __launch_bounds__(512, 1) k_mix(int units, int active_warps_per_
   }
 }
 
+// TM = 5 analogue with the loads software-pipelined: 32-column chunks, the next
+// chunk's tcgen05.ld issued before the current chunk is computed (wait::ld waits
+// for every outstanding load, so the wait of chunk c + 1 follows chunk c's math)
+__device__ __forceinline__ void mix32(const uint32_t (&r)[32], const float *lse, int pbase, uint64_t (&dacc)[4],
+                                      uint32_t *pk) {
+  const uint64_t l2e2 = f2(1.4426950f, 1.4426950f), b2c2 = f2(0.1f, 0.1f);
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    uint64_t x = ffma2(f2(__uint_as_float(r[2 * p]), __uint_as_float(r[2 * p + 1])), l2e2, b2c2);
+    const float2 lv = reinterpret_cast<const float2 *>(lse)[pbase + p];
+    x = fsub2(x, f2(lv.x, lv.y));
+    float x0, x1;
+    f2split(x, x0, x1);
+    const float e0 = ex2(x0), e1 = ex2(x1);
+    dacc[p & 3] = fadd2(dacc[p & 3], f2(e0, e1));
+    pk[p] = pack_bf16x2(e0, e1);
+  }
+}
+__global__ void __launch_bounds__(512, 1) k_pipe(int units, int active_warps_per_smsp, long long *cyc, uint32_t *sink) {
+  const int warp = threadIdx.x >> 5;
+  __shared__ uint32_t tslot;
+  __shared__ __align__(16) float lse[64];
+  if (threadIdx.x < 64) lse[threadIdx.x] = 3.0f + 0.001f * threadIdx.x;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"((uint32_t)__cvta_generic_to_shared(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tl = tslot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
+  const bool active = warp / 4 < active_warps_per_smsp;
+  uint32_t acc = 0;
+  float db2 = 0.f;
+  const long long t0 = clock64();
+  uint32_t ra[32], rb[32];
+  if (active) { TLD32(tl, ra); TWAITLD(ra); }
+  for (int u = 0; u < (active ? units : 0); ++u) {
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      uint64_t dacc[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t pk[32];
+      TLD32(tl + 64 * half + 32, rb);                 // chunk 1 in flight during chunk 0
+      mix32(ra, lse, 0, dacc, pk);
+      TWAITLD(rb);
+      TLD32(tl + 64 * (half ^ 1), ra);                // next half's chunk 0 during chunk 1
+      mix32(rb, lse, 16, dacc, pk + 16);
+      TST32(tl + 64 * half, pk);
+      TWAITLD(ra);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      float d0, d1;
+      f2split(fadd2(fadd2(dacc[0], dacc[1]), fadd2(dacc[2], dacc[3])), d0, d1);
+      db2 += d0 + d1;
+#pragma unroll
+      for (int p = 0; p < 32; ++p) acc ^= pk[p];
+    }
+  }
+  const long long t1 = clock64();
+  if (active && (threadIdx.x & 31) == 0) cyc[blockIdx.x * 32 + warp] = t1 - t0;
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc ^ __float_as_uint(db2);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tslot));
+}
+
 int main() {
   const int blocks = 148, threads = 512, units = 2000;
   long long *cyc;
   uint32_t *sink;
   cudaMalloc(&cyc, 8 * blocks * 32);
   cudaMalloc(&sink, 4 * blocks * threads);
-  const char *names[] = {"registers", "ld x32 + st", "ld x32 only", "st only", "ld x64 + st"};
-  for (int v = 0; v < 5; ++v)
+  const char *names[] = {"registers", "ld x32 + st", "ld x32 only", "st only", "ld x64 + st", "pipelined ld"};
+  for (int v = 0; v < 6; ++v)
   for (int w = 1; w <= 4; w += (w == 1 ? 1 : 2)) {
     cudaMemset(cyc, 0, 8 * blocks * 32);
-    auto kf = v == 0 ? k_mix<0, 0> : v == 1 ? k_mix<0, 1> : v == 2 ? k_mix<0, 2> : v == 3 ? k_mix<0, 3> : k_mix<0, 4>;
+    auto kf = v == 0 ? k_mix<0, 0> : v == 1 ? k_mix<0, 1> : v == 2 ? k_mix<0, 2> : v == 3 ? k_mix<0, 3> : v == 4 ? k_mix<0, 4> : k_pipe;
     kf<<<blocks, threads>>>(10, w, cyc, sink);
     kf<<<blocks, threads>>>(units, w, cyc, sink);
     cudaDeviceSynchronize();
