@@ -274,3 +274,19 @@ def test_replay_state_scaling_period_vs_oracle():
             period, dirs = osched.scale_period(b, nb, dirs, period, 4)
             b, since = nb, 0
         assert (st_.b, st_.period) == (b, period)
+
+
+def test_binding_constants_match_header():
+    """The ctypes binding's enum values are the header's (include/adasgd.h is the
+    contract; the binding only marshals)."""
+    import re
+    from paper_2110_07029_b200 import _lib as L
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "adasgd.h")).read()
+    vals = {m.group(1): int(m.group(2)) for m in re.finditer(r"\b(AS_[A-Z0-9_]+)\s*=\s*(-?\d+)", hdr)}
+    for name in ("AS_FLAG_DEBUG_GRADS", "AS_FLAG_NORM_UB", "AS_NORM_METRIC_SHIFT", "AS_FLAG_R14_LITERAL",
+                 "AS_NORM_UPDATES", "AS_NORM_UB", "AS_NORM_R14_LITERAL"):
+        assert name in vals, name
+        assert getattr(L, name) == vals[name], name
+    # the R14 flag does not collide with the metric bits (flags |= metric << 2)
+    assert vals["AS_FLAG_R14_LITERAL"] & (3 << vals["AS_NORM_METRIC_SHIFT"]) == 0
