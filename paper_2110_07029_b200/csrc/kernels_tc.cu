@@ -1600,7 +1600,13 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
     int jj = 0;                               // units of this WG so far
     uint32_t sph = 0u;
     for (int gu = g; gu < NT; gu += 2, ++jj) {
+      // a class block change commits the next block's state prefetch in this
+      // iteration, before the next unit's bitmap: the bitmap wait below could
+      // leave two groups pending there (AS_X_GRP2) -- measured slower (Amazon-670K
+      // step 0.6534 -> 0.6568 ms, AmazonCat-13K 0.1204 -> 0.1220 ms), off
+      bool newblk = false;
       if (kb != kb_cur) {                     // new class block: per-class state
+        newblk = true;
         kb_cur = kb;
         const bool ok = cls_ok(kb);
         b2c = ok ? sB2r[(kb & 1) * 256 + tix] * LOG2E : -INFINITY;
@@ -1637,7 +1643,13 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
       // label term needs it, after the first half's exponentials (LATEMK), so the
       // cp.async completion wait is off the unit's critical path
       auto read_mk = [&]() {
+#ifndef AS_X_GRP2
+        (void)newblk;
         cp_async_wait<1>();
+#else
+        if (newblk) cp_async_wait<2>();
+        else cp_async_wait<1>();
+#endif
         if constexpr (UNIT == 128) {
           const uint4 q4 = sMk[(jj & 1) * 256 + tix];
           mk[0] = q4.x; mk[1] = q4.y; mk[2] = q4.z; mk[3] = q4.w;
