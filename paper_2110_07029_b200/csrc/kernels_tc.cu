@@ -996,6 +996,14 @@ struct BwdCfg {
 #else
   static constexpr bool W2S = ONEB && H == 256;
 #endif
+  // TR64 (W2S): four stages of 64-row H tiles instead of two of 128 rows.  Measured
+  // equal (AmazonCat-13K out_bwd 0.0350 vs 0.0355 ms): the S^T waits come from the
+  // in-order dW chain across the two WGs, not from the stage count.  Switch AS_X_TR64.
+#ifdef AS_X_TR64
+  static constexpr bool NOTR64_ = false;
+#else
+  static constexpr bool NOTR64_ = true;
+#endif
   // FOLD (h = 128): b2_c and -(LSE_r + ln B) enter the S^T MMA as one more
   // K-step of 16 (a per-class tile A_ext = [b2 in three bf16 parts, 1, 1, 1, 0..]
   // and a per-row tile B_ext = [1, 1, 1, -(LSE + ln B) in three parts, 0..],
@@ -1017,7 +1025,9 @@ struct BwdCfg {
 #ifdef AS_X_HALFUPD
   static constexpr int NSH = H == 128 ? (FOLD ? 4 : 5) : 2;    // H tile stages (128 rows each)
 #else
-  static constexpr int NSH = H == 128 ? (FOLD ? 3 : 4) : 2;    // H tile stages (128 rows each)
+  // W2S (h = 256) with TR64: four stages of 64-row tiles (a stage refills one
+  // unit after its dW MMA instead of two); default two 128-row stages
+  static constexpr int NSH = H == 128 ? (FOLD ? 3 : 4) : (W2S && !NOTR64_ ? 4 : 2);
 #endif
 #endif
   static constexpr int HXB = FOLD ? BM * 32 : 0;  // B_ext tile of an H stage (128 rows x 16 bf16)
@@ -1028,14 +1038,16 @@ struct BwdCfg {
   static constexpr int NSB = H == 128 ? 4 : 2;
 #else
   static constexpr int UNIT = H == 128 ? 128 : 64; // batch rows per unit = S^T columns per buffer
-  static constexpr int HPT = 128 / UNIT;          // units per 128-row H tile
+  static constexpr int TR = (W2S && !NOTR64_) ? 64 : BM;   // rows of an H tile
+  static constexpr int HPT = TR / UNIT;           // units per H tile
   static constexpr int NSB = W2S ? 4 : 2;         // S^T unit buffers
 #endif
   static constexpr int NWT = H == 128 ? 2 : 1;    // W2T blocks resident in TMEM (A operand)
   static constexpr int WCOLS = H / 2;             // TMEM columns of one W2T block (bf16 pairs)
   static constexpr int WTM = W2S ? 0 : NWT * WCOLS;  // TMEM columns of the W2T blocks
   static constexpr int W2SMEM = W2S ? BM * H * 2 : 0; // shared-memory W2T block (W2S)
-  static constexpr int TILE = BM * H * 2;
+  static constexpr int TILE = TR * H * 2;         // bytes of an H tile
+  static constexpr int HATOM = TR * 128;          // one 64-column SW128 atom of an H tile
   static constexpr int THREADS = 16 * 32;        // 4 warpgroups (setmaxnreg granularity)
   // h = 128: the fp32 W2T block (4 swizzled 32-column boxes) is TMA-loaded one
   // block ahead, updated in shared memory from the TMEM dW2T accumulator and
@@ -1206,7 +1218,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
   if (W2S && (int)gridDim.x < n_cblocks) __trap();    // W2S: one class block per CTA
 
   const int B = desc->rows;
-  const int RT = (B + BM - 1) / BM;               // 128-row H tiles
+  const int RT = (B + Cfg::TR - 1) / Cfg::TR;     // H tiles of TR rows
   const int NU = HPT * RT;                        // units per class block
   // every CTA sweeps the row tiles of a class block starting at its own
   // offset, so the 148 CTAs do not all fetch the same H tile from L2 at once
@@ -1284,28 +1296,38 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
       for (int kb = 0; kb < NB; ++kb)
         for (int t = 0; t < RT; ++t, ++it) {
           const int st = it % NSH;
-          if (it >= NSH) mbar_wait_idle(&h_empty[st], ((it / NSH) - 1) & 1);
+          if (it >= NSH) {                    // W2S: on the critical path, no suspend hint
+            if constexpr (W2S) mbar_wait(&h_empty[st], ((it / NSH) - 1) & 1);
+            else mbar_wait_idle(&h_empty[st], ((it / NSH) - 1) & 1);
+          }
           TRACE(2, true, 10, t);
 #ifdef AS_X_NOTMA
           if (it >= NSH) { mbar_arrive(&h_full[st]); continue; }
 #endif
-          mbar_expect_tx(&h_full[st], TILE + HXB + (FOLD ? 1 : 2) * BM * 4);
+          mbar_expect_tx(&h_full[st], TILE + HXB + (FOLD ? 1 : 2) * Cfg::TR * 4);
           const int tr = t + rot < RT ? t + rot : t + rot - RT;    // rotated row tile
           for (int a = 0; a < H / 64; ++a)
-            tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * ATOM_BYTES, a * 64, tr * BM);
+            tma_load_2d(&mapH, &h_full[st], sHt + st * TILE + a * Cfg::HATOM, a * 64, tr * Cfg::TR);
           if constexpr (FOLD) tma_load_2d(&mapHx, &h_full[st], sHx + st * HXB, 0, tr * BM);
-          else bulk_load_1d(sL + st * BM, lsep + tr * BM, BM * 4, &h_full[st]);
-          bulk_load_1d(sWr + st * BM, wrow + tr * BM, BM * 4, &h_full[st]);
+          else bulk_load_1d(sL + st * BM, lsep + tr * Cfg::TR, Cfg::TR * 4, &h_full[st]);
+          bulk_load_1d(sWr + st * BM, wrow + tr * Cfg::TR, Cfg::TR * 4, &h_full[st]);
         }
       if constexpr (W2S) {
         // the block's fp32 W2T (the update's staging) in two 64 KB halves, each
         // into an H stage as soon as its last tile's dW MMAs have read it
-        for (int k = 0; k < 2 && NB > 0; ++k, ++it) {
+        // (BPS 32-column boxes per stage; half k = boxes 4k .. 4k + 3 on wf2[k])
+        constexpr int BPS = TILE / 16384, NQ = (H / 32) / BPS;
+        for (int q = 0; q < NQ && NB > 0; ++q, ++it) {
           const int st = it % NSH;
-          if (it >= NSH) mbar_wait_idle(&h_empty[st], ((it / NSH) - 1) & 1);
-          mbar_expect_tx(&wf2[k], BM * 128 * 4);
-          for (int c = 0; c < 4; ++c)
-            tma_load_2d(&mapWf, &wf2[k], sHt + st * TILE + c * 16384, (4 * k + c) * 32, (int)blockIdx.x * BM);
+          if (it >= NSH) {                    // W2S: on the critical path, no suspend hint
+            if constexpr (W2S) mbar_wait(&h_empty[st], ((it / NSH) - 1) & 1);
+            else mbar_wait_idle(&h_empty[st], ((it / NSH) - 1) & 1);
+          }
+          if ((q * BPS) % 4 == 0) mbar_expect_tx(&wf2[(q * BPS) / 4], BM * 128 * 4);
+          for (int c = 0; c < BPS; ++c) {
+            const int bx = q * BPS + c;
+            tma_load_2d(&mapWf, &wf2[bx / 4], sHt + st * TILE + c * 16384, bx * 32, (int)blockIdx.x * BM);
+          }
         }
       }
     }
@@ -1346,7 +1368,9 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
         // this warp: tcgen05.mma executes in issue order
         const uint64_t dB = sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), 16, 1024);
 #ifndef AS_X_NOMMA1
-        if constexpr (W2S)
+        if constexpr (W2S && Cfg::TR == 64)  // H atoms of 64 rows (8 KB), W2T atoms of 128 (16 KB)
+          mma_grp_ss_kk_16_b64(tmem + c.b * UNIT, sdesc(smem_u32(sW2), 16, 1024), dB, idS, 0u);
+        else if constexpr (W2S)
           mma_grp_ss_kk_16(tmem + c.b * UNIT, sdesc(smem_u32(sW2), 16, 1024), dB, idS, 0u);
         else if constexpr (H == 128)
           mma_grp_ts_k_8(tmem + c.b * UNIT, tmem + COL_W + c.wb * WCOLS, dB, idS, 0u);
@@ -1373,7 +1397,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
                           sdesc(aH + c.st * TILE + 64 * 128, ATOM_BYTES, 1024), idW, 1u);
         } else {
           mma_grp_ts_mn_4(tmem + COL_DW, tmem + c.b * UNIT,
-                          sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), ATOM_BYTES, 1024), idW,
+                          sdesc(aH + c.st * TILE + c.hh * (UNIT * 128), Cfg::HATOM, 1024), idW,
                           c.v > 0 ? 1u : 0u);
         }
 #else
@@ -2166,7 +2190,10 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
           // box c (32 columns): W2S -- half c / 4 in the stage the producer
           // filled after the H tiles; else both stages, loaded here
           auto box = [&](int c) -> uint8_t * {
-            if constexpr (W2S) return sHt + ((NB * RT + (c >> 2)) % NSH) * TILE + (c & 3) * 16384;
+            if constexpr (W2S) {
+              constexpr int BPS = TILE / 16384;
+              return sHt + ((NB * RT + c / BPS) % NSH) * TILE + (c % BPS) * 16384;
+            }
             else return sHt + c * 16384;
           };
           if (!W2S && ut == 0) {
@@ -2798,12 +2825,12 @@ static PFN_encodeTiled get_encode() {
 }
 
 // bf16 row-major [rows][cols] with a {64, 128} box and 128-byte swizzle
-static int make_map(CUtensorMap *m, const void *base, long long rows, int cols) {
+static int make_map(CUtensorMap *m, const void *base, long long rows, int cols, int box_rows = 128) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return -1;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -2812,7 +2839,7 @@ static int make_map(CUtensorMap *m, const void *base, long long rows, int cols) 
 }
 
 struct TcPlan {
-  CUtensorMap mapH, mapW, mapWf, mapHx;
+  CUtensorMap mapH, mapW, mapWf, mapHx, mapH64;   // mapH64: 64-row H boxes (one-block pass 2 at h = 256)
   const void *Hb;
   int h, b_max, bpad, n_cblocks, num_sms, max_splits;
   long long C;
@@ -2867,6 +2894,7 @@ int tc_plan_init(TcPlan *plan, int h, int b_max, long long C, int num_sms, const
   plan->num_sms = num_sms < 160 ? num_sms : 160;   // partial buffers sized for 160
   plan->max_splits = tc_splits(h, b_max, C, plan->num_sms);
   if (make_map(&plan->mapH, Hb, plan->bpad, h) != 0) return -1;
+  if (make_map(&plan->mapH64, Hb, plan->bpad, h, 64) != 0) return -1;
   if (make_map(&plan->mapW, W2b, C, h) != 0) return -1;
   if (make_map_f32(&plan->mapWf, W2T, C, h) != 0) return -1;
   if (make_map_x(&plan->mapHx, Hx, plan->bpad) != 0) return -1;
@@ -2942,7 +2970,7 @@ void launch_out_bwd_tc(cudaStream_t s, const TcPlan *p, const StepDesc *desc, co
         b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
   else if (p->n_cblocks <= grid)             // one class block per CTA (AmazonCat-13K)
     tc::k_out_bwd<256, true><<<grid, tc::BwdCfg<256, true>::THREADS, tc::BwdCfg<256, true>::SMEM, s>>>(
-        p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
+        tc::BwdCfg<256, true>::TR == 64 ? p->mapH64 : p->mapH, p->mapW, p->mapWf, p->mapHx, desc, lsep, (int)p->C, p->n_cblocks, cls_lab, lbits, lbw, wrow, W2T,
         b2, W2b, lr, dbg_dW2T, dbg_db2, dw);
   else
     tc::k_out_bwd<256, false><<<grid, tc::BwdCfg<256>::THREADS, tc::BwdCfg<256>::SMEM, s>>>(
