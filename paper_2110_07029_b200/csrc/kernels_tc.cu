@@ -95,6 +95,27 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t *b, uint32_t parity) {
   } while (!ok);
 #endif
 }
+// the update warps' long waits (a whole class block): poll with a plain
+// nanosleep between phase tests.  The try_wait suspend of mbar_wait_idle wakes on
+// barrier traffic, and pass 2 has plenty: measured ~7 000 wake-ups per warp per
+// launch (16 M of the kernel's 176 M warp-instructions, on the softmax warps'
+// sub-partitions).  Measured slightly slower (Amazon-670K step 0.6673 -> 0.6694 ms):
+// off unless AS_X_SLEEPY.
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t *b, uint32_t parity, uint32_t ns) {
+#ifndef AS_X_SLEEPY
+  (void)ns;
+  mbar_wait_idle(b, parity);
+#else
+  for (;;) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    if (ok) break;
+    __nanosleep(ns);
+  }
+#endif
+}
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst,
                                             int c0, int c1) {
   asm volatile(
@@ -1958,7 +1979,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
       const bool last_smem = W2S || (!TMAUPD && Cfg::LASTSMEM && kb == NB - 1);   // W2S: NB = 1
       if (!last_smem) ld_chunk(0, wq);
       TRACE(3, ut == 0, 11, kb);
-      mbar_wait_idle(dw_full, kb & 1);        // also: every S of block kb completed
+      mbar_wait_sleepy(dw_full, kb & 1, 256);   // also: every S of block kb completed
       TRACE(3, ut == 0, 12, kb);
       fence_after();
       if constexpr (HALF || PING) {
@@ -2325,7 +2346,7 @@ __global__ void __launch_bounds__(BwdCfg<H, ONEB>::THREADS, 1)
       }
       // db2 (thread ut = class ut of the block; label term already in G), SGD on b2
       TRACE(3, ut == 0, 13, kb);
-      mbar_wait_idle(db_full, kb & 1);
+      mbar_wait_sleepy(db_full, kb & 1, 128);
       const float dsum = sDB[ut] + sDB[BM + ut];
       named_bar(3, 128);
       if (lane == 0) mbar_arrive(db_empty);
