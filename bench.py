@@ -353,6 +353,8 @@ def main():
 
     pos = [0]
 
+    traj = []                                            # (b_i, u_i) per mega-batch (Alg. 1 / routing)
+
     def mega_step(host=False):
         """One mega-batch: a1 route, a2-a8 steps of my batches, a9-a13 merge, a14 scaling."""
         log, u, _ = state.route(ds.row_ptr, ds.n, pos[0], M)
@@ -377,6 +379,7 @@ def main():
                 rep.load_batch_stream(gp, r)
                 rep.train_step(False)
         b_used = list(state.b)
+        traj.append({"b": [int(x) for x in b_used], "u": [int(x) for x in u]})
         rep.merge(u, b_used, want_alpha=host)            # D2H of alpha on the e2e path
         state.rescale(u)
         rep.set_batch_sizes(state.b, state.lr)
@@ -520,6 +523,7 @@ def main():
                         "d2h_bytes_per_step": int(world * (4 + 8 * world))},
                 "gpu_launches": launches_total, "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
                 "phases_ms": phase,
+                "replay": {"costs": [list(c) for c in costs], "last_megabatches": traj[-6:]},
                 "phase_timing": {"ms_per_step_profiled": t_prof_ms / args.steps,
                                  "note": "phases_ms and roofline launch durations come from a second, "
                                          "identical K-step region with per-phase CUDA events on; the "
