@@ -523,7 +523,8 @@ def main():
                         "d2h_bytes_per_step": int(world * (4 + 8 * world))},
                 "gpu_launches": launches_total, "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
                 "phases_ms": phase,
-                "replay": {"costs": [list(c) for c in costs], "last_megabatches": traj[-6:]},
+                "replay": {"costs": [[int(c.c0), int(c.c_row), int(c.c_nnz), int(c.num), int(c.den)] for c in costs],
+                           "last_megabatches": traj[-6:]},
                 "phase_timing": {"ms_per_step_profiled": t_prof_ms / args.steps,
                                  "note": "phases_ms and roofline launch durations come from a second, "
                                          "identical K-step region with per-phase CUDA events on; the "
