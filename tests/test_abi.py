@@ -290,3 +290,31 @@ def test_binding_constants_match_header():
         assert getattr(L, name) == vals[name], name
     # the R14 flag does not collide with the metric bits (flags |= metric << 2)
     assert vals["AS_FLAG_R14_LITERAL"] & (3 << vals["AS_NORM_METRIC_SHIFT"]) == 0
+
+
+def test_alg1_dynamics_two_replicas_hetero():
+    """Replay routing + Alg. 1 over mega-batches (the C++ scheduler through
+    driver.ReplayState) for two replicas, one 32% slower, at b_max = 1024:
+    with the paper's beta = b_min / 2 = 64 the first correction overshoots and the
+    literal bound check (R11) then refuses every step, leaving the batch sizes
+    inverted; beta = 16 settles at equal update counts (DESIGN, R11)."""
+    from paper_2110_07029_b200 import driver
+    costs = synthgen.make_cost_models(2, hetero=True)
+    n = 400_000
+    rp = np.arange(n + 1, dtype=np.int64) * 41
+
+    def run(beta, k):
+        st = driver.ReplayState(2, 1024, 128, beta, 0.1, costs)
+        pos, out = 0, []
+        for _ in range(k):
+            _, u, _ = st.route(rp, n, pos, 102_400)
+            out.append((list(st.b), list(u)))
+            st.rescale(u)
+            pos += 102_400
+        return out
+
+    hi = run(64, 5)
+    assert hi[0] == ([1024, 1024], [56, 44])
+    assert hi[2:] == [([640, 1024], [90, 44])] * 3
+    lo = run(16, 8)
+    assert lo[-1][1][0] == lo[-1][1][1] and lo[-1][0][0] == 1024 and lo[-1][0][1] < 1024
