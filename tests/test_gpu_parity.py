@@ -136,6 +136,15 @@ CASES = [
     (4000, 30000, 128, 1200, 1024, 1024),  # multi-block pipelines: 13 class blocks per pass-1 CTA
     (3000, 20000, 256, 800, 512, 512),   # h = 256, W ring wraps (2 stages)
 ]
+# seeded random shapes (ragged batches, small and odd C, both hidden widths; h = 256
+# with C <= 128 SMs takes the one-block pass 2)
+_rng = np.random.default_rng(20260)
+RANDOM_CASES = []
+for _k in range(8):
+    _bm = int(_rng.choice([64, 128, 256, 512]))
+    _B = int(_rng.integers(1, _bm + 1))
+    RANDOM_CASES.append((int(_rng.integers(300, 5000)), int(_rng.integers(60, 6000)), int(_rng.choice([128, 256])),
+                         max(_B + 16, 200), _B, _bm))
 
 
 def _one_step(case, precision):
@@ -178,7 +187,7 @@ def test_transposes_bit_exact(gpu_lib, case):
 
 
 @pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 2e-2)])
-@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("case", CASES + RANDOM_CASES)
 def test_one_step_parity(gpu_lib, case, precision, tol):
     cfg, ds, sub, rep, loss, ref, p = _one_step(case, precision)
     d, C, h, n, B, b_max = case
