@@ -13,6 +13,7 @@ numbers here say nothing about the paper's datasets.
 """
 import json
 import os
+import re
 import sys
 import time
 
@@ -42,14 +43,18 @@ for name in ALGOS:
     algo = "adaptive" if name.startswith("adaptive") else name
     # "..._sfK": adaptive scaling frequency (R27) with p_max = K
     pert_thr = 0.0 if name.startswith("adaptive_np") else 0.1
-    pmax = int(name.split("_sf")[1]) if "_sf" in name else 1
+    pmax = int(re.search(r"_sf(\d+)", name).group(1)) if "_sf" in name else 1
+    # "..._bK": Alg. 1 scaling parameter beta = K (P:274 / Fig. 10b: b_min / 2 and
+    # one smaller and one larger value); default b_min / 2
+    mb = re.search(r"_b(\d+)", name)
+    beta = int(mb.group(1)) if mb else b_min // 2
     M = N * b_max if algo == "sync" else 20 * b_max       # sync: one batch per replica per merge
     gamma = 0.9 if algo == "adaptive" else 0.0
-    reps = [Replica(cfg.d, cfg.C, cfg.h, b_max, p0, b_min=b_min, beta=b_min // 2, megabatch=M,
+    reps = [Replica(cfg.d, cfg.C, cfg.h, b_max, p0, b_min=b_min, beta=beta, megabatch=M,
                     max_row_nnz=int(np.diff(full.row_ptr).max()), max_row_labels=int(np.diff(full.lab_ptr).max()),
                     lr0=lr0, gamma=gamma, pert_thr=pert_thr, precision="bf16", rank=i, world=N, algo=algo)
             for i in range(N)]
-    st = driver.ReplayState(N, b_max, b_min, b_min // 2, lr0, costs, algo=algo, scale_pmax=pmax)
+    st = driver.ReplayState(N, b_max, b_min, beta, lr0, costs, algo=algo, scale_pmax=pmax)
     for r in reps:
         r.upload_dataset(train)
     n = len(train.row_ptr) - 1
