@@ -50,6 +50,10 @@ for name in ALGOS:
     beta = int(mb.group(1)) if mb else b_min // 2
     M = N * b_max if algo == "sync" else 20 * b_max       # sync: one batch per replica per merge
     gamma = 0.9 if algo == "adaptive" else 0.0
+    # "..._gK": momentum gamma = K / 100 of the merge (Alg. 2 line 11)
+    mg = re.search(r"_g(\d+)", name)
+    if mg:
+        gamma = int(mg.group(1)) / 100.0
     reps = [Replica(cfg.d, cfg.C, cfg.h, b_max, p0, b_min=b_min, beta=beta, megabatch=M,
                     max_row_nnz=int(np.diff(full.row_ptr).max()), max_row_labels=int(np.diff(full.lab_ptr).max()),
                     lr0=lr0, gamma=gamma, pert_thr=pert_thr, precision="bf16", rank=i, world=N, algo=algo)
