@@ -1,0 +1,4 @@
+# transposes forked after pass 1 (overlapping the combine only) vs after the SpMM (product)
+mkdir -p gpurun_out
+export ADASGD_NO_BUILD=1
+for k in 1 2 3; do timeout -s KILL 300 bash scripts/x_probe.sh amazon670k; done
