@@ -367,7 +367,11 @@ __device__ __forceinline__ uint32_t swz(int i, int c) {
 
 template <int H>
 struct FwdCfg {
+#ifdef AS_X_P1NST
+  static constexpr int NST = H == 128 ? AS_X_P1NST : 2;   // experiment: W stages
+#else
   static constexpr int NST = H == 128 ? 4 : 2;    // W stages
+#endif
   static constexpr int TILE = BM * H * 2;         // bytes of a 128 x H bf16 tile
   static constexpr int THREADS = 12 * 32;        // 3 warpgroups (setmaxnreg granularity)
   // P1WB2: every softmax warp keeps its own copy of the block's b2 (loaded as
